@@ -351,3 +351,67 @@ def groupby_numpy(keys: list, cols: list, spec: OSpec, bind=None,
         else:
             out[:, fi] = np.maximum.reduceat(vv, starts).astype(np.float64)
     return ks[starts], out, counts
+
+
+# ---------------------------------------------------------------------------
+# budget translation for the CPU baseline (hash_table.py:31-45, hybrid.py:89-132)
+# ---------------------------------------------------------------------------
+
+
+def frames_for_budget(target_groups: float, group_bytes: float, G_total: float,
+                      frame_size: int = 32768, algo: str = "pre_partitioning",
+                      fudge: float = 1.2, slot_ratio: float = 1.0) -> int:
+    """Smallest memory_frames M whose resident table holds >= target_groups
+    under the reference's planning (what BASELINE states as a group budget)."""
+    import math
+    bloom_cost = 1 if algo == "pre_partitioning" else 0
+    G = G_total * group_bytes / frame_size
+    for M in range(4, 1 << 20):
+        F = (group_bytes + 8 + slot_ratio * (8 + bloom_cost)) * fudge / group_bytes
+        gf = G * F
+        P = 0 if gf <= M else max(1, min(math.ceil((gf - M) / (M - 2)), M - 2))
+        frames = M - P if P >= 1 else M - 1
+        bloom = algo == "pre_partitioning" and P > 1
+        per = group_bytes + 8 + slot_ratio * (8 + (1 if bloom else 0))
+        cap = int(frames * frame_size / per)
+        if cap >= target_groups:
+            return M
+    raise ValueError("budget too large")
+
+
+def timed_port_run(algo: str, keys: list, vals: list, aggs, bind, budget_groups: int,
+                   threads: int = 1, frame_size: int = 32768, seed: int = 7):
+    """Run the C port over a sample, key-hash-sharded over `threads` independent
+    operator instances (the reference's concurrency model: independent
+    instances).  Each shard gets budget/threads groups.
+    Returns (seconds, groups, metrics of shard 0); frame packing is excluded."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+    sp = ospec(aggs)
+    states = init_states(sp, vals, list(bind))
+    kr = key_rows(keys)
+    kb = np.concatenate([kr[:, i:i + 1].astype(">u8").view(np.uint8).reshape(len(kr), 8)
+                         if np.asarray(keys[i]).dtype.itemsize == 8 else
+                         (kr[:, i].astype(np.uint32)).astype(">u4").view(np.uint8).reshape(len(kr), 4)
+                         for i in range(len(keys))], axis=1)
+    h = hash_bytes(kb, 0x5eed) % np.uint64(threads) if threads > 1 else np.zeros(len(kb), np.uint64)
+    jobs = []
+    for t in range(threads):
+        sel = np.flatnonzero(h == t)
+        g_t = len(np.unique(kb[sel], axis=0)) if len(sel) else 0
+        rec = 2 + kb.shape[1] + 8 * sp.state_width
+        fr = pack_frames(kb[sel], states[sel], frame_size)
+        M = frames_for_budget(max(1, budget_groups / threads), rec, max(g_t, 1), frame_size, algo)
+        stats = (max(fr.shape[0], 1), len(sel), g_t * rec / frame_size, g_t)
+        jobs.append((fr, M, stats))
+
+    def one(job):
+        fr, M, stats = job
+        return run_port(algo, fr, sp, memory_frames=M, frame_size=frame_size, stats=stats,
+                        seed=seed, kmax=kb.shape[1])
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        outs = list(ex.map(one, jobs))
+    dt = time.perf_counter() - t0
+    return dt, sum(len(o.klens) for o in outs), outs[0].metrics

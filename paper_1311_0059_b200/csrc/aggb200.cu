@@ -1,0 +1,1419 @@
+// aggb200.cu — host orchestrator + C ABI (include/aggb200.h) of the B200
+// group-by hot path.
+//
+// Planning restates the reference's (operators/hybrid.py:89-163,
+// hash_table.py:31-45, operators/base.py:141-147): the frame budget M x p
+// becomes a resident-table capacity in groups; Formula-1 partition counts are a
+// lower bound on the spill fan-out, which is raised until every child
+// partition fits a shared-memory table.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aggb200.h"
+#include "kernels.cuh"
+
+using namespace aggb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(x)                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) return fail(AGGB_CUDA_ERROR, "%s: %s (%s:%d)", #x,            \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__);      \
+  } while (0)
+
+#define TRY(x)                  \
+  do {                          \
+    int s_ = (x);               \
+    if (s_ != AGGB_OK) return s_; \
+  } while (0)
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need, size_t* hw) {
+    if (need <= bytes) return AGGB_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t nb = std::max(need, (size_t)256);
+    cudaError_t e = cudaMalloc(&p, nb);
+    if (e != cudaSuccess) return fail(AGGB_CUDA_ERROR, "cudaMalloc(%zu): %s", nb, cudaGetErrorString(e));
+    bytes = nb;
+    if (hw) *hw += nb;
+    return AGGB_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return (T*)p; }
+};
+
+uint64_t splitmix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// role salts as in the reference (hybrid.py:57-60, hash_sort.py:32-33)
+enum { SALT_PART = 0x11, SALT_SLOT = 0x22, SALT_SPILL = 0x33, SALT_EXCH = 0x77 };
+uint64_t level_seed(uint64_t seed, int salt, int level) {
+  return splitmix(splitmix(seed) ^ ((uint64_t)salt + ((uint64_t)level << 8)));
+}
+
+int64_t next_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// reference planning, restated (hybrid.py:89-132, hash_table.py:31-45)
+// ---------------------------------------------------------------------------
+
+double ref_group_bytes(const aggb_config& c, int ref_width, double G, double G_t) {
+  double floor_b = 2 + 1 + 8.0 * ref_width;
+  if (G_t > 0 && G > 0) return std::max(G * c.frame_size / G_t, floor_b);
+  return 2 + 16 + 8.0 * ref_width;
+}
+
+double fudge_factor(double gb, double extra, double slot_ratio, bool bloom) {
+  double per = gb + 8 + slot_ratio * (8 + (bloom ? 1 : 0));
+  return per * extra / std::max(gb, 1e-300);
+}
+
+int plan_partitions(double gf, int M) {
+  if (gf <= M) return 0;
+  double p = std::ceil((gf - M) / (M - 2));
+  return (int)std::max(1.0, std::min(p, (double)(M - 2)));
+}
+
+int64_t plan_table_cap(int n_frames, int p, double gb, double slot_ratio, bool bloom) {
+  double per = gb + 8 + slot_ratio * (8 + (bloom ? 1 : 0));
+  return (int64_t)(n_frames * (double)p / per);
+}
+
+struct Compiled {
+  DevSpec ds;
+  int kw = 1;
+  int nv = 0;
+  int ref_width = 0;  // reference state width (core.py:137)
+  int out_type[AGGB_MAX_FNS];
+};
+
+int compile_spec(const aggb_spec& s, Compiled& c) {
+  memset(&c.ds, 0, sizeof(c.ds));
+  if (s.n_fns < 1 || s.n_fns > AGGB_MAX_FNS) return fail(AGGB_SPEC_ERROR, "need 1..%d aggregate functions", AGGB_MAX_FNS);
+  if (s.n_keys < 1 || s.n_keys > 2) return fail(AGGB_SPEC_ERROR, "need 1 or 2 key columns");
+  if (s.n_vals < 0 || s.n_vals > AGGB_MAX_VALS) return fail(AGGB_SPEC_ERROR, "too many value columns");
+  for (int i = 0; i < s.n_keys; i++)
+    if (s.key_type[i] != AGGB_I64 && s.key_type[i] != AGGB_I32) return fail(AGGB_SPEC_ERROR, "key columns must be int64/int32");
+  c.kw = s.n_keys;
+  DevSpec& d = c.ds;
+  bool states = s.input_kind == AGGB_INPUT_STATES;
+  d.nv = s.n_vals;
+  for (int w = 0; w < s.n_vals; w++) d.vty[w] = (s.val_type[w] == AGGB_F64) ? TY_F64 : TY_I64;
+  auto add_field = [&](uint8_t op, uint8_t ty, uint8_t sk, int8_t src, bool dedup) -> int {
+    if (dedup)
+      for (int j = 0; j < d.ns; j++)
+        if (d.op[j] == op && d.ty[j] == ty && d.srck[j] == sk && d.src[j] == src) return j;
+    if (d.ns >= MAX_STATES) return -1;
+    d.op[d.ns] = op;
+    d.ty[d.ns] = ty;
+    d.srck[d.ns] = sk;
+    d.src[d.ns] = src;
+    return d.ns++;
+  };
+  int soff = 0;
+  c.ref_width = 0;
+  for (int i = 0; i < s.n_fns; i++) {
+    int fn = s.fn[i];
+    int col = s.col[i];
+    int a = -1, b = -1;
+    bool div = false;
+    if (fn < 0 || fn > 4) return fail(AGGB_SPEC_ERROR, "unknown aggregate function id %d", fn);
+    int width = (fn == AGGB_FN_AVG) ? 2 : 1;
+    c.ref_width += width;
+    if (states) {
+      if (soff + width > s.n_vals) return fail(AGGB_SPEC_ERROR, "state columns do not cover the spec");
+      if (fn == AGGB_FN_COUNT) a = add_field(OP_ADD, TY_I64, SRC_STATE_F64, soff, false);
+      else if (fn == AGGB_FN_SUM) a = add_field(OP_ADD, TY_F64, SRC_STATE_F64, soff, false);
+      else if (fn == AGGB_FN_MIN) a = add_field(OP_MIN, TY_F64, SRC_STATE_F64, soff, false);
+      else if (fn == AGGB_FN_MAX) a = add_field(OP_MAX, TY_F64, SRC_STATE_F64, soff, false);
+      else {
+        a = add_field(OP_ADD, TY_F64, SRC_STATE_F64, soff, false);
+        b = add_field(OP_ADD, TY_I64, SRC_STATE_F64, soff + 1, false);
+        div = true;
+      }
+      soff += width;
+    } else {
+      if (fn != AGGB_FN_COUNT && (col < 0 || col >= s.n_vals))
+        return fail(AGGB_SPEC_ERROR, "function %d bound to missing value column %d", i, col);
+      uint8_t ty = (fn == AGGB_FN_COUNT) ? TY_I64 : d.vty[col];
+      if (fn == AGGB_FN_COUNT) a = add_field(OP_ADD, TY_I64, SRC_ONE, -1, true);
+      else if (fn == AGGB_FN_SUM) a = add_field(OP_ADD, ty, SRC_VAL, (int8_t)col, true);
+      else if (fn == AGGB_FN_MIN) a = add_field(OP_MIN, ty, SRC_VAL, (int8_t)col, true);
+      else if (fn == AGGB_FN_MAX) a = add_field(OP_MAX, ty, SRC_VAL, (int8_t)col, true);
+      else {
+        a = add_field(OP_ADD, ty, SRC_VAL, (int8_t)col, true);
+        b = add_field(OP_ADD, TY_I64, SRC_ONE, -1, true);
+        div = true;
+      }
+    }
+    if (a < 0 || (div && b < 0)) return fail(AGGB_SPEC_ERROR, "more than %d state fields", MAX_STATES);
+    d.fin_div[i] = div;
+    d.fin_a[i] = (uint8_t)a;
+    d.fin_b[i] = (uint8_t)(b < 0 ? 0 : b);
+    uint8_t oty = div ? TY_F64 : d.ty[a];
+    d.out_ty[i] = oty;
+    c.out_type[i] = (oty == TY_F64) ? AGGB_F64 : AGGB_I64;
+  }
+  d.nout = s.n_fns;
+  c.nv = states ? s.n_vals : s.n_vals;
+  return AGGB_OK;
+}
+
+int nwt_for(int words) {
+  int w = 1;
+  while (w < words) w <<= 1;
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch tables
+// ---------------------------------------------------------------------------
+
+typedef void (*pass_fn)(PassArgs);
+typedef void (*child_fn)(ChildArgs);
+constexpr int BLOCK = 512;
+
+template <int KW, int NWT>
+constexpr int pass_R() { return NWT <= 1 ? 4 : NWT == 2 ? 4 : NWT == 4 ? 2 : 1; }
+
+int g_pass_variant = -1;
+int pass_variant() {
+  if (g_pass_variant < 0) {
+    const char* e = getenv("AGGB_PASS_VARIANT");
+    g_pass_variant = e ? atoi(e) : 2;
+  }
+  return g_pass_variant;
+}
+
+template <int KW>
+pass_fn pass_kernel(int nwt, int* R, int* blk) {
+  *blk = 512;
+  switch (nwt) {
+    case 1:
+      if (pass_variant() == 1) { *R = 4; return k_pass<KW, 1, 4, 512, 1>; }
+      if (pass_variant() == 2) { *R = 2; *blk = 1024; return k_pass<KW, 1, 2, 1024, 1>; }
+      *R = pass_R<KW, 1>(); return k_pass<KW, 1, pass_R<KW, 1>()>;
+    case 2: *R = pass_R<KW, 2>(); return k_pass<KW, 2, pass_R<KW, 2>()>;
+    case 4: *R = pass_R<KW, 4>(); return k_pass<KW, 4, pass_R<KW, 4>()>;
+    case 8: *R = pass_R<KW, 8>(); return k_pass<KW, 8, pass_R<KW, 8>()>;
+    case 16: *R = pass_R<KW, 16>(); return k_pass<KW, 16, pass_R<KW, 16>()>;
+    default: *R = pass_R<KW, 32>(); return k_pass<KW, 32, pass_R<KW, 32>()>;
+  }
+}
+template <int KW>
+child_fn child_kernel(int nwt) {
+  switch (nwt) {
+    case 1: return k_child<KW, 1, 4>;
+    case 2: return k_child<KW, 2, 4>;
+    case 4: return k_child<KW, 4, 2>;
+    case 8: return k_child<KW, 8, 1>;
+    case 16: return k_child<KW, 16, 1>;
+    default: return k_child<KW, 32, 1>;
+  }
+}
+
+constexpr uint32_t PAGE_BYTES = 8192;
+constexpr size_t CHILD_SMEM = 100 * 1024;
+constexpr int MAX_PARTS = 4096;
+
+struct SetInfo {
+  SpillSet ss;
+  uint32_t first_page;  // pages of this set start at or after here
+};
+
+struct Handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  aggb_config cfg{};
+  aggb_spec spec{};
+  Compiled cs;
+  int kw = 1;
+  int sms = 148;
+  size_t hw = 0;
+  // plan
+  int64_t budget = 0;       // resident capacity (groups)
+  bool unlimited = false;
+  int P0 = 1;               // level-0 spill fan-out
+  int child_slots_log2 = 11;
+  int child_cap = 1024;
+  // level-0 table
+  GTable tab{};
+  DBuf tkeys, tstates, thdr;
+  bool has_table = false;
+  // page pool
+  DBuf pool_base, page_part, page_fill, page_set, pool_ctr;  // pool_ctr: [0]=next_page [1]=overflow
+  uint32_t pool_cap = 0;
+  uint64_t pool_bound = 0;  // upper bound of pages used since reset
+  // spill sets
+  int next_set_id = 1;
+  SetInfo raw0{}, part0{};
+  bool raw0_live = false, part0_live = false;
+  // deferral
+  DBuf defer;
+  int64_t defer_cap = 0;
+  // scratch: [0..7] stats, [8] tile counter A, [9] tile counter B, [10] defer count, [11] ovf count,
+  // [12] item counter, [13] out count
+  DBuf scratch;
+  DBuf hscratch_dev;
+  // output
+  DBuf out_keys, out_vals, out_i32[2];
+  int64_t out_cap = 0;
+  // host-side state
+  int64_t records = 0;
+  int launches = 0;
+  bool finished = false;
+  aggb_result result{};
+  aggb_metrics met{};
+  int64_t hash_sort_runs = 0;
+  // recursion scratch
+  DBuf part_records, part_pages, cursor, plist, item_off, ovf;
+  int64_t ovf_cap = 0;
+  // sort path
+  DBuf sort_keys, sort_vals;
+  int64_t sort_n = 0, sort_cap = 0;
+  // staging for host inputs (grow-only)
+  DBuf stage;
+  // per-kernel CUDA-event timing (aggb_profile)
+  bool prof = false;
+  struct Ev { int kid; cudaEvent_t a, b; };
+  std::vector<Ev> evs;
+  std::vector<cudaEvent_t> free_events;
+  double kms[16] = {0};
+  int64_t kcount[16] = {0};
+};
+
+const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
+                        "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
+                        "k_exchange_pack", "k_segreduce"};
+constexpr int NKINDS = 12;
+
+int prof_begin(Handle* h, int kid) {
+  if (!h->prof) return -1;
+  Handle::Ev e;
+  e.kid = kid;
+  for (cudaEvent_t* x : {&e.a, &e.b}) {
+    if (!h->free_events.empty()) {
+      *x = h->free_events.back();
+      h->free_events.pop_back();
+    } else {
+      cudaEventCreate(x);
+    }
+  }
+  cudaEventRecord(e.a, h->st);
+  h->evs.push_back(e);
+  return (int)h->evs.size() - 1;
+}
+void prof_end(Handle* h, int idx) {
+  if (idx < 0) return;
+  cudaEventRecord(h->evs[idx].b, h->st);
+}
+void prof_collect(Handle* h) {
+  if (h->evs.empty()) return;
+  cudaStreamSynchronize(h->st);
+  for (auto& e : h->evs) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    h->kms[e.kid] += ms;
+    h->kcount[e.kid]++;
+    h->free_events.push_back(e.a);
+    h->free_events.push_back(e.b);
+  }
+  h->evs.clear();
+}
+
+unsigned long long* SC(Handle* h) { return h->scratch.as<unsigned long long>(); }
+
+int pool_ensure(Handle* h, uint64_t extra_pages) {
+  uint64_t need = h->pool_bound + extra_pages;
+  if (need > 0xFFFFFFF0ull) return fail(AGGB_CAPACITY_EXCEEDED, "spill pool would exceed 2^32 pages");
+  h->pool_bound = need;
+  if (need <= h->pool_cap) return AGGB_OK;
+  // grow: one contiguous allocation; used pages and metadata are copied over
+  uint64_t cap = std::max<uint64_t>(need + need / 4, 4096);
+  uint32_t used = 0;
+  if (h->pool_cap) {
+    CU(cudaMemcpyAsync(&used, h->pool_ctr.p, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    used = std::min<uint32_t>(used, h->pool_cap);
+  }
+  DBuf np, nf, ns, nb;
+  TRY(np.ensure(cap * 4, &h->hw));
+  TRY(nf.ensure(cap * 4, &h->hw));
+  TRY(ns.ensure(cap * 4, &h->hw));
+  TRY(nb.ensure(cap * (size_t)PAGE_BYTES, &h->hw));
+  if (used) {
+    CU(cudaMemcpyAsync(np.p, h->page_part.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaMemcpyAsync(nf.p, h->page_fill.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaMemcpyAsync(ns.p, h->page_set.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaMemcpyAsync(nb.p, h->pool_base.p, (size_t)used * PAGE_BYTES, cudaMemcpyDeviceToDevice, h->st));
+  }
+  CU(cudaStreamSynchronize(h->st));
+  h->page_part.release();
+  h->page_fill.release();
+  h->page_set.release();
+  h->pool_base.release();
+  h->page_part = np;
+  h->page_fill = nf;
+  h->page_set = ns;
+  h->pool_base = nb;
+  h->pool_cap = (uint32_t)cap;
+  return AGGB_OK;
+}
+
+PagePool pool_of(Handle* h) {
+  PagePool pp;
+  pp.base = h->pool_base.as<uint8_t>();
+  pp.page_bytes = PAGE_BYTES;
+  pp.next_page = h->pool_ctr.as<uint32_t>();
+  pp.overflow = h->pool_ctr.as<uint32_t>() + 1;
+  pp.capacity = h->pool_cap;
+  pp.page_part = h->page_part.as<int32_t>();
+  pp.page_fill = h->page_fill.as<int32_t>();
+  pp.page_set = h->page_set.as<int32_t>();
+  return pp;
+}
+
+SpillSet make_set(Handle* h, int nparts, int payload_words, int kind, uint64_t seed) {
+  SpillSet s;
+  s.id = h->next_set_id++;
+  s.nparts = nparts;
+  s.rw = h->kw + payload_words;
+  s.per_page = (int)(PAGE_BYTES / (8u * s.rw));
+  s.seed = seed;
+  s.kind = kind;
+  return s;
+}
+
+int grid_for(const void* fn, size_t smem, int sms) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BLOCK, smem);
+  return std::max(1, occ) * sms;
+}
+
+size_t pass_smem(int P) { return (size_t)P * 24 + 64; }
+
+bool dense8(const ColSrc& c, int kw) {
+  for (int w = 0; w < kw; w++)
+    if (c.kty[w] == TY_I32 || c.kstride[w] != 8) return false;
+  for (int w = 0; w < c.nv; w++)
+    if (c.vty[w] == TY_I32 || c.vstride[w] != 8) return false;
+  return true;
+}
+
+// one k_pass launch
+struct PassPlan {
+  int mode;
+  const aggb_input* in;      // columnar source (may be null)
+  ColSrc col{};
+  bool use_start = false;    // start from tile counter A (after FILL)
+  const uint64_t* lin = nullptr;
+  int64_t lin_stride = 0;
+  const unsigned long long* lin_count = nullptr;
+  int lin_kind = 0;
+  int lin_words = 0;
+  SpillSet ss{};
+  uint32_t cut0 = 0;
+  uint64_t part_seed = 0;
+  unsigned long long* counter = nullptr;
+};
+
+int launch_pass(Handle* h, PassPlan& pp) {
+  int payload = std::max(pp.col.nv, pp.lin_words);
+  if (pp.mode != MODE_FILL) payload = std::max(payload, pp.ss.rw - h->kw);
+  int nwt = nwt_for(std::max(payload, 1));
+  if (nwt > 32) return fail(AGGB_SPEC_ERROR, "record payload of %d words exceeds 32", payload);
+  int R = 1, blk = BLOCK;
+  pass_fn fn = h->kw == 1 ? pass_kernel<1>(nwt, &R, &blk) : pass_kernel<2>(nwt, &R, &blk);
+  int T = R * blk;
+  int P = pp.mode == MODE_FILL ? 1 : pp.ss.nparts;
+  size_t smem = pass_smem(P);
+  if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
+  CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, blk, smem);
+  int grid = std::max(1, occ) * h->sms;
+  PassArgs a;
+  memset(&a, 0, sizeof(a));
+  a.sp = h->cs.ds;
+  a.mode = pp.mode;
+  a.t = h->tab;
+  a.col = pp.col;
+  a.col_dense = dense8(pp.col, h->kw) ? 1 : 0;
+  a.start_tiles = pp.use_start ? SC(h) + 8 : nullptr;
+  a.start_T = T;
+  if (pp.lin) {
+    a.lin.n = 0;
+    for (int w = 0; w < h->kw; w++) {
+      a.lin.key[w] = (const uint8_t*)(pp.lin + (size_t)w * pp.lin_stride);
+      a.lin.kstride[w] = 8;
+      a.lin.kty[w] = TY_I64;
+    }
+    a.lin.nv = pp.lin_words;
+    for (int w = 0; w < pp.lin_words; w++) {
+      a.lin.val[w] = (const uint8_t*)(pp.lin + (size_t)(h->kw + w) * pp.lin_stride);
+      a.lin.vstride[w] = 8;
+      a.lin.vty[w] = TY_I64;
+    }
+  }
+  a.lin_count = pp.lin ? pp.lin_count : nullptr;
+  a.lin_kind = pp.lin_kind;
+  a.pool = pool_of(h);
+  a.ss = pp.ss;
+  a.cut0 = pp.cut0;
+  a.part_seed = pp.part_seed;
+  a.defer = h->defer.as<uint64_t>();
+  a.defer_stride = h->defer_cap;
+  a.defer_count = SC(h) + 10;
+  a.tile_counter = pp.counter;
+  a.stats = SC(h);
+  if (pp.mode != MODE_FILL) {
+    // upper bound of pages this pass can allocate
+    int64_t recs = pp.col.n + (pp.lin_count ? (pp.lin_stride) : 0);
+    uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + (uint64_t)grid * P + 16;
+    TRY(pool_ensure(h, pages));
+    a.pool = pool_of(h);
+  }
+  CU(cudaMemsetAsync(pp.counter, 0, 8, h->st));
+  int pe = prof_begin(h, pp.mode);
+  fn<<<grid, blk, smem, h->st>>>(a);
+  prof_end(h, pe);
+  h->launches++;
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+int ensure_out(Handle* h, int64_t need) {
+  if (need <= h->out_cap) return AGGB_OK;
+  int64_t cap = std::max<int64_t>(need, 1024);
+  int wv = std::max(h->cs.ds.nout, h->cs.ds.ns);
+  unsigned long long cnt = 0;
+  if (h->out_cap) {
+    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  }
+  DBuf nk, nv;
+  TRY(nk.ensure((size_t)cap * h->kw * 8, &h->hw));
+  TRY(nv.ensure((size_t)cap * wv * 8, &h->hw));
+  if (cnt) {
+    int64_t c = std::min<int64_t>((int64_t)cnt, h->out_cap);
+    for (int w = 0; w < h->kw; w++)
+      CU(cudaMemcpyAsync(nk.as<uint64_t>() + w * cap, h->out_keys.as<uint64_t>() + w * h->out_cap, c * 8,
+                         cudaMemcpyDeviceToDevice, h->st));
+    for (int j = 0; j < wv; j++)
+      CU(cudaMemcpyAsync(nv.as<uint64_t>() + j * cap, h->out_vals.as<uint64_t>() + j * h->out_cap, c * 8,
+                         cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  }
+  h->out_keys.release();
+  h->out_vals.release();
+  h->out_keys = nk;
+  h->out_vals = nv;
+  h->out_cap = cap;
+  return AGGB_OK;
+}
+
+OutBuf outbuf(Handle* h, int partial) {
+  OutBuf o;
+  o.keys = h->out_keys.as<uint64_t>();
+  o.vals = h->out_vals.as<uint64_t>();
+  o.cap = h->out_cap;
+  o.count = SC(h) + 13;
+  o.partial = partial;
+  return o;
+}
+
+int flush_table(Handle* h, bool partial, OutBuf* dst) {
+  int64_t cap_needed;
+  OutBuf o;
+  if (dst) {
+    o = *dst;
+  } else {
+    unsigned long long cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    cap_needed = (int64_t)cnt + (int64_t)h->tab.cap + 2;
+    TRY(ensure_out(h, cap_needed));
+    o = outbuf(h, partial ? 1 : 0);
+  }
+  int grid = h->sms * 4;
+  int pe = prof_begin(h, 5);
+  if (h->kw == 1) k_flush_table<1><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+  else k_flush_table<2><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+  prof_end(h, pe);
+  h->launches++;
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+int table_reset(Handle* h) {
+  int grid = std::min<int64_t>((int64_t)h->sms * 8, (int64_t)((h->tab.stride + 255) / 256));
+  int pe = prof_begin(h, 6);
+  k_table_init<<<std::max(grid, 1), 256, 0, h->st>>>(h->tab, h->kw, h->cs.ds);
+  prof_end(h, pe);
+  h->launches++;
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+ColSrc col_of(Handle* h, const aggb_input* in, const void* const* kptr, const void* const* vptr) {
+  ColSrc c;
+  memset(&c, 0, sizeof(c));
+  c.n = in->n_rows;
+  for (int w = 0; w < h->kw; w++) {
+    c.key[w] = (const uint8_t*)kptr[w];
+    c.kty[w] = h->spec.key_type[w] == AGGB_I32 ? TY_I32 : TY_I64;
+    c.kstride[w] = in->key_stride[w] ? in->key_stride[w] : (c.kty[w] == TY_I32 ? 4 : 8);
+  }
+  c.nv = h->spec.n_vals;
+  for (int w = 0; w < c.nv; w++) {
+    c.val[w] = (const uint8_t*)vptr[w];
+    c.vty[w] = h->spec.val_type[w] == AGGB_I32 ? TY_I32 : (h->spec.val_type[w] == AGGB_F64 ? TY_F64 : TY_I64);
+    c.vstride[w] = in->val_stride[w] ? in->val_stride[w] : (c.vty[w] == TY_I32 ? 4 : 8);
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// planning
+// ---------------------------------------------------------------------------
+
+int plan(Handle* h) {
+  const aggb_config& c = h->cfg;
+  int M = c.memory_frames;
+  int algo = c.algo;
+  if (algo < 0 || algo > 5) return fail(AGGB_SPEC_ERROR, "unknown algorithm id %d", algo);
+  double G = c.stats_G, G_t = c.stats_G_t;
+  if (c.group_estimate >= 0 && c.level == 0) {  // _effective_stats (hybrid.py:193-203)
+    double bg = ref_group_bytes(c, h->cs.ref_width, G, G_t);
+    double gt = std::max(1.0, c.group_estimate);
+    G = gt * bg / std::max(c.frame_size, 1);
+    G_t = gt;
+  }
+  int ns = h->cs.ds.ns;
+  // child shared-memory table geometry
+  size_t per_slot = (size_t)(h->kw + ns) * 8;
+  int lg = 6;
+  while (((size_t)(1 << (lg + 1)) + 1) * per_slot <= CHILD_SMEM && lg < 16) lg++;
+  h->child_slots_log2 = lg;
+  int64_t ccap = (int64_t)((1 << lg) * 0.7);
+
+  if (c.budget_groups > 0) {
+    h->budget = c.budget_groups;
+    h->unlimited = false;
+  } else if (c.budget_groups < 0) {
+    h->unlimited = true;
+    h->budget = (int64_t)std::max(1024.0, G_t * 1.25 + 1024);
+  } else {
+    // frame-derived capacity (InvalidBudget floors: test_operators.py:181-192)
+    if (M < 2) return fail(AGGB_INVALID_BUDGET, "need at least 2 frames, got %d", M);
+    int floor_m = (algo == AGGB_SORT_BASED || algo == AGGB_HASH_SORT) ? 3 : (algo == AGGB_DYNAMIC_DESTAGING ? 5 : 4);
+    if (M < floor_m) return fail(AGGB_INVALID_BUDGET, "algorithm %d needs M >= %d, got %d", algo, floor_m, M);
+    double bg = ref_group_bytes(c, h->cs.ref_width, G, G_t);
+    int p = c.frame_size;
+    int frames = M - 1;
+    bool bloom = false;
+    if (algo != AGGB_SORT_BASED && algo != AGGB_HASH_SORT) {
+      bool pp = algo == AGGB_PRE_PARTITIONING;
+      double F = fudge_factor(bg, c.fudge, c.slot_ratio, pp);
+      int Pref = plan_partitions(G * F, M);
+      if (Pref >= 1) {
+        frames = M - Pref;
+        bloom = pp && Pref > 1;
+      }
+    }
+    h->budget = std::max<int64_t>(1, plan_table_cap(frames, p, bg, c.slot_ratio, bloom));
+    h->unlimited = false;
+  }
+  h->child_cap = (int)std::max<int64_t>(1, std::min<int64_t>(ccap, h->budget));
+  // spill fan-out: every child partition should fit half a child table
+  double spill_groups = std::max(0.0, std::max(G_t, 1.0) - (double)h->budget);
+  int P = (int)std::ceil(spill_groups / std::max(1.0, 0.5 * h->child_cap));
+  P = std::max(P, 1);
+  if (c.budget_groups == 0 && M >= 3) {
+    double bg = ref_group_bytes(c, h->cs.ref_width, G, G_t);
+    double F = fudge_factor(bg, c.fudge, c.slot_ratio, algo == AGGB_PRE_PARTITIONING);
+    P = std::max(P, plan_partitions(G * F, M));  // Formula 1 as the floor
+  }
+  h->P0 = std::min(P, MAX_PARTS);
+  return AGGB_OK;
+}
+
+int setup_table(Handle* h) {
+  int64_t slots = next_pow2(std::max<int64_t>(64, 2 * h->budget));
+  GTable& t = h->tab;
+  t.stride = (uint64_t)slots + 1;
+  t.mask = (uint64_t)slots - 1;
+  t.bmask = (uint64_t)(slots / (h->kw == 1 ? 4 : 2)) - 1;
+  t.cap = (uint64_t)h->budget;
+  t.seed = level_seed(h->cfg.seed, SALT_SLOT, h->cfg.level);
+  TRY(h->tkeys.ensure((size_t)(t.stride + 1) * h->kw * 8, &h->hw));
+  TRY(h->tstates.ensure((size_t)t.stride * std::max(1, h->cs.ds.ns) * 8, &h->hw));
+  TRY(h->thdr.ensure(sizeof(TableHdr), &h->hw));
+  t.keys = h->tkeys.as<uint64_t>();
+  t.states = h->tstates.as<uint64_t>();
+  t.hdr = h->thdr.as<TableHdr>();
+  h->has_table = true;
+  return table_reset(h);
+}
+
+int begin_run(Handle* h) {
+  CU(cudaMemsetAsync(h->scratch.p, 0, h->scratch.bytes, h->st));
+  CU(cudaMemsetAsync(h->pool_ctr.p, 0, h->pool_ctr.bytes, h->st));
+  h->pool_bound = 0;
+  h->next_set_id = 1;
+  h->records = 0;
+  h->launches = 0;
+  h->finished = false;
+  h->hash_sort_runs = 0;
+  h->sort_n = 0;
+  memset(&h->met, 0, sizeof(h->met));
+  memset(&h->result, 0, sizeof(h->result));
+  int algo = h->cfg.algo;
+  uint64_t seed = h->cfg.seed;
+  int lv = h->cfg.level;
+  if (algo == AGGB_ORIGINAL_HH) {
+    h->raw0 = {make_set(h, h->P0 + 1, h->cs.nv, 0, level_seed(seed, SALT_SPILL, lv)), 0};
+    h->part0 = {make_set(h, h->P0 + 1, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
+  } else {
+    h->raw0 = {make_set(h, h->P0, h->cs.nv, 0, level_seed(seed, SALT_SPILL, lv)), 0};
+    h->part0 = {make_set(h, h->P0, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
+  }
+  h->raw0_live = h->part0_live = false;
+  if (h->has_table) TRY(table_reset(h));
+  return AGGB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// push
+// ---------------------------------------------------------------------------
+
+struct Staged {
+  const void* k[AGGB_MAX_KEYS];
+  const void* v[AGGB_MAX_VALS];
+  std::vector<DBuf> owned;
+};
+
+int stage_input(Handle* h, const aggb_input* in, Staged& sg) {
+  for (int w = 0; w < h->kw; w++) sg.k[w] = in->key[w];
+  for (int w = 0; w < h->spec.n_vals; w++) sg.v[w] = in->val[w];
+  if (!in->on_host) return AGGB_OK;
+  // host pointers: copy each column (strided rows whole) into the handle's
+  // grow-only staging buffer; the caller's memory should be pinned for speed
+  size_t total = 0;
+  std::vector<size_t> off;
+  auto span = [&](int64_t stride, int elem) {
+    int64_t sb = stride ? stride : elem;
+    return (size_t)((in->n_rows - 1) * sb + elem);
+  };
+  for (int w = 0; w < h->kw; w++) {
+    off.push_back(total);
+    total += (span(in->key_stride[w], h->spec.key_type[w] == AGGB_I32 ? 4 : 8) + 255) & ~(size_t)255;
+  }
+  for (int w = 0; w < h->spec.n_vals; w++) {
+    off.push_back(total);
+    total += (span(in->val_stride[w], h->spec.val_type[w] == AGGB_I32 ? 4 : 8) + 255) & ~(size_t)255;
+  }
+  TRY(h->stage.ensure(total, &h->hw));
+  int q = 0;
+  for (int w = 0; w < h->kw; w++, q++) {
+    size_t b = span(in->key_stride[w], h->spec.key_type[w] == AGGB_I32 ? 4 : 8);
+    CU(cudaMemcpyAsync(h->stage.as<uint8_t>() + off[q], in->key[w], b, cudaMemcpyHostToDevice, h->st));
+    sg.k[w] = h->stage.as<uint8_t>() + off[q];
+  }
+  for (int w = 0; w < h->spec.n_vals; w++, q++) {
+    size_t b = span(in->val_stride[w], h->spec.val_type[w] == AGGB_I32 ? 4 : 8);
+    CU(cudaMemcpyAsync(h->stage.as<uint8_t>() + off[q], in->val[w], b, cudaMemcpyHostToDevice, h->st));
+    sg.v[w] = h->stage.as<uint8_t>() + off[q];
+  }
+  return AGGB_OK;
+}
+
+int ensure_defer(Handle* h, int64_t T) {
+  int64_t need = (int64_t)h->sms * 4 * T + 4096;
+  if (need <= h->defer_cap) return AGGB_OK;
+  TRY(h->defer.ensure((size_t)need * (h->kw + std::max(1, h->cs.nv)) * 8, &h->hw));
+  h->defer_cap = need;
+  return AGGB_OK;
+}
+
+int push_hybrid(Handle* h, const ColSrc& col) {
+  int algo = h->cfg.algo;
+  unsigned long long* ctrA = SC(h) + 8;
+  unsigned long long* ctrB = SC(h) + 9;
+  if (algo == AGGB_ORIGINAL_HH) {
+    PassPlan pp;
+    pp.mode = MODE_ROUTE;
+    pp.col = col;
+    pp.ss = h->raw0.ss;
+    // partition-0 share: the resident table should end ~90% full (the reference leaves the
+    // same slack through the fudge factor, hybrid.py:89-99, :123-131)
+    double G_t = std::max(1.0, h->cfg.stats_G_t);
+    double r_res = h->cfg.stats_G_t > 0 ? std::min(1.0, 0.9 * (double)h->budget / G_t) : 1.0;
+    double c0 = std::floor(r_res * 4294967296.0);
+    pp.cut0 = (uint32_t)std::min(4294967295.0, std::max(1.0, c0));
+    if (r_res >= 1.0) pp.cut0 = 0xFFFFFFFFu;
+    pp.part_seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+    pp.counter = ctrB;
+    TRY(launch_pass(h, pp));
+    h->raw0_live = true;
+    return AGGB_OK;
+  }
+  // pre_partitioning / hash_sort: FILL then PROBE (kernel boundary = freeze point)
+  int R = 1, blk = BLOCK;
+  int nwt = nwt_for(std::max(1, col.nv));
+  if (h->kw == 1) pass_kernel<1>(nwt, &R, &blk);
+  else pass_kernel<2>(nwt, &R, &blk);
+  TRY(ensure_defer(h, (int64_t)R * blk));
+  CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+  PassPlan f;
+  f.mode = MODE_FILL;
+  f.col = col;
+  f.counter = ctrA;
+  TRY(launch_pass(h, f));
+  if (algo == AGGB_HASH_SORT) return AGGB_OK;  // handled by push_hash_sort
+  // pre_partitioning: PROBE the remainder and the deferred records against the frozen table
+  PassPlan p;
+  p.mode = MODE_PROBE;
+  p.col = col;
+  p.use_start = true;
+  p.lin = h->defer.as<uint64_t>();
+  p.lin_stride = h->defer_cap;
+  p.lin_count = SC(h) + 10;
+  p.lin_kind = 0;
+  p.lin_words = col.nv;
+  p.ss = h->raw0.ss;
+  p.counter = ctrB;
+  TRY(launch_pass(h, p));
+  h->raw0_live = true;
+  return AGGB_OK;
+}
+
+
+// hash_sort (hash_sort.py:40-78): aggregate; when the table is full, cut it to a
+// run of partial states (hash-partitioned so the final merge-with-fold runs as
+// shared-memory children), reset, and continue with the deferred records and
+// the rest of the batch.
+int cut_run(Handle* h) {
+  unsigned long long groups = 0;
+  CU(cudaMemcpyAsync(&groups, &h->tab.hdr->groups, 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  int words = h->kw + h->cs.ds.ns;
+  int64_t n = (int64_t)groups + 2;
+  DBuf tmp;
+  TRY(tmp.ensure((size_t)n * words * 8, nullptr));
+  OutBuf o;
+  o.keys = tmp.as<uint64_t>();
+  o.vals = tmp.as<uint64_t>() + (size_t)h->kw * n;
+  o.cap = n;
+  o.count = SC(h) + 11;
+  o.partial = 1;
+  CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+  TRY(flush_table(h, true, &o));
+  PassPlan g;
+  g.mode = MODE_GRACE;
+  g.lin = tmp.as<uint64_t>();
+  g.lin_stride = n;
+  g.lin_count = SC(h) + 11;
+  g.lin_kind = 1;
+  g.lin_words = h->cs.ds.ns;
+  g.ss = h->part0.ss;
+  g.counter = SC(h) + 9;
+  TRY(launch_pass(h, g));
+  CU(cudaStreamSynchronize(h->st));
+  tmp.release();
+  h->part0_live = true;
+  h->hash_sort_runs++;
+  return table_reset(h);
+}
+
+int push_hash_sort(Handle* h, const ColSrc& col0) {
+  int R = 1, blk = BLOCK;
+  int nwt = nwt_for(std::max(1, col0.nv));
+  if (h->kw == 1) pass_kernel<1>(nwt, &R, &blk);
+  else pass_kernel<2>(nwt, &R, &blk);
+  int64_t T = (int64_t)R * blk;
+  TRY(ensure_defer(h, T));
+  std::vector<ColSrc> queue{col0};
+  std::vector<DBuf> temps;
+  int rc = AGGB_OK;
+  while (!queue.empty() && rc == AGGB_OK) {
+    ColSrc cur = queue.back();
+    queue.pop_back();
+    if (cur.n <= 0) continue;
+    CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+    PassPlan f;
+    f.mode = MODE_FILL;
+    f.col = cur;
+    f.counter = SC(h) + 8;
+    if ((rc = launch_pass(h, f))) break;
+    unsigned long long tiles = 0, nd = 0;
+    int frozen = 0;
+    CU(cudaMemcpyAsync(&tiles, SC(h) + 8, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&nd, SC(h) + 10, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (!frozen) continue;
+    int64_t start = std::min<int64_t>(cur.n, (int64_t)tiles * T);
+    // keep the deferred records (the deferral buffer is reused by the next FILL)
+    ColSrc dc;
+    memset(&dc, 0, sizeof(dc));
+    if (nd) {
+      DBuf tmp;
+      int words = h->kw + cur.nv;
+      if ((rc = tmp.ensure((size_t)nd * words * 8, nullptr))) break;
+      for (int w = 0; w < words; w++)
+        CU(cudaMemcpyAsync(tmp.as<uint64_t>() + w * nd, h->defer.as<uint64_t>() + w * h->defer_cap, nd * 8,
+                           cudaMemcpyDeviceToDevice, h->st));
+      dc.n = (int64_t)nd;
+      for (int w = 0; w < h->kw; w++) {
+        dc.key[w] = (const uint8_t*)(tmp.as<uint64_t>() + w * nd);
+        dc.kstride[w] = 8;
+        dc.kty[w] = TY_I64;
+      }
+      dc.nv = cur.nv;
+      for (int w = 0; w < cur.nv; w++) {
+        dc.val[w] = (const uint8_t*)(tmp.as<uint64_t>() + (h->kw + w) * nd);
+        dc.vstride[w] = 8;
+        dc.vty[w] = (h->cs.ds.vty[w] == TY_F64) ? TY_F64 : TY_I64;
+      }
+      temps.push_back(tmp);
+    }
+    if ((rc = cut_run(h))) break;
+    if (start < cur.n) {
+      ColSrc rest = cur;
+      rest.n = cur.n - start;
+      for (int w = 0; w < h->kw; w++) rest.key[w] = cur.key[w] + start * cur.kstride[w];
+      for (int w = 0; w < cur.nv; w++) rest.val[w] = cur.val[w] + start * cur.vstride[w];
+      queue.push_back(rest);
+    }
+    if (nd) queue.push_back(dc);  // deferred records first
+  }
+  cudaStreamSynchronize(h->st);
+  for (auto& t : temps) t.release();
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// recursion over spilled partitions (hybrid.py:244-277)
+// ---------------------------------------------------------------------------
+
+int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) {
+  int depth = level;
+  for (int guard = 0; guard < 24; guard++) {
+    if (!a_live && !b_live) return AGGB_OK;
+    if (!a_live) {  // normalize: the live set first
+      std::swap(a, b);
+      std::swap(a_live, b_live);
+    }
+    int nparts = std::max(a.ss.nparts, b_live ? b.ss.nparts : 0);
+    int nsets = b_live ? 2 : 1;
+    TRY(h->part_records.ensure((size_t)nparts * 8, &h->hw));
+    TRY(h->part_pages.ensure((size_t)nparts * 8, &h->hw));
+    TRY(h->cursor.ensure((size_t)nparts * 8, &h->hw));
+    CU(cudaMemsetAsync(h->part_records.p, 0, (size_t)nparts * 8, h->st));
+    CU(cudaMemsetAsync(h->part_pages.p, 0, (size_t)nparts * 8, h->st));
+    PagePool pp = pool_of(h);
+    uint32_t first = 0;
+    const uint32_t* last = h->pool_ctr.as<uint32_t>();
+    int hg = h->sms * 4;
+    SetInfo sets[2] = {a, b};
+    for (int q = 0; q < nsets; q++) {
+      int pe = prof_begin(h, 7);
+      k_page_hist<<<hg, 256, 0, h->st>>>(pp, first, last, sets[q].ss.id, nparts, h->part_records.as<unsigned long long>(),
+                                          h->part_pages.as<uint32_t>() + (size_t)q * nparts);
+      prof_end(h, pe);
+      h->launches++;
+    }
+    std::vector<unsigned long long> recs(nparts);
+    std::vector<uint32_t> pages(2 * (size_t)nparts, 0);
+    uint32_t ovfl = 0;
+    CU(cudaMemcpyAsync(recs.data(), h->part_records.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(pages.data(), h->part_pages.p, (size_t)nparts * 4 * nsets, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
+    std::vector<uint32_t> offs(2 * (size_t)nparts);
+    std::vector<int64_t> item_off;
+    uint32_t tot = 0;
+    int nonempty = 0;
+    int64_t max_items_out = 0;
+    for (int p = 0; p < nparts; p++) {
+      uint32_t na = pages[p], nb = nsets > 1 ? pages[nparts + p] : 0;
+      offs[p] = tot;
+      offs[nparts + p] = tot + na;
+      if (na + nb) {
+        item_off.push_back(tot);
+        item_off.push_back(tot + na);
+        nonempty++;
+      }
+      tot += na + nb;
+    }
+    item_off.push_back(tot);
+    h->met.spilled_partitions += nonempty;
+    if (!nonempty) return AGGB_OK;
+    h->met.recursion_depth = std::max<int64_t>(h->met.recursion_depth, depth + 1);
+    TRY(h->plist.ensure((size_t)tot * 4, &h->hw));
+    TRY(h->item_off.ensure(item_off.size() * 8, &h->hw));
+    CU(cudaMemcpyAsync(h->cursor.p, offs.data(), (size_t)nparts * 4 * nsets, cudaMemcpyHostToDevice, h->st));
+    CU(cudaMemcpyAsync(h->item_off.p, item_off.data(), item_off.size() * 8, cudaMemcpyHostToDevice, h->st));
+    for (int q = 0; q < nsets; q++) {
+      int pe = prof_begin(h, 7);
+      k_page_scatter<<<hg, 256, 0, h->st>>>(pp, first, last, sets[q].ss.id, nparts,
+                                             h->cursor.as<uint32_t>() + (size_t)q * nparts, h->plist.as<int32_t>());
+      prof_end(h, pe);
+      h->launches++;
+    }
+    // child pass: output room + overflow room
+    max_items_out = (int64_t)nonempty * (h->child_cap + 1);
+    unsigned long long cnt = 0;
+    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    TRY(ensure_out(h, (int64_t)cnt + max_items_out + 16));
+    int64_t total_recs = 0;
+    for (int p = 0; p < nparts; p++) total_recs += (int64_t)recs[p];
+    int ovw = h->kw + h->cs.ds.ns;
+    if (total_recs + 16 > h->ovf_cap) {
+      TRY(h->ovf.ensure((size_t)(total_recs + 16) * ovw * 8, &h->hw));
+      h->ovf_cap = total_recs + 16;
+    }
+    CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+    CU(cudaMemsetAsync(SC(h) + 12, 0, 8, h->st));
+    int payload = std::max(a.ss.rw, b_live ? b.ss.rw : 0) - h->kw;
+    int nwt = nwt_for(std::max(1, payload));
+    child_fn fn = h->kw == 1 ? child_kernel<1>(nwt) : child_kernel<2>(nwt);
+    size_t smem = ((size_t)(1 << h->child_slots_log2) + 1) * (h->kw + h->cs.ds.ns) * 8;
+    CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int grid = std::min(grid_for((const void*)fn, smem, h->sms), nonempty);
+    ChildArgs ca;
+    memset(&ca, 0, sizeof(ca));
+    ca.sp = h->cs.ds;
+    ca.pool = pp;
+    ca.sets[0] = a.ss;
+    ca.sets[1] = b_live ? b.ss : a.ss;
+    ca.plist = h->plist.as<int32_t>();
+    ca.item_off = h->item_off.as<int64_t>();
+    ca.nitems = nonempty;
+    ca.slots_log2 = h->child_slots_log2;
+    ca.cap = h->child_cap;
+    ca.seed = level_seed(h->cfg.seed, SALT_SLOT, depth + 1);
+    ca.out = outbuf(h, 0);
+    ca.ovf = h->ovf.as<uint64_t>();
+    ca.ovf_stride = h->ovf_cap;
+    ca.ovf_count = SC(h) + 11;
+    ca.item_counter = SC(h) + 12;
+    ca.stats = SC(h);
+    int pe = prof_begin(h, 4);
+    fn<<<grid, BLOCK, smem, h->st>>>(ca);
+    prof_end(h, pe);
+    h->launches++;
+    CU(cudaGetLastError());
+    unsigned long long novf = 0;
+    CU(cudaMemcpyAsync(&novf, SC(h) + 11, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (!novf) return AGGB_OK;
+    // next level: grace-partition the overflow with fresh seeds (fresh per level, hybrid.py:181-184)
+    depth++;
+    int P = (int)std::min<int64_t>(MAX_PARTS, std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.25 * h->child_cap))));
+    SetInfo nxt{make_set(h, P, h->cs.ds.ns, 1, level_seed(h->cfg.seed, SALT_SPILL, depth)), 0};
+    // move the overflow list into a staging copy (ovf is reused by the next child pass)
+    DBuf tmp;
+    TRY(tmp.ensure((size_t)novf * ovw * 8, nullptr));
+    for (int w = 0; w < ovw; w++)
+      CU(cudaMemcpyAsync(tmp.as<uint64_t>() + w * novf, h->ovf.as<uint64_t>() + w * h->ovf_cap, novf * 8,
+                         cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaMemcpyAsync(SC(h) + 11, &novf, 8, cudaMemcpyHostToDevice, h->st));
+    PassPlan g;
+    g.mode = MODE_GRACE;
+    g.lin = tmp.as<uint64_t>();
+    g.lin_stride = (int64_t)novf;
+    g.lin_count = SC(h) + 11;
+    g.lin_kind = 1;
+    g.lin_words = h->cs.ds.ns;
+    g.ss = nxt.ss;
+    g.counter = SC(h) + 9;
+    TRY(launch_pass(h, g));
+    CU(cudaStreamSynchronize(h->st));
+    tmp.release();
+    a = nxt;
+    a_live = true;
+    b_live = false;
+  }
+  return fail(AGGB_CAPACITY_EXCEEDED, "recursion did not converge");
+}
+
+int aggb_sort_push(Handle* h, const ColSrc& col);
+int aggb_sort_finish(Handle* h);
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+const char* aggb_last_error(void) { return g_err.c_str(); }
+
+const char* aggb_version(void) { return "aggb200 0.1 sm_100a"; }
+
+int aggb_create(int device, const aggb_config* cfg, const aggb_spec* spec, void* stream, void** handle) {
+  if (!cfg || !spec || !handle) return fail(AGGB_INVALID_ARG, "null argument");
+  *handle = nullptr;
+  Handle* h = new Handle();
+  h->device = device;
+  h->cfg = *cfg;
+  h->spec = *spec;
+  int s = compile_spec(*spec, h->cs);
+  if (s) {
+    delete h;
+    return s;
+  }
+  h->kw = h->cs.kw;
+  if (h->cfg.algo == AGGB_SHARED_HASH || h->cfg.algo == AGGB_DYNAMIC_DESTAGING) {
+    // same primitives; both run the pre-partitioning schedule on the GPU
+  }
+  s = plan(h);
+  if (s) {
+    delete h;
+    return s;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(AGGB_CUDA_ERROR, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  }
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+  if (stream) {
+    h->st = (cudaStream_t)stream;
+  } else {
+    cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+    h->own_stream = true;
+  }
+  if ((s = h->scratch.ensure(64 * 8, &h->hw)) || (s = h->pool_ctr.ensure(64, &h->hw))) {
+    aggb_destroy(h);
+    return s;
+  }
+  if (h->cfg.algo != AGGB_SORT_BASED) {
+    if ((s = setup_table(h))) {
+      aggb_destroy(h);
+      return s;
+    }
+  }
+  if ((s = begin_run(h))) {
+    aggb_destroy(h);
+    return s;
+  }
+  *handle = h;
+  return AGGB_OK;
+}
+
+int aggb_reset(void* handle) {
+  Handle* h = (Handle*)handle;
+  if (!h) return fail(AGGB_INVALID_ARG, "null handle");
+  prof_collect(h);
+  return begin_run(h);
+}
+
+int aggb_profile(void* handle, int enable) {
+  Handle* h = (Handle*)handle;
+  if (!h) return fail(AGGB_INVALID_ARG, "null handle");
+  prof_collect(h);
+  h->prof = enable != 0;
+  for (int i = 0; i < 16; i++) {
+    h->kms[i] = 0;
+    h->kcount[i] = 0;
+  }
+  return AGGB_OK;
+}
+
+int aggb_kernel_stats(void* handle, int i, const char** name, int64_t* launches, double* total_ms) {
+  Handle* h = (Handle*)handle;
+  if (!h) return fail(AGGB_INVALID_ARG, "null handle");
+  if (i < 0 || i >= NKINDS) return fail(AGGB_INVALID_ARG, "kernel index out of range");
+  prof_collect(h);
+  if (name) *name = KNAMES[i];
+  if (launches) *launches = h->kcount[i];
+  if (total_ms) *total_ms = h->kms[i];
+  return AGGB_OK;
+}
+
+void aggb_destroy(void* handle) {
+  Handle* h = (Handle*)handle;
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->pool_base, &h->page_part, &h->page_fill, &h->page_set,
+                  &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
+                  &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
+                  &h->item_off, &h->ovf, &h->sort_keys, &h->sort_vals};
+  for (DBuf* b : bufs) b->release();
+  h->stage.release();
+  for (auto& e : h->evs) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : h->free_events) cudaEventDestroy(e);
+  if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+
+int aggb_push(void* handle, const aggb_input* in) {
+  Handle* h = (Handle*)handle;
+  if (!h || !in) return fail(AGGB_INVALID_ARG, "null argument");
+  if (h->finished) return fail(AGGB_INVALID_ARG, "push after finish; call aggb_reset");
+  if (in->n_rows < 0) return fail(AGGB_INVALID_ARG, "negative row count");
+  if (in->n_rows == 0) return AGGB_OK;
+  cudaSetDevice(h->device);
+  Staged sg;
+  TRY(stage_input(h, in, sg));
+  ColSrc col = col_of(h, in, sg.k, sg.v);
+  h->records += in->n_rows;
+  int s;
+  if (h->cfg.algo == AGGB_SORT_BASED) s = aggb_sort_push(h, col);
+  else if (h->cfg.algo == AGGB_HASH_SORT) s = push_hash_sort(h, col);
+  else s = push_hybrid(h, col);
+  if (!sg.owned.empty()) {
+    cudaStreamSynchronize(h->st);
+    for (auto& b : sg.owned) b.release();
+  }
+  return s;
+}
+
+int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
+  Handle* h = (Handle*)handle;
+  if (!h) return fail(AGGB_INVALID_ARG, "null handle");
+  if (n_records <= 0) return AGGB_OK;
+  // partial records (SoA: kw key words then ns state words, stride n_records) are
+  // merged through a GRACE pass into the partial spill set, then drained at finish.
+  cudaSetDevice(h->device);
+  CU(cudaMemcpyAsync(SC(h) + 11, &n_records, 8, cudaMemcpyHostToDevice, h->st));
+  PassPlan g;
+  g.mode = MODE_GRACE;
+  g.lin = (const uint64_t*)recv;
+  g.lin_stride = n_records;
+  g.lin_count = SC(h) + 11;
+  g.lin_kind = 1;
+  g.lin_words = h->cs.ds.ns;
+  g.ss = h->part0.ss;
+  g.counter = SC(h) + 9;
+  TRY(launch_pass(h, g));
+  CU(cudaStreamSynchronize(h->st));
+  h->part0_live = true;
+  return AGGB_OK;
+}
+
+int aggb_finish(void* handle, aggb_result* out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !out) return fail(AGGB_INVALID_ARG, "null argument");
+  cudaSetDevice(h->device);
+  if (!h->finished) {
+    if (h->cfg.algo == AGGB_SORT_BASED) {
+      TRY(aggb_sort_finish(h));
+    } else {
+      int frozen = 0;
+      unsigned long long groups = 0;
+      CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&groups, &h->tab.hdr->groups, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      h->met.resident_groups = (int64_t)groups;
+      if (h->cfg.algo == AGGB_ORIGINAL_HH && frozen) {
+        // overflow: cut the table into partition 0 as partial states (hybrid.py:431-451)
+        unsigned long long cnt = 0;
+        CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaStreamSynchronize(h->st));
+        int words = h->kw + h->cs.ds.ns;
+        DBuf tmp;
+        int64_t n = (int64_t)groups + 2;
+        TRY(tmp.ensure((size_t)n * words * 8, nullptr));
+        OutBuf o;
+        o.keys = tmp.as<uint64_t>();
+        o.vals = tmp.as<uint64_t>() + (size_t)h->kw * n;
+        o.cap = n;
+        o.count = SC(h) + 11;
+        o.partial = 1;
+        CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+        TRY(flush_table(h, true, &o));
+        PassPlan g;
+        g.mode = MODE_GRACE;
+        g.lin = tmp.as<uint64_t>();
+        g.lin_stride = n;
+        g.lin_count = SC(h) + 11;
+        g.lin_kind = 1;
+        g.lin_words = h->cs.ds.ns;
+        // partition 0 of the raw set: all records to partition 0 of the partial set
+        SpillSet s0 = h->part0.ss;
+        s0.nparts = 1;
+        g.ss = s0;
+        g.counter = SC(h) + 9;
+        TRY(launch_pass(h, g));
+        CU(cudaStreamSynchronize(h->st));
+        tmp.release();
+        h->part0_live = true;
+        h->part0.ss.nparts = h->raw0.ss.nparts;
+      } else if (h->cfg.algo == AGGB_HASH_SORT && h->hash_sort_runs > 0) {
+        TRY(cut_run(h));  // last run; the merge-with-fold is the drain below
+      } else {
+        TRY(flush_table(h, false, nullptr));
+      }
+      {
+        unsigned long long sp0 = 0;
+        CU(cudaMemcpyAsync(&sp0, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaStreamSynchronize(h->st));
+        h->met.level0_spilled_records = (int64_t)sp0;
+      }
+      TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
+    }
+    unsigned long long cnt = 0, st[ST_NSTATS];
+    uint32_t ovfl = 0;
+    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
+    if ((int64_t)cnt > h->out_cap) return fail(AGGB_CAPACITY_EXCEEDED, "output buffer overflow (%llu > %lld)", cnt, (long long)h->out_cap);
+    // typed key columns
+    aggb_result& r = h->result;
+    memset(&r, 0, sizeof(r));
+    r.n_groups = (int64_t)cnt;
+    for (int w = 0; w < h->kw; w++) {
+      uint64_t* col = h->out_keys.as<uint64_t>() + (size_t)w * h->out_cap;
+      if (h->spec.key_type[w] == AGGB_I32) {
+        TRY(h->out_i32[w].ensure(std::max<size_t>(cnt, 1) * 4, &h->hw));
+        if (cnt) {
+          k_key_to_i32<<<h->sms * 4, 256, 0, h->st>>>(col, h->out_i32[w].as<int32_t>(), (int64_t)cnt);
+          h->launches++;
+        }
+        r.key[w] = h->out_i32[w].p;
+      } else {
+        r.key[w] = col;
+      }
+    }
+    for (int j = 0; j < h->cs.ds.nout; j++) {
+      r.out[j] = h->out_vals.as<uint64_t>() + (size_t)j * h->out_cap;
+      r.out_type[j] = h->cs.out_type[j];
+    }
+    r.sorted = h->cfg.algo == AGGB_SORT_BASED ? 1 : 0;
+    CU(cudaStreamSynchronize(h->st));
+    h->met.records = h->records;
+    h->met.output_groups = (int64_t)cnt;
+    h->met.spilled_records = (int64_t)st[ST_SPILLED];
+    h->met.spilled_bytes = (int64_t)st[ST_SPILLED] * 8 * (h->kw + h->cs.nv);
+    h->met.budget_groups = h->budget;
+    h->met.partitions_level0 = h->P0;
+    h->finished = true;
+    prof_collect(h);
+  }
+  h->met.kernel_launches = h->launches;
+  h->met.high_water_bytes = (int64_t)h->hw;
+  *out = h->result;
+  return AGGB_OK;
+}
+
+int aggb_copy_result(void* handle, void* const* host_keys, void* const* host_out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !h->finished) return fail(AGGB_INVALID_ARG, "no finished result");
+  int64_t n = h->result.n_groups;
+  if (n == 0) return AGGB_OK;
+  for (int w = 0; w < h->kw; w++)
+    if (host_keys && host_keys[w])
+      CU(cudaMemcpyAsync(host_keys[w], h->result.key[w], (size_t)n * (h->spec.key_type[w] == AGGB_I32 ? 4 : 8),
+                         cudaMemcpyDefault, h->st));
+  for (int j = 0; j < h->cs.ds.nout; j++)
+    if (host_out && host_out[j])
+      CU(cudaMemcpyAsync(host_out[j], h->result.out[j], (size_t)n * 8, cudaMemcpyDefault, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  return AGGB_OK;
+}
+
+int aggb_metrics_get(void* handle, aggb_metrics* out) {
+  Handle* h = (Handle*)handle;
+  if (!h || !out) return fail(AGGB_INVALID_ARG, "null argument");
+  h->met.kernel_launches = h->launches;
+  h->met.high_water_bytes = (int64_t)h->hw;
+  h->met.budget_groups = h->budget;
+  h->met.partitions_level0 = h->P0;
+  *out = h->met;
+  return AGGB_OK;
+}
+
+int aggb_generate(void* stream, int kind, uint64_t seed, uint64_t stream_id, int64_t start, int64_t n, int64_t lo,
+                  int64_t range, const double* cdf, int64_t K, uint64_t a, uint64_t b, void* out, int64_t out_stride) {
+  if (n <= 0) return AGGB_OK;
+  if ((kind == 0 || kind == 4) && range <= 0) return fail(AGGB_INVALID_ARG, "range must be positive");
+  auto base_of = [](uint64_t s, uint64_t sid) {
+    uint64_t z = s * 0x9E3779B97F4A7C15ull + sid * 0xD1B54A32D192ED03ull;
+    return mix64_sm(z);
+  };
+  uint64_t base = base_of(seed, stream_id);
+  uint64_t base2 = base_of(seed, stream_id + 100);
+  int elem = (kind == 4) ? 4 : 8;
+  k_gen<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(kind, base, base2, start, n, lo, range, cdf, K, a, b, (uint8_t*)out,
+                                                   out_stride ? out_stride : elem);
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+int aggb_l2_flush(void* stream, void* scratch, int64_t bytes) {
+  static uint32_t salt = 1;
+  k_l2flush<<<148 * 4, 256, 0, (cudaStream_t)stream>>>((uint4*)scratch, bytes / 16, salt++);
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int aggb_sort_push(Handle*, const ColSrc&) { return fail(AGGB_SPEC_ERROR, "sort_based: not built yet"); }
+int aggb_sort_finish(Handle*) { return fail(AGGB_SPEC_ERROR, "sort_based: not built yet"); }
+}  // namespace
+
+extern "C" {
+int64_t aggb_exchange_record_bytes(void* handle) {
+  Handle* h = (Handle*)handle;
+  return h ? (int64_t)(h->kw + h->cs.ds.ns) * 8 : 0;
+}
+int aggb_exchange_pack(void*, int, void*, int64_t*) { return fail(AGGB_SPEC_ERROR, "exchange: not built yet"); }
+}

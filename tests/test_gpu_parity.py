@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path against the reference (goldens) and the oracle.
+
+All calls go through the C ABI (libaggb200.so via paper_1311_0059_b200.engine).
+Bar (BASELINE.json north_star): identical group sets, bit-exact COUNT and
+integer SUM/MIN/MAX, fp64 SUM/AVG within 1e-9 relative; compared after sorting
+by key.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import (assert_values_match, float_out_cols, golden_files, golden_inputs,
+                      load_golden)
+
+pytestmark = pytest.mark.gpu
+
+ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort")
+
+
+def _engine():
+    from paper_1311_0059_b200 import engine
+    return engine
+
+
+def _agg(cfg):
+    from paper_1311_0059_b200.core import AggSpec
+    return AggSpec.from_names(list(cfg.aggs), bind=list(cfg.bind))
+
+
+def _types(arrs):
+    return ["i64" if a.dtype == np.int64 else "i32" if a.dtype == np.int32 else "f64" for a in arrs]
+
+
+def run_gpu(algo, cfg, keys, vals, chunks=1, **kw):
+    E = _engine()
+    agg = _agg(cfg)
+    with E.GroupBy(algo, agg, _types(keys), _types(vals), **kw) as g:
+        n = len(keys[0])
+        step = -(-n // chunks) if n else 0
+        for s in range(0, n, max(step, 1)):
+            g.push([k[s:s + step] for k in keys], [v[s:s + step] for v in vals])
+        res = g.result().sorted_by_key()
+        met = g.metrics()
+    return res, met
+
+
+def key_bytes_of(res):
+    from paper_1311_0059_b200 import datagen as D
+    return D.key_bytes(res.keys)
+
+
+def check_against(res, gkeys, gvals, cfg):
+    assert res.n_groups == gkeys.shape[0], (res.n_groups, gkeys.shape[0])
+    assert np.array_equal(key_bytes_of(res), gkeys)
+    assert_values_match(res.as_float64(), gvals, float_out_cols(cfg))
+
+
+GOLD = [p for p in golden_files() if "__sort_based" not in p]
+
+
+@pytest.mark.parametrize("path", GOLD, ids=lambda p: os.path.basename(p)[:-4])
+def test_golden_same_budget(path):
+    """Same algorithm, same frame budget (M, p) as the reference run."""
+    meta, gkeys, gvals = load_golden(path)
+    cfg, keys, vals = golden_inputs(meta)
+    from paper_1311_0059_b200.core import DatasetStats
+    st = DatasetStats(*meta["stats"])
+    res, met = run_gpu(meta["algo"], cfg, keys, vals, memory_frames=meta["memory_frames"],
+                       frame_size=meta["frame_size"], budget_groups=0, stats=st,
+                       seed=meta["engine_seed"])
+    check_against(res, gkeys, gvals, cfg)
+
+
+@pytest.mark.parametrize("algo", ALGOS_GPU)
+@pytest.mark.parametrize("case", ["C1", "C2s", "C3s15", "C4s", "C5s"])
+def test_golden_tight_budget_chunked(algo, case):
+    """Every algorithm, a budget of 1/8 of the groups (forces spill + recursion
+    where the algorithm spills) and the input pushed in 3 batches."""
+    path = [p for p in GOLD if os.path.basename(p).startswith(case + "__")][0]
+    meta, gkeys, gvals = load_golden(path)
+    cfg, keys, vals = golden_inputs(meta)
+    budget = max(8, gkeys.shape[0] // 8)
+    from paper_1311_0059_b200.core import DatasetStats
+    st = DatasetStats(*meta["stats"])
+    res, met = run_gpu(algo, cfg, keys, vals, chunks=3, budget_groups=budget, stats=st, seed=11)
+    check_against(res, gkeys, gvals, cfg)
+    if algo in ("pre_partitioning", "original_hh", "hash_sort") and gkeys.shape[0] > budget:
+        assert met["spilled_records"] > 0 or algo == "hash_sort"
+
+
+@pytest.mark.parametrize("algo", ALGOS_GPU)
+def test_unknown_cardinality_in_memory_plan(algo):
+    """Stats claim few groups (the plan is in-memory) but there are many:
+    the table overflows and the spill path must still give exact results."""
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    from paper_1311_0059_b200.core import DatasetStats
+    cfg = D.scaled(D.CONFIGS["C2"], 300_000, key_range=50_000)
+    keys, vals = D.generate(cfg)
+    res, met = run_gpu(algo, cfg, keys, vals, budget_groups=3000,
+                       stats=DatasetStats(R=1, R_t=300_000, G=0.01, G_t=10), seed=5)
+    uk, out, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs), list(cfg.bind))
+    assert res.n_groups == len(uk)
+    assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+    assert np.array_equal(res.as_float64(), out)
+
+
+@pytest.mark.parametrize("algo", ALGOS_GPU)
+def test_edge_empty_and_single(algo):
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    cfg = D.scaled(D.CONFIGS["C2"], 1000)
+    E = _engine()
+    agg = _agg(cfg)
+    with E.GroupBy(algo, agg, ["i64"], ["i64"], budget_groups=16) as g:
+        r = g.result()
+        assert r.n_groups == 0
+    keys = [np.full(5000, 42, np.int64)]
+    vals = [np.arange(5000, dtype=np.int64) % 997]
+    res, _ = run_gpu(algo, cfg, keys, vals, budget_groups=4)
+    uk, out, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert res.n_groups == 1 and np.array_equal(res.as_float64(), out)
+
+
+@pytest.mark.parametrize("algo", ALGOS_GPU)
+def test_edge_extreme_keys(algo):
+    """int64 extremes including the table's empty-slot pattern (INT64_MIN)."""
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    cfg = D.scaled(D.CONFIGS["C2"], 1000)
+    rng = np.random.default_rng(3)
+    pool = np.array([np.iinfo(np.int64).min, np.iinfo(np.int64).max, -1, 0, 1,
+                     np.iinfo(np.int64).min + 1], np.int64)
+    keys = [rng.choice(pool, 20000)]
+    vals = [rng.integers(-(1 << 40), 1 << 40, 20000)]
+    res, _ = run_gpu(algo, cfg, keys, vals, budget_groups=2)
+    uk, out, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+    assert np.array_equal(res.as_float64(), out)
+
+
+def test_pre_partitioning_residency():
+    """Resident keys are never spilled (reference test_operators.py:242-269).
+
+    The level-0 table is flushed first, so the first ``resident_groups`` rows of
+    the unsorted result are the resident groups.  If a resident key had also
+    been spilled it would come out twice (duplicate check), and the resident
+    groups' counts must add up to exactly the records not spilled."""
+    from paper_1311_0059_b200 import datagen as D
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C2"], 400_000, key_range=20_000)
+    keys, vals = D.generate(cfg)
+    with E.GroupBy("pre_partitioning", _agg(cfg), ["i64"], ["i64"], budget_groups=2500,
+                   seed=9) as g:
+        g.push(keys, vals)
+        res = g.result()
+        met = g.metrics()
+    R = met["resident_groups"]
+    assert 0.8 * 2500 <= R <= 2500
+    assert len(np.unique(res.keys[0])) == res.n_groups == 20_000
+    assert int(res.values[0][:R].sum()) == met["records"] - met["level0_spilled_records"]
+    assert met["level0_spilled_records"] > 0
