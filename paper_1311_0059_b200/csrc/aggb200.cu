@@ -15,15 +15,35 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <time.h>
 
 #include "../../include/aggb200.h"
-#include "kernels.cuh"
+#include "pass.cuh"
 
 using namespace aggb;
 
 namespace {
 
 thread_local std::string g_err;
+
+// AGGB_TRACE=1: host-side phase timings on stderr (synchronizes the stream)
+struct Trace {
+  bool on;
+  double t0;
+  Trace() : on(getenv("AGGB_TRACE") != nullptr), t0(now()) {}
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  void mark(cudaStream_t st, const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    double t = now();
+    fprintf(stderr, "[aggb] %-28s %8.3f ms\n", what, t - t0);
+    t0 = t;
+  }
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -57,7 +77,7 @@ struct DBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    size_t nb = std::max(need, (size_t)256);
+    size_t nb = std::max(need + need / 4, (size_t)256);  // headroom: sizes vary run to run
     cudaError_t e = cudaMalloc(&p, nb);
     if (e != cudaSuccess) return fail(AGGB_CUDA_ERROR, "cudaMalloc(%zu): %s", nb, cudaGetErrorString(e));
     bytes = nb;
@@ -212,47 +232,81 @@ typedef void (*pass_fn)(PassArgs);
 typedef void (*child_fn)(ChildArgs);
 constexpr int BLOCK = 512;
 
-template <int KW, int NWT>
-constexpr int pass_R() { return NWT <= 1 ? 4 : NWT == 2 ? 4 : NWT == 4 ? 2 : 1; }
+// field-program ids: 0 runtime (PD), 1 C1/C4, 2 C2, 3 C3, 5 C5
+int detect_prog(const DevSpec& d, int kw) {
+  static const uint32_t c1[] = {0x000, 0x010};
+  static const uint32_t c2[] = {0x000, 0x010, 0x011, 0x012};
+  static const uint32_t c3[] = {0x000, 0x054};
+  static const uint32_t c5[] = {0x000, 0x010, 0x011, 0x012, 0x110, 0x111, 0x112,
+                                0x254, 0x255, 0x256, 0x354, 0x355, 0x356};
+  auto eq = [&](const uint32_t* f, int n) {
+    if (d.ns != n) return false;
+    for (int j = 0; j < n; j++)
+      if (field_desc(d, j) != f[j]) return false;
+    return true;
+  };
+  if (kw == 1 && d.nv == 1 && eq(c1, 2)) return 1;
+  if (kw == 1 && d.nv == 1 && eq(c2, 4)) return 2;
+  if (kw == 1 && d.nv == 1 && eq(c3, 2)) return 3;
+  if (kw == 2 && d.nv == 4 && eq(c5, 13)) return 5;
+  return 0;
+}
 
-int g_pass_variant = -1;
-int pass_variant() {
-  if (g_pass_variant < 0) {
-    const char* e = getenv("AGGB_PASS_VARIANT");
-    g_pass_variant = e ? atoi(e) : 2;
+struct PassCfg {
+  pass_fn fn;
+  int R, blk;
+};
+
+template <int KW, int NWT, int R, int BLK, class PG>
+PassCfg pc() { return PassCfg{k_pass<KW, NWT, R, BLK, 1, PG>, R, BLK}; }
+
+template <int KW>
+PassCfg pass_kernel(int nwt, int prog) {
+  if (KW == 1 && nwt == 1) {
+    if (prog == 1) return pc<1, 1, 2, 1024, ProgC1>();
+    if (prog == 2) return pc<1, 1, 2, 1024, ProgC2>();
+    if (prog == 3) return pc<1, 1, 2, 1024, ProgC3>();
   }
-  return g_pass_variant;
+  if (KW == 2 && nwt == 4 && prog == 5) return pc<2, 4, 1, 1024, ProgC5>();
+  switch (nwt) {
+    case 1: return pc<KW, 1, 2, 1024, PD>();
+    case 2: return pc<KW, 2, 2, 1024, PD>();
+    case 4: return pc<KW, 4, 1, 1024, PD>();
+    case 8: return pc<KW, 8, 1, 512, PD>();
+    case 16: return pc<KW, 16, 1, 512, PD>();
+    default: return pc<KW, 32, 1, 256, PD>();
+  }
 }
 
 template <int KW>
-pass_fn pass_kernel(int nwt, int* R, int* blk) {
-  *blk = 512;
-  switch (nwt) {
-    case 1:
-      if (pass_variant() == 1) { *R = 4; return k_pass<KW, 1, 4, 512, 1>; }
-      if (pass_variant() == 2) { *R = 2; *blk = 1024; return k_pass<KW, 1, 2, 1024, 1>; }
-      *R = pass_R<KW, 1>(); return k_pass<KW, 1, pass_R<KW, 1>()>;
-    case 2: *R = pass_R<KW, 2>(); return k_pass<KW, 2, pass_R<KW, 2>()>;
-    case 4: *R = pass_R<KW, 4>(); return k_pass<KW, 4, pass_R<KW, 4>()>;
-    case 8: *R = pass_R<KW, 8>(); return k_pass<KW, 8, pass_R<KW, 8>()>;
-    case 16: *R = pass_R<KW, 16>(); return k_pass<KW, 16, pass_R<KW, 16>()>;
-    default: *R = pass_R<KW, 32>(); return k_pass<KW, 32, pass_R<KW, 32>()>;
+child_fn child_kernel(int nwt, int prog) {
+  if (KW == 1 && nwt == 1) {
+    if (prog == 1) return k_child<1, 1, 4, ProgC1>;
+    if (prog == 2) return k_child<1, 1, 4, ProgC2>;
+    if (prog == 3) return k_child<1, 1, 4, ProgC3>;
   }
-}
-template <int KW>
-child_fn child_kernel(int nwt) {
+  if (KW == 2 && nwt == 4 && prog == 5) return k_child<2, 4, 2, ProgC5>;
   switch (nwt) {
-    case 1: return k_child<KW, 1, 4>;
-    case 2: return k_child<KW, 2, 4>;
-    case 4: return k_child<KW, 4, 2>;
-    case 8: return k_child<KW, 8, 1>;
-    case 16: return k_child<KW, 16, 1>;
-    default: return k_child<KW, 32, 1>;
+    case 1: return k_child<KW, 1, 4, PD>;
+    case 2: return k_child<KW, 2, 4, PD>;
+    case 4: return k_child<KW, 4, 2, PD>;
+    case 8: return k_child<KW, 8, 1, PD>;
+    case 16: return k_child<KW, 16, 1, PD>;
+    default: return k_child<KW, 32, 1, PD>;
   }
 }
 
 constexpr uint32_t PAGE_BYTES = 8192;
 constexpr size_t CHILD_SMEM = 100 * 1024;
+
+int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+int group_of(int rw) { return 4 / gcd_i(rw, 4); }
+// largest fan-out whose per-partition SMEM state (sector residual + page
+// bookkeeping) fits one CTA of k_pass
+int max_parts_for(int rw) {
+  size_t per = (size_t)(group_of(rw) - 1) * rw * 8 + 36;
+  return (int)std::min<size_t>(4096, (200 * 1024) / per);
+}
 constexpr int MAX_PARTS = 4096;
 
 struct SetInfo {
@@ -306,7 +360,12 @@ struct Handle {
   aggb_metrics met{};
   int64_t hash_sort_runs = 0;
   // recursion scratch
-  DBuf part_records, part_pages, cursor, plist, item_off, ovf;
+  DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend;
+  int prog = 0;
+  // blocked bloom filter of the frozen level-0 table (PROBE)
+  DBuf bloom;
+  int64_t bloom_words = 0;
+  uint64_t bloom_seed = 0;
   int64_t ovf_cap = 0;
   // sort path
   DBuf sort_keys, sort_vals;
@@ -324,8 +383,8 @@ struct Handle {
 
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
-                        "k_exchange_pack", "k_segreduce"};
-constexpr int NKINDS = 12;
+                        "k_exchange_pack", "k_segreduce", "k_bloom_build"};
+constexpr int NKINDS = 13;
 
 int prof_begin(Handle* h, int kid) {
   if (!h->prof) return -1;
@@ -418,7 +477,8 @@ SpillSet make_set(Handle* h, int nparts, int payload_words, int kind, uint64_t s
   s.id = h->next_set_id++;
   s.nparts = nparts;
   s.rw = h->kw + payload_words;
-  s.per_page = (int)(PAGE_BYTES / (8u * s.rw));
+  int G = group_of(s.rw);
+  s.per_page = (int)(PAGE_BYTES / (8u * s.rw)) / G * G;
   s.seed = seed;
   s.kind = kind;
   return s;
@@ -430,7 +490,9 @@ int grid_for(const void* fn, size_t smem, int sms) {
   return std::max(1, occ) * sms;
 }
 
-size_t pass_smem(int P) { return (size_t)P * 24 + 64; }
+size_t pass_smem(int P, int G, int rw, int bloom_words) {
+  return (size_t)bloom_words * 8 + (size_t)P * (G - 1) * rw * 8 + (size_t)P * 36 + 64;
+}
 
 bool dense8(const ColSrc& c, int kw) {
   for (int w = 0; w < kw; w++)
@@ -462,11 +524,24 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (pp.mode != MODE_FILL) payload = std::max(payload, pp.ss.rw - h->kw);
   int nwt = nwt_for(std::max(payload, 1));
   if (nwt > 32) return fail(AGGB_SPEC_ERROR, "record payload of %d words exceeds 32", payload);
-  int R = 1, blk = BLOCK;
-  pass_fn fn = h->kw == 1 ? pass_kernel<1>(nwt, &R, &blk) : pass_kernel<2>(nwt, &R, &blk);
+  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+  pass_fn fn = pcfg.fn;
+  int R = pcfg.R, blk = pcfg.blk;
   int T = R * blk;
   int P = pp.mode == MODE_FILL ? 1 : pp.ss.nparts;
-  size_t smem = pass_smem(P);
+  int G = pp.mode == MODE_FILL ? 1 : group_of(pp.ss.rw);
+  int rw = pp.mode == MODE_FILL ? 1 : pp.ss.rw;
+  Bloom bl{nullptr, 0, 0};
+  if (pp.mode == MODE_PROBE && h->bloom_words) {
+    bl.words = h->bloom.as<uint64_t>();
+    bl.mask = (uint32_t)h->bloom_words - 1;
+    bl.seed = h->bloom_seed;
+  }
+  size_t smem = pass_smem(P, G, rw, bl.words ? h->bloom_words : 0);
+  if (smem > 227 * 1024 && bl.words) {  // no room: probe without the filter
+    bl.words = nullptr;
+    smem = pass_smem(P, G, rw, 0);
+  }
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
   CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -500,6 +575,8 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.lin_kind = pp.lin_kind;
   a.pool = pool_of(h);
   a.ss = pp.ss;
+  a.bloom = bl;
+  a.group = G;
   a.cut0 = pp.cut0;
   a.part_seed = pp.part_seed;
   a.defer = h->defer.as<uint64_t>();
@@ -510,7 +587,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (pp.mode != MODE_FILL) {
     // upper bound of pages this pass can allocate
     int64_t recs = pp.col.n + (pp.lin_count ? (pp.lin_stride) : 0);
-    uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + (uint64_t)grid * P + 16;
+    uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + 2ull * grid * P + 16;
     TRY(pool_ensure(h, pages));
     a.pool = pool_of(h);
   }
@@ -675,7 +752,8 @@ int plan(Handle* h) {
     double F = fudge_factor(bg, c.fudge, c.slot_ratio, algo == AGGB_PRE_PARTITIONING);
     P = std::max(P, plan_partitions(G * F, M));  // Formula 1 as the floor
   }
-  h->P0 = std::min(P, MAX_PARTS);
+  int rw0 = h->kw + h->cs.nv;
+  h->P0 = std::min(P, std::min(MAX_PARTS, max_parts_for(rw0)));
   return AGGB_OK;
 }
 
@@ -694,6 +772,16 @@ int setup_table(Handle* h) {
   t.states = h->tstates.as<uint64_t>();
   t.hdr = h->thdr.as<TableHdr>();
   h->has_table = true;
+  // bloom: ~8 bits per resident key, at most 128 KB (it lives in SMEM), off when too sparse
+  if (h->cfg.algo == AGGB_PRE_PARTITIONING && !getenv("AGGB_NO_BLOOM")) {
+    int64_t words = next_pow2(std::max<int64_t>(1, (int64_t)(8 * t.cap) / 64));
+    words = std::min<int64_t>(words, 16384);
+    if (words * 64 >= 4 * (int64_t)t.cap) {
+      h->bloom_words = words;
+      h->bloom_seed = level_seed(h->cfg.seed, 0x66, h->cfg.level);
+      TRY(h->bloom.ensure((size_t)words * 8, &h->hw));
+    }
+  }
   return table_reset(h);
 }
 
@@ -800,11 +888,9 @@ int push_hybrid(Handle* h, const ColSrc& col) {
     return AGGB_OK;
   }
   // pre_partitioning / hash_sort: FILL then PROBE (kernel boundary = freeze point)
-  int R = 1, blk = BLOCK;
   int nwt = nwt_for(std::max(1, col.nv));
-  if (h->kw == 1) pass_kernel<1>(nwt, &R, &blk);
-  else pass_kernel<2>(nwt, &R, &blk);
-  TRY(ensure_defer(h, (int64_t)R * blk));
+  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+  TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk));
   CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
   PassPlan f;
   f.mode = MODE_FILL;
@@ -812,7 +898,21 @@ int push_hybrid(Handle* h, const ColSrc& col) {
   f.counter = ctrA;
   TRY(launch_pass(h, f));
   if (algo == AGGB_HASH_SORT) return AGGB_OK;  // handled by push_hash_sort
-  // pre_partitioning: PROBE the remainder and the deferred records against the frozen table
+  // pre_partitioning: PROBE the remainder and the deferred records against the frozen table.
+  // The filter is rebuilt from the table as it stands after FILL (a kernel boundary, so
+  // the key set is final once frozen); while the table is not frozen PROBE has no work.
+  if (h->bloom_words) {
+    CU(cudaMemsetAsync(h->bloom.p, 0, (size_t)h->bloom_words * 8, h->st));
+    int pe = prof_begin(h, 12);
+    if (h->kw == 1)
+      k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1,
+                                                      h->bloom_seed);
+    else
+      k_bloom_build<2><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1,
+                                                      h->bloom_seed);
+    prof_end(h, pe);
+    h->launches++;
+  }
   PassPlan p;
   p.mode = MODE_PROBE;
   p.col = col;
@@ -868,11 +968,9 @@ int cut_run(Handle* h) {
 }
 
 int push_hash_sort(Handle* h, const ColSrc& col0) {
-  int R = 1, blk = BLOCK;
   int nwt = nwt_for(std::max(1, col0.nv));
-  if (h->kw == 1) pass_kernel<1>(nwt, &R, &blk);
-  else pass_kernel<2>(nwt, &R, &blk);
-  int64_t T = (int64_t)R * blk;
+  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+  int64_t T = (int64_t)pcfg.R * pcfg.blk;
   TRY(ensure_defer(h, T));
   std::vector<ColSrc> queue{col0};
   std::vector<DBuf> temps;
@@ -940,6 +1038,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
 
 int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) {
   int depth = level;
+  Trace tr;
   for (int guard = 0; guard < 24; guard++) {
     if (!a_live && !b_live) return AGGB_OK;
     if (!a_live) {  // normalize: the live set first
@@ -997,6 +1096,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     TRY(h->item_off.ensure(item_off.size() * 8, &h->hw));
     CU(cudaMemcpyAsync(h->cursor.p, offs.data(), (size_t)nparts * 4 * nsets, cudaMemcpyHostToDevice, h->st));
     CU(cudaMemcpyAsync(h->item_off.p, item_off.data(), item_off.size() * 8, cudaMemcpyHostToDevice, h->st));
+    tr.mark(h->st, "drain: page hist + D2H");
     for (int q = 0; q < nsets; q++) {
       int pe = prof_begin(h, 7);
       k_page_scatter<<<hg, 256, 0, h->st>>>(pp, first, last, sets[q].ss.id, nparts,
@@ -1021,7 +1121,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     CU(cudaMemsetAsync(SC(h) + 12, 0, 8, h->st));
     int payload = std::max(a.ss.rw, b_live ? b.ss.rw : 0) - h->kw;
     int nwt = nwt_for(std::max(1, payload));
-    child_fn fn = h->kw == 1 ? child_kernel<1>(nwt) : child_kernel<2>(nwt);
+    child_fn fn = h->kw == 1 ? child_kernel<1>(nwt, h->prog) : child_kernel<2>(nwt, h->prog);
     size_t smem = ((size_t)(1 << h->child_slots_log2) + 1) * (h->kw + h->cs.ds.ns) * 8;
     CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -1042,8 +1142,16 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     ca.ovf = h->ovf.as<uint64_t>();
     ca.ovf_stride = h->ovf_cap;
     ca.ovf_count = SC(h) + 11;
+    {
+      unsigned long long maxrec = 0;
+      for (int p = 0; p < nparts; p++) maxrec = std::max(maxrec, recs[p]);
+      TRY(h->pend.ensure((size_t)grid * (maxrec + 1) * ovw * 8, &h->hw));
+      ca.pend = h->pend.as<uint64_t>();
+      ca.pend_cap = (int64_t)maxrec + 1;
+    }
     ca.item_counter = SC(h) + 12;
     ca.stats = SC(h);
+    tr.mark(h->st, "drain: scatter + buffers");
     int pe = prof_begin(h, 4);
     fn<<<grid, BLOCK, smem, h->st>>>(ca);
     prof_end(h, pe);
@@ -1052,10 +1160,12 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     unsigned long long novf = 0;
     CU(cudaMemcpyAsync(&novf, SC(h) + 11, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    tr.mark(h->st, "drain: child");
     if (!novf) return AGGB_OK;
     // next level: grace-partition the overflow with fresh seeds (fresh per level, hybrid.py:181-184)
     depth++;
-    int P = (int)std::min<int64_t>(MAX_PARTS, std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.25 * h->child_cap))));
+    int P = (int)std::min<int64_t>(max_parts_for(h->kw + h->cs.ds.ns),
+                                   std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.5 * h->child_cap))));
     SetInfo nxt{make_set(h, P, h->cs.ds.ns, 1, level_seed(h->cfg.seed, SALT_SPILL, depth)), 0};
     // move the overflow list into a staging copy (ovf is reused by the next child pass)
     DBuf tmp;
@@ -1111,6 +1221,8 @@ int aggb_create(int device, const aggb_config* cfg, const aggb_spec* spec, void*
     return s;
   }
   h->kw = h->cs.kw;
+  h->prog = detect_prog(h->cs.ds, h->kw);
+  if (getenv("AGGB_NO_SPECIALIZE")) h->prog = 0;
   if (h->cfg.algo == AGGB_SHARED_HASH || h->cfg.algo == AGGB_DYNAMIC_DESTAGING) {
     // same primitives; both run the pre-partitioning schedule on the GPU
   }
@@ -1187,7 +1299,7 @@ void aggb_destroy(void* handle) {
   DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->pool_base, &h->page_part, &h->page_fill, &h->page_set,
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
-                  &h->item_off, &h->ovf, &h->sort_keys, &h->sort_vals};
+                  &h->item_off, &h->ovf, &h->pend, &h->bloom, &h->sort_keys, &h->sort_vals};
   for (DBuf* b : bufs) b->release();
   h->stage.release();
   for (auto& e : h->evs) {
@@ -1212,9 +1324,11 @@ int aggb_push(void* handle, const aggb_input* in) {
   ColSrc col = col_of(h, in, sg.k, sg.v);
   h->records += in->n_rows;
   int s;
+  Trace tr;
   if (h->cfg.algo == AGGB_SORT_BASED) s = aggb_sort_push(h, col);
   else if (h->cfg.algo == AGGB_HASH_SORT) s = push_hash_sort(h, col);
   else s = push_hybrid(h, col);
+  tr.mark(h->st, "push");
   if (!sg.owned.empty()) {
     cudaStreamSynchronize(h->st);
     for (auto& b : sg.owned) b.release();
@@ -1249,6 +1363,7 @@ int aggb_finish(void* handle, aggb_result* out) {
   Handle* h = (Handle*)handle;
   if (!h || !out) return fail(AGGB_INVALID_ARG, "null argument");
   cudaSetDevice(h->device);
+  Trace tr;
   if (!h->finished) {
     if (h->cfg.algo == AGGB_SORT_BASED) {
       TRY(aggb_sort_finish(h));
@@ -1298,6 +1413,7 @@ int aggb_finish(void* handle, aggb_result* out) {
       } else {
         TRY(flush_table(h, false, nullptr));
       }
+      tr.mark(h->st, "finish: level-0 flush");
       {
         unsigned long long sp0 = 0;
         CU(cudaMemcpyAsync(&sp0, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToHost, h->st));
@@ -1345,6 +1461,7 @@ int aggb_finish(void* handle, aggb_result* out) {
     h->met.partitions_level0 = h->P0;
     h->finished = true;
     prof_collect(h);
+    tr.mark(h->st, "finish: tail");
   }
   h->met.kernel_launches = h->launches;
   h->met.high_water_bytes = (int64_t)h->hw;

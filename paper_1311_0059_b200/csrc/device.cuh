@@ -220,6 +220,77 @@ __device__ __forceinline__ uint64_t contrib_fd(uint32_t fd, int kind, int j, con
 }
 
 // ---------------------------------------------------------------------------
+// field programs: the per-record update sequence of a compiled AggSpec.
+//   PD           runtime program (descriptors in shared memory, any spec)
+//   PS<F...>     compile-time program: the benchmark specs get straight-line
+//                update code with every op/type/source branch folded away
+// ---------------------------------------------------------------------------
+
+struct PD {
+  static constexpr int N = 0;
+};
+template <uint32_t... F>
+struct PS {
+  static constexpr int N = sizeof...(F);
+};
+
+// global (L2) updates
+template <int NWT, uint32_t F, uint32_t... Fs>
+__device__ __forceinline__ void gupd_s(uint64_t* st, uint64_t stride, uint64_t s, int kind, int j,
+                                       const uint64_t (&v)[NWT]) {
+  gupdate(st + (uint64_t)j * stride + s, F & 3, (F >> 2) & 3, contrib_fd<NWT>(F, kind, j, v));
+  if constexpr (sizeof...(Fs) > 0) gupd_s<NWT, Fs...>(st, stride, s, kind, j + 1, v);
+}
+template <class PG>
+struct Upd;
+template <>
+struct Upd<PD> {
+  template <int NWT>
+  static __device__ __forceinline__ void g(uint64_t* st, uint64_t stride, uint64_t s, int kind, const uint32_t* fd,
+                                           int ns, const uint64_t (&v)[NWT]) {
+    for (int j = 0; j < ns; j++) {
+      uint32_t f = fd[j];
+      gupdate(st + (uint64_t)j * stride + s, f & 3, (f >> 2) & 3, contrib_fd<NWT>(f, kind, j, v));
+    }
+  }
+  template <int NWT>
+  static __device__ __forceinline__ void sm(uint64_t* st, int stride, int s, int kind, const uint32_t* fd, int ns,
+                                            const uint64_t (&v)[NWT]) {
+    for (int j = 0; j < ns; j++) {
+      uint32_t f = fd[j];
+      supdate(st + (size_t)j * stride + s, f & 3, (f >> 2) & 3, contrib_fd<NWT>(f, kind, j, v));
+    }
+  }
+};
+
+template <int NWT, uint32_t F, uint32_t... Fs>
+__device__ __forceinline__ void supd_s(uint64_t* st, int stride, int s, int kind, int j, const uint64_t (&v)[NWT]) {
+  supdate(st + (size_t)j * stride + s, F & 3, (F >> 2) & 3, contrib_fd<NWT>(F, kind, j, v));
+  if constexpr (sizeof...(Fs) > 0) supd_s<NWT, Fs...>(st, stride, s, kind, j + 1, v);
+}
+
+template <uint32_t... F>
+struct Upd<PS<F...>> {
+  template <int NWT>
+  static __device__ __forceinline__ void g(uint64_t* st, uint64_t stride, uint64_t s, int kind, const uint32_t*, int,
+                                           const uint64_t (&v)[NWT]) {
+    gupd_s<NWT, F...>(st, stride, s, kind, 0, v);
+  }
+  template <int NWT>
+  static __device__ __forceinline__ void sm(uint64_t* st, int stride, int s, int kind, const uint32_t*, int,
+                                            const uint64_t (&v)[NWT]) {
+    supd_s<NWT, F...>(st, stride, s, kind, 0, v);
+  }
+};
+
+// the benchmark specs (descriptor = op | ty<<2 | srck<<4 | vty<<6 | src<<8)
+using ProgC1 = PS<0x000, 0x010>;                           // COUNT, SUM(i64)        C1, C4
+using ProgC2 = PS<0x000, 0x010, 0x011, 0x012>;             // COUNT, SUM, MIN, MAX   C2
+using ProgC3 = PS<0x000, 0x054>;                           // COUNT, SUM(f64) (+AVG) C3
+using ProgC5 = PS<0x000, 0x010, 0x011, 0x012, 0x110, 0x111, 0x112,
+                  0x254, 0x255, 0x256, 0x354, 0x355, 0x356>;  // C5: 13 fields
+
+// ---------------------------------------------------------------------------
 // 128-bit CAS (two-word keys, e.g. C5's int64 || int32)
 // ---------------------------------------------------------------------------
 
@@ -264,7 +335,8 @@ __device__ __forceinline__ int32_t page_alloc(const PagePool& pp, int32_t part, 
   return (int32_t)pg;
 }
 
-// a spill set: records of `rw` 8-byte words (key words first), SoA inside a page
+// a spill set: records of `rw` 8-byte words (key words first), stored record
+// after record (AoS) inside a page, so a 32-byte sector holds whole records
 struct SpillSet {
   int32_t id;
   int32_t nparts;
@@ -274,9 +346,8 @@ struct SpillSet {
   int32_t kind;             // 0 raw payload, 1 native partial states
 };
 
-__device__ __forceinline__ uint64_t* page_word(const PagePool& pp, uint32_t pg, const SpillSet& ss, int w,
-                                               int slot) {
-  return (uint64_t*)page_ptr(pp, pg) + (size_t)w * ss.per_page + slot;
+__device__ __forceinline__ uint64_t* page_rec(const PagePool& pp, uint32_t pg, int rw, int slot) {
+  return (uint64_t*)page_ptr(pp, pg) + (size_t)slot * rw;
 }
 
 }  // namespace aggb

@@ -157,6 +157,36 @@ __device__ __forceinline__ int64_t gtable_lookup(const GTable& t, const uint64_t
   return gt_resolve<KW>(t, k, b, w, insert, res);
 }
 
+// ---------------------------------------------------------------------------
+// blocked bloom filter of the frozen resident keys (the reference keeps a
+// bloom byte per slot for pre-partitioning's probe stage, _kernels.py:388-390,
+// :938-942; here one 64-bit block per key, 4 bits, held in SMEM by k_pass)
+// ---------------------------------------------------------------------------
+
+struct Bloom {
+  const uint64_t* words;  // nullptr: disabled
+  uint32_t mask;          // nblocks - 1 (blocks are 64-bit words)
+  uint64_t seed;
+};
+
+__device__ __forceinline__ uint64_t bloom_bits(uint64_t h) {
+  return (1ull << ((h >> 32) & 63)) | (1ull << ((h >> 38) & 63)) | (1ull << ((h >> 44) & 63)) |
+         (1ull << ((h >> 50) & 63));
+}
+
+template <int KW>
+__global__ void k_bloom_build(GTable t, uint64_t* bloom, uint32_t mask, uint64_t seed) {
+  uint64_t n = t.mask + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = t.keys[i * KW + w];
+    if (is_sentinel<KW>(k)) continue;
+    uint64_t h = hash_key<KW>(k, seed);
+    atomicOr((unsigned long long*)&bloom[h & mask], (unsigned long long)bloom_bits(h));
+  }
+}
+
 __global__ void k_table_init(GTable t, int kw, DevSpec sp) {
   uint64_t n = t.stride;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -273,306 +303,6 @@ __device__ uint32_t block_exscan(uint32_t* a, int n, uint32_t* scratch /* >= 33 
 // k_pass
 // ---------------------------------------------------------------------------
 
-struct PassArgs {
-  DevSpec sp;
-  int32_t mode;
-  GTable t;
-  // source 1: columnar batch rows [start, n), start = min(n, *start_tiles * start_T)
-  ColSrc col;
-  int32_t col_dense;                      // all key/value columns 8-byte, stride 8
-  const unsigned long long* start_tiles;  // nullable
-  int64_t start_T;
-  // source 2: SoA list (deferred / overflow records) described as dense columns
-  ColSrc lin;                             // lin.nv = payload words of the list
-  const unsigned long long* lin_count;    // nullable -> no list
-  int32_t lin_kind;                       // 0 raw payload, 1 native partial
-  // spill target
-  PagePool pool;
-  SpillSet ss;
-  // ROUTE (original_hh): u32 part hash < cut0 -> partition 0 (table)
-  uint32_t cut0;
-  uint64_t part_seed;
-  // FILL deferral target (raw records, SoA, KW + nv words)
-  uint64_t* defer;
-  int64_t defer_stride;
-  unsigned long long* defer_count;
-  unsigned long long* tile_counter;
-  unsigned long long* stats;
-};
-
-template <int KW, int NWT>
-__device__ __forceinline__ void load_rec(const ColSrc& c, bool dense, int nv, int64_t i, uint64_t (&k)[KW],
-                                         uint64_t (&v)[NWT]) {
-  if (dense) {
-#pragma unroll
-    for (int w = 0; w < KW; w++) k[w] = (uint64_t)__ldcs((const long long*)c.key[w] + i);
-#pragma unroll
-    for (int w = 0; w < NWT; w++) v[w] = (w < nv) ? (uint64_t)__ldcs((const long long*)c.val[w] + i) : 0ull;
-  } else {
-    col_key<KW>(c, i, k);
-#pragma unroll
-    for (int w = 0; w < NWT; w++) {
-      if (w < nv) {
-        const uint8_t* p = c.val[w] + i * c.vstride[w];
-        v[w] = (c.vty[w] == TY_I32) ? (uint64_t)(long long)__ldcs((const int*)p) : (uint64_t)__ldcs((const long long*)p);
-      } else {
-        v[w] = 0ull;
-      }
-    }
-  }
-}
-
-// Persistent, tile-scheduled pass.  Per tile: [A] issue the first-bucket loads
-// of the current tile's records and prefetch the next tile's records into
-// registers, resolve the current records (aggregate hits, rank misses per
-// partition in SMEM); [B] one thread per partition reserves page space (CTA-
-// private pages, one global atomic per new page) and thread 0 grabs the tile
-// after next; [C] every thread writes its spilled / deferred records straight
-// from registers.  Two barriers per tile.
-template <int KW, int NWT, int R, int BLK = 512, int MINB = 2>
-__global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int B = BLK, tid = threadIdx.x;
-  const int T = R * BLK;
-  const bool spills = (a.mode != MODE_FILL);
-  const int P = spills ? a.ss.nparts : 1;
-  const int S = spills ? a.ss.per_page : 1;
-
-  uint32_t* hist = (uint32_t*)smem;       // P: records of the tile per partition (ranks)
-  int32_t* pcur = (int32_t*)(hist + P);   // P: CTA's current page per partition
-  int32_t* pfill = pcur + P;              // P: records in that page
-  int32_t* bpg = pfill + P;               // P: tile write base: page
-  int32_t* bslot = bpg + P;               // P: tile write base: slot (room = S - bslot)
-  int32_t* pnew = bslot + P;              // P: first page allocated for this tile
-  __shared__ uint32_t s_fd[MAX_STATES];
-  __shared__ unsigned long long s_grab, s_defer_base;
-  __shared__ uint32_t s_ndefer;
-  __shared__ unsigned long long s_cnt[ST_NSTATS];
-
-  const int ns = a.sp.ns;
-  if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
-  for (int p = tid; p < P; p += B) {
-    hist[p] = 0;
-    pcur[p] = -1;
-    pfill[p] = S;
-  }
-  if (tid < ST_NSTATS) s_cnt[tid] = 0;
-  const int64_t n = a.col.n;
-  const int64_t col_start =
-      a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
-  const int64_t col_tiles = (n - col_start + T - 1) / T;
-  const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
-  const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
-  const bool use_table = (a.mode == MODE_FILL || a.mode == MODE_PROBE || a.mode == MODE_ROUTE);
-  const bool insert = (a.mode != MODE_PROBE);
-  const int nvc = a.col.nv, nvl = a.lin.nv;
-
-  auto grab = [&]() -> unsigned long long {
-    if (a.mode == MODE_FILL && *(volatile int*)&a.t.hdr->frozen) return ~0ull;
-    return atomicAdd(a.tile_counter, 1ull);
-  };
-  auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
-    const bool fc = (int64_t)tile < col_tiles;
-    const int64_t base = fc ? col_start + (int64_t)tile * T : ((int64_t)tile - col_tiles) * T;
-    const int64_t end = fc ? n : n_lin;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      int64_t i = base + (int64_t)r * B + tid;
-      live[r] = (tile < total) && (i < end);
-      if (live[r]) {
-        if (fc) load_rec<KW, NWT>(a.col, a.col_dense != 0, nvc, i, k[r], v[r]);
-        else load_rec<KW, NWT>(a.lin, true, nvl, i, k[r], v[r]);
-      }
-    }
-  };
-
-  if (tid == 0) {
-    s_ndefer = 0;
-    s_grab = grab();
-  }
-  __syncthreads();
-  unsigned long long cur = s_grab;
-  __syncthreads();
-  if (tid == 0) s_grab = (cur < total) ? grab() : ~0ull;
-  uint64_t kc[R][KW], vc[R][NWT];
-  bool lc[R];
-  load_tile(cur, kc, vc, lc);
-  __syncthreads();
-  unsigned long long nxt = s_grab;
-
-  uint32_t c_hit = 0, c_ins = 0, c_rec = 0, c_sp = 0, c_def = 0;
-  while (cur < total) {
-    const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
-    // ---- [A] first-bucket loads for the current records
-    uint64_t bk[R];
-    uint64_t bw[R][4];
-    int part[R];
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      part[r] = -2;
-      if (!lc[r]) continue;
-      part[r] = -1;
-      if (a.mode == MODE_ROUTE) {
-        uint32_t u = (uint32_t)(hash_key<KW>(kc[r], a.part_seed) >> 32);
-        if (u >= a.cut0) {
-          int pp = 1 + (int)(((uint64_t)(u - a.cut0) * (uint64_t)(P - 1)) / (0x100000000ull - a.cut0));
-          part[r] = pp > P - 1 ? P - 1 : pp;
-        }
-      } else if (a.mode == MODE_GRACE) {
-        part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
-      }
-      if (use_table && part[r] == -1 && !is_sentinel<KW>(kc[r])) {
-        bk[r] = hash_key<KW>(kc[r], a.t.seed) & a.t.bmask;
-        ld_bucket(a.t.keys, bk[r], bw[r]);
-      }
-    }
-    // ---- prefetch the next tile while the buckets are in flight
-    uint64_t kn[R][KW], vn[R][NWT];
-    bool ln[R];
-    load_tile(nxt, kn, vn, ln);
-    // ---- resolve
-    uint32_t tag[R];  // spill: (p << 16 | rank) + 1; defer: 0x80000000 | rank; 0 done
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      tag[r] = 0;
-      if (part[r] == -2) continue;
-      c_rec++;
-      if (part[r] == -1) {
-        int res;
-        int64_t s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, res)
-                                            : gt_resolve<KW>(a.t, kc[r], bk[r], bw[r], insert, res);
-        if (res == R_HIT || res == R_INSERTED) {
-          for (int j = 0; j < ns; j++) {
-            uint32_t fd = s_fd[j];
-            gupdate(a.t.states + (uint64_t)j * a.t.stride + s, fd & 3, (fd >> 2) & 3,
-                    contrib_fd<NWT>(fd, kind, j, vc[r]));
-          }
-          c_hit += (res == R_HIT);
-          c_ins += (res == R_INSERTED);
-          continue;
-        }
-        if (res == R_MISS) {
-          part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
-        } else if (a.mode == MODE_FILL) {
-          tag[r] = 0x80000000u | atomicAdd(&s_ndefer, 1u);
-          c_def++;
-          continue;
-        } else {
-          part[r] = 0;  // ROUTE overflow: partition 0 spills raw (hybrid.py:431-451)
-        }
-      }
-      tag[r] = (((uint32_t)part[r] << 16) | atomicAdd(&hist[part[r]], 1u)) + 1u;
-      c_sp++;
-    }
-    __syncthreads();
-    // ---- [B] reserve page space per partition; grab the tile after next
-    if (spills) {
-      for (int p = tid; p < P; p += B) {
-        int cnt = (int)hist[p];
-        if (!cnt) continue;
-        hist[p] = 0;
-        int room = S - pfill[p];
-        bpg[p] = pcur[p];
-        bslot[p] = pfill[p];
-        if (cnt > room) {
-          int need = (cnt - room + S - 1) / S;
-          uint32_t first = atomicAdd(a.pool.next_page, (uint32_t)need);
-          if (first + need > a.pool.capacity) {
-            atomicExch(a.pool.overflow, 1u);
-            pnew[p] = -1;
-            pcur[p] = -1;
-            pfill[p] = S;
-          } else {
-            for (int q = 0; q < need; q++) {
-              a.pool.page_part[first + q] = p;
-              a.pool.page_set[first + q] = a.ss.id;
-              a.pool.page_fill[first + q] = S;
-            }
-            pnew[p] = (int32_t)first;
-            pcur[p] = (int32_t)(first + need - 1);
-            pfill[p] = (cnt - room) - (need - 1) * S;
-          }
-          if (bpg[p] >= 0) a.pool.page_fill[bpg[p]] = S;
-        } else {
-          pfill[p] += cnt;
-        }
-      }
-    }
-    if (tid == 0) {
-      if (s_ndefer) {
-        s_defer_base = atomicAdd(a.defer_count, (unsigned long long)s_ndefer);
-        s_ndefer = 0;
-      }
-      s_grab = (nxt < total) ? grab() : ~0ull;
-    }
-    __syncthreads();
-    // ---- [C] write spilled / deferred records from registers
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      uint32_t tg = tag[r];
-      if (!tg) continue;
-      if (tg & 0x80000000u) {
-        int64_t d = (int64_t)s_defer_base + (tg & 0x7FFFFFFFu);
-#pragma unroll
-        for (int w = 0; w < KW; w++) a.defer[w * a.defer_stride + d] = kc[r][w];
-#pragma unroll
-        for (int w = 0; w < NWT; w++)
-          if (w < nvc) a.defer[(KW + w) * a.defer_stride + d] = vc[r][w];
-        continue;
-      }
-      tg -= 1u;
-      int p = (int)(tg >> 16);
-      int rank = (int)(tg & 0xFFFFu);
-      int room = S - bslot[p];
-      int32_t pg;
-      int slot;
-      if (rank < room) {
-        pg = bpg[p];
-        slot = bslot[p] + rank;
-      } else {
-        if (pnew[p] < 0) continue;
-        int j = rank - room;
-        pg = pnew[p] + j / S;
-        slot = j % S;
-      }
-      uint64_t* dst = (uint64_t*)page_ptr(a.pool, (uint32_t)pg) + slot;
-#pragma unroll
-      for (int w = 0; w < KW; w++) dst[(size_t)w * S] = kc[r][w];
-      const int nw = a.ss.rw - KW;
-#pragma unroll
-      for (int w = 0; w < NWT; w++)
-        if (w < nw) dst[(size_t)(KW + w) * S] = vc[r][w];
-    }
-    // ---- rotate
-    cur = nxt;
-    nxt = s_grab;
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      lc[r] = ln[r];
-#pragma unroll
-      for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
-#pragma unroll
-      for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
-    }
-  }
-  // seal partially filled pages
-  if (spills)
-    for (int p = tid; p < P; p += B)
-      if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
-  // counters: warp reduce then one shared atomic per warp
-  uint32_t cs[5] = {c_sp, c_hit, c_ins, c_def, c_rec};
-  const int ids[5] = {ST_SPILLED, ST_HITS, ST_INSERTS, ST_DEFERRED, ST_RECORDS};
-#pragma unroll
-  for (int q = 0; q < 5; q++) {
-    uint32_t x = cs[q];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if ((tid & 31) == 0 && x) atomicAdd(&s_cnt[ids[q]], (unsigned long long)x);
-  }
-  __syncthreads();
-  if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
-}
-
 // ---------------------------------------------------------------------------
 // output buffers + table flush
 // ---------------------------------------------------------------------------
@@ -641,24 +371,6 @@ __global__ void k_flush_table(GTable t, DevSpec sp, OutBuf o) {
 // k_child: per-partition shared-memory aggregation (one recursion level)
 // ---------------------------------------------------------------------------
 
-struct ChildArgs {
-  DevSpec sp;
-  PagePool pool;
-  SpillSet sets[2];         // pages of item i: sets[0] in [off[2i], off[2i+1]), sets[1] in [off[2i+1], off[2i+2])
-  const int32_t* plist;     // page ids, grouped by item (set 0 pages first)
-  const int64_t* item_off;  // [2 * nitems + 1]
-  int32_t nitems;
-  int32_t slots_log2;       // SMEM table slots
-  int32_t cap;              // group capacity (<= budget)
-  uint64_t seed;            // slot hash seed of this level
-  OutBuf out;
-  uint64_t* ovf;            // overflow list: native partial records, SoA KW + ns words
-  int64_t ovf_stride;
-  unsigned long long* ovf_count;
-  unsigned long long* item_counter;
-  unsigned long long* stats;
-};
-
 template <int KW>
 __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap, const uint64_t (&k)[KW], uint64_t seed,
                                              bool insert, int* s_groups, int* s_frozen, int* s_esc, int& res) {
@@ -714,187 +426,6 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
     }
     s = (s + 1) & mask;
   }
-}
-
-// One CTA aggregates one spilled partition (a child operator at level + 1,
-// hybrid.py:244-277) in a shared-memory table.  Threads map onto (page, slot)
-// across B / per_page pages per row and R rows per round, and the next round's
-// records are prefetched into registers while the current round aggregates.
-// A refused insert (table full) freezes the table; after the round's barrier
-// the key set is immutable, so refused records re-probe and either aggregate
-// or go to the overflow list (the next recursion level).
-template <int KW, int NWT, int R>
-__global__ void __launch_bounds__(512) k_child(ChildArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int B = blockDim.x, tid = threadIdx.x;
-  const int nslots = 1 << a.slots_log2;
-  const int stride = nslots + 1;
-  const int ns = a.sp.ns;
-  uint64_t* skeys = (uint64_t*)smem;                       // stride * KW
-  uint64_t* sst = skeys + (size_t)stride * KW;             // ns * stride
-  __shared__ int s_groups, s_frozen, s_esc;
-  __shared__ unsigned long long s_item;
-  __shared__ unsigned long long s_cnt[ST_NSTATS];
-  __shared__ uint32_t s_fd[MAX_STATES];
-  if (tid < ST_NSTATS) s_cnt[tid] = 0;
-  if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
-  uint32_t nrec = 0, novf = 0;
-
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(a.item_counter, 1ull);
-    for (int i = tid; i < stride; i += B) {
-#pragma unroll
-      for (int w = 0; w < KW; w++) skeys[(size_t)i * KW + w] = EMPTY;
-      for (int j = 0; j < ns; j++) sst[(size_t)j * stride + i] = state_identity(a.sp.op[j], a.sp.ty[j]);
-    }
-    if (tid == 0) {
-      s_groups = 0;
-      s_frozen = 0;
-      s_esc = 0;
-    }
-    __syncthreads();
-    unsigned long long item = s_item;
-    if (item >= (unsigned long long)a.nitems) break;
-    for (int sidx = 0; sidx < 2; sidx++) {
-      const int64_t qa = a.item_off[2 * item + sidx], qb = a.item_off[2 * item + sidx + 1];
-      if (qa >= qb) continue;
-      const SpillSet ss = a.sets[sidx];
-      const int kind = ss.kind;
-      const int nw = ss.rw - KW;
-      const int S = ss.per_page;
-      const int ppr = B / S;                   // pages per row
-      const int prow = tid / S, slot = tid % S;
-      const int64_t per_round = (int64_t)R * ppr;
-      auto load_round = [&](int64_t q0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          int64_t q = q0 + (int64_t)r * ppr + prow;
-          live[r] = false;
-          if (prow < ppr && q < qb) {
-            uint32_t pg = (uint32_t)a.plist[q];
-            if (slot < a.pool.page_fill[pg]) {
-              live[r] = true;
-              soa_load<KW, NWT>((const uint64_t*)page_ptr(a.pool, pg), S, slot, nw, k[r], v[r]);
-            }
-          }
-        }
-      };
-      uint64_t kc[R][KW], vc[R][NWT];
-      bool lc[R];
-      load_round(qa, kc, vc, lc);
-      for (int64_t q0 = qa; q0 < qb; q0 += per_round) {
-        uint64_t kn[R][KW], vn[R][NWT];
-        bool ln[R];
-        load_round(q0 + per_round, kn, vn, ln);
-        bool refused[R];
-        bool any_ref = false;
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          refused[r] = false;
-          if (!lc[r]) continue;
-          nrec++;
-          int res;
-          int s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, &s_groups, &s_frozen, &s_esc, res);
-          if (res == R_REFUSED) {
-            refused[r] = true;
-            any_ref = true;
-            continue;
-          }
-          for (int j = 0; j < ns; j++) {
-            uint32_t fd = s_fd[j];
-            supdate(sst + (size_t)j * stride + s, fd & 3, (fd >> 2) & 3, contrib_fd<NWT>(fd, kind, j, vc[r]));
-          }
-        }
-        // the table's key set is immutable once frozen and this barrier has passed
-        if (__syncthreads_or(any_ref)) {
-#pragma unroll
-          for (int r = 0; r < R; r++) {
-            if (!refused[r]) continue;
-            int res;
-            int s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, false, &s_groups, &s_frozen, &s_esc, res);
-            if (res == R_HIT) {
-              for (int j = 0; j < ns; j++) {
-                uint32_t fd = s_fd[j];
-                supdate(sst + (size_t)j * stride + s, fd & 3, (fd >> 2) & 3, contrib_fd<NWT>(fd, kind, j, vc[r]));
-              }
-            } else {
-              unsigned long long d = atomicAdd(a.ovf_count, 1ull);
-              novf++;
-#pragma unroll
-              for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
-              for (int j = 0; j < ns; j++) a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
-            }
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          lc[r] = ln[r];
-#pragma unroll
-          for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
-#pragma unroll
-          for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
-        }
-      }
-    }
-    __syncthreads();
-    // flush the item's groups: block compaction then one global reservation
-    {
-      __shared__ unsigned long long s_base;
-      __shared__ uint32_t s_wsum[33];
-      int per = (stride + B - 1) / B;
-      int lo = tid * per, hi = min(stride, lo + per);
-      uint32_t mine = 0;
-      for (int s = lo; s < hi; s++) {
-        uint64_t kk[KW];
-#pragma unroll
-        for (int w = 0; w < KW; w++) kk[w] = skeys[(size_t)s * KW + w];
-        mine += (s == nslots) ? (s_esc != 0) : !is_sentinel<KW>(kk);
-      }
-      int lane = tid & 31, wid = tid >> 5;
-      uint32_t x = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (lane == 31) s_wsum[wid] = x;
-      __syncthreads();
-      if (tid == 0) {
-        uint32_t acc = 0;
-        int nwp = (B + 31) >> 5;
-        for (int w = 0; w < nwp; w++) {
-          uint32_t t2 = s_wsum[w];
-          s_wsum[w] = acc;
-          acc += t2;
-        }
-        s_base = acc ? atomicAdd(a.out.count, (unsigned long long)acc) : 0ull;
-      }
-      __syncthreads();
-      int64_t idx = (int64_t)s_base + s_wsum[wid] + (x - mine);
-      for (int s = lo; s < hi; s++) {
-        uint64_t kk[KW];
-#pragma unroll
-        for (int w = 0; w < KW; w++) kk[w] = skeys[(size_t)s * KW + w];
-        bool occ = (s == nslots) ? (s_esc != 0) : !is_sentinel<KW>(kk);
-        if (!occ) continue;
-        uint64_t st[MAX_STATES];
-        for (int j = 0; j < ns; j++) st[j] = sst[(size_t)j * stride + s];
-        emit_group<KW>(a.sp, a.out, idx++, kk, st);
-      }
-    }
-    __syncthreads();
-  }
-  uint32_t cs[2] = {nrec, novf};
-  const int ids[2] = {ST_RECORDS, ST_OVERFLOW};
-#pragma unroll
-  for (int q = 0; q < 2; q++) {
-    uint32_t x = cs[q];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if ((tid & 31) == 0 && x) atomicAdd(&s_cnt[ids[q]], (unsigned long long)x);
-  }
-  __syncthreads();
-  if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
 }
 
 // ---------------------------------------------------------------------------

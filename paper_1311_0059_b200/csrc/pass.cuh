@@ -1,0 +1,621 @@
+// pass.cuh — the two record-streaming kernels of the hot path (sm_100a).
+//
+//   k_pass   level-0 pass over a batch against the L2-resident table
+//            (_kernels.py k_table_insert :353-392 / k_pp_probe :917-962 /
+//            k_hh_push :865-914), spilling misses to per-partition HBM pages
+//   k_child  one recursion level: each CTA aggregates one spilled partition
+//            in a shared-memory table (hybrid.py:244-277 _drain_runs child)
+//
+// Both are templated on a field program PG (device.cuh): PS<...> for the
+// benchmark specs (straight-line updates), PD for any other spec.
+#pragma once
+#include "kernels.cuh"
+
+namespace aggb {
+
+struct PassArgs {
+  DevSpec sp;
+  int32_t mode;
+  GTable t;
+  // source 1: columnar batch rows [start, n), start = min(n, *start_tiles * start_T)
+  ColSrc col;
+  int32_t col_dense;                      // all key/value columns 8-byte, stride 8
+  const unsigned long long* start_tiles;  // nullable
+  int64_t start_T;
+  // source 2: SoA list (deferred / overflow records) described as dense columns
+  ColSrc lin;                             // lin.nv = payload words of the list
+  const unsigned long long* lin_count;    // nullable -> no list
+  int32_t lin_kind;                       // 0 raw payload, 1 native partial
+  // spill target
+  PagePool pool;
+  SpillSet ss;
+  int32_t group;                          // records per whole-sector group (4 / gcd(rw, 4))
+  // ROUTE (original_hh): u32 part hash < cut0 -> partition 0 (table)
+  uint32_t cut0;
+  uint64_t part_seed;
+  // PROBE: bloom filter of the frozen resident keys (copied into SMEM)
+  Bloom bloom;
+  // FILL deferral target (raw records, SoA, KW + nv words)
+  uint64_t* defer;
+  int64_t defer_stride;
+  unsigned long long* defer_count;
+  unsigned long long* tile_counter;
+  unsigned long long* stats;
+};
+
+template <int KW, int NWT>
+__device__ __forceinline__ void load_rec(const ColSrc& c, bool dense, int nv, int64_t i, uint64_t (&k)[KW],
+                                         uint64_t (&v)[NWT]) {
+  if (dense) {
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = (uint64_t)__ldcs((const long long*)c.key[w] + i);
+#pragma unroll
+    for (int w = 0; w < NWT; w++) v[w] = (w < nv) ? (uint64_t)__ldcs((const long long*)c.val[w] + i) : 0ull;
+  } else {
+    col_key<KW>(c, i, k);
+#pragma unroll
+    for (int w = 0; w < NWT; w++) {
+      if (w < nv) {
+        const uint8_t* p = c.val[w] + i * c.vstride[w];
+        v[w] = (c.vty[w] == TY_I32) ? (uint64_t)(long long)__ldcs((const int*)p) : (uint64_t)__ldcs((const long long*)p);
+      } else {
+        v[w] = 0ull;
+      }
+    }
+  }
+}
+
+// write one record (key words + nw payload words) at slot `slot` of an AoS page
+template <int KW, int NWT>
+__device__ __forceinline__ void put_rec(uint64_t* dst, const uint64_t (&k)[KW], const uint64_t (&v)[NWT], int nw) {
+#pragma unroll
+  for (int w = 0; w < KW; w++) dst[w] = k[w];
+#pragma unroll
+  for (int w = 0; w < NWT; w++)
+    if (w < nw) dst[KW + w] = v[w];
+}
+
+// ---------------------------------------------------------------------------
+// k_pass
+//
+// Persistent, tile-scheduled.  Per tile of T = R * BLK records:
+//  [A] issue the first-bucket loads of the current records, prefetch the next
+//      tile's records into registers, then resolve: hits aggregate with L2
+//      atomics (RED), misses get a rank in their partition (SMEM atomic);
+//  [B] one thread per touched partition reserves page space in the CTA's own
+//      page for that partition (one global atomic per new page) for the
+//      records that complete whole 32-byte sectors, and copies the partition's
+//      sector residual (< group records, kept in SMEM) in front of them;
+//  [C] every thread writes its records from registers: into the page when
+//      they complete a sector group, otherwise into the SMEM residual.
+// Records therefore reach L2 as complete sectors within one tile, so L2
+// never evicts a half-written sector (which ECC DRAM would read-modify-write).
+// ---------------------------------------------------------------------------
+
+template <int KW, int NWT, int R, int BLK, int MINB, class PG>
+__global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int B = BLK, tid = threadIdx.x;
+  const int T = R * BLK;
+  const bool spills = (a.mode != MODE_FILL);
+  const int P = spills ? a.ss.nparts : 1;
+  const int S = spills ? a.ss.per_page : 1;
+  const int G = spills ? a.group : 1;
+  const int rw = spills ? a.ss.rw : 1;
+  const int nw = rw - KW;
+
+  const bool use_bloom = (a.mode == MODE_PROBE) && a.bloom.words != nullptr;
+  const int nbw = use_bloom ? (int)a.bloom.mask + 1 : 0;
+  uint64_t* sbloom = (uint64_t*)smem;                        // nbw words
+  uint64_t* resid = sbloom + nbw;                            // P * (G - 1) * rw words
+  uint32_t* hist = (uint32_t*)(resid + (size_t)P * (G - 1) * rw);
+  int32_t* pcur = (int32_t*)(hist + P);
+  int32_t* pfill = pcur + P;
+  int32_t* bpg = pfill + P;
+  int32_t* bslot = bpg + P;
+  int32_t* pnew = bslot + P;
+  uint32_t* rcnt = (uint32_t*)(pnew + P);
+  uint32_t* rprev = rcnt + P;
+  uint32_t* emitn = rprev + P;
+  __shared__ uint32_t s_fd[MAX_STATES];
+  __shared__ unsigned long long s_grab, s_defer_base;
+  __shared__ uint32_t s_ndefer;
+  __shared__ unsigned long long s_cnt[ST_NSTATS];
+
+  const int ns = a.sp.ns;
+  if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
+  for (int p = tid; p < P; p += B) {
+    hist[p] = 0;
+    pcur[p] = -1;
+    pfill[p] = S;
+    rcnt[p] = 0;
+  }
+  if (tid < ST_NSTATS) s_cnt[tid] = 0;
+  for (int i = tid; i < nbw; i += B) sbloom[i] = __ldcg((const unsigned long long*)a.bloom.words + i);
+  const int64_t n = a.col.n;
+  const int64_t col_start =
+      a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
+  const int64_t col_tiles = (n - col_start + T - 1) / T;
+  const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
+  const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
+  const bool use_table = (a.mode == MODE_FILL || a.mode == MODE_PROBE || a.mode == MODE_ROUTE);
+  const bool insert = (a.mode != MODE_PROBE);
+  const int nvc = a.col.nv, nvl = a.lin.nv;
+
+  auto grab = [&]() -> unsigned long long {
+    if (a.mode == MODE_FILL && *(volatile int*)&a.t.hdr->frozen) return ~0ull;
+    return atomicAdd(a.tile_counter, 1ull);
+  };
+  auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
+    const bool fc = (int64_t)tile < col_tiles;
+    const int64_t base = fc ? col_start + (int64_t)tile * T : ((int64_t)tile - col_tiles) * T;
+    const int64_t end = fc ? n : n_lin;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      int64_t i = base + (int64_t)r * B + tid;
+      live[r] = (tile < total) && (i < end);
+      if (live[r]) {
+        if (fc) load_rec<KW, NWT>(a.col, a.col_dense != 0, nvc, i, k[r], v[r]);
+        else load_rec<KW, NWT>(a.lin, true, nvl, i, k[r], v[r]);
+      }
+    }
+  };
+  // emission position -> (page, slot) for partition p in this tile
+  auto emit_at = [&](int p, int pos, int32_t& pg, int& slot) -> bool {
+    int room = S - bslot[p];
+    if (pos < room) {
+      pg = bpg[p];
+      slot = bslot[p] + pos;
+      return pg >= 0;
+    }
+    if (pnew[p] < 0) return false;
+    int j = pos - room;
+    pg = pnew[p] + j / S;
+    slot = j % S;
+    return true;
+  };
+
+  if (tid == 0) {
+    s_ndefer = 0;
+    s_grab = grab();
+  }
+  __syncthreads();
+  unsigned long long cur = s_grab;
+  __syncthreads();
+  if (tid == 0) s_grab = (cur < total) ? grab() : ~0ull;
+  uint64_t kc[R][KW], vc[R][NWT];
+  bool lc[R];
+  load_tile(cur, kc, vc, lc);
+  __syncthreads();
+  unsigned long long nxt = s_grab;
+
+  uint32_t c_hit = 0, c_ins = 0, c_rec = 0, c_sp = 0, c_def = 0;
+  while (cur < total) {
+    const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
+    // ---- [A] first-bucket loads for the current records
+    uint64_t bk[R];
+    uint64_t bw[R][4];
+    int part[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      part[r] = -2;
+      if (!lc[r]) continue;
+      part[r] = -1;
+      if (a.mode == MODE_ROUTE) {
+        uint32_t u = (uint32_t)(hash_key<KW>(kc[r], a.part_seed) >> 32);
+        if (u >= a.cut0) {
+          int pp = 1 + (int)(((uint64_t)(u - a.cut0) * (uint64_t)(P - 1)) / (0x100000000ull - a.cut0));
+          part[r] = pp > P - 1 ? P - 1 : pp;
+        }
+      } else if (a.mode == MODE_GRACE) {
+        part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+      }
+      if (use_table && part[r] == -1 && !is_sentinel<KW>(kc[r])) {
+        if (use_bloom) {
+          uint64_t hb = hash_key<KW>(kc[r], a.bloom.seed);
+          uint64_t bits = bloom_bits(hb);
+          if ((sbloom[hb & a.bloom.mask] & bits) != bits) {  // definitely not resident
+            part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+            continue;
+          }
+        }
+        bk[r] = hash_key<KW>(kc[r], a.t.seed) & a.t.bmask;
+        ld_bucket(a.t.keys, bk[r], bw[r]);
+      }
+    }
+    // ---- prefetch the next tile while the buckets are in flight
+    uint64_t kn[R][KW], vn[R][NWT];
+    bool ln[R];
+    load_tile(nxt, kn, vn, ln);
+    // ---- resolve
+    uint32_t tag[R];  // spill: (p << 16 | rank) + 1; defer: 0x80000000 | rank; 0 done
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      tag[r] = 0;
+      int res = R_MISS;
+      int64_t s = -1;
+      if (part[r] != -2) c_rec++;
+      if (part[r] == -1)
+        s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, res)
+                                   : gt_resolve<KW>(a.t, kc[r], bk[r], bw[r], insert, res);
+      __syncwarp();  // reconverge after the divergent probe before the updates
+      if (part[r] == -1) {
+        if (res == R_HIT || res == R_INSERTED) {
+          Upd<PG>::template g<NWT>(a.t.states, a.t.stride, (uint64_t)s, kind, s_fd, ns, vc[r]);
+          c_hit += (res == R_HIT);
+          c_ins += (res == R_INSERTED);
+          part[r] = -2;
+        } else if (res == R_MISS) {
+          part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+        } else if (a.mode == MODE_FILL) {
+          tag[r] = 0x80000000u | atomicAdd(&s_ndefer, 1u);
+          c_def++;
+          part[r] = -2;
+        } else {
+          part[r] = 0;  // ROUTE overflow: partition 0 spills raw (hybrid.py:431-451)
+        }
+      }
+      if (part[r] >= 0) {
+        tag[r] = (((uint32_t)part[r] << 16) | atomicAdd(&hist[part[r]], 1u)) + 1u;
+        c_sp++;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- [B] per touched partition: reserve whole sector groups, drain the residual
+    if (spills) {
+      for (int p = tid; p < P; p += B) {
+        int c = (int)hist[p];
+        if (!c) continue;
+        hist[p] = 0;
+        int r0 = (int)rcnt[p];
+        int t = r0 + c;
+        int e = (t / G) * G;
+        rprev[p] = (uint32_t)r0;
+        emitn[p] = (uint32_t)e;
+        rcnt[p] = (uint32_t)(t - e);
+        if (!e) continue;
+        int room = S - pfill[p];
+        bpg[p] = pcur[p];
+        bslot[p] = pfill[p];
+        pnew[p] = -1;
+        if (e > room) {
+          int need = (e - room + S - 1) / S;
+          uint32_t first = atomicAdd(a.pool.next_page, (uint32_t)need);
+          if (first + need > a.pool.capacity) {
+            atomicExch(a.pool.overflow, 1u);
+            pcur[p] = -1;
+            pfill[p] = S;
+          } else {
+            for (int q = 0; q < need; q++) {
+              a.pool.page_part[first + q] = p;
+              a.pool.page_set[first + q] = a.ss.id;
+              a.pool.page_fill[first + q] = S;
+            }
+            pnew[p] = (int32_t)first;
+            pcur[p] = (int32_t)(first + need - 1);
+            pfill[p] = (e - room) - (need - 1) * S;
+          }
+          if (bpg[p] >= 0) a.pool.page_fill[bpg[p]] = S;
+        } else {
+          pfill[p] += e;
+        }
+        // the residual records lead this tile's emission
+        for (int q = 0; q < r0; q++) {
+          int32_t pg;
+          int slot;
+          if (!emit_at(p, q, pg, slot)) continue;
+          uint64_t* dst = (uint64_t*)page_ptr(a.pool, (uint32_t)pg) + (size_t)slot * rw;
+          const uint64_t* src = resid + ((size_t)p * (G - 1) + q) * rw;
+          for (int w = 0; w < rw; w++) dst[w] = src[w];
+        }
+      }
+    }
+    if (tid == 0) {
+      if (s_ndefer) {
+        s_defer_base = atomicAdd(a.defer_count, (unsigned long long)s_ndefer);
+        s_ndefer = 0;
+      }
+      s_grab = (nxt < total) ? grab() : ~0ull;
+    }
+    __syncthreads();
+    // ---- [C] write spilled / deferred records from registers
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      uint32_t tg = tag[r];
+      if (!tg) continue;
+      if (tg & 0x80000000u) {
+        int64_t d = (int64_t)s_defer_base + (tg & 0x7FFFFFFFu);
+#pragma unroll
+        for (int w = 0; w < KW; w++) a.defer[w * a.defer_stride + d] = kc[r][w];
+#pragma unroll
+        for (int w = 0; w < NWT; w++)
+          if (w < nvc) a.defer[(KW + w) * a.defer_stride + d] = vc[r][w];
+        continue;
+      }
+      tg -= 1u;
+      int p = (int)(tg >> 16);
+      int pos = (int)rprev[p] + (int)(tg & 0xFFFFu);
+      int e = (int)emitn[p];
+      if (pos < e) {
+        int32_t pg;
+        int slot;
+        if (emit_at(p, pos, pg, slot))
+          put_rec<KW, NWT>((uint64_t*)page_ptr(a.pool, (uint32_t)pg) + (size_t)slot * rw, kc[r], vc[r], nw);
+      } else {
+        put_rec<KW, NWT>(resid + ((size_t)p * (G - 1) + (pos - e)) * rw, kc[r], vc[r], nw);
+      }
+    }
+    // ---- rotate
+    cur = nxt;
+    nxt = s_grab;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      lc[r] = ln[r];
+#pragma unroll
+      for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
+#pragma unroll
+      for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
+    }
+  }
+  __syncthreads();
+  // drain the residuals (partial sectors, once per partition) and seal the pages
+  if (spills) {
+    for (int p = tid; p < P; p += B) {
+      int r0 = (int)rcnt[p];
+      if (r0) {
+        if (S - pfill[p] < r0) {
+          uint32_t pg = atomicAdd(a.pool.next_page, 1u);
+          if (pg >= a.pool.capacity) {
+            atomicExch(a.pool.overflow, 1u);
+            continue;
+          }
+          a.pool.page_part[pg] = p;
+          a.pool.page_set[pg] = a.ss.id;
+          if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
+          pcur[p] = (int32_t)pg;
+          pfill[p] = 0;
+        }
+        uint64_t* dst = (uint64_t*)page_ptr(a.pool, (uint32_t)pcur[p]) + (size_t)pfill[p] * rw;
+        const uint64_t* src = resid + (size_t)p * (G - 1) * rw;
+        for (int w = 0; w < r0 * rw; w++) dst[w] = src[w];
+        pfill[p] += r0;
+      }
+      if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
+    }
+  }
+  // counters: warp reduce then one shared atomic per warp
+  uint32_t cs[5] = {c_sp, c_hit, c_ins, c_def, c_rec};
+  const int ids[5] = {ST_SPILLED, ST_HITS, ST_INSERTS, ST_DEFERRED, ST_RECORDS};
+#pragma unroll
+  for (int q = 0; q < 5; q++) {
+    uint32_t x = cs[q];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((tid & 31) == 0 && x) atomicAdd(&s_cnt[ids[q]], (unsigned long long)x);
+  }
+  __syncthreads();
+  if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
+}
+
+// ---------------------------------------------------------------------------
+// k_child
+// ---------------------------------------------------------------------------
+
+struct ChildArgs {
+  DevSpec sp;
+  PagePool pool;
+  SpillSet sets[2];         // pages of item i: sets[0] in [off[2i], off[2i+1]), sets[1] in [off[2i+1], off[2i+2])
+  const int32_t* plist;     // page ids, grouped by item (set 0 pages first)
+  const int64_t* item_off;  // [2 * nitems + 1]
+  int32_t nitems;
+  int32_t slots_log2;       // SMEM table slots
+  int32_t cap;              // group capacity (<= budget)
+  uint64_t seed;            // slot hash seed of this level
+  OutBuf out;
+  uint64_t* ovf;            // overflow list: native partial records, SoA KW + ns words
+  int64_t ovf_stride;
+  unsigned long long* ovf_count;
+  uint64_t* pend;           // CTA-private pending lists (AoS, KW + ns words)
+  int64_t pend_cap;         // records per CTA
+  unsigned long long* item_counter;
+  unsigned long long* stats;
+};
+
+// One CTA aggregates one spilled partition (a child operator at level + 1,
+// hybrid.py:244-277) in a shared-memory table.  Threads map onto (page, slot)
+// across B / per_page pages per row and R rows per round; the next round's
+// records are prefetched into registers while the current one aggregates.
+// There is no barrier per round: an insert refused because the table is full
+// (the child's budget) parks the record in the CTA's pending list; after the
+// item's last barrier the key set is final, so pending records re-probe and
+// either aggregate or go to the overflow list (the next recursion level).
+template <int KW, int NWT, int R, class PG>
+__global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int B = blockDim.x, tid = threadIdx.x;
+  const int nslots = 1 << a.slots_log2;
+  const int stride = nslots + 1;
+  const int ns = a.sp.ns;
+  const int pw = KW + ns;  // pending / overflow record words
+  uint64_t* skeys = (uint64_t*)smem;                       // stride * KW
+  uint64_t* sst = skeys + (size_t)stride * KW;             // ns * stride
+  __shared__ int s_groups, s_frozen, s_esc;
+  __shared__ unsigned long long s_item;
+  __shared__ unsigned long long s_cnt[ST_NSTATS];
+  __shared__ uint32_t s_fd[MAX_STATES];
+  __shared__ uint32_t s_npend;
+  if (tid < ST_NSTATS) s_cnt[tid] = 0;
+  if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
+  uint64_t* pend = a.pend + (size_t)blockIdx.x * a.pend_cap * pw;
+  uint32_t nrec = 0, novf = 0;
+
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.item_counter, 1ull);
+    for (int i = tid; i < stride; i += B) {
+#pragma unroll
+      for (int w = 0; w < KW; w++) skeys[(size_t)i * KW + w] = EMPTY;
+      for (int j = 0; j < ns; j++) sst[(size_t)j * stride + i] = state_identity(a.sp.op[j], a.sp.ty[j]);
+    }
+    if (tid == 0) {
+      s_groups = 0;
+      s_frozen = 0;
+      s_esc = 0;
+      s_npend = 0;
+    }
+    __syncthreads();
+    unsigned long long item = s_item;
+    if (item >= (unsigned long long)a.nitems) break;
+    for (int sidx = 0; sidx < 2; sidx++) {
+      const int64_t qa = a.item_off[2 * item + sidx], qb = a.item_off[2 * item + sidx + 1];
+      if (qa >= qb) continue;
+      const SpillSet ss = a.sets[sidx];
+      const int kind = ss.kind;
+      const int nw = ss.rw - KW;
+      const int rw = ss.rw;
+      const int S = ss.per_page;
+      const int ppr = B / S;  // pages per row
+      const int prow = tid / S, slot = tid % S;
+      const int64_t per_round = (int64_t)R * ppr;
+      auto load_round = [&](int64_t q0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          int64_t q = q0 + (int64_t)r * ppr + prow;
+          live[r] = false;
+          if (prow < ppr && q < qb) {
+            uint32_t pg = (uint32_t)a.plist[q];
+            if (slot < a.pool.page_fill[pg]) {
+              live[r] = true;
+              const uint64_t* src = (const uint64_t*)page_ptr(a.pool, pg) + (size_t)slot * rw;
+#pragma unroll
+              for (int w = 0; w < KW; w++) k[r][w] = __ldcs((const unsigned long long*)src + w);
+#pragma unroll
+              for (int w = 0; w < NWT; w++)
+                v[r][w] = (w < nw) ? (uint64_t)__ldcs((const unsigned long long*)src + KW + w) : 0ull;
+            }
+          }
+        }
+      };
+      uint64_t kc[R][KW], vc[R][NWT];
+      bool lc[R];
+      load_round(qa, kc, vc, lc);
+      for (int64_t q0 = qa; q0 < qb; q0 += per_round) {
+        uint64_t kn[R][KW], vn[R][NWT];
+        bool ln[R];
+        load_round(q0 + per_round, kn, vn, ln);
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          int res = R_MISS, s = -1;
+          if (lc[r]) {
+            nrec++;
+            s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, &s_groups, &s_frozen, &s_esc, res);
+          }
+          __syncwarp();  // reconverge after the divergent probe before the updates
+          if (res == R_HIT || res == R_INSERTED) {
+            Upd<PG>::template sm<NWT>(sst, stride, s, kind, s_fd, ns, vc[r]);
+          } else if (res == R_REFUSED) {
+            uint32_t d = atomicAdd(&s_npend, 1u);
+            if (d < (uint32_t)a.pend_cap) {
+              uint64_t* dst = pend + (size_t)d * pw;
+#pragma unroll
+              for (int w = 0; w < KW; w++) dst[w] = kc[r][w];
+              for (int j = 0; j < ns; j++) dst[KW + j] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
+            }
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          lc[r] = ln[r];
+#pragma unroll
+          for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
+#pragma unroll
+          for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
+        }
+      }
+    }
+    __syncthreads();
+    // the table is final: resolve the pending records (native partial form)
+    const uint32_t npend = min(s_npend, (uint32_t)a.pend_cap);
+    for (uint32_t i = tid; i < npend; i += B) {
+      const uint64_t* src = pend + (size_t)i * pw;
+      uint64_t k[KW];
+#pragma unroll
+      for (int w = 0; w < KW; w++) k[w] = src[w];
+      int res;
+      int s = stable_lookup<KW>(skeys, nslots, a.cap, k, a.seed, false, &s_groups, &s_frozen, &s_esc, res);
+      if (res == R_HIT) {
+        for (int j = 0; j < ns; j++) {
+          uint32_t fd = s_fd[j];
+          supdate(sst + (size_t)j * stride + s, fd & 3, (fd >> 2) & 3, src[KW + j]);
+        }
+      } else {
+        unsigned long long d = atomicAdd(a.ovf_count, 1ull);
+        novf++;
+#pragma unroll
+        for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = k[w];
+        for (int j = 0; j < ns; j++) a.ovf[(KW + j) * a.ovf_stride + d] = src[KW + j];
+      }
+    }
+    __syncthreads();
+    // flush the item's groups: block compaction then one global reservation
+    {
+      __shared__ unsigned long long s_base;
+      __shared__ uint32_t s_wsum[33];
+      int per = (stride + B - 1) / B;
+      int lo = tid * per, hi = min(stride, lo + per);
+      uint32_t mine = 0;
+      for (int s = lo; s < hi; s++) {
+        uint64_t kk[KW];
+#pragma unroll
+        for (int w = 0; w < KW; w++) kk[w] = skeys[(size_t)s * KW + w];
+        mine += (s == nslots) ? (s_esc != 0) : !is_sentinel<KW>(kk);
+      }
+      int lane = tid & 31, wid = tid >> 5;
+      uint32_t x = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_wsum[wid] = x;
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t acc = 0;
+        int nwp = (B + 31) >> 5;
+        for (int w = 0; w < nwp; w++) {
+          uint32_t t2 = s_wsum[w];
+          s_wsum[w] = acc;
+          acc += t2;
+        }
+        s_base = acc ? atomicAdd(a.out.count, (unsigned long long)acc) : 0ull;
+      }
+      __syncthreads();
+      int64_t idx = (int64_t)s_base + s_wsum[wid] + (x - mine);
+      for (int s = lo; s < hi; s++) {
+        uint64_t kk[KW];
+#pragma unroll
+        for (int w = 0; w < KW; w++) kk[w] = skeys[(size_t)s * KW + w];
+        bool occ = (s == nslots) ? (s_esc != 0) : !is_sentinel<KW>(kk);
+        if (!occ) continue;
+        uint64_t st[MAX_STATES];
+        for (int j = 0; j < ns; j++) st[j] = sst[(size_t)j * stride + s];
+        emit_group<KW>(a.sp, a.out, idx++, kk, st);
+      }
+    }
+    __syncthreads();
+  }
+  uint32_t cs[2] = {nrec, novf};
+  const int ids[2] = {ST_RECORDS, ST_OVERFLOW};
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    uint32_t x = cs[q];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((tid & 31) == 0 && x) atomicAdd(&s_cnt[ids[q]], (unsigned long long)x);
+  }
+  __syncthreads();
+  if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
+}
+
+}  // namespace aggb
