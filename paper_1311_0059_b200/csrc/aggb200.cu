@@ -264,7 +264,11 @@ template <int KW>
 PassCfg pass_kernel(int nwt, int prog) {
   if (KW == 1 && nwt == 1) {
     if (prog == 1) return pc<1, 1, 2, 1024, ProgC1>();
-    if (prog == 2) return pc<1, 1, 2, 1024, ProgC2>();
+    if (prog == 2) {
+      const char* v = getenv("AGGB_PASS_VARIANT");
+      if (v && atoi(v) == 1) return pc<1, 1, 4, 512, ProgC2>();
+      return pc<1, 1, 2, 1024, ProgC2>();
+    }
     if (prog == 3) return pc<1, 1, 2, 1024, ProgC3>();
   }
   if (KW == 2 && nwt == 4 && prog == 5) return pc<2, 4, 1, 1024, ProgC5>();
@@ -297,14 +301,17 @@ child_fn child_kernel(int nwt, int prog) {
 }
 
 constexpr uint32_t PAGE_BYTES = 8192;
-constexpr size_t CHILD_SMEM = 100 * 1024;
+size_t child_smem_budget() {
+  const char* e = getenv("AGGB_CHILD_SMEM_KB");
+  return (size_t)(e ? atoi(e) : 100) * 1024;
+}
 
 int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
 int group_of(int rw) { return 4 / gcd_i(rw, 4); }
 // largest fan-out whose per-partition SMEM state (sector residual + page
 // bookkeeping) fits one CTA of k_pass
 int max_parts_for(int rw) {
-  size_t per = (size_t)(group_of(rw) - 1) * rw * 8 + 36;
+  size_t per = (size_t)(group_of(rw) - 1) * rw * 8 + 38;
   return (int)std::min<size_t>(4096, (200 * 1024) / per);
 }
 constexpr int MAX_PARTS = 4096;
@@ -491,7 +498,7 @@ int grid_for(const void* fn, size_t smem, int sms) {
 }
 
 size_t pass_smem(int P, int G, int rw, int bloom_words) {
-  return (size_t)bloom_words * 8 + (size_t)P * (G - 1) * rw * 8 + (size_t)P * 36 + 64;
+  return (size_t)bloom_words * 8 + (size_t)P * (G - 1) * rw * 8 + (size_t)P * 38 + 64;
 }
 
 bool dense8(const ColSrc& c, int kw) {
@@ -711,7 +718,7 @@ int plan(Handle* h) {
   // child shared-memory table geometry
   size_t per_slot = (size_t)(h->kw + ns) * 8;
   int lg = 6;
-  while (((size_t)(1 << (lg + 1)) + 1) * per_slot <= CHILD_SMEM && lg < 16) lg++;
+  while (((size_t)(1 << (lg + 1)) + 1) * per_slot <= child_smem_budget() && lg < 16) lg++;
   h->child_slots_log2 = lg;
   int64_t ccap = (int64_t)((1 << lg) * 0.7);
 
@@ -905,11 +912,9 @@ int push_hybrid(Handle* h, const ColSrc& col) {
     CU(cudaMemsetAsync(h->bloom.p, 0, (size_t)h->bloom_words * 8, h->st));
     int pe = prof_begin(h, 12);
     if (h->kw == 1)
-      k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1,
-                                                      h->bloom_seed);
+      k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1);
     else
-      k_bloom_build<2><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1,
-                                                      h->bloom_seed);
+      k_bloom_build<2><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1);
     prof_end(h, pe);
     h->launches++;
   }

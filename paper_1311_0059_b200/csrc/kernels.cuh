@@ -174,16 +174,21 @@ __device__ __forceinline__ uint64_t bloom_bits(uint64_t h) {
          (1ull << ((h >> 50) & 63));
 }
 
+// The filter is keyed off the table's own hash (k_pass derives bucket, spill
+// partition and bloom probe from one 64-bit hash): hb = h * golden, block =
+// (hb >> 8) & mask, bits = bloom_bits(hb).
+__device__ __forceinline__ uint64_t bloom_remix(uint64_t h) { return h * 0x9E3779B97F4A7C15ull; }
+
 template <int KW>
-__global__ void k_bloom_build(GTable t, uint64_t* bloom, uint32_t mask, uint64_t seed) {
+__global__ void k_bloom_build(GTable t, uint64_t* bloom, uint32_t mask) {
   uint64_t n = t.mask + 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k[KW];
 #pragma unroll
     for (int w = 0; w < KW; w++) k[w] = t.keys[i * KW + w];
     if (is_sentinel<KW>(k)) continue;
-    uint64_t h = hash_key<KW>(k, seed);
-    atomicOr((unsigned long long*)&bloom[h & mask], (unsigned long long)bloom_bits(h));
+    uint64_t hb = bloom_remix(hash_key<KW>(k, t.seed));
+    atomicOr((unsigned long long*)&bloom[(hb >> 8) & mask], (unsigned long long)bloom_bits(hb));
   }
 }
 

@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   uint32_t* rcnt = (uint32_t*)(pnew + P);
   uint32_t* rprev = rcnt + P;
   uint32_t* emitn = rprev + P;
+  uint16_t* touched = (uint16_t*)(emitn + P);                // P: partitions touched by the tile
+  __shared__ uint32_t s_ntouched[2];  // by tile parity: A fills one while the other is reset
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_grab, s_defer_base;
   __shared__ uint32_t s_ndefer;
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
 
   if (tid == 0) {
     s_ndefer = 0;
+    s_ntouched[0] = s_ntouched[1] = 0;
     s_grab = grab();
   }
   __syncthreads();
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   unsigned long long nxt = s_grab;
 
   uint32_t c_hit = 0, c_ins = 0, c_rec = 0, c_sp = 0, c_def = 0;
+  int par = 0;
   while (cur < total) {
     const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
     // ---- [A] first-bucket loads for the current records
@@ -211,16 +215,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
       }
       if (use_table && part[r] == -1 && !is_sentinel<KW>(kc[r])) {
+        // one 64-bit hash per record at this level: bucket from the low bits,
+        // spill partition from the high bits, bloom probe from a remix
+        const uint64_t h = hash_key<KW>(kc[r], a.t.seed);
+        bk[r] = h;
         if (use_bloom) {
-          uint64_t hb = hash_key<KW>(kc[r], a.bloom.seed);
-          uint64_t bits = bloom_bits(hb);
-          if ((sbloom[hb & a.bloom.mask] & bits) != bits) {  // definitely not resident
-            part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+          const uint64_t hb = bloom_remix(h);
+          const uint64_t bits = bloom_bits(hb);
+          if ((sbloom[(hb >> 8) & a.bloom.mask] & bits) != bits) {  // definitely not resident
+            part[r] = (int)reduce32(h, (uint32_t)P);
             continue;
           }
         }
-        bk[r] = hash_key<KW>(kc[r], a.t.seed) & a.t.bmask;
-        ld_bucket(a.t.keys, bk[r], bw[r]);
+        ld_bucket(a.t.keys, h & a.t.bmask, bw[r]);
       }
     }
     // ---- prefetch the next tile while the buckets are in flight
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       if (part[r] != -2) c_rec++;
       if (part[r] == -1)
         s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, res)
-                                   : gt_resolve<KW>(a.t, kc[r], bk[r], bw[r], insert, res);
+                                   : gt_resolve<KW>(a.t, kc[r], bk[r] & a.t.bmask, bw[r], insert, res);
       __syncwarp();  // reconverge after the divergent probe before the updates
       if (part[r] == -1) {
         if (res == R_HIT || res == R_INSERTED) {
@@ -246,7 +253,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
           c_ins += (res == R_INSERTED);
           part[r] = -2;
         } else if (res == R_MISS) {
-          part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+          part[r] = is_sentinel<KW>(kc[r]) ? 0 : (int)reduce32(bk[r], (uint32_t)P);
         } else if (a.mode == MODE_FILL) {
           tag[r] = 0x80000000u | atomicAdd(&s_ndefer, 1u);
           c_def++;
@@ -256,7 +263,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         }
       }
       if (part[r] >= 0) {
-        tag[r] = (((uint32_t)part[r] << 16) | atomicAdd(&hist[part[r]], 1u)) + 1u;
+        uint32_t rank = atomicAdd(&hist[part[r]], 1u);
+        if (rank == 0) touched[atomicAdd(&s_ntouched[par], 1u)] = (uint16_t)part[r];
+        tag[r] = (((uint32_t)part[r] << 16) | rank) + 1u;
         c_sp++;
       }
       __syncwarp();
@@ -264,9 +273,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     __syncthreads();
     // ---- [B] per touched partition: reserve whole sector groups, drain the residual
     if (spills) {
-      for (int p = tid; p < P; p += B) {
+      const int nt = (int)s_ntouched[par];
+      for (int ti = tid; ti < nt; ti += B) {
+        const int p = touched[ti];
         int c = (int)hist[p];
-        if (!c) continue;
         hist[p] = 0;
         int r0 = (int)rcnt[p];
         int t = r0 + c;
@@ -317,6 +327,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         s_ndefer = 0;
       }
       s_grab = (nxt < total) ? grab() : ~0ull;
+      s_ntouched[par ^ 1] = 0;  // last read in the previous tile's phase B
     }
     __syncthreads();
     // ---- [C] write spilled / deferred records from registers
@@ -347,6 +358,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       }
     }
     // ---- rotate
+    par ^= 1;
     cur = nxt;
     nxt = s_grab;
 #pragma unroll
