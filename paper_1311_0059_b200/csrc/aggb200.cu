@@ -594,7 +594,10 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (pp.mode != MODE_FILL) {
     // upper bound of pages this pass can allocate
     int64_t recs = pp.col.n + (pp.lin_count ? (pp.lin_stride) : 0);
-    uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + 2ull * grid * P + 16;
+    // each (CTA, partition) pair that receives a record may hold one partly
+    // filled page plus one residual-flush page: at most 2 per record
+    uint64_t pairs = std::min<uint64_t>(2ull * grid * P, 2ull * (uint64_t)recs);
+    uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + pairs + 16;
     TRY(pool_ensure(h, pages));
     a.pool = pool_of(h);
   }
@@ -812,7 +815,8 @@ int begin_run(Handle* h) {
     h->part0 = {make_set(h, h->P0 + 1, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
   } else {
     h->raw0 = {make_set(h, h->P0, h->cs.nv, 0, level_seed(seed, SALT_SPILL, lv)), 0};
-    h->part0 = {make_set(h, h->P0, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
+    int pp = std::min(h->P0, max_parts_for(h->kw + h->cs.ds.ns));
+    h->part0 = {make_set(h, pp, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
   }
   h->raw0_live = h->part0_live = false;
   if (h->has_table) TRY(table_reset(h));
@@ -1245,7 +1249,11 @@ int aggb_create(int device, const aggb_config* cfg, const aggb_spec* spec, void*
   if (stream) {
     h->st = (cudaStream_t)stream;
   } else {
-    cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+    e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete h;
+      return fail(AGGB_CUDA_ERROR, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
     h->own_stream = true;
   }
   if ((s = h->scratch.ensure(64 * 8, &h->hw)) || (s = h->pool_ctr.ensure(64, &h->hw))) {
