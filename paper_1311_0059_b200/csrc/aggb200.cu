@@ -19,6 +19,7 @@
 
 #include "../../include/aggb200.h"
 #include "pass.cuh"
+#include "sort.cuh"
 
 using namespace aggb;
 
@@ -1536,8 +1537,169 @@ int aggb_l2_flush(void* stream, void* scratch, int64_t bytes) {
 }  // extern "C"
 
 namespace {
-int aggb_sort_push(Handle*, const ColSrc&) { return fail(AGGB_SPEC_ERROR, "sort_based: not built yet"); }
-int aggb_sort_finish(Handle*) { return fail(AGGB_SPEC_ERROR, "sort_based: not built yet"); }
+
+int sort_words(Handle* h) { return h->kw + h->cs.nv; }
+
+SortBuf sortbuf(Handle* h, DBuf& b, int64_t cap) {
+  SortBuf s;
+  memset(&s, 0, sizeof(s));
+  s.nw = sort_words(h);
+  for (int w = 0; w < s.nw; w++) s.w[w] = b.as<uint64_t>() + (size_t)w * cap;
+  return s;
+}
+
+// sort_based push: append the batch to the load (k_sort_load, _kernels.py:544-581)
+int aggb_sort_push(Handle* h, const ColSrc& col) {
+  int64_t need = h->sort_n + col.n;
+  int nw = sort_words(h);
+  if (need > h->sort_cap) {
+    int64_t cap = std::max<int64_t>(need + need / 4, 1 << 16);
+    DBuf nb;
+    TRY(nb.ensure((size_t)cap * nw * 8, &h->hw));
+    for (int w = 0; w < nw && h->sort_n; w++)
+      CU(cudaMemcpyAsync(nb.as<uint64_t>() + (size_t)w * cap, h->sort_keys.as<uint64_t>() + (size_t)w * h->sort_cap,
+                         (size_t)h->sort_n * 8, cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    h->sort_keys.release();
+    h->sort_keys = nb;
+    h->sort_vals.release();
+    TRY(h->sort_vals.ensure((size_t)cap * nw * 8, &h->hw));
+    h->sort_cap = cap;
+  }
+  SortBuf a = sortbuf(h, h->sort_keys, h->sort_cap);
+  int pe = prof_begin(h, 9);
+  if (h->kw == 1) k_sort_append<1, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n);
+  else k_sort_append<2, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n);
+  prof_end(h, pe);
+  h->launches++;
+  CU(cudaGetLastError());
+  h->sort_n = need;
+  return AGGB_OK;
+}
+
+int scan_u32(Handle* h, const uint32_t* in, int64_t n, unsigned long long* out, DBuf& tmp) {
+  int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  TRY(tmp.ensure((size_t)(nb + 1) * 8, &h->hw));
+  unsigned long long* bs = tmp.as<unsigned long long>();
+  k_scan_reduce<<<(unsigned)std::max<int64_t>(nb, 1), 256, 0, h->st>>>(in, n, bs);
+  k_scan_top<<<1, 1024, 0, h->st>>>(bs, nb);
+  k_scan_down<<<(unsigned)std::max<int64_t>(nb, 1), 256, 0, h->st>>>(in, n, bs, out);
+  h->launches += 3;
+  CU(cudaGetLastError());
+  return AGGB_OK;
+}
+
+template <int KW>
+int seg_reduce(Handle* h, SortBuf cur, int64_t n) {
+  int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
+  DBuf th, toff, tmp, heads, longl;
+  TRY(th.ensure((size_t)ntiles * 4, nullptr));
+  TRY(toff.ensure((size_t)(ntiles + 1) * 8, nullptr));
+  int grid = (int)std::min<int64_t>(ntiles, (int64_t)h->sms * 8);
+  int pe = prof_begin(h, 11);
+  k_head_count<KW><<<grid, SORT_BLOCK, 0, h->st>>>(cur, n, th.as<uint32_t>(), ntiles);
+  TRY(scan_u32(h, th.as<uint32_t>(), ntiles, toff.as<unsigned long long>(), tmp));
+  unsigned long long last_off = 0;
+  uint32_t last_cnt = 0;
+  CU(cudaMemcpyAsync(&last_off, toff.as<unsigned long long>() + ntiles - 1, 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(&last_cnt, th.as<uint32_t>() + ntiles - 1, 4, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  int64_t G = (int64_t)last_off + last_cnt;
+  TRY(heads.ensure((size_t)std::max<int64_t>(G, 1) * 8, nullptr));
+  TRY(longl.ensure((size_t)std::max<int64_t>(G, 1) * 8, nullptr));
+  k_head_compact<KW><<<grid, SORT_BLOCK, 0, h->st>>>(cur, n, toff.as<unsigned long long>(), ntiles,
+                                                     heads.as<int64_t>());
+  TRY(ensure_out(h, G + 16));
+  CU(cudaMemsetAsync(SC(h) + 14, 0, 8, h->st));
+  OutBuf o = outbuf(h, 0);
+  int nwt = nwt_for(std::max(1, cur.nw - KW));
+  int sg = (int)std::min<int64_t>((G + 255) / 256, (int64_t)h->sms * 16);
+  sg = std::max(sg, 1);
+  switch (nwt) {
+#define SEG_CASE(NW)                                                                                          \
+  case NW:                                                                                                    \
+    k_seg_reduce<KW, NW><<<sg, 256, 0, h->st>>>(cur, h->cs.ds, 0, n, heads.as<int64_t>(), G, o,               \
+                                                longl.as<int64_t>(), SC(h) + 14);                             \
+    k_seg_reduce_long<KW, NW><<<h->sms, SORT_BLOCK, 0, h->st>>>(cur, h->cs.ds, 0, n, heads.as<int64_t>(), G, o, \
+                                                                longl.as<int64_t>(), SC(h) + 14);             \
+    break;
+    SEG_CASE(1) SEG_CASE(2) SEG_CASE(4) SEG_CASE(8) SEG_CASE(16)
+    default: SEG_CASE(32)
+#undef SEG_CASE
+  }
+  prof_end(h, pe);
+  h->launches += 4;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(SC(h) + 13, &G, 8, cudaMemcpyHostToDevice, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  th.release();
+  toff.release();
+  tmp.release();
+  heads.release();
+  longl.release();
+  return AGGB_OK;
+}
+
+// sort_based close: radix sort + fold (sort_based.py:135-211, k_fold_sorted :601-638)
+int aggb_sort_finish(Handle* h) {
+  int64_t n = h->sort_n;
+  if (n == 0) return AGGB_OK;
+  SortBuf a = sortbuf(h, h->sort_keys, h->sort_cap);
+  SortBuf b = sortbuf(h, h->sort_vals, h->sort_cap);
+  if (h->cfg.input_sorted) {  // streamed fold with the order contract
+    int bad = 0;
+    CU(cudaMemsetAsync(SC(h) + 15, 0, 8, h->st));
+    if (h->kw == 1) k_check_sorted<1><<<h->sms * 4, 256, 0, h->st>>>(a, n, (int*)(SC(h) + 15));
+    else k_check_sorted<2><<<h->sms * 4, 256, 0, h->st>>>(a, n, (int*)(SC(h) + 15));
+    CU(cudaMemcpyAsync(&bad, SC(h) + 15, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (bad) return fail(AGGB_ORDER_ERROR, "input declared sorted but a key decreased");
+  } else {
+    DBuf hist, keyptrs;
+    TRY(hist.ensure(16 * 256 * 8, nullptr));
+    TRY(keyptrs.ensure(2 * 8, nullptr));
+    CU(cudaMemsetAsync(hist.p, 0, 16 * 256 * 8, h->st));
+    const uint64_t* kp[2] = {a.w[0], h->kw > 1 ? a.w[1] : a.w[0]};
+    CU(cudaMemcpyAsync(keyptrs.p, kp, sizeof(kp), cudaMemcpyHostToDevice, h->st));
+    int pe = prof_begin(h, 9);
+    k_digit_hist8<<<h->sms * 4, 256, 0, h->st>>>(keyptrs.as<const uint64_t*>(), h->kw, n,
+                                                 hist.as<unsigned long long>());
+    prof_end(h, pe);
+    std::vector<unsigned long long> hh(16 * 256);
+    CU(cudaMemcpyAsync(hh.data(), hist.p, 16 * 256 * 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    // LSD order: least significant word last in the key, lowest byte first
+    std::vector<std::pair<int, int>> passes;
+    for (int w = h->kw - 1; w >= 0; w--)
+      for (int by = 0; by < 8; by++) {
+        const unsigned long long* row = &hh[(size_t)(w * 8 + by) * 256];
+        int nz = 0;
+        for (int d = 0; d < 256; d++) nz += row[d] != 0;
+        if (nz > 1) passes.push_back({w, by});
+      }
+    int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
+    DBuf counts, offs, tmp;
+    TRY(counts.ensure((size_t)ntiles * 256 * 4, nullptr));
+    TRY(offs.ensure((size_t)ntiles * 256 * 8, nullptr));
+    int grid = (int)std::min<int64_t>(ntiles, (int64_t)h->sms * 8);
+    for (auto& pw : passes) {
+      int pe2 = prof_begin(h, 9);
+      k_tile_hist<<<grid, 256, 0, h->st>>>(a.w[pw.first], 8 * pw.second, n, counts.as<uint32_t>(), ntiles);
+      TRY(scan_u32(h, counts.as<uint32_t>(), ntiles * 256, offs.as<unsigned long long>(), tmp));
+      k_scatter<<<grid, SORT_BLOCK, 0, h->st>>>(a, b, pw.first, 8 * pw.second, n, offs.as<unsigned long long>(),
+                                                ntiles);
+      prof_end(h, pe2);
+      h->launches += 2;
+      CU(cudaGetLastError());
+      std::swap(a, b);
+    }
+    CU(cudaStreamSynchronize(h->st));
+    counts.release();
+    offs.release();
+    tmp.release();
+  }
+  return h->kw == 1 ? seg_reduce<1>(h, a, n) : seg_reduce<2>(h, a, n);
+}
 }  // namespace
 
 extern "C" {

@@ -1,0 +1,391 @@
+// sort.cuh — the sort path (sort_based.py:24-211): LSD radix sort of the
+// records by key words, then a segmented reduction over runs of equal keys.
+//
+//   k_digit_hist8    one read of all keys: 256-bin histograms of every byte
+//                    position (decides which digit passes are needed: a byte
+//                    that is equal in every key needs no pass)
+//   k_tile_hist      per-tile digit counts for one pass   -> counts[d][tile]
+//   k_scan_*         3-phase exclusive scan of the digit-major counts
+//   k_scatter        stable scatter of one pass (warp match_any ranking)
+//   k_heads / k_seg  segment heads -> compaction -> per-segment reduction
+//                    (thread per short segment, block per long segment)
+//
+// Records are SoA arrays of 8-byte words (KW key words, then payload words)
+// ping-ponged between two buffers.  The key order is unsigned word order,
+// which is the reference's byte order (_kernels.py:121-131).
+#pragma once
+#include "kernels.cuh"
+
+namespace aggb {
+
+constexpr int SORT_BLOCK = 256;
+constexpr int SORT_IPT = 16;                       // items per thread
+constexpr int SORT_TILE = SORT_BLOCK * SORT_IPT;   // 4096
+
+struct SortBuf {
+  uint64_t* w[MAX_STATES + 2];  // word columns (KW key words first)
+  int nw;
+};
+
+// 256-bin histograms for 8 * KW byte positions (digit index = word * 8 + byte)
+__global__ void k_digit_hist8(const uint64_t* const* keys, int kw, int64_t n, unsigned long long* hist /* [16][256] */) {
+  __shared__ unsigned int sh[16][256];
+  for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int w = 0; w < kw; w++) {
+      uint64_t k = keys[w][i];
+#pragma unroll
+      for (int b = 0; b < 8; b++) atomicAdd(&sh[w * 8 + b][(k >> (8 * b)) & 255], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kw * 8 * 256; i += blockDim.x)
+    if ((&sh[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&sh[0][0])[i]);
+}
+
+__global__ void k_tile_hist(const uint64_t* key, int shift, int64_t n, uint32_t* counts /* [256][ntiles] */,
+                            int64_t ntiles) {
+  __shared__ unsigned int sh[256];
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    int64_t base = t * SORT_TILE;
+    for (int j = threadIdx.x; j < SORT_TILE; j += blockDim.x) {
+      int64_t i = base + j;
+      if (i < n) atomicAdd(&sh[(key[i] >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) counts[(int64_t)d * ntiles + t] = sh[d];
+    __syncthreads();
+  }
+}
+
+// ---- 3-phase exclusive scan (u32 in, u64 out) ------------------------------
+
+constexpr int SCAN_CHUNK = 8192;
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long x) {
+  __shared__ unsigned long long sw[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) sw[wid] = x;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; w++) t += sw[w];
+  __syncthreads();
+  if (threadIdx.x == 0) sw[0] = t;
+  __syncthreads();
+  t = sw[0];
+  __syncthreads();
+  return t;
+}
+
+__global__ void k_scan_reduce(const uint32_t* in, int64_t n, unsigned long long* bsum) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+  unsigned long long s = 0;
+  for (int j = threadIdx.x; j < SCAN_CHUNK; j += blockDim.x)
+    if (base + j < n) s += in[base + j];
+  s = block_sum_u64(s);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = s;
+}
+
+// single block: exclusive scan of nb block sums (in place), total at [nb]
+__global__ void k_scan_top(unsigned long long* bsum, int64_t nb) {
+  __shared__ unsigned long long carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    unsigned long long x = i < nb ? bsum[i] : 0;
+    // block inclusive scan
+    __shared__ unsigned long long sw[33];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) sw[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long acc = 0;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; w++) {
+        unsigned long long t = sw[w];
+        sw[w] = acc;
+        acc += t;
+      }
+      sw[32] = acc;
+    }
+    __syncthreads();
+    unsigned long long excl = carry + sw[wid] + v - x;
+    if (i < nb) bsum[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += sw[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void k_scan_down(const uint32_t* in, int64_t n, const unsigned long long* bsum, unsigned long long* out) {
+  int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+  __shared__ unsigned long long carry;
+  __shared__ unsigned long long sw[33];
+  if (threadIdx.x == 0) carry = bsum[blockIdx.x];
+  __syncthreads();
+  for (int j0 = 0; j0 < SCAN_CHUNK; j0 += blockDim.x) {
+    int64_t i = base + j0 + threadIdx.x;
+    unsigned long long x = i < n ? in[i] : 0;
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long v = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) sw[wid] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long acc = 0;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; w++) {
+        unsigned long long t = sw[w];
+        sw[w] = acc;
+        acc += t;
+      }
+      sw[32] = acc;
+    }
+    __syncthreads();
+    if (i < n) out[i] = carry + sw[wid] + v - x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += sw[32];
+    __syncthreads();
+  }
+}
+
+// ---- stable scatter of one digit pass --------------------------------------
+// Thread t of a tile holds items t*IPT .. t*IPT+IPT-1 (consecutive), so the
+// tile order is thread-major and ranks are computed in that order: per item
+// slot j, warps rank their lanes' digits with match_any, and a running SMEM
+// counter per digit carries the order across (slot, warp) steps.
+
+__global__ void __launch_bounds__(SORT_BLOCK) k_scatter(SortBuf src, SortBuf dst, int key_word, int shift, int64_t n,
+                                                        const unsigned long long* offs /* [256][ntiles] excl */,
+                                                        int64_t ntiles) {
+  __shared__ unsigned int run[256];          // running count per digit within the tile
+  __shared__ unsigned int wcnt[SORT_BLOCK / 32][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwarps = SORT_BLOCK / 32;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) run[i] = 0;
+    __syncthreads();
+    const int64_t base = t * SORT_TILE;
+    // items of this thread: base + threadIdx.x * IPT + j; ranks in (thread, j) order require
+    // ordering by thread first, so process slot by slot but count a thread's earlier slots:
+    // instead use the layout index = base + j * SORT_BLOCK + threadIdx.x (slot-major order).
+    for (int j = 0; j < SORT_IPT; j++) {
+      const int64_t i = base + (int64_t)j * SORT_BLOCK + threadIdx.x;
+      const bool live = i < n;
+      uint64_t kw = live ? src.w[key_word][i] : 0;
+      int d = live ? (int)((kw >> shift) & 255) : 256;
+      unsigned peers = __match_any_sync(0xffffffffu, d);
+      unsigned lower = peers & ((1u << lane) - 1);
+      int rank_in_warp = __popc(lower);
+      int leader = __ffs(peers) - 1;
+      for (int q = threadIdx.x; q < nwarps * 256; q += blockDim.x) (&wcnt[0][0])[q] = 0;
+      __syncthreads();
+      if (live && lane == leader) wcnt[wid][d] = __popc(peers);
+      __syncthreads();
+      // exclusive prefix over warps per digit, plus the running count
+      for (int dd = threadIdx.x; dd < 256; dd += blockDim.x) {
+        unsigned acc = run[dd];
+        for (int w = 0; w < nwarps; w++) {
+          unsigned c = wcnt[w][dd];
+          wcnt[w][dd] = acc;
+          acc += c;
+        }
+        run[dd] = acc;
+      }
+      __syncthreads();
+      if (live) {
+        unsigned long long pos = offs[(int64_t)d * ntiles + t] + wcnt[wid][d] + rank_in_warp;
+        for (int w = 0; w < src.nw; w++) dst.w[w][pos] = (w == key_word) ? kw : src.w[w][i];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- segmented reduction ----------------------------------------------------
+
+template <int KW>
+__global__ void k_head_count(const SortBuf s, int64_t n, uint32_t* tile_heads, int64_t ntiles) {
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    unsigned c = 0;
+    for (int j = threadIdx.x; j < SORT_TILE; j += blockDim.x) {
+      int64_t i = t * SORT_TILE + j;
+      if (i >= n) continue;
+      bool head = (i == 0);
+      if (!head)
+        for (int w = 0; w < KW; w++) head = head || (s.w[w][i] != s.w[w][i - 1]);
+      c += head;
+    }
+    unsigned long long tot = block_sum_u64(c);
+    if (threadIdx.x == 0) tile_heads[t] = (uint32_t)tot;
+  }
+}
+
+template <int KW>
+__global__ void k_head_compact(const SortBuf s, int64_t n, const unsigned long long* tile_off, int64_t ntiles,
+                               int64_t* heads) {
+  __shared__ unsigned long long sbase;
+  __shared__ unsigned int wsum[SORT_BLOCK / 32 + 1];
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (threadIdx.x == 0) sbase = tile_off[t];
+    __syncthreads();
+    for (int j0 = 0; j0 < SORT_TILE; j0 += blockDim.x) {
+      int64_t i = t * SORT_TILE + j0 + threadIdx.x;
+      bool head = false;
+      if (i < n) {
+        head = (i == 0);
+        if (!head)
+          for (int w = 0; w < KW; w++) head = head || (s.w[w][i] != s.w[w][i - 1]);
+      }
+      unsigned m = __ballot_sync(0xffffffffu, head);
+      int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      if (lane == 0) wsum[wid] = __popc(m);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int w = 0; w < SORT_BLOCK / 32; w++) {
+          unsigned c = wsum[w];
+          wsum[w] = acc;
+          acc += c;
+        }
+        wsum[SORT_BLOCK / 32] = acc;
+      }
+      __syncthreads();
+      if (head) heads[sbase + wsum[wid] + __popc(m & ((1u << lane) - 1))] = i;
+      __syncthreads();
+      if (threadIdx.x == 0) sbase += wsum[SORT_BLOCK / 32];
+      __syncthreads();
+    }
+  }
+}
+
+constexpr int64_t SEG_SHORT = 256;
+
+// contribution of sorted record i (payload words from the SoA buffer)
+template <int KW, int NWT>
+__device__ __forceinline__ void seg_load(const SortBuf& s, int64_t i, int nw, uint64_t (&v)[NWT]) {
+#pragma unroll
+  for (int w = 0; w < NWT; w++) v[w] = (w < nw) ? s.w[KW + w][i] : 0ull;
+}
+
+template <int KW, int NWT>
+__global__ void k_seg_reduce(const SortBuf s, DevSpec sp, int kind, int64_t n, const int64_t* heads, int64_t G,
+                             OutBuf o, int64_t* long_list, unsigned long long* nlong) {
+  const int ns = sp.ns;
+  __shared__ uint32_t s_fd[MAX_STATES];
+  if (threadIdx.x < ns) s_fd[threadIdx.x] = field_desc(sp, threadIdx.x);
+  __syncthreads();
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = heads[g], b = (g + 1 < G) ? heads[g + 1] : n;
+    if (b - a > SEG_SHORT) {
+      long_list[atomicAdd(nlong, 1ull)] = g;
+      continue;
+    }
+    uint64_t st[MAX_STATES];
+    for (int j = 0; j < ns; j++) st[j] = state_identity(sp.op[j], sp.ty[j]);
+    for (int64_t i = a; i < b; i++) {
+      uint64_t v[NWT];
+      seg_load<KW, NWT>(s, i, s.nw - KW, v);
+      for (int j = 0; j < ns; j++) {
+        uint32_t fd = s_fd[j];
+        st[j] = merge_word(st[j], contrib_fd<NWT>(fd, kind, j, v), fd & 3, (fd >> 2) & 3);
+      }
+    }
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = s.w[w][a];
+    emit_group<KW>(sp, o, g, k, st);
+  }
+}
+
+// block per long segment: strided partial states, then a shared reduction
+template <int KW, int NWT>
+__global__ void k_seg_reduce_long(const SortBuf s, DevSpec sp, int kind, int64_t n, const int64_t* heads, int64_t G,
+                                  OutBuf o, const int64_t* long_list, const unsigned long long* nlong) {
+  const int ns = sp.ns;
+  __shared__ uint32_t s_fd[MAX_STATES];
+  __shared__ uint64_t part[SORT_BLOCK];
+  if (threadIdx.x < ns) s_fd[threadIdx.x] = field_desc(sp, threadIdx.x);
+  __syncthreads();
+  for (unsigned long long q = blockIdx.x; q < *nlong; q += gridDim.x) {
+    int64_t g = long_list[q];
+    int64_t a = heads[g], b = (g + 1 < G) ? heads[g + 1] : n;
+    uint64_t st_out[MAX_STATES];
+    for (int j = 0; j < ns; j++) {
+      uint32_t fd = s_fd[j];
+      uint64_t acc = state_identity(fd & 3, (fd >> 2) & 3);
+      for (int64_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        uint64_t v[NWT];
+        seg_load<KW, NWT>(s, i, s.nw - KW, v);
+        acc = merge_word(acc, contrib_fd<NWT>(fd, kind, j, v), fd & 3, (fd >> 2) & 3);
+      }
+      part[threadIdx.x] = acc;
+      __syncthreads();
+      for (int stp = blockDim.x / 2; stp; stp >>= 1) {
+        if (threadIdx.x < stp) part[threadIdx.x] = merge_word(part[threadIdx.x], part[threadIdx.x + stp], fd & 3, (fd >> 2) & 3);
+        __syncthreads();
+      }
+      st_out[j] = part[0];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      uint64_t k[KW];
+#pragma unroll
+      for (int w = 0; w < KW; w++) k[w] = s.w[w][a];
+      emit_group<KW>(sp, o, g, k, st_out);
+    }
+    __syncthreads();
+  }
+}
+
+// input_sorted: any key[i] < key[i-1] sets the flag (k_stream_fold order check,
+// _kernels.py:655-694 -> MergeOrderError)
+template <int KW>
+__global__ void k_check_sorted(const SortBuf s, int64_t n, int* bad) {
+  for (int64_t i = 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool lt = false, eq = true;
+#pragma unroll
+    for (int w = 0; w < KW; w++) {
+      uint64_t x = s.w[w][i], y = s.w[w][i - 1];
+      if (eq && x != y) {
+        lt = x < y;
+        eq = false;
+      }
+    }
+    if (lt) atomicExch(bad, 1);
+  }
+}
+
+// append a columnar batch to the sort buffer as words (keys, payload words)
+template <int KW, int NWT>
+__global__ void k_sort_append(ColSrc c, int nv, SortBuf s, int64_t at) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+    col_key<KW>(c, i, k);
+#pragma unroll
+    for (int w = 0; w < KW; w++) s.w[w][at + i] = k[w];
+    for (int w = 0; w < nv; w++) {
+      const uint8_t* p = c.val[w] + i * c.vstride[w];
+      s.w[KW + w][at + i] =
+          (c.vty[w] == TY_I32) ? (uint64_t)(long long)*(const int*)p : (uint64_t)*(const long long*)p;
+    }
+  }
+}
+
+}  // namespace aggb

@@ -10,7 +10,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 GPU_ALGOS = ("pre_partitioning", "original_hh", "hash_sort", "shared_hash",
-             "dynamic_destaging")
+             "dynamic_destaging", "sort_based")
 
 
 def build_dataset(n, m, seed, agg_names=("sum", "count"), dist="uniform", frame_size=1024,
@@ -110,7 +110,8 @@ def test_misestimated_cardinality_stays_correct(algo, wrong):
           EngineConfig(memory_frames=6, frame_size=1024, seed=4, group_estimate=wrong), want)
 
 
-@pytest.mark.parametrize("algo,min_m", [("hash_sort", 3), ("original_hh", 4), ("shared_hash", 4),
+@pytest.mark.parametrize("algo,min_m", [("sort_based", 3), ("hash_sort", 3), ("original_hh", 4),
+                                        ("shared_hash", 4),
                                         ("dynamic_destaging", 5), ("pre_partitioning", 4)])
 def test_budget_floor(algo, min_m):
     from paper_1311_0059_b200.core import InvalidBudget
@@ -119,3 +120,28 @@ def test_budget_floor(algo, min_m):
     with pytest.raises(InvalidBudget):
         drive(algo, frames, stats, agg, EngineConfig(memory_frames=min_m - 1, frame_size=1024))
     drive(algo, frames, stats, agg, EngineConfig(memory_frames=min_m, frame_size=1024), want)
+
+
+def test_sorted_input_streams_and_output_sorted():
+    from paper_1311_0059_b200.operators import EngineConfig
+    frames, want, stats, agg = build_dataset(3000, 700, seed=6, sort_keys=True)
+    cfg = EngineConfig(memory_frames=4, frame_size=1024, seed=6, input_sorted=True)
+    got, met = drive("sort_based", frames, stats, agg, cfg, want)
+    assert list(got) == sorted(got)
+
+
+def test_sorted_flag_rejects_unsorted_input():
+    from paper_1311_0059_b200.core import MergeOrderError
+    from paper_1311_0059_b200.operators import EngineConfig
+    frames, _, stats, agg = build_dataset(2000, 500, seed=7)
+    cfg = EngineConfig(memory_frames=4, frame_size=1024, seed=7, input_sorted=True)
+    with pytest.raises(MergeOrderError):
+        drive("sort_based", frames, stats, agg, cfg)
+
+
+def test_sort_based_output_is_key_sorted_after_spill():
+    from paper_1311_0059_b200.operators import EngineConfig
+    frames, want, stats, agg = build_dataset(4000, 1500, seed=8)
+    got, _ = drive("sort_based", frames, stats, agg,
+                   EngineConfig(memory_frames=5, frame_size=1024, seed=8), want)
+    assert list(got) == sorted(got)

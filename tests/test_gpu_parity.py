@@ -16,7 +16,7 @@ from conftest import (assert_values_match, float_out_cols, golden_files, golden_
 
 pytestmark = pytest.mark.gpu
 
-ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort")
+ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort", "sort_based")
 
 
 def _engine():
@@ -57,7 +57,7 @@ def check_against(res, gkeys, gvals, cfg):
     assert_values_match(res.as_float64(), gvals, float_out_cols(cfg))
 
 
-GOLD = [p for p in golden_files() if "__sort_based" not in p]
+GOLD = golden_files()
 
 
 @pytest.mark.parametrize("path", GOLD, ids=lambda p: os.path.basename(p)[:-4])
@@ -162,3 +162,40 @@ def test_pre_partitioning_residency():
     assert len(np.unique(res.keys[0])) == res.n_groups == 20_000
     assert int(res.values[0][:R].sum()) == met["records"] - met["level0_spilled_records"]
     assert met["level0_spilled_records"] > 0
+
+
+def test_sort_based_output_is_key_sorted():
+    """sort_based emits groups in key order (reference test_operators.py:167-173)."""
+    from paper_1311_0059_b200 import datagen as D
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C4"], 300_000)
+    keys, vals = D.generate(cfg)
+    with E.GroupBy("sort_based", _agg(cfg), ["i64"], ["i64"], budget_groups=-1) as g:
+        g.push(keys, vals)
+        res = g.result()
+    assert res.sorted
+    k = res.keys[0].view(np.uint64)
+    assert np.all(k[1:] > k[:-1])
+
+
+def test_sort_based_sorted_input_contract():
+    """input_sorted: a sorted batch streams straight into the fold; a key that
+    decreases raises MergeOrderError (reference sort_based.py:56-75)."""
+    from paper_1311_0059_b200 import datagen as D
+    from paper_1311_0059_b200.core import MergeOrderError
+    from oracle import oracle as O
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C2"], 50_000)
+    keys, vals = D.generate(cfg)
+    order = np.argsort(keys[0], kind="stable")
+    sk, sv = [keys[0][order]], [vals[0][order]]
+    with E.GroupBy("sort_based", _agg(cfg), ["i64"], ["i64"], input_sorted=True) as g:
+        g.push(sk, sv)
+        res = g.result()
+    uk, out, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+    assert np.array_equal(res.as_float64(), out)
+    with E.GroupBy("sort_based", _agg(cfg), ["i64"], ["i64"], input_sorted=True) as g:
+        g.push(keys, vals)
+        with pytest.raises(MergeOrderError):
+            g.finish()
