@@ -173,12 +173,13 @@ def run_ours(args, rank, world, device):
     stream = torch.cuda.Stream(device=device)
     agg = spec_of(cfg)
     g = GroupBy(args.algo, agg, types_of(keys), types_of(vals), budget_groups=budget_of(cfg, n),
-                stats=stats, seed=1234, device=device.index, stream=stream)
+                stats=stats, seed=1234, device=device.index, stream=stream,
+                emit_partials=world > 1)
     xg = None
     if world > 1:
         from paper_1311_0059_b200.exchange import Exchanger
         xg = Exchanger(g, agg, types_of(keys), types_of(vals), device, stream, rank, world,
-                       stats=stats)
+                       stats=stats, seed=1234, budget_groups=budget_of(cfg, n))
 
     def step():
         g.reset()
@@ -210,6 +211,11 @@ def run_ours(args, rank, world, device):
     ks = g.kernel_stats()
     met = g.metrics()
     res_groups = met["output_groups"]
+    if xg is not None:
+        res_groups = xg.merge.metrics()["output_groups"]
+        t = torch.tensor([res_groups], dtype=torch.int64, device=device)
+        torch.distributed.all_reduce(t)
+        res_groups = int(t.item())
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

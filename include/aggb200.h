@@ -81,7 +81,9 @@ typedef struct {
   double group_estimate;    /* EngineConfig.group_estimate; < 0 means None   */
   double stats_R, stats_R_t, stats_G, stats_G_t;  /* DatasetStats            */
   int32_t level;            /* Operator(..., level) (base.py:131-137)        */
-  int32_t reserved_[7];
+  int32_t emit_partials;    /* 1: finish() leaves unfinalized state columns (multi-GPU combine
+                               step; the reference's unfinalized runs, _emit_record finalize=0) */
+  int32_t reserved_[6];
 } aggb_config;
 
 /* AggSpec (core.py:126-185) + an explicit key / value-column binding. */
@@ -162,12 +164,14 @@ int aggb_finish(void* handle, aggb_result* out);
  * sizeof(key_type[i]); out[j]: n_groups * 8.  NULL entries are skipped. */
 int aggb_copy_result(void* handle, void* const* host_keys, void* const* host_out);
 
-/* Multi-GPU exchange helpers (new): after aggb_finish, pack
- * this rank's partial groups (unfinalized states) by destination
- * dest = hash(key, exchange seed) % nranks.  send: device buffer of
- * aggb_exchange_bytes() bytes; counts: host array[nranks] of records per dest.
- * The caller moves the buffers (NCCL all-to-allv via torch.distributed) and
- * pushes the received records back with aggb_push_partials into a merge handle. */
+/* Multi-GPU exchange helpers (new).  After aggb_finish on a
+ * handle created with emit_partials = 1, aggb_exchange_pack writes this rank's
+ * partial groups as records of aggb_exchange_record_bytes() bytes (key words,
+ * then state words) into the device buffer `send`, grouped by destination
+ * dest = hash(key, exchange seed) % nranks, and fills counts[nranks] (host) with
+ * records per destination.  The caller moves the bytes (NCCL all-to-allv via
+ * torch.distributed) and merges what it received with aggb_push_partials
+ * (same record layout, device pointer) on a handle of the same spec. */
 int64_t aggb_exchange_record_bytes(void* handle);
 int aggb_exchange_pack(void* handle, int nranks, void* send, int64_t* counts);
 int aggb_push_partials(void* handle, const void* recv, int64_t n_records);

@@ -52,7 +52,7 @@ class Config(ctypes.Structure):
                 ("group_estimate", ctypes.c_double), ("stats_R", ctypes.c_double),
                 ("stats_R_t", ctypes.c_double), ("stats_G", ctypes.c_double),
                 ("stats_G_t", ctypes.c_double), ("level", ctypes.c_int32),
-                ("reserved_", ctypes.c_int32 * 7)]
+                ("emit_partials", ctypes.c_int32), ("reserved_", ctypes.c_int32 * 6)]
 
 
 class Spec(ctypes.Structure):

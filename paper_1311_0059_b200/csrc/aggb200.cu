@@ -1148,7 +1148,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     ca.slots_log2 = h->child_slots_log2;
     ca.cap = h->child_cap;
     ca.seed = level_seed(h->cfg.seed, SALT_SLOT, depth + 1);
-    ca.out = outbuf(h, 0);
+    ca.out = outbuf(h, h->cfg.emit_partials ? 1 : 0);
     ca.ovf = h->ovf.as<uint64_t>();
     ca.ovf_stride = h->ovf_cap;
     ca.ovf_count = SC(h) + 11;
@@ -1353,14 +1353,22 @@ int aggb_push(void* handle, const aggb_input* in) {
 int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   Handle* h = (Handle*)handle;
   if (!h) return fail(AGGB_INVALID_ARG, "null handle");
+  if (h->finished) return fail(AGGB_INVALID_ARG, "push after finish; call aggb_reset");
   if (n_records <= 0) return AGGB_OK;
-  // partial records (SoA: kw key words then ns state words, stride n_records) are
-  // merged through a GRACE pass into the partial spill set, then drained at finish.
+  if (h->cfg.algo == AGGB_SORT_BASED) return fail(AGGB_SPEC_ERROR, "partials merge through a hash algorithm");
   cudaSetDevice(h->device);
+  // partial records (AoS: kw key words then ns state words) are transposed to
+  // the list layout and partitioned into the partial spill set; the children
+  // of aggb_finish merge them (merge ops only, like the reference's runs)
+  int rw = h->kw + h->cs.ds.ns;
+  DBuf soa;
+  TRY(soa.ensure((size_t)n_records * rw * 8, nullptr));
+  k_aos_to_soa<<<h->sms * 8, 256, 0, h->st>>>((const uint64_t*)recv, n_records, rw, soa.as<uint64_t>());
+  h->launches++;
   CU(cudaMemcpyAsync(SC(h) + 11, &n_records, 8, cudaMemcpyHostToDevice, h->st));
   PassPlan g;
   g.mode = MODE_GRACE;
-  g.lin = (const uint64_t*)recv;
+  g.lin = soa.as<uint64_t>();
   g.lin_stride = n_records;
   g.lin_count = SC(h) + 11;
   g.lin_kind = 1;
@@ -1369,7 +1377,9 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   g.counter = SC(h) + 9;
   TRY(launch_pass(h, g));
   CU(cudaStreamSynchronize(h->st));
+  soa.release();
   h->part0_live = true;
+  h->records += n_records;
   return AGGB_OK;
 }
 
@@ -1425,7 +1435,7 @@ int aggb_finish(void* handle, aggb_result* out) {
       } else if (h->cfg.algo == AGGB_HASH_SORT && h->hash_sort_runs > 0) {
         TRY(cut_run(h));  // last run; the merge-with-fold is the drain below
       } else {
-        TRY(flush_table(h, false, nullptr));
+        TRY(flush_table(h, h->cfg.emit_partials != 0, nullptr));
       }
       tr.mark(h->st, "finish: level-0 flush");
       {
@@ -1461,9 +1471,11 @@ int aggb_finish(void* handle, aggb_result* out) {
         r.key[w] = col;
       }
     }
-    for (int j = 0; j < h->cs.ds.nout; j++) {
+    int ncols = h->cfg.emit_partials ? h->cs.ds.ns : h->cs.ds.nout;
+    for (int j = 0; j < ncols; j++) {
       r.out[j] = h->out_vals.as<uint64_t>() + (size_t)j * h->out_cap;
-      r.out_type[j] = h->cs.out_type[j];
+      r.out_type[j] = h->cfg.emit_partials ? (h->cs.ds.ty[j] == TY_F64 && h->cs.ds.op[j] == OP_ADD ? AGGB_F64 : AGGB_I64)
+                                           : h->cs.out_type[j];
     }
     r.sorted = h->cfg.algo == AGGB_SORT_BASED ? 1 : 0;
     CU(cudaStreamSynchronize(h->st));
@@ -1611,7 +1623,7 @@ int seg_reduce(Handle* h, SortBuf cur, int64_t n) {
                                                      heads.as<int64_t>());
   TRY(ensure_out(h, G + 16));
   CU(cudaMemsetAsync(SC(h) + 14, 0, 8, h->st));
-  OutBuf o = outbuf(h, 0);
+  OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
   int nwt = nwt_for(std::max(1, cur.nw - KW));
   int sg = (int)std::min<int64_t>((G + 255) / 256, (int64_t)h->sms * 16);
   sg = std::max(sg, 1);
@@ -1707,5 +1719,46 @@ int64_t aggb_exchange_record_bytes(void* handle) {
   Handle* h = (Handle*)handle;
   return h ? (int64_t)(h->kw + h->cs.ds.ns) * 8 : 0;
 }
-int aggb_exchange_pack(void*, int, void*, int64_t*) { return fail(AGGB_SPEC_ERROR, "exchange: not built yet"); }
+
+int aggb_exchange_pack(void* handle, int nranks, void* send, int64_t* counts) {
+  Handle* h = (Handle*)handle;
+  if (!h || !counts || nranks < 1 || nranks > 256) return fail(AGGB_INVALID_ARG, "bad exchange arguments");
+  if (!h->finished) return fail(AGGB_INVALID_ARG, "exchange_pack before finish");
+  if (!h->cfg.emit_partials) return fail(AGGB_SPEC_ERROR, "exchange needs a handle created with emit_partials=1");
+  cudaSetDevice(h->device);
+  int64_t n = h->result.n_groups;
+  for (int i = 0; i < nranks; i++) counts[i] = 0;
+  if (n == 0) return AGGB_OK;
+  if (!send) return fail(AGGB_INVALID_ARG, "null send buffer");
+  uint64_t seed = level_seed(h->cfg.seed, SALT_EXCH, 0);
+  DBuf c;
+  TRY(c.ensure(2 * 256 * 8, nullptr));
+  unsigned long long* cnt = c.as<unsigned long long>();
+  CU(cudaMemsetAsync(cnt, 0, 256 * 8, h->st));
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sms * 8);
+  int pe = prof_begin(h, 10);
+  if (h->kw == 1) k_exch_count<1><<<grid, 256, 0, h->st>>>(h->out_keys.as<uint64_t>(), h->out_cap, n, seed, nranks, cnt);
+  else k_exch_count<2><<<grid, 256, 0, h->st>>>(h->out_keys.as<uint64_t>(), h->out_cap, n, seed, nranks, cnt);
+  std::vector<unsigned long long> hc(nranks), off(nranks);
+  CU(cudaMemcpyAsync(hc.data(), cnt, nranks * 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  unsigned long long acc = 0;
+  for (int i = 0; i < nranks; i++) {
+    off[i] = acc;
+    acc += hc[i];
+    counts[i] = (int64_t)hc[i];
+  }
+  CU(cudaMemcpyAsync(cnt + 256, off.data(), nranks * 8, cudaMemcpyHostToDevice, h->st));
+  if (h->kw == 1)
+    k_exch_scatter<1><<<grid, 256, 0, h->st>>>(h->out_keys.as<uint64_t>(), h->out_vals.as<uint64_t>(), h->out_cap, n,
+                                               h->cs.ds.ns, seed, nranks, cnt + 256, (uint64_t*)send);
+  else
+    k_exch_scatter<2><<<grid, 256, 0, h->st>>>(h->out_keys.as<uint64_t>(), h->out_vals.as<uint64_t>(), h->out_cap, n,
+                                               h->cs.ds.ns, seed, nranks, cnt + 256, (uint64_t*)send);
+  prof_end(h, pe);
+  h->launches += 2;
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->st));
+  return AGGB_OK;
+}
 }

@@ -66,9 +66,13 @@ __device__ __forceinline__ uint64_t hash_key(const uint64_t (&k)[KW], uint64_t s
   return h;
 }
 
-// range-reduce the top 32 bits of a hash onto [0, n)
+// range-reduce the top 32 bits of a hash onto [0, n).  Written with __umulhi:
+// nvcc 12.9 lowered the equivalent (uint32_t)(((h >> 32) * (uint64_t)n) >> 32)
+// into a wrong shared-memory address computation when the result indexed a
+// __shared__ array directly (k_exch_count counted every record into bin 0;
+// profiles/r01_notes.md).
 __device__ __forceinline__ uint32_t reduce32(uint64_t h, uint32_t n) {
-  return (uint32_t)(((h >> 32) * (uint64_t)n) >> 32);
+  return __umulhi((uint32_t)(h >> 32), n);
 }
 
 template <int KW>

@@ -466,6 +466,50 @@ __global__ void k_page_scatter(PagePool pool, uint32_t first, const uint32_t* la
 // output egress: key words -> typed key columns
 // ---------------------------------------------------------------------------
 
+// ---------------------------------------------------------------------------
+// multi-GPU exchange: pack partial groups by destination rank (AoS records)
+// ---------------------------------------------------------------------------
+
+template <int KW>
+__global__ void k_exch_count(const uint64_t* keys, int64_t cap, int64_t n, uint64_t seed, int nranks,
+                             unsigned long long* counts) {
+  __shared__ unsigned int sh[256];
+  for (int i = threadIdx.x; i < nranks; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = keys[w * cap + i];
+    atomicAdd(&sh[reduce32(hash_key<KW>(k, seed), (uint32_t)nranks)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nranks; i += blockDim.x)
+    if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
+}
+
+template <int KW>
+__global__ void k_exch_scatter(const uint64_t* keys, const uint64_t* states, int64_t cap, int64_t n, int ns,
+                               uint64_t seed, int nranks, unsigned long long* cursor, uint64_t* send) {
+  const int rw = KW + ns;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = keys[w * cap + i];
+    unsigned d = reduce32(hash_key<KW>(k, seed), (uint32_t)nranks);
+    unsigned long long at = atomicAdd(&cursor[d], 1ull);
+    uint64_t* dst = send + at * rw;
+#pragma unroll
+    for (int w = 0; w < KW; w++) dst[w] = k[w];
+    for (int j = 0; j < ns; j++) dst[KW + j] = states[(int64_t)j * cap + i];
+  }
+}
+
+// AoS partial records -> SoA (the pass kernels' list layout)
+__global__ void k_aos_to_soa(const uint64_t* in, int64_t n, int rw, uint64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int w = 0; w < rw; w++) out[(int64_t)w * n + i] = in[i * rw + w];
+}
+
 __global__ void k_key_to_i32(const uint64_t* w, int32_t* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)(uint32_t)(w[i] >> 32);

@@ -86,7 +86,8 @@ class GroupBy:
                  memory_frames: int = 0, frame_size: int = 32768, budget_groups: int = -1,
                  stats: DatasetStats | None = None, seed: int = 0, fudge: float = 1.2,
                  slot_ratio: float = 1.0, group_estimate=None, input_sorted: bool = False,
-                 level: int = 0, device: int = 0, stream=None, input_kind: str = "raw"):
+                 level: int = 0, device: int = 0, stream=None, input_kind: str = "raw",
+                 emit_partials: bool = False):
         self.L = N.load()
         if algo not in N.ALGO:
             raise SpecError(f"unknown algorithm {algo!r}")
@@ -108,6 +109,8 @@ class GroupBy:
             cfg.stats_R, cfg.stats_R_t, cfg.stats_G, cfg.stats_G_t = (
                 float(stats.R), float(stats.R_t), float(stats.G), float(stats.G_t))
         cfg.level = level
+        cfg.emit_partials = int(emit_partials)
+        self.emit_partials = emit_partials
         sp = N.Spec()
         sp.n_fns = len(agg.fns)
         for i, (f, b) in enumerate(zip(agg.fns, agg.bind)):
@@ -174,6 +177,22 @@ class GroupBy:
             inp.val[i], inp.val_stride[i] = p, s
         inp.on_host = on_host
         N.check(self.L.aggb_push(self.h, ctypes.byref(inp)), "aggb_push")
+
+    def push_partials(self, records, n: int) -> None:
+        """Merge packed partial records (aggb_exchange_pack layout, device memory)."""
+        ptr = records.data_ptr() if hasattr(records, "data_ptr") else int(records)
+        N.check(self.L.aggb_push_partials(self.h, ctypes.c_void_p(ptr), n), "aggb_push_partials")
+
+    def pack(self, nranks: int):
+        """Pack this handle's partial groups by destination rank -> (uint8 tensor, counts)."""
+        import torch
+        res = self._result or self.finish()
+        rb = int(self.L.aggb_exchange_record_bytes(self.h))
+        buf = torch.empty(max(res.n_groups, 1) * rb, dtype=torch.uint8, device="cuda")
+        counts = (ctypes.c_int64 * nranks)()
+        N.check(self.L.aggb_exchange_pack(self.h, nranks, ctypes.c_void_p(buf.data_ptr()), counts),
+                "aggb_exchange_pack")
+        return buf, [int(c) for c in counts], rb
 
     def finish(self) -> N.Result:
         res = N.Result()

@@ -1,0 +1,84 @@
+"""Multi-GPU group-by: local combine -> hash exchange -> merge.
+
+One process per GPU.  Every rank aggregates its own shard with a handle that
+keeps unfinalized states (``emit_partials``); ``aggb_exchange_pack`` groups
+the partial groups by ``dest = hash(key, exchange seed) % world`` into one
+device buffer; one all-to-all of counts and one all-to-allv of the packed
+records (torch.distributed over NCCL / NVLink) move them; a merge handle of the
+same spec folds what this rank received (merge ops only) and finishes.  Key
+sets are disjoint across ranks after the exchange, so the job's output is the
+concatenation of the ranks' outputs.  The exchange seed is independent of the
+table, partition and level seeds.
+
+``exchange_records`` is the collective alone (byte buffers + per-destination
+record counts); it has no CUDA dependency and is tested with gloo on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from paper_1311_0059_b200 import _native as N
+
+
+def exchange_records(send: torch.Tensor, send_counts: list, record_bytes: int, group=None):
+    """All-to-allv of packed records.
+
+    send: 1-D uint8 tensor, records grouped by destination rank in rank order.
+    send_counts: records per destination (len == world size).
+    Returns (recv uint8 tensor, recv_counts list).
+    """
+    world = dist.get_world_size(group)
+    dev = send.device
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = [int(x) for x in rc.cpu().tolist()]
+    recv = torch.empty(sum(recv_counts) * record_bytes, dtype=torch.uint8, device=dev)
+    dist.all_to_all_single(recv, send[: sum(send_counts) * record_bytes],
+                           output_split_sizes=[c * record_bytes for c in recv_counts],
+                           input_split_sizes=[c * record_bytes for c in send_counts], group=group)
+    return recv, recv_counts
+
+
+class Exchanger:
+    """Drives the exchange + merge after a local handle has finished.
+
+    ``local`` must be a GroupBy created with ``emit_partials=True``; the merge
+    handle is created here with the same spec and budget.
+    """
+
+    def __init__(self, local, agg, key_types, val_types, device, stream, rank, world, **kw):
+        from paper_1311_0059_b200.engine import GroupBy
+        self.local = local
+        self.rank, self.world = rank, world
+        self.device = device
+        self.merge = GroupBy(local.algo if local.algo != "sort_based" else "pre_partitioning",
+                             agg, key_types, val_types, device=device.index, stream=stream,
+                             budget_groups=kw.pop("budget_groups", -1), **kw)
+        self.rec_bytes = int(local.L.aggb_exchange_record_bytes(local.h))
+        self._send = None
+        self.last_counts = None
+
+    def run(self):
+        L = self.local.L
+        res = self.local._result
+        n = res.n_groups
+        need = max(n, 1) * self.rec_bytes
+        if self._send is None or self._send.numel() < need:
+            self._send = torch.empty(int(need * 1.25), dtype=torch.uint8, device=self.device)
+        counts = (ctypes.c_int64 * self.world)()
+        N.check(L.aggb_exchange_pack(self.local.h, self.world, ctypes.c_void_p(self._send.data_ptr()),
+                                     counts), "aggb_exchange_pack")
+        send_counts = [int(c) for c in counts]
+        recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
+        self.last_counts = (send_counts, recv_counts)
+        self.merge.reset()
+        total = sum(recv_counts)
+        if total:
+            N.check(L.aggb_push_partials(self.merge.h, ctypes.c_void_p(recv.data_ptr()), total),
+                    "aggb_push_partials")
+        return self.merge.finish()

@@ -199,3 +199,47 @@ def test_sort_based_sorted_input_contract():
         g.push(keys, vals)
         with pytest.raises(MergeOrderError):
             g.finish()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_pack_merge_simulated_ranks(world):
+    """The multi-GPU data path on one device: `world` shards aggregate locally
+    with partial output, pack by destination, the per-destination segments are
+    handed to `world` merge handles (what all-to-allv would deliver); the union
+    of the merged outputs is the global group-by, key sets disjoint."""
+    import torch
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C2"], 600_000, key_range=60_000)
+    keys, vals = D.generate(cfg)
+    agg = _agg(cfg)
+    n = cfg.n // world
+    segs = [[] for _ in range(world)]
+    for r in range(world):
+        with E.GroupBy("pre_partitioning", agg, ["i64"], ["i64"], budget_groups=8000,
+                       emit_partials=True, seed=42) as g:
+            g.push([k[r * n:(r + 1) * n] for k in keys], [v[r * n:(r + 1) * n] for v in vals])
+            g.finish()
+            buf, counts, rb = g.pack(world)
+            off = 0
+            for d in range(world):
+                segs[d].append(buf[off * rb:(off + counts[d]) * rb].clone())
+                off += counts[d]
+    outk, outv = [], []
+    for d in range(world):
+        recv = torch.cat(segs[d])
+        with E.GroupBy("pre_partitioning", agg, ["i64"], ["i64"], budget_groups=8000, seed=42) as m:
+            m.push_partials(recv, recv.numel() // rb)
+            r = m.result()
+        outk.append(r.keys[0])
+        outv.append(r.as_float64())
+    for a in range(world):
+        for b in range(a + 1, world):
+            assert len(np.intersect1d(outk[a], outk[b])) == 0
+    allk = np.concatenate(outk)
+    allv = np.concatenate(outv)
+    order = np.argsort(allk)
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert np.array_equal(allk[order], uk[:, 0].view(np.int64))
+    assert np.array_equal(allv[order], want)
