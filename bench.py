@@ -103,18 +103,33 @@ def make_inputs(cfg, start, n, device):
     L = N.load()
     st = torch.cuda.current_stream().cuda_stream
 
-    def gen(kind, stream_id, lo=0, rng=1, dtype=torch.int64, cdf=None, K=0, a=0, b=0):
-        out = torch.empty(n, dtype=dtype, device=device)
+    def gen(kind, stream_id, lo=0, rng=1, dtype=torch.int64, cdf=None, K=0, a=0, b=0, out=None,
+            stride=0):
+        out = torch.empty(n, dtype=dtype, device=device) if out is None else out
         N.check(L.aggb_generate(st, kind, cfg.seed, stream_id, start, n, lo, rng,
                                 cdf.data_ptr() if cdf is not None else None, K, a, b,
-                                out.data_ptr(), 0), "aggb_generate")
+                                out.data_ptr(), stride), "aggb_generate")
         return out
 
     if cfg.wide:
-        keys = [gen(0, D.S_KEY, 0, cfg.k0_range), gen(4, D.S_K1, 0, cfg.k1_range, torch.int32)]
-        vals = [gen(0, D.S_V0, 0, 1 << 20), gen(0, D.S_V1, 0, 1 << 20),
-                gen(2, D.S_V2, dtype=torch.float64), gen(2, D.S_V3, dtype=torch.float64)]
-        return keys, vals
+        # C5: 64-byte rows  k0 i64 | k1 i32 | pad | v0 v1 i64 | v2 v3 f64 | pad (datagen.wide_rows)
+        rows = torch.zeros((n, 64), dtype=torch.uint8, device=device)
+
+        def field(off, dt):
+            w = torch.tensor([], dtype=dt).element_size()
+            return rows[:, off:off + w].view(dt)[:, 0]
+
+        k0, k1 = field(0, torch.int64), field(8, torch.int32)
+        v = [field(16, torch.int64), field(24, torch.int64), field(32, torch.float64),
+             field(40, torch.float64)]
+        gen(0, D.S_KEY, 0, cfg.k0_range, out=k0, stride=64)
+        gen(4, D.S_K1, 0, cfg.k1_range, out=k1, stride=64)
+        gen(0, D.S_V0, 0, 1 << 20, out=v[0], stride=64)
+        gen(0, D.S_V1, 0, 1 << 20, out=v[1], stride=64)
+        gen(2, D.S_V2, out=v[2], stride=64)
+        gen(2, D.S_V3, out=v[3], stride=64)
+        make_inputs.rows = rows
+        return [k0, k1], v
     if cfg.zipf_k:
         cdf = torch.from_numpy(D.zipf_cdf(cfg.zipf_k, cfg.zipf_s)).to(device)
         a, b = D.zipf_perm_params(cfg.zipf_k, cfg.seed)

@@ -80,7 +80,11 @@ struct DBuf {
     bytes = 0;
     size_t nb = std::max(need + need / 4, (size_t)256);  // headroom: sizes vary run to run
     cudaError_t e = cudaMalloc(&p, nb);
-    if (e != cudaSuccess) return fail(AGGB_CUDA_ERROR, "cudaMalloc(%zu): %s", nb, cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();  // do not leave the failure to a later launch check
+      return fail(AGGB_CUDA_ERROR, "cudaMalloc(%zu): %s", nb, cudaGetErrorString(e));
+    }
     bytes = nb;
     if (hw) *hw += nb;
     return AGGB_OK;
@@ -1001,7 +1005,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
     CU(cudaMemcpyAsync(&nd, SC(h) + 10, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
-    if (!frozen) continue;
+    if (!frozen && !nd) continue;
     int64_t start = std::min<int64_t>(cur.n, (int64_t)tiles * T);
     // keep the deferred records (the deferral buffer is reused by the next FILL)
     ColSrc dc;
@@ -1027,7 +1031,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
       }
       temps.push_back(tmp);
     }
-    if ((rc = cut_run(h))) break;
+    if (frozen && (rc = cut_run(h))) break;
     if (start < cur.n) {
       ColSrc rest = cur;
       rest.n = cur.n - start;
@@ -1152,13 +1156,6 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     ca.ovf = h->ovf.as<uint64_t>();
     ca.ovf_stride = h->ovf_cap;
     ca.ovf_count = SC(h) + 11;
-    {
-      unsigned long long maxrec = 0;
-      for (int p = 0; p < nparts; p++) maxrec = std::max(maxrec, recs[p]);
-      TRY(h->pend.ensure((size_t)grid * (maxrec + 1) * ovw * 8, &h->hw));
-      ca.pend = h->pend.as<uint64_t>();
-      ca.pend_cap = (int64_t)maxrec + 1;
-    }
     ca.item_counter = SC(h) + 12;
     ca.stats = SC(h);
     tr.mark(h->st, "drain: scatter + buffers");
@@ -1172,7 +1169,11 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     CU(cudaStreamSynchronize(h->st));
     tr.mark(h->st, "drain: child");
     if (!novf) return AGGB_OK;
-    // next level: grace-partition the overflow with fresh seeds (fresh per level, hybrid.py:181-184)
+    // next level: grace-partition the overflow with fresh seeds (fresh per level, hybrid.py:181-184).
+    // Every page of this level has been consumed by the children, so the pool
+    // is recycled: the next level writes its pages from page 0 again.
+    CU(cudaMemsetAsync(h->pool_ctr.p, 0, 8, h->st));
+    h->pool_bound = 0;
     depth++;
     int P = (int)std::min<int64_t>(max_parts_for(h->kw + h->cs.ds.ns),
                                    std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.5 * h->child_cap))));
@@ -1392,11 +1393,13 @@ int aggb_finish(void* handle, aggb_result* out) {
     if (h->cfg.algo == AGGB_SORT_BASED) {
       TRY(aggb_sort_finish(h));
     } else {
-      int frozen = 0;
+      int frozen = 0, refused = 0;
       unsigned long long groups = 0;
       CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&refused, &h->tab.hdr->pad, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&groups, &h->tab.hdr->groups, 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
+      if (h->cfg.algo == AGGB_ORIGINAL_HH && refused) frozen = 1;  // partition 0 spilled: cut the table
       h->met.resident_groups = (int64_t)groups;
       if (h->cfg.algo == AGGB_ORIGINAL_HH && frozen) {
         // overflow: cut the table into partition 0 as partial states (hybrid.py:431-451)

@@ -31,10 +31,11 @@ enum { ST_SPILLED = 0, ST_HITS = 1, ST_INSERTS = 2, ST_DEFERRED = 3, ST_RECORDS 
        ST_NSTATS = 8 };
 
 struct TableHdr {
-  unsigned long long groups;
+  unsigned long long groups;     // reservations held + committed inserts
   int frozen;
   int esc;
-  unsigned long long pad[2];
+  unsigned long long committed;  // keys actually inserted
+  unsigned long long pad;
 };
 
 struct GTable {
@@ -60,16 +61,25 @@ struct Bkt {
 // diverge on long probe chains), CAS-claimed keys, capacity-bounded inserts.
 // ---------------------------------------------------------------------------
 
+// A reservation that finds the counter at capacity freezes the table only when
+// the capacity is really taken by committed keys.  Otherwise the excess is
+// transient (threads racing to insert one key each reserve before their CAS
+// shows the key is already there): the record is refused without freezing and
+// takes the refusal path (FILL defers it to the PROBE pass, ROUTE spills it to
+// partition 0 and marks the table for the overflow cut).  Never wait here: a
+// lane spinning on a reservation held by a lane of its own warp deadlocks at
+// the loop's reconvergence point.
 __device__ __forceinline__ bool reserve_capacity(const GTable& t) {
   if (*(volatile int*)&t.hdr->frozen) return false;
   unsigned long long old = atomicAdd(&t.hdr->groups, 1ull);
-  if (old >= t.cap) {
-    atomicAdd(&t.hdr->groups, ~0ull);
-    atomicExch(&t.hdr->frozen, 1);
-    return false;
-  }
-  return true;
+  if (old < t.cap) return true;
+  atomicAdd(&t.hdr->groups, ~0ull);
+  if (*(volatile unsigned long long*)&t.hdr->committed >= t.cap) atomicExch(&t.hdr->frozen, 1);
+  atomicExch((int*)&t.hdr->pad, 1);  // some insert was refused (ROUTE: cut the table at close)
+  return false;
 }
+
+__device__ __forceinline__ void commit_insert(const GTable& t) { atomicAdd(&t.hdr->committed, 1ull); }
 
 __device__ __forceinline__ void ld_bucket(const uint64_t* keys, uint64_t b, uint64_t (&w)[4]) {
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(keys + b * 4);
@@ -87,7 +97,7 @@ __device__ __forceinline__ int64_t gt_escape(const GTable& t, bool insert, int& 
   if (*(volatile int*)&t.hdr->esc) { res = R_HIT; return s; }
   if (!insert) { res = R_MISS; return -1; }
   if (!reserve_capacity(t)) { res = R_REFUSED; return -1; }
-  if (atomicCAS(&t.hdr->esc, 0, 1) == 0) { res = R_INSERTED; return s; }
+  if (atomicCAS(&t.hdr->esc, 0, 1) == 0) { commit_insert(t); res = R_INSERTED; return s; }
   atomicAdd(&t.hdr->groups, ~0ull);
   res = R_HIT;
   return s;
@@ -129,12 +139,12 @@ __device__ __forceinline__ int64_t gt_resolve(const GTable& t, const uint64_t (&
       uint64_t* kp = t.keys + (b * BK + emp) * KW;
       if (KW == 1) {
         unsigned long long prev = atomicCAS((unsigned long long*)kp, EMPTY, k[0]);
-        if (prev == EMPTY) { res = R_INSERTED; return (int64_t)(b * BK + emp); }
+        if (prev == EMPTY) { commit_insert(t); res = R_INSERTED; return (int64_t)(b * BK + emp); }
         if (prev == k[0]) { atomicAdd(&t.hdr->groups, ~0ull); res = R_HIT; return (int64_t)(b * BK + emp); }
       } else {
         uint64_t x, y;
         cas128(kp, EMPTY, EMPTY, k[0], k[KW - 1], x, y);
-        if (x == EMPTY && y == EMPTY) { res = R_INSERTED; return (int64_t)(b * BK + emp); }
+        if (x == EMPTY && y == EMPTY) { commit_insert(t); res = R_INSERTED; return (int64_t)(b * BK + emp); }
         if (x == k[0] && y == k[KW - 1]) { atomicAdd(&t.hdr->groups, ~0ull); res = R_HIT; return (int64_t)(b * BK + emp); }
       }
       // another key took the slot: rescan this bucket after it
@@ -202,6 +212,8 @@ __global__ void k_table_init(GTable t, int kw, DevSpec sp) {
     t.hdr->groups = 0;
     t.hdr->frozen = 0;
     t.hdr->esc = 0;
+    t.hdr->committed = 0;
+    t.hdr->pad = 0;
   }
 }
 
@@ -376,18 +388,39 @@ __global__ void k_flush_table(GTable t, DevSpec sp, OutBuf o) {
 // k_child: per-partition shared-memory aggregation (one recursion level)
 // ---------------------------------------------------------------------------
 
+// Shared-memory table lookup of the child operators.  `s_inflight` counts
+// threads between a capacity reservation and the end of their key CAS; once
+// the table is frozen no reservation succeeds, so when a refused thread sees
+// `s_inflight == 0` the key set is final and its re-probe is exact — a key is
+// either resident (aggregate) or not (overflow), never both.
 template <int KW>
 __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap, const uint64_t (&k)[KW], uint64_t seed,
-                                             bool insert, int* s_groups, int* s_frozen, int* s_esc, int& res) {
+                                             bool insert, int* s_groups, int* s_frozen, int* s_esc, int* s_inflight,
+                                             int& res) {
+  // s_groups[0]: reservations + committed inserts; s_groups[1]: committed inserts.
+  // A transient excess (racing reservations) refuses without freezing; the
+  // caller re-probes once no insert is in flight (stable_resolve_refused).
+  auto reserve = [&]() -> bool {
+    atomicAdd(s_inflight, 1);
+    if (!*(volatile int*)s_frozen) {
+      int old = atomicAdd(s_groups, 1);
+      if (old < cap) return true;  // s_inflight released by the caller after the key CAS
+      atomicSub(s_groups, 1);
+      if (*(volatile int*)(s_groups + 1) >= cap) atomicExch(s_frozen, 1);
+    }
+    atomicSub(s_inflight, 1);
+    return false;
+  };
   if (is_sentinel<KW>(k)) {
     if (*(volatile int*)s_esc) { res = R_HIT; return nslots; }
     if (!insert) { res = R_MISS; return -1; }
-    if (*(volatile int*)s_frozen) { res = R_REFUSED; return -1; }
-    int old = atomicAdd(s_groups, 1);
-    if (old >= cap) { atomicSub(s_groups, 1); atomicExch(s_frozen, 1); res = R_REFUSED; return -1; }
-    if (atomicCAS(s_esc, 0, 1) == 0) { res = R_INSERTED; return nslots; }
-    atomicSub(s_groups, 1);
-    res = R_HIT;
+    if (!reserve()) { res = R_REFUSED; return -1; }
+    int won = atomicCAS(s_esc, 0, 1) == 0;
+    if (!won) atomicSub(s_groups, 1);
+    else atomicAdd(s_groups + 1, 1);
+    __threadfence_block();
+    atomicSub(s_inflight, 1);
+    res = won ? R_INSERTED : R_HIT;
     return nslots;
   }
   int mask = nslots - 1;
@@ -406,30 +439,59 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
       empty = (a == EMPTY) && (b == EMPTY);
     }
     if (match) {
-      if (reserved) atomicSub(s_groups, 1);
+      if (reserved) {
+        atomicSub(s_groups, 1);
+        atomicSub(s_inflight, 1);
+      }
       res = R_HIT;
       return s;
     }
     if (empty) {
       if (!insert) { res = R_MISS; return -1; }
       if (!reserved) {
-        if (*(volatile int*)s_frozen) { res = R_REFUSED; return -1; }
-        int old = atomicAdd(s_groups, 1);
-        if (old >= cap) { atomicSub(s_groups, 1); atomicExch(s_frozen, 1); res = R_REFUSED; return -1; }
+        if (!reserve()) { res = R_REFUSED; return -1; }
         reserved = true;
       }
+      bool won, same;
       if (KW == 1) {
         unsigned long long prev = atomicCAS((unsigned long long*)kp, EMPTY, k[0]);
-        if (prev == EMPTY) { res = R_INSERTED; return s; }
-        if (prev == k[0]) { atomicSub(s_groups, 1); res = R_HIT; return s; }
+        won = prev == EMPTY;
+        same = prev == k[0];
       } else {
         uint64_t a, b;
         cas128(kp, EMPTY, EMPTY, k[0], k[KW - 1], a, b);
-        if (a == EMPTY && b == EMPTY) { res = R_INSERTED; return s; }
-        if (a == k[0] && b == k[KW - 1]) { atomicSub(s_groups, 1); res = R_HIT; return s; }
+        won = (a == EMPTY && b == EMPTY);
+        same = (a == k[0] && b == k[KW - 1]);
+      }
+      if (won || same) {
+        if (same) atomicSub(s_groups, 1);
+        else atomicAdd(s_groups + 1, 1);
+        __threadfence_block();
+        atomicSub(s_inflight, 1);
+        res = won ? R_INSERTED : R_HIT;
+        return s;
       }
     }
     s = (s + 1) & mask;
+  }
+}
+
+// A refused record may go to the overflow list only when the table can no
+// longer change for its key: the table is frozen and no insert is in flight.
+// A transient refusal (racing reservations, table not frozen) retries the
+// insert once the in-flight inserts have drained; if that keeps failing the
+// table is frozen explicitly, which makes the final probe exact.
+template <int KW>
+__device__ __forceinline__ int stable_resolve_refused(uint64_t* keys, int nslots, int cap, const uint64_t (&k)[KW],
+                                                      uint64_t seed, int* s_groups, int* s_frozen, int* s_esc,
+                                                      int* s_inflight, int& res) {
+  for (int tries = 0;; tries++) {
+    for (int spin = 0; *(volatile int*)s_inflight > 0 && spin < (1 << 22); spin++) __nanosleep(32);
+    __threadfence_block();
+    const bool frozen = *(volatile int*)s_frozen != 0;
+    int s = stable_lookup<KW>(keys, nslots, cap, k, seed, !frozen, s_groups, s_frozen, s_esc, s_inflight, res);
+    if (res != R_REFUSED) return s;  // hit, inserted, or (frozen) a final miss
+    if (tries >= 16) atomicExch(s_frozen, 1);
   }
 }
 

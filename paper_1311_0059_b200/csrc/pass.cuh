@@ -396,6 +396,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
     }
   }
+  // PROBE spilled records: the resident set is final from now on (a later
+  // push's FILL must not insert a key that already went to a partition)
+  if (a.mode == MODE_PROBE && c_sp) atomicExch(&a.t.hdr->frozen, 1);
   // counters: warp reduce then one shared atomic per warp
   uint32_t cs[5] = {c_sp, c_hit, c_ins, c_def, c_rec};
   const int ids[5] = {ST_SPILLED, ST_HITS, ST_INSERTS, ST_DEFERRED, ST_RECORDS};
@@ -428,8 +431,6 @@ struct ChildArgs {
   uint64_t* ovf;            // overflow list: native partial records, SoA KW + ns words
   int64_t ovf_stride;
   unsigned long long* ovf_count;
-  uint64_t* pend;           // CTA-private pending lists (AoS, KW + ns words)
-  int64_t pend_cap;         // records per CTA
   unsigned long long* item_counter;
   unsigned long long* stats;
 };
@@ -438,10 +439,10 @@ struct ChildArgs {
 // hybrid.py:244-277) in a shared-memory table.  Threads map onto (page, slot)
 // across B / per_page pages per row and R rows per round; the next round's
 // records are prefetched into registers while the current one aggregates.
-// There is no barrier per round: an insert refused because the table is full
-// (the child's budget) parks the record in the CTA's pending list; after the
-// item's last barrier the key set is final, so pending records re-probe and
-// either aggregate or go to the overflow list (the next recursion level).
+// There is no barrier per round.  An insert refused because the table is full
+// (the child's budget: the reference's TABLE_FULL + freeze) waits until no
+// insert is in flight — the key set is then final — and re-probes: resident
+// keys aggregate in place, the rest go to the overflow list (next level).
 template <int KW, int NWT, int R, class PG>
 __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -449,17 +450,14 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
   const int nslots = 1 << a.slots_log2;
   const int stride = nslots + 1;
   const int ns = a.sp.ns;
-  const int pw = KW + ns;  // pending / overflow record words
   uint64_t* skeys = (uint64_t*)smem;                       // stride * KW
   uint64_t* sst = skeys + (size_t)stride * KW;             // ns * stride
-  __shared__ int s_groups, s_frozen, s_esc;
+  __shared__ int s_groups[2], s_frozen, s_esc, s_inflight;
   __shared__ unsigned long long s_item;
   __shared__ unsigned long long s_cnt[ST_NSTATS];
   __shared__ uint32_t s_fd[MAX_STATES];
-  __shared__ uint32_t s_npend;
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
-  uint64_t* pend = a.pend + (size_t)blockIdx.x * a.pend_cap * pw;
   uint32_t nrec = 0, novf = 0;
 
   for (;;) {
@@ -470,10 +468,10 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
       for (int j = 0; j < ns; j++) sst[(size_t)j * stride + i] = state_identity(a.sp.op[j], a.sp.ty[j]);
     }
     if (tid == 0) {
-      s_groups = 0;
+      s_groups[0] = s_groups[1] = 0;
       s_frozen = 0;
       s_esc = 0;
-      s_npend = 0;
+      s_inflight = 0;
     }
     __syncthreads();
     unsigned long long item = s_item;
@@ -520,19 +518,21 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
           int res = R_MISS, s = -1;
           if (lc[r]) {
             nrec++;
-            s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, &s_groups, &s_frozen, &s_esc, res);
+            s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, s_groups, &s_frozen, &s_esc,
+                                  &s_inflight, res);
+            if (res == R_REFUSED)
+              s = stable_resolve_refused<KW>(skeys, nslots, a.cap, kc[r], a.seed, s_groups, &s_frozen, &s_esc,
+                                             &s_inflight, res);
           }
           __syncwarp();  // reconverge after the divergent probe before the updates
           if (res == R_HIT || res == R_INSERTED) {
             Upd<PG>::template sm<NWT>(sst, stride, s, kind, s_fd, ns, vc[r]);
-          } else if (res == R_REFUSED) {
-            uint32_t d = atomicAdd(&s_npend, 1u);
-            if (d < (uint32_t)a.pend_cap) {
-              uint64_t* dst = pend + (size_t)d * pw;
+          } else if (lc[r]) {  // not resident: the next recursion level
+            unsigned long long d = atomicAdd(a.ovf_count, 1ull);
+            novf++;
 #pragma unroll
-              for (int w = 0; w < KW; w++) dst[w] = kc[r][w];
-              for (int j = 0; j < ns; j++) dst[KW + j] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
-            }
+            for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
+            for (int j = 0; j < ns; j++) a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
           }
           __syncwarp();
         }
@@ -544,29 +544,6 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
 #pragma unroll
           for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
         }
-      }
-    }
-    __syncthreads();
-    // the table is final: resolve the pending records (native partial form)
-    const uint32_t npend = min(s_npend, (uint32_t)a.pend_cap);
-    for (uint32_t i = tid; i < npend; i += B) {
-      const uint64_t* src = pend + (size_t)i * pw;
-      uint64_t k[KW];
-#pragma unroll
-      for (int w = 0; w < KW; w++) k[w] = src[w];
-      int res;
-      int s = stable_lookup<KW>(skeys, nslots, a.cap, k, a.seed, false, &s_groups, &s_frozen, &s_esc, res);
-      if (res == R_HIT) {
-        for (int j = 0; j < ns; j++) {
-          uint32_t fd = s_fd[j];
-          supdate(sst + (size_t)j * stride + s, fd & 3, (fd >> 2) & 3, src[KW + j]);
-        }
-      } else {
-        unsigned long long d = atomicAdd(a.ovf_count, 1ull);
-        novf++;
-#pragma unroll
-        for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = k[w];
-        for (int j = 0; j < ns; j++) a.ovf[(KW + j) * a.ovf_stride + d] = src[KW + j];
       }
     }
     __syncthreads();
