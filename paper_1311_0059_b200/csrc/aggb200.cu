@@ -874,7 +874,8 @@ int stage_input(Handle* h, const aggb_input* in, Staged& sg) {
 }
 
 int ensure_defer(Handle* h, int64_t T) {
-  int64_t need = (int64_t)h->sms * 4 * T + 4096;
+  // in flight at a freeze: every CTA's current and prefetched tile (x2 headroom)
+  int64_t need = (int64_t)h->sms * 8 * T + 4096;
   if (need <= h->defer_cap) return AGGB_OK;
   TRY(h->defer.ensure((size_t)need * (h->kw + std::max(1, h->cs.nv)) * 8, &h->hw));
   h->defer_cap = need;

@@ -324,6 +324,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     if (tid == 0) {
       if (s_ndefer) {
         s_defer_base = atomicAdd(a.defer_count, (unsigned long long)s_ndefer);
+        // deferral pressure (transient refusals while the table is not full):
+        // freeze early so the rest of the batch goes to PROBE — budget-safe
+        if (s_defer_base + s_ndefer > (unsigned long long)a.defer_stride / 2) atomicExch(&a.t.hdr->frozen, 1);
         s_ndefer = 0;
       }
       s_grab = (nxt < total) ? grab() : ~0ull;
@@ -337,6 +340,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       if (!tg) continue;
       if (tg & 0x80000000u) {
         int64_t d = (int64_t)s_defer_base + (tg & 0x7FFFFFFFu);
+        if (d >= a.defer_stride) {  // cannot happen with the early freeze; never write out of bounds
+          atomicExch(a.pool.overflow, 2u);
+          continue;
+        }
 #pragma unroll
         for (int w = 0; w < KW; w++) a.defer[w * a.defer_stride + d] = kc[r][w];
 #pragma unroll
