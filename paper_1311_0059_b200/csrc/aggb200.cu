@@ -267,20 +267,18 @@ PassCfg pc() { return PassCfg{k_pass<KW, NWT, R, BLK, 1, PG>, R, BLK}; }
 
 template <int KW>
 PassCfg pass_kernel(int nwt, int prog) {
+  // 512 threads x 4 records, up to 128 registers, 1 CTA/SM: the 1024 x 2 shape
+  // spilled at its 64-register cap (profiles/r01_notes.md)
   if (KW == 1 && nwt == 1) {
-    if (prog == 1) return pc<1, 1, 2, 1024, ProgC1>();
-    if (prog == 2) {
-      const char* v = getenv("AGGB_PASS_VARIANT");
-      if (v && atoi(v) == 1) return pc<1, 1, 4, 512, ProgC2>();
-      return pc<1, 1, 2, 1024, ProgC2>();
-    }
-    if (prog == 3) return pc<1, 1, 2, 1024, ProgC3>();
+    if (prog == 1) return pc<1, 1, 4, 512, ProgC1>();
+    if (prog == 2) return pc<1, 1, 4, 512, ProgC2>();
+    if (prog == 3) return pc<1, 1, 4, 512, ProgC3>();
   }
-  if (KW == 2 && nwt == 4 && prog == 5) return pc<2, 4, 1, 1024, ProgC5>();
+  if (KW == 2 && nwt == 4 && prog == 5) return pc<2, 4, 2, 512, ProgC5>();
   switch (nwt) {
-    case 1: return pc<KW, 1, 2, 1024, PD>();
-    case 2: return pc<KW, 2, 2, 1024, PD>();
-    case 4: return pc<KW, 4, 1, 1024, PD>();
+    case 1: return pc<KW, 1, 4, 512, PD>();
+    case 2: return pc<KW, 2, 4, 512, PD>();
+    case 4: return pc<KW, 4, 2, 512, PD>();
     case 8: return pc<KW, 8, 1, 512, PD>();
     case 16: return pc<KW, 16, 1, 512, PD>();
     default: return pc<KW, 32, 1, 256, PD>();
@@ -289,15 +287,17 @@ PassCfg pass_kernel(int nwt, int prog) {
 
 template <int KW>
 child_fn child_kernel(int nwt, int prog) {
+  // R = 2 records per thread in flight (R = 4 spilled registers at the 64-register
+  // cap of 2 CTAs/SM and ran 2.7x slower, profiles/r01_notes.md)
   if (KW == 1 && nwt == 1) {
-    if (prog == 1) return k_child<1, 1, 4, ProgC1>;
-    if (prog == 2) return k_child<1, 1, 4, ProgC2>;
-    if (prog == 3) return k_child<1, 1, 4, ProgC3>;
+    if (prog == 1) return k_child<1, 1, 2, ProgC1>;
+    if (prog == 2) return k_child<1, 1, 2, ProgC2>;
+    if (prog == 3) return k_child<1, 1, 2, ProgC3>;
   }
   if (KW == 2 && nwt == 4 && prog == 5) return k_child<2, 4, 2, ProgC5>;
   switch (nwt) {
-    case 1: return k_child<KW, 1, 4, PD>;
-    case 2: return k_child<KW, 2, 4, PD>;
+    case 1: return k_child<KW, 1, 2, PD>;
+    case 2: return k_child<KW, 2, 2, PD>;
     case 4: return k_child<KW, 4, 2, PD>;
     case 8: return k_child<KW, 8, 1, PD>;
     case 16: return k_child<KW, 16, 1, PD>;

@@ -74,7 +74,11 @@ __device__ __forceinline__ bool reserve_capacity(const GTable& t) {
   unsigned long long old = atomicAdd(&t.hdr->groups, 1ull);
   if (old < t.cap) return true;
   atomicAdd(&t.hdr->groups, ~0ull);
-  if (*(volatile unsigned long long*)&t.hdr->committed >= t.cap) atomicExch(&t.hdr->frozen, 1);
+  // within a small margin of the capacity a failure is treated as real: near the
+  // limit, thousands of racing reservations would otherwise keep the last slots
+  // transiently saturated and the table would never freeze
+  const unsigned long long margin = t.cap / 32 < 4096ull ? t.cap / 32 : 4096ull;
+  if (*(volatile unsigned long long*)&t.hdr->committed + margin >= t.cap) atomicExch(&t.hdr->frozen, 1);
   atomicExch((int*)&t.hdr->pad, 1);  // some insert was refused (ROUTE: cut the table at close)
   return false;
 }
@@ -406,7 +410,7 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
       int old = atomicAdd(s_groups, 1);
       if (old < cap) return true;  // s_inflight released by the caller after the key CAS
       atomicSub(s_groups, 1);
-      if (*(volatile int*)(s_groups + 1) >= cap) atomicExch(s_frozen, 1);
+      if (*(volatile int*)(s_groups + 1) + max(1, cap / 32) > cap) atomicExch(s_frozen, 1);
     }
     atomicSub(s_inflight, 1);
     return false;
@@ -418,8 +422,7 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
     int won = atomicCAS(s_esc, 0, 1) == 0;
     if (!won) atomicSub(s_groups, 1);
     else atomicAdd(s_groups + 1, 1);
-    __threadfence_block();
-    atomicSub(s_inflight, 1);
+    atomicSub(s_inflight, 1);  // after the CAS: same-thread shared atomics complete in order
     res = won ? R_INSERTED : R_HIT;
     return nslots;
   }
@@ -466,8 +469,7 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
       if (won || same) {
         if (same) atomicSub(s_groups, 1);
         else atomicAdd(s_groups + 1, 1);
-        __threadfence_block();
-        atomicSub(s_inflight, 1);
+        atomicSub(s_inflight, 1);  // after the CAS: same-thread shared atomics complete in order
         res = won ? R_INSERTED : R_HIT;
         return s;
       }
