@@ -19,6 +19,7 @@
 
 #include "../../include/aggb200.h"
 #include "pass.cuh"
+#include "probe.cuh"
 #include "sort.cuh"
 
 using namespace aggb;
@@ -285,6 +286,18 @@ PassCfg pass_kernel(int nwt, int prog) {
   }
 }
 
+// PROBE specialised for one-word keys and one dense 8-byte value column (probe.cuh)
+PassCfg probe_kernel(int prog) {
+  if (prog == 1) return PassCfg{k_probe<4, 512, ProgC1>, 4, 512};
+  if (prog == 2) return PassCfg{k_probe<4, 512, ProgC2>, 4, 512};
+  if (prog == 3) return PassCfg{k_probe<4, 512, ProgC3>, 4, 512};
+  return PassCfg{k_probe<4, 512, PD>, 4, 512};
+}
+
+size_t probe_smem(int P, int bloom_words, int blk) {
+  return (size_t)((bloom_words + 1) & ~1) * 8 + (size_t)(blk / 32) * PQ_RING * 16 + (size_t)P * (16 + 36 + 2) + 64;
+}
+
 template <int KW>
 child_fn child_kernel(int nwt, int prog) {
   // R = 2 records per thread in flight (R = 4 spilled registers at the 64-register
@@ -537,22 +550,29 @@ int launch_pass(Handle* h, PassPlan& pp) {
   int nwt = nwt_for(std::max(payload, 1));
   if (nwt > 32) return fail(AGGB_SPEC_ERROR, "record payload of %d words exceeds 32", payload);
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
-  pass_fn fn = pcfg.fn;
-  int R = pcfg.R, blk = pcfg.blk;
-  int T = R * blk;
   int P = pp.mode == MODE_FILL ? 1 : pp.ss.nparts;
   int G = pp.mode == MODE_FILL ? 1 : group_of(pp.ss.rw);
   int rw = pp.mode == MODE_FILL ? 1 : pp.ss.rw;
+  // k_probe: 16-byte raw records from dense 8-byte columns (and the SoA deferral list)
+  const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 &&
+                          pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 1 && pp.lin_kind == 0)) &&
+                          dense8(pp.col, 1) && !getenv("AGGB_GENERIC_PROBE");
+  const int T_fill = pcfg.R * pcfg.blk;  // tile size of the FILL pass (start_tiles counts its tiles)
+  if (fast_probe) pcfg = probe_kernel(h->prog);
+  pass_fn fn = pcfg.fn;
+  int R = pcfg.R, blk = pcfg.blk;
+  int T = R * blk;
   Bloom bl{nullptr, 0, 0};
   if (pp.mode == MODE_PROBE && h->bloom_words) {
     bl.words = h->bloom.as<uint64_t>();
     bl.mask = (uint32_t)h->bloom_words - 1;
     bl.seed = h->bloom_seed;
   }
-  size_t smem = pass_smem(P, G, rw, bl.words ? h->bloom_words : 0);
+  auto smem_of = [&](int bw) { return fast_probe ? probe_smem(P, bw, blk) : pass_smem(P, G, rw, bw); };
+  size_t smem = smem_of(bl.words ? (int)h->bloom_words : 0);
   if (smem > 227 * 1024 && bl.words) {  // no room: probe without the filter
     bl.words = nullptr;
-    smem = pass_smem(P, G, rw, 0);
+    smem = smem_of(0);
   }
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
   CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -568,7 +588,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.col = pp.col;
   a.col_dense = dense8(pp.col, h->kw) ? 1 : 0;
   a.start_tiles = pp.use_start ? SC(h) + 8 : nullptr;
-  a.start_T = T;
+  a.start_T = T_fill;
   if (pp.lin) {
     a.lin.n = 0;
     for (int w = 0; w < h->kw; w++) {
@@ -603,6 +623,11 @@ int launch_pass(Handle* h, PassPlan& pp) {
     // filled page plus one residual-flush page: at most 2 per record
     uint64_t pairs = std::min<uint64_t>(2ull * grid * P, 2ull * (uint64_t)recs);
     uint64_t pages = (uint64_t)((recs + pp.ss.per_page - 1) / pp.ss.per_page) + pairs + 16;
+    // CTA-local page stash: worth it when a CTA fills several pages per refill
+    // window; each CTA may leave one unused refill behind
+    const uint64_t per_cta = pages / (uint64_t)grid;
+    a.stash = per_cta >= 64 ? 32 : 0;
+    pages += (uint64_t)grid * 2 * a.stash;
     TRY(pool_ensure(h, pages));
     a.pool = pool_of(h);
   }
@@ -769,6 +794,7 @@ int plan(Handle* h) {
   }
   int rw0 = h->kw + h->cs.nv;
   h->P0 = std::min(P, std::min(MAX_PARTS, max_parts_for(rw0)));
+  if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment
   return AGGB_OK;
 }
 

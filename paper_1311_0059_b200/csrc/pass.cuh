@@ -41,6 +41,7 @@ struct PassArgs {
   unsigned long long* defer_count;
   unsigned long long* tile_counter;
   unsigned long long* stats;
+  int32_t stash;                          // pages per CTA-local page-stash refill (0: global atomics only)
 };
 
 template <int KW, int NWT>
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_grab, s_defer_base;
   __shared__ uint32_t s_ndefer;
+  __shared__ uint32_t s_sbase, s_sused, s_scap;  // CTA-local page stash [s_sbase, s_sbase + s_scap)
   __shared__ unsigned long long s_cnt[ST_NSTATS];
 
   const int ns = a.sp.ns;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
 
   if (tid == 0) {
     s_ndefer = 0;
+    s_sbase = s_sused = s_scap = 0;
     s_ntouched[0] = s_ntouched[1] = 0;
     s_grab = grab();
   }
@@ -196,6 +199,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   int par = 0;
   while (cur < total) {
     const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
+    // page-stash refill: phase A never overlaps phase B (the only consumer),
+    // the atomic's latency hides behind this warp's phase A
+    const bool refill = spills && a.stash && tid == 0 && s_scap - min(s_sused, s_scap) < (uint32_t)a.stash / 2;
+    uint32_t ref_first = 0;
+    if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
     // ---- [A] first-bucket loads for the current records
     uint64_t bk[R];
     uint64_t bw[R][4];
@@ -270,6 +278,18 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       }
       __syncwarp();
     }
+    if (refill) {
+      for (uint32_t q = min(s_sused, s_scap); q < s_scap; q++) a.pool.page_set[s_sbase + q] = -1;  // leftover
+      if (ref_first + (uint32_t)a.stash <= a.pool.capacity) {
+        s_sbase = ref_first;
+        s_scap = (uint32_t)a.stash;
+      } else {
+        for (uint32_t q = ref_first; q < min(ref_first + (uint32_t)a.stash, a.pool.capacity); q++)
+          a.pool.page_set[q] = -1;
+        s_scap = 0;
+      }
+      s_sused = 0;
+    }
     __syncthreads();
     // ---- [B] per touched partition: reserve whole sector groups, drain the residual
     if (spills) {
@@ -291,7 +311,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         pnew[p] = -1;
         if (e > room) {
           int need = (e - room + S - 1) / S;
-          uint32_t first = atomicAdd(a.pool.next_page, (uint32_t)need);
+          uint32_t first;
+          const uint32_t off = atomicAdd(&s_sused, (uint32_t)need);
+          if (off + need <= s_scap) {
+            first = s_sbase + off;
+          } else {  // the stash cannot serve it: release the part taken (disjoint per taker)
+            for (uint32_t q = off; q < min(off + (uint32_t)need, s_scap); q++) a.pool.page_set[s_sbase + q] = -1;
+            first = atomicAdd(a.pool.next_page, (uint32_t)need);
+          }
           if (first + need > a.pool.capacity) {
             atomicExch(a.pool.overflow, 1u);
             pcur[p] = -1;
@@ -378,6 +405,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     }
   }
   __syncthreads();
+  if (spills)
+    for (uint32_t q = min(s_sused, s_scap) + tid; q < s_scap; q += B) a.pool.page_set[s_sbase + q] = -1;
   // drain the residuals (partial sectors, once per partition) and seal the pages
   if (spills) {
     for (int p = tid; p < P; p += B) {
