@@ -295,7 +295,7 @@ PassCfg probe_kernel(int prog) {
 }
 
 size_t probe_smem(int P, int bloom_words, int blk) {
-  return (size_t)((bloom_words + 1) & ~1) * 8 + (size_t)(blk / 32) * PQ_RING * 16 + (size_t)P * (16 + 36 + 2) + 64;
+  return (size_t)((bloom_words + 1) & ~1) * 8 + (size_t)(blk / 32) * PQ_RING * 16 + (size_t)P * (4 + 4 * 8) + 64;
 }
 
 template <int KW>
@@ -556,7 +556,11 @@ int launch_pass(Handle* h, PassPlan& pp) {
   // k_probe: 16-byte raw records from dense 8-byte columns (and the SoA deferral list)
   const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 &&
                           pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 1 && pp.lin_kind == 0)) &&
-                          dense8(pp.col, 1) && !getenv("AGGB_GENERIC_PROBE");
+                          dense8(pp.col, 1) && pp.ss.per_page == 512 &&
+                          // page ids are 24-bit in k_probe's page map (conservative pool estimate)
+                          h->pool_bound + (uint64_t)(pp.col.n + pp.lin_stride) / 256 +
+                                  (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
+                          !getenv("AGGB_GENERIC_PROBE");
   const int T_fill = pcfg.R * pcfg.blk;  // tile size of the FILL pass (start_tiles counts its tiles)
   if (fast_probe) pcfg = probe_kernel(h->prog);
   pass_fn fn = pcfg.fn;

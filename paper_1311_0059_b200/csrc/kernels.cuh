@@ -184,8 +184,11 @@ struct Bloom {
 };
 
 __device__ __forceinline__ uint64_t bloom_bits(uint64_t h) {
-  return (1ull << ((h >> 32) & 63)) | (1ull << ((h >> 38) & 63)) | (1ull << ((h >> 44) & 63)) |
-         (1ull << ((h >> 50) & 63));
+  // four bits of the 64-bit block, two per 32-bit half (32-bit shifts only)
+  const uint32_t x = (uint32_t)(h >> 32);
+  const uint32_t lo = (1u << (x & 31)) | (1u << ((x >> 5) & 31));
+  const uint32_t hi = (1u << ((x >> 10) & 31)) | (1u << ((x >> 15) & 31));
+  return ((uint64_t)hi << 32) | lo;
 }
 
 // The filter is keyed off the table's own hash (k_pass derives bucket, spill

@@ -22,23 +22,25 @@ namespace aggb {
 
 constexpr int PQ_RING = 64;  // per-warp ring of bloom-positive records (two rounds of 32)
 
+// Resolve key k (value v) against the frozen table: aggregate with L2 atomics if
+// resident.  The first bucket (b, x, y) was loaded by the caller.
 template <class PG>
-__device__ __forceinline__ bool probe_resolve(const PassArgs& a, uint64_t k, uint64_t v, const uint32_t* s_fd, int ns) {
+__device__ __forceinline__ bool probe_finish(const PassArgs& a, uint64_t k, uint64_t v, uint64_t b, ulonglong2 x,
+                                             ulonglong2 y, const uint32_t* s_fd, int ns) {
   int64_t s = -1;
   if (k == EMPTY) {  // escape slot: the key whose word equals the sentinel
     if (*(volatile int*)&a.t.hdr->esc) s = (int64_t)a.t.mask + 1;
   } else {
-    const uint64_t kk[1] = {k};
-    uint64_t b = hash_key<1>(kk, a.t.seed) & a.t.bmask;
     for (;;) {
-      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
-      const ulonglong2 x = __ldcg(p), y = __ldcg(p + 1);
       if (x.x == k) { s = (int64_t)(b * 4); break; }
       if (x.y == k) { s = (int64_t)(b * 4 + 1); break; }
       if (y.x == k) { s = (int64_t)(b * 4 + 2); break; }
       if (y.y == k) { s = (int64_t)(b * 4 + 3); break; }
       if ((x.x == EMPTY) | (x.y == EMPTY) | (y.x == EMPTY) | (y.y == EMPTY)) break;
       b = (b + 1) & a.t.bmask;
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
+      x = __ldcg(p);
+      y = __ldcg(p + 1);
     }
   }
   if (s < 0) return false;
@@ -47,30 +49,41 @@ __device__ __forceinline__ bool probe_resolve(const PassArgs& a, uint64_t k, uin
   return true;
 }
 
+__device__ __forceinline__ void probe_issue(const PassArgs& a, uint64_t k, uint64_t& b, ulonglong2& x, ulonglong2& y) {
+  const uint64_t kk[1] = {k};
+  b = hash_key<1>(kk, a.t.seed) & a.t.bmask;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
+  x = __ldcg(p);
+  y = __ldcg(p + 1);
+}
+
+// Spill layout: each CTA appends a partition's records to its own chain of
+// 8 KB pages (512 records).  A record claims its index in the chain with one
+// shared-memory atomic (cnt[p]); the claimer of a page's first slot allocates
+// the page (from a CTA-local stash) and publishes it in the partition's page
+// map ent[p][j mod 8] tagged with j; everyone else writes straight into the
+// page the map names.  A record whose page is not published yet (its
+// allocator is still in flight) is written after the tile's barrier, when
+// every allocation of the tile is visible.  8 map entries cover a tile: a map
+// entry is reused only 7 pages (3584 records) later, more than a tile holds.
 template <int R, int BLK, class PG>
 __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   constexpr int T = R * BLK, NWARP = BLK / 32;
+  constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
+  constexpr int NE = 8;                   // page-map entries per partition
+  static_assert((NE - 1) * S >= T, "a page-map entry must outlive a tile");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int P = a.ss.nparts, S = a.ss.per_page;
+  const int P = a.ss.nparts;
   const int nbw = a.bloom.words ? (int)a.bloom.mask + 1 : 0;
   uint64_t* sbloom = (uint64_t*)smem;
   ulonglong2* ring = (ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + wid * PQ_RING;  // this warp's ring (16-B aligned)
-  ulonglong2* resid = (ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + NWARP * PQ_RING;  // P: one pending record each
-  uint32_t* hist = (uint32_t*)(resid + P);
-  int32_t* pcur = (int32_t*)(hist + P);
-  int32_t* pfill = pcur + P;
-  int32_t* bpg = pfill + P;
-  int32_t* bslot = bpg + P;
-  int32_t* pnew = bslot + P;
-  uint32_t* rcnt = (uint32_t*)(pnew + P);
-  uint32_t* rprev = rcnt + P;
-  uint32_t* emitn = rprev + P;
-  uint16_t* touched = (uint16_t*)(emitn + P);
-  __shared__ uint32_t s_ntouched[2];
+  uint32_t* cnt = (uint32_t*)((ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + NWARP * PQ_RING);  // P
+  uint32_t* ent = cnt + P;                                                                 // P * NE
+  __shared__ uint32_t s_hm[NWARP][R];
   __shared__ uint32_t s_fd[MAX_STATES];
-  __shared__ unsigned long long s_grab;
-  __shared__ uint32_t s_sbase, s_sused, s_scap;
+  __shared__ unsigned long long s_grab[2];
+  __shared__ uint32_t s_sb[2], s_su[2], s_sc[2];  // page stash by tile parity: base, used, capacity
   __shared__ unsigned long long s_cnt[ST_NSTATS];
 
   const int64_t n = a.col.n;
@@ -79,18 +92,15 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   const int64_t col_tiles = (n - col_start + T - 1) / T;
   const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
   const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
-  if (total == 0) return;  // FILL took the whole batch: no spill state to seal
+  if (total == 0) return;  // FILL took the whole batch: nothing to spill
 
   const int ns = a.sp.ns;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
-  for (int p = tid; p < P; p += BLK) {
-    hist[p] = 0;
-    pcur[p] = -1;
-    pfill[p] = S;
-    rcnt[p] = 0;
-  }
+  for (int p = tid; p < P; p += BLK) cnt[p] = 0;
+  for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
   for (int i = tid; i < nbw; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom.words + i);
+  uint64_t* const pool = (uint64_t*)a.pool.base;
 
   auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R], uint64_t (&v)[R], bool (&live)[R]) {
     const int src = (int64_t)tile < col_tiles ? 0 : 1;
@@ -108,43 +118,39 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       }
     }
   };
-  auto emit_at = [&](int p, int pos, int32_t& pg, int& slot) -> bool {
-    const int room = S - bslot[p];
-    if (pos < room) {
-      pg = bpg[p];
-      slot = bslot[p] + pos;
-      return pg >= 0;
-    }
-    if (pnew[p] < 0) return false;
-    const int j = pos - room;
-    pg = pnew[p] + j / S;
-    slot = j % S;
-    return true;
+  auto put = [&](uint32_t pg, uint32_t slot, uint64_t k, uint64_t v) {
+    if (pg < 0xFFFFFFu) __stcg((ulonglong2*)(pool + (((size_t)pg << SLOG) + slot) * 2), make_ulonglong2(k, v));
   };
 
+  // tiles are grabbed two ahead: s_grab[t & 1] holds the index of this CTA's tile t
   if (tid == 0) {
-    s_sbase = s_sused = s_scap = 0;
-    s_ntouched[0] = s_ntouched[1] = 0;
-    s_grab = atomicAdd(a.tile_counter, 1ull);
+    s_sb[0] = s_sb[1] = s_su[0] = s_su[1] = s_sc[0] = s_sc[1] = 0;
+    s_grab[0] = atomicAdd(a.tile_counter, 1ull);
+    s_grab[1] = atomicAdd(a.tile_counter, 1ull);
   }
   __syncthreads();
-  unsigned long long cur = s_grab;
-  __syncthreads();
-  if (tid == 0) s_grab = (cur < total) ? atomicAdd(a.tile_counter, 1ull) : ~0ull;
+  unsigned long long cur = s_grab[0], nxt = s_grab[1];
   uint64_t kc[R], vc[R];
   bool lc[R];
   load_tile(cur, kc, vc, lc);
-  __syncthreads();
-  unsigned long long nxt = s_grab;
 
   uint32_t c_hit = 0, c_rec = 0, c_sp = 0;
   int par = 0;
   const uint32_t lt_mask = (1u << lane) - 1u;
   while (cur < total) {
-    const bool refill = a.stash && tid == 0 && s_scap - min(s_sused, s_scap) < (uint32_t)a.stash / 2;
+    // thread 0 grabs tile t + 2 (into s_grab[t & 1], read by all before the last
+    // barrier) and refills the other parity's page stash (idle during this tile);
+    // the atomics' latency hides behind phase A
+    unsigned long long g_next = 0;
     uint32_t ref_first = 0;
-    if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
-    // ---- [A] classify: hash once, partition from the high bits, bloom from a remix
+    bool refill = false;
+    if (tid == 0) {
+      g_next = atomicAdd(a.tile_counter, 1ull);
+      const int q = par ^ 1;
+      refill = a.stash && s_sc[q] - min(s_su[q], s_sc[q]) < (uint32_t)a.stash / 2;
+      if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
+    }
+    // ---- [A] classify: one hash; partition from its high bits, bloom from a remix
     int part[R];
     uint32_t seq[R];  // ring sequence number of a bloom-positive record, ~0u otherwise
 #pragma unroll
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       if (nbw && kc[r] != EMPTY) {
         const uint64_t hb = bloom_remix(h);
         const uint64_t bits = bloom_bits(hb);
-        posv = posv && (sbloom[(hb >> 8) & a.bloom.mask] & bits) == bits;
+        posv = posv && (sbloom[(uint32_t)(hb >> 8) & a.bloom.mask] & bits) == bits;
       }
       seq[r] = posv ? 0u : ~0u;
     }
@@ -165,10 +171,21 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
     bool ln[R];
     load_tile(nxt, kn, vn, ln);
     // ---- resolve the bloom positives 32 at a time
-    uint32_t hm[R];  // hit mask of round q (records with seq in [32q, 32q + 32))
-#pragma unroll
-    for (int q = 0; q < R; q++) hm[q] = 0;
     uint32_t qt = 0, qh = 0;  // warp-uniform ring tail / head
+    auto round = [&](uint32_t cnt_in) {  // resolve ring entries [qh, qh + cnt_in)
+      __syncwarp();
+      bool hit = false;
+      if (lane < (int)cnt_in) {
+        const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
+        uint64_t b = 0;
+        ulonglong2 x = make_ulonglong2(0, 0), y = x;
+        if (e.x != EMPTY) probe_issue(a, e.x, b, x, y);
+        hit = probe_finish<PG>(a, e.x, e.y, b, x, y, s_fd, ns);
+      }
+      const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) s_hm[wid][qh >> 5] = hb;
+      __syncwarp();
+    };
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const bool posv = seq[r] == 0u;
@@ -179,144 +196,89 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       }
       qt += __popc(m);
       if (qt - qh >= 32) {
-        __syncwarp();
-        const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
-        const bool hit = probe_resolve<PG>(a, e.x, e.y, s_fd, ns);
-        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-#pragma unroll
-        for (int q = 0; q < R; q++)
-          if ((int)(qh >> 5) == q) hm[q] = hb;
+        round(32);
         qh += 32;
-        __syncwarp();
       }
     }
-    if (qt != qh) {
-      __syncwarp();
-      bool hit = false;
-      if (lane < (int)(qt - qh)) {
-        const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
-        hit = probe_resolve<PG>(a, e.x, e.y, s_fd, ns);
-      }
-      const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-#pragma unroll
-      for (int q = 0; q < R; q++)
-        if ((int)(qh >> 5) == q) hm[q] = hb;
-      __syncwarp();
-    }
-    // ---- claim spill ranks
-    uint32_t tag[R];  // (p << 16 | rank) + 1, 0 = nothing to write
+    if (qt != qh) round(qt - qh);
+    __syncwarp();
+    // ---- claim chain positions and write the spilled records
+    uint32_t pend = 0, pidx[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      tag[r] = 0;
+      pidx[r] = 0;
       c_rec += lc[r];
       bool spill = lc[r];
       if (seq[r] != ~0u) {
-        uint32_t m = 0;
-#pragma unroll
-        for (int q = 0; q < R; q++)
-          if ((int)(seq[r] >> 5) == q) m = hm[q];
-        const bool hit = (m >> (seq[r] & 31)) & 1u;
+        const bool hit = (s_hm[wid][seq[r] >> 5] >> (seq[r] & 31)) & 1u;
         c_hit += hit;
         spill = !hit;
       }
-      if (spill) {
-        const uint32_t rank = atomicAdd(&hist[part[r]], 1u);
-        if (rank == 0) touched[atomicAdd(&s_ntouched[par], 1u)] = (uint16_t)part[r];
-        tag[r] = (((uint32_t)part[r] << 16) | rank) + 1u;
-        c_sp++;
-      }
-    }
-    if (refill) {
-      for (uint32_t q = min(s_sused, s_scap); q < s_scap; q++) a.pool.page_set[s_sbase + q] = -1;
-      if (ref_first + (uint32_t)a.stash <= a.pool.capacity) {
-        s_sbase = ref_first;
-        s_scap = (uint32_t)a.stash;
-      } else {
-        for (uint32_t q = ref_first; q < min(ref_first + (uint32_t)a.stash, a.pool.capacity); q++)
-          a.pool.page_set[q] = -1;
-        s_scap = 0;
-      }
-      s_sused = 0;
-    }
-    __syncthreads();
-    // ---- [B] per touched partition: reserve whole sectors (pairs), drain the residual
-    {
-      const int nt = (int)s_ntouched[par];
-      for (int ti = tid; ti < nt; ti += BLK) {
-        const int p = touched[ti];
-        const int c = (int)hist[p];
-        hist[p] = 0;
-        const int r0 = (int)rcnt[p];
-        const int t = r0 + c;
-        const int e = t & ~1;
-        rprev[p] = (uint32_t)r0;
-        emitn[p] = (uint32_t)e;
-        rcnt[p] = (uint32_t)(t & 1);
-        if (!e) continue;
-        const int room = S - pfill[p];
-        bpg[p] = pcur[p];
-        bslot[p] = pfill[p];
-        pnew[p] = -1;
-        if (e > room) {
-          const int need = (e - room + S - 1) / S;
-          uint32_t first;
-          const uint32_t off = atomicAdd(&s_sused, (uint32_t)need);
-          if (off + need <= s_scap) {
-            first = s_sbase + off;
-          } else {
-            for (uint32_t q = off; q < min(off + (uint32_t)need, s_scap); q++) a.pool.page_set[s_sbase + q] = -1;
-            first = atomicAdd(a.pool.next_page, (uint32_t)need);
-          }
-          if (first + need > a.pool.capacity) {
-            atomicExch(a.pool.overflow, 1u);
-            pcur[p] = -1;
-            pfill[p] = S;
-          } else {
-            for (int q = 0; q < need; q++) {
-              a.pool.page_part[first + q] = p;
-              a.pool.page_set[first + q] = a.ss.id;
-              a.pool.page_fill[first + q] = S;
-            }
-            pnew[p] = (int32_t)first;
-            pcur[p] = (int32_t)(first + need - 1);
-            pfill[p] = (e - room) - (need - 1) * S;
-          }
-          if (bpg[p] >= 0) a.pool.page_fill[bpg[p]] = S;
+      if (!spill) continue;
+      c_sp++;
+      const int p = part[r];
+      const uint32_t idx = atomicAdd(&cnt[p], 1u);
+      const uint32_t j = idx >> SLOG, slot = idx & (S - 1);
+      uint32_t* ep = &ent[p * NE + (j & (NE - 1))];
+      uint32_t pg;
+      if (slot == 0) {  // first record of page j: allocate it and publish it
+        const uint32_t off = atomicAdd(&s_su[par], 1u);
+        if (off < s_sc[par]) {
+          pg = s_sb[par] + off;
         } else {
-          pfill[p] += e;
+          pg = atomicAdd(a.pool.next_page, 1u);
+          if (pg >= a.pool.capacity) {
+            atomicExch(a.pool.overflow, 1u);
+            pg = 0xFFFFFFu;
+          }
         }
-        if (r0) {  // the pending record leads this tile's emission
-          int32_t pg;
-          int slot;
-          if (emit_at(p, 0, pg, slot)) *((ulonglong2*)page_ptr(a.pool, (uint32_t)pg) + slot) = resid[p];
+        if (pg < 0xFFFFFFu) {
+          a.pool.page_part[pg] = p;
+          a.pool.page_set[pg] = a.ss.id;
+          a.pool.page_fill[pg] = S;
         }
+        *(volatile uint32_t*)ep = (pg << 8) | (j & 0xFFu);
+      } else {
+        const uint32_t e = *(volatile uint32_t*)ep;
+        pg = ((e & 0xFFu) == (j & 0xFFu)) ? (e >> 8) : 0xFFFFFFFFu;
+      }
+      if (pg == 0xFFFFFFFFu) {
+        pend |= 1u << r;
+        pidx[r] = idx;
+      } else {
+        put(pg, slot, kc[r], vc[r]);
       }
     }
     if (tid == 0) {
-      s_grab = (nxt < total) ? atomicAdd(a.tile_counter, 1ull) : ~0ull;
-      s_ntouched[par ^ 1] = 0;
-    }
-    __syncthreads();
-    // ---- [C] write the spilled records from registers
-#pragma unroll
-    for (int r = 0; r < R; r++) {
-      uint32_t tg = tag[r];
-      if (!tg) continue;
-      tg -= 1u;
-      const int p = (int)(tg >> 16);
-      const int pos = (int)rprev[p] + (int)(tg & 0xFFFFu);
-      const ulonglong2 rec = make_ulonglong2(kc[r], vc[r]);
-      if (pos < (int)emitn[p]) {
-        int32_t pg;
-        int slot;
-        if (emit_at(p, pos, pg, slot)) *((ulonglong2*)page_ptr(a.pool, (uint32_t)pg) + slot) = rec;
-      } else {
-        resid[p] = rec;
+      s_grab[par] = g_next;
+      if (refill) {
+        const int q = par ^ 1;
+        for (uint32_t x = min(s_su[q], s_sc[q]); x < s_sc[q]; x++) a.pool.page_set[s_sb[q] + x] = -1;
+        const bool fits = ref_first + (uint32_t)a.stash <= a.pool.capacity;
+        if (!fits)
+          for (uint32_t x = ref_first; x < min(ref_first + (uint32_t)a.stash, a.pool.capacity); x++)
+            a.pool.page_set[x] = -1;
+        s_sb[q] = ref_first;
+        s_sc[q] = fits ? (uint32_t)a.stash : 0u;
+        s_su[q] = 0;
       }
     }
-    par ^= 1;
+    __syncthreads();
+    // ---- records whose page was published by another thread after they looked
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if (!((pend >> r) & 1u)) continue;
+      const uint32_t idx = pidx[r], j = idx >> SLOG;
+      const uint32_t e = ent[part[r] * NE + (j & (NE - 1))];
+      if ((e & 0xFFu) != (j & 0xFFu)) {
+        atomicExch(a.pool.overflow, 3u);  // cannot happen: the allocation precedes the barrier
+        continue;
+      }
+      put(e >> 8, idx & (S - 1), kc[r], vc[r]);
+    }
     cur = nxt;
-    nxt = s_grab;
+    nxt = s_grab[par];
+    par ^= 1;
 #pragma unroll
     for (int r = 0; r < R; r++) {
       lc[r] = ln[r];
@@ -325,27 +287,16 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
     }
   }
   __syncthreads();
-  for (uint32_t q = min(s_sused, s_scap) + tid; q < s_scap; q += BLK) a.pool.page_set[s_sbase + q] = -1;
-  // flush the pending records (one per partition at most) and seal the pages
+  // seal: the last page of every chain holds cnt mod S records; unused stash pages leave the set
   for (int p = tid; p < P; p += BLK) {
-    if (rcnt[p]) {
-      if (S - pfill[p] < 1) {
-        const uint32_t pg = atomicAdd(a.pool.next_page, 1u);
-        if (pg >= a.pool.capacity) {
-          atomicExch(a.pool.overflow, 1u);
-          continue;
-        }
-        a.pool.page_part[pg] = p;
-        a.pool.page_set[pg] = a.ss.id;
-        if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
-        pcur[p] = (int32_t)pg;
-        pfill[p] = 0;
-      }
-      *((ulonglong2*)page_ptr(a.pool, (uint32_t)pcur[p]) + pfill[p]) = resid[p];
-      pfill[p] += 1;
-    }
-    if (pcur[p] >= 0) a.pool.page_fill[pcur[p]] = pfill[p];
+    const uint32_t c = cnt[p];
+    if (!c) continue;
+    const uint32_t j = (c - 1) >> SLOG;
+    const uint32_t e = ent[p * NE + (j & (NE - 1))];
+    if ((e >> 8) < 0xFFFFFFu) a.pool.page_fill[e >> 8] = (int32_t)(c - (j << SLOG));
   }
+  for (int q = 0; q < 2; q++)
+    for (uint32_t x = min(s_su[q], s_sc[q]) + tid; x < s_sc[q]; x += BLK) a.pool.page_set[s_sb[q] + x] = -1;
   if (c_sp) atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
   uint32_t cs[3] = {c_sp, c_hit, c_rec};
   const int ids[3] = {ST_SPILLED, ST_HITS, ST_RECORDS};
