@@ -1137,7 +1137,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     h->met.spilled_partitions += nonempty;
     if (!nonempty) return AGGB_OK;
     h->met.recursion_depth = std::max<int64_t>(h->met.recursion_depth, depth + 1);
-    TRY(h->plist.ensure((size_t)tot * 4, &h->hw));
+    TRY(h->plist.ensure((size_t)tot * 8, &h->hw));
     TRY(h->item_off.ensure(item_off.size() * 8, &h->hw));
     CU(cudaMemcpyAsync(h->cursor.p, offs.data(), (size_t)nparts * 4 * nsets, cudaMemcpyHostToDevice, h->st));
     CU(cudaMemcpyAsync(h->item_off.p, item_off.data(), item_off.size() * 8, cudaMemcpyHostToDevice, h->st));
@@ -1145,7 +1145,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     for (int q = 0; q < nsets; q++) {
       int pe = prof_begin(h, 7);
       k_page_scatter<<<hg, 256, 0, h->st>>>(pp, first, last, sets[q].ss.id, nparts,
-                                             h->cursor.as<uint32_t>() + (size_t)q * nparts, h->plist.as<int32_t>());
+                                             h->cursor.as<uint32_t>() + (size_t)q * nparts, h->plist.as<uint2>());
       prof_end(h, pe);
       h->launches++;
     }
@@ -1177,7 +1177,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     ca.pool = pp;
     ca.sets[0] = a.ss;
     ca.sets[1] = b_live ? b.ss : a.ss;
-    ca.plist = h->plist.as<int32_t>();
+    ca.plist = h->plist.as<uint2>();
     ca.item_off = h->item_off.as<int64_t>();
     ca.nitems = nonempty;
     ca.slots_log2 = h->child_slots_log2;

@@ -430,8 +430,48 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
     return nslots;
   }
   int mask = nslots - 1;
-  int s = (int)(hash_key<KW>(k, seed) & (uint64_t)mask);
   bool reserved = false;
+  if (KW == 1) {
+    // slots probed in aligned pairs, one 16-byte shared load per pair; the probe
+    // sequence starts at the pair of the home slot (inserts and lookups agree)
+    int s = (int)(hash_key<KW>(k, seed) & (uint64_t)mask) & ~1;
+    for (;;) {
+      uint64_t w0, w1;
+      asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(w0), "=l"(w1)
+                   : "r"((uint32_t)__cvta_generic_to_shared(keys + s)));
+      int at = -1;
+      if (w0 == k[0]) at = s;
+      else if (w1 == k[0]) at = s + 1;
+      if (at >= 0) {
+        if (reserved) {
+          atomicSub(s_groups, 1);
+          atomicSub(s_inflight, 1);
+        }
+        res = R_HIT;
+        return at;
+      }
+      const int e = (w0 == EMPTY) ? s : ((w1 == EMPTY) ? s + 1 : -1);
+      if (e >= 0) {
+        if (!insert) { res = R_MISS; return -1; }
+        if (!reserved) {
+          if (!reserve()) { res = R_REFUSED; return -1; }
+          reserved = true;
+        }
+        const unsigned long long prev = atomicCAS((unsigned long long*)(keys + e), EMPTY, k[0]);
+        if (prev == EMPTY || prev == k[0]) {
+          if (prev == k[0]) atomicSub(s_groups, 1);
+          else atomicAdd(s_groups + 1, 1);
+          atomicSub(s_inflight, 1);  // after the CAS: same-thread shared atomics complete in order
+          res = prev == EMPTY ? R_INSERTED : R_HIT;
+          return e;
+        }
+        continue;  // another key took the slot: re-read the pair
+      }
+      s = (s + 2) & mask;
+    }
+  }
+  int s = (int)(hash_key<KW>(k, seed) & (uint64_t)mask);
   for (;;) {
     uint64_t* kp = keys + (size_t)s * KW;
     uint64_t w0 = *(volatile uint64_t*)kp;
@@ -517,7 +557,7 @@ __global__ void k_page_hist(PagePool pool, uint32_t first, const uint32_t* last_
 }
 
 __global__ void k_page_scatter(PagePool pool, uint32_t first, const uint32_t* last_ptr, int set_id, int nparts,
-                               uint32_t* cursor /* exclusive offsets, advanced */, int32_t* plist) {
+                               uint32_t* cursor /* exclusive offsets, advanced */, uint2* plist) {
   uint32_t last = min(*last_ptr, pool.capacity);
   for (uint32_t pg = first + blockIdx.x * blockDim.x + threadIdx.x; pg < last; pg += gridDim.x * blockDim.x) {
     if (pool.page_set[pg] != set_id) continue;
@@ -525,7 +565,7 @@ __global__ void k_page_scatter(PagePool pool, uint32_t first, const uint32_t* la
     if (p < 0 || p >= nparts) continue;
     if (pool.page_fill[pg] == 0) continue;
     uint32_t at = atomicAdd(&cursor[p], 1u);
-    plist[at] = (int32_t)pg;
+    plist[at] = make_uint2(pg, (uint32_t)pool.page_fill[pg]);  // fill travels with the id
   }
 }
 

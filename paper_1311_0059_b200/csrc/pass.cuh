@@ -457,7 +457,7 @@ struct ChildArgs {
   DevSpec sp;
   PagePool pool;
   SpillSet sets[2];         // pages of item i: sets[0] in [off[2i], off[2i+1]), sets[1] in [off[2i+1], off[2i+2])
-  const int32_t* plist;     // page ids, grouped by item (set 0 pages first)
+  const uint2* plist;       // {page id, records in it}, grouped by item (set 0 pages first)
   const int64_t* item_off;  // [2 * nitems + 1]
   int32_t nitems;
   int32_t slots_log2;       // SMEM table slots
@@ -529,8 +529,9 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
           int64_t q = q0 + (int64_t)r * ppr + prow;
           live[r] = false;
           if (prow < ppr && q < qb) {
-            uint32_t pg = (uint32_t)a.plist[q];
-            if (slot < a.pool.page_fill[pg]) {
+            const uint2 pe = a.plist[q];
+            const uint32_t pg = pe.x;
+            if (slot < (int)pe.y) {
               live[r] = true;
               const uint64_t* src = (const uint64_t*)page_ptr(a.pool, pg) + (size_t)slot * rw;
 #pragma unroll
