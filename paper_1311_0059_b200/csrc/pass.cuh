@@ -492,6 +492,8 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
   __shared__ unsigned long long s_item;
   __shared__ unsigned long long s_cnt[ST_NSTATS];
   __shared__ uint32_t s_fd[MAX_STATES];
+  constexpr int CHP = 512;  // pages staged per chunk
+  __shared__ uint32_t s_pg[CHP], s_off[CHP], s_scr[33];
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
   uint32_t nrec = 0, novf = 0;
@@ -519,21 +521,29 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
       const int kind = ss.kind;
       const int nw = ss.rw - KW;
       const int rw = ss.rw;
-      const int S = ss.per_page;
-      const int ppr = B / S;  // pages per row
-      const int prow = tid / S, slot = tid % S;
-      const int64_t per_round = (int64_t)R * ppr;
-      auto load_round = [&](int64_t q0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
+      // the item's records, concatenated over its pages, map onto the threads
+      // (CTA-private page chains leave most pages partly filled: a page-per-row
+      // mapping idled the high warps).  Pages are staged CHP at a time: ids and
+      // exclusive record offsets in shared memory, one forward cursor per thread.
+      for (int64_t c0 = qa; c0 < qb; c0 += CHP) {
+        const int np = (int)min((int64_t)CHP, qb - c0);
+        __syncthreads();  // the previous chunk's readers are done with s_pg / s_off
+        for (int q = tid; q < np; q += B) {
+          const uint2 pe = a.plist[c0 + q];
+          s_pg[q] = pe.x;
+          s_off[q] = pe.y;
+        }
+        __syncthreads();
+        const uint32_t tot = block_exscan(s_off, np, s_scr);
+        int cur = 0;
+        auto load_round = [&](uint32_t i0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
 #pragma unroll
-        for (int r = 0; r < R; r++) {
-          int64_t q = q0 + (int64_t)r * ppr + prow;
-          live[r] = false;
-          if (prow < ppr && q < qb) {
-            const uint2 pe = a.plist[q];
-            const uint32_t pg = pe.x;
-            if (slot < (int)pe.y) {
-              live[r] = true;
-              const uint64_t* src = (const uint64_t*)page_ptr(a.pool, pg) + (size_t)slot * rw;
+          for (int r = 0; r < R; r++) {
+            const uint32_t i = i0 + (uint32_t)(r * B + tid);
+            live[r] = i < tot;
+            if (live[r]) {
+              while (cur + 1 < np && s_off[cur + 1] <= i) cur++;
+              const uint64_t* src = (const uint64_t*)page_ptr(a.pool, s_pg[cur]) + (size_t)(i - s_off[cur]) * rw;
 #pragma unroll
               for (int w = 0; w < KW; w++) k[r][w] = __ldcs((const unsigned long long*)src + w);
 #pragma unroll
@@ -541,45 +551,46 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
                 v[r][w] = (w < nw) ? (uint64_t)__ldcs((const unsigned long long*)src + KW + w) : 0ull;
             }
           }
-        }
-      };
-      uint64_t kc[R][KW], vc[R][NWT];
-      bool lc[R];
-      load_round(qa, kc, vc, lc);
-      for (int64_t q0 = qa; q0 < qb; q0 += per_round) {
-        uint64_t kn[R][KW], vn[R][NWT];
-        bool ln[R];
-        load_round(q0 + per_round, kn, vn, ln);
+        };
+        uint64_t kc[R][KW], vc[R][NWT];
+        bool lc[R];
+        load_round(0, kc, vc, lc);
+        for (uint32_t i0 = 0; i0 < tot; i0 += (uint32_t)(R * B)) {
+          uint64_t kn[R][KW], vn[R][NWT];
+          bool ln[R];
+          load_round(i0 + (uint32_t)(R * B), kn, vn, ln);
 #pragma unroll
-        for (int r = 0; r < R; r++) {
-          int res = R_MISS, s = -1;
-          if (lc[r]) {
-            nrec++;
-            s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, s_groups, &s_frozen, &s_esc,
-                                  &s_inflight, res);
-            if (res == R_REFUSED)
-              s = stable_resolve_refused<KW>(skeys, nslots, a.cap, kc[r], a.seed, s_groups, &s_frozen, &s_esc,
-                                             &s_inflight, res);
+          for (int r = 0; r < R; r++) {
+            int res = R_MISS, s = -1;
+            if (lc[r]) {
+              nrec++;
+              s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, s_groups, &s_frozen, &s_esc,
+                                    &s_inflight, res);
+              if (res == R_REFUSED)
+                s = stable_resolve_refused<KW>(skeys, nslots, a.cap, kc[r], a.seed, s_groups, &s_frozen, &s_esc,
+                                               &s_inflight, res);
+            }
+            __syncwarp();  // reconverge after the divergent probe before the updates
+            if (res == R_HIT || res == R_INSERTED) {
+              Upd<PG>::template sm<NWT>(sst, stride, s, kind, s_fd, ns, vc[r]);
+            } else if (lc[r]) {  // not resident: the next recursion level
+              unsigned long long d = atomicAdd(a.ovf_count, 1ull);
+              novf++;
+#pragma unroll
+              for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
+              for (int j = 0; j < ns; j++)
+                a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
+            }
+            __syncwarp();
           }
-          __syncwarp();  // reconverge after the divergent probe before the updates
-          if (res == R_HIT || res == R_INSERTED) {
-            Upd<PG>::template sm<NWT>(sst, stride, s, kind, s_fd, ns, vc[r]);
-          } else if (lc[r]) {  // not resident: the next recursion level
-            unsigned long long d = atomicAdd(a.ovf_count, 1ull);
-            novf++;
 #pragma unroll
-            for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
-            for (int j = 0; j < ns; j++) a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
+          for (int r = 0; r < R; r++) {
+            lc[r] = ln[r];
+#pragma unroll
+            for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
+#pragma unroll
+            for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
           }
-          __syncwarp();
-        }
-#pragma unroll
-        for (int r = 0; r < R; r++) {
-          lc[r] = ln[r];
-#pragma unroll
-          for (int w = 0; w < KW; w++) kc[r][w] = kn[r][w];
-#pragma unroll
-          for (int w = 0; w < NWT; w++) vc[r][w] = vn[r][w];
         }
       }
     }
