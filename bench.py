@@ -54,6 +54,8 @@ class Clocks:
         self.p = None
 
     def __enter__(self):
+        import threading
+        self.lines = []
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -61,18 +63,33 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+            return self
+        self.first = threading.Event()
+
+        def reader():
+            for ln in self.p.stdout:
+                if ln.strip():
+                    self.lines.append(ln)
+                    self.first.set()
+        self.t = threading.Thread(target=reader, daemon=True)
+        self.t.start()
         return self
 
+    def wait_sampling(self, timeout=5.0):
+        """Block until the sampler is up (NVML initialised), so its start-up
+        does not overlap the timed region."""
+        if self.p is not None:
+            self.first.wait(timeout)
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.p is not None:
             time.sleep(0.15)
             self.p.terminate()
             try:
-                out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
-                out = ""
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+                pass
+            self.t.join(timeout=2)
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
@@ -203,27 +220,35 @@ def run_ours(args, rank, world, device):
         if xg is not None:
             xg.run()
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    g.profile(True)
-    launches = 0
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(device.index) as clk:
+    clk = Clocks(device.index)
+    with clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        clk.wait_sampling()
+        launches = 0
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
             step()
             launches += g.metrics()["kernel_launches"]
         e1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    ks = g.kernel_stats()
+        if world > 1:
+            torch.distributed.barrier()
+        ms = e0.elapsed_time(e1) / args.steps
+        # per-kernel durations: the same K steps again with a CUDA event pair around
+        # every launch (kept out of the region above: the event records and their
+        # collection add ~0.4 ms per step)
+        g.profile(True)
+        for _ in range(args.steps):
+            step()
+        ks = g.kernel_stats()
+        g.profile(False)
     met = g.metrics()
     res_groups = met["output_groups"]
     if xg is not None:
