@@ -981,7 +981,7 @@ int push_hybrid(Handle* h, const ColSrc& col) {
 // the rest of the batch.
 int cut_run(Handle* h) {
   unsigned long long groups = 0;
-  CU(cudaMemcpyAsync(&groups, &h->tab.hdr->groups, 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(&groups, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
   int words = h->kw + h->cs.ds.ns;
   int64_t n = (int64_t)groups + 2;
@@ -1428,7 +1428,7 @@ int aggb_finish(void* handle, aggb_result* out) {
       unsigned long long groups = 0;
       CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&refused, &h->tab.hdr->pad, 4, cudaMemcpyDeviceToHost, h->st));
-      CU(cudaMemcpyAsync(&groups, &h->tab.hdr->groups, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&groups, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
       if (h->cfg.algo == AGGB_ORIGINAL_HH && refused) frozen = 1;  // partition 0 spilled: cut the table
       h->met.resident_groups = (int64_t)groups;

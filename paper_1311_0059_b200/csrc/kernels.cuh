@@ -31,10 +31,10 @@ enum { ST_SPILLED = 0, ST_HITS = 1, ST_INSERTS = 2, ST_DEFERRED = 3, ST_RECORDS 
        ST_NSTATS = 8 };
 
 struct TableHdr {
-  unsigned long long groups;     // reservations held + committed inserts
+  unsigned long long groups;     // capacity handed out to CTAs (chunks, may pass cap)
   int frozen;
   int esc;
-  unsigned long long committed;  // keys actually inserted
+  unsigned long long committed;  // keys actually inserted (each CTA adds its count at exit)
   unsigned long long pad;
 };
 
@@ -61,29 +61,45 @@ struct Bkt {
 // diverge on long probe chains), CAS-claimed keys, capacity-bounded inserts.
 // ---------------------------------------------------------------------------
 
-// A reservation that finds the counter at capacity freezes the table only when
-// the capacity is really taken by committed keys.  Otherwise the excess is
-// transient (threads racing to insert one key each reserve before their CAS
-// shows the key is already there): the record is refused without freezing and
-// takes the refusal path (FILL defers it to the PROBE pass, ROUTE spills it to
-// partition 0 and marks the table for the overflow cut).  Never wait here: a
-// lane spinning on a reservation held by a lane of its own warp deadlocks at
-// the loop's reconvergence point.
-__device__ __forceinline__ bool reserve_capacity(const GTable& t) {
-  if (*(volatile int*)&t.hdr->frozen) return false;
-  unsigned long long old = atomicAdd(&t.hdr->groups, 1ull);
-  if (old < t.cap) return true;
-  atomicAdd(&t.hdr->groups, ~0ull);
-  // within a small margin of the capacity a failure is treated as real: near the
-  // limit, thousands of racing reservations would otherwise keep the last slots
-  // transiently saturated and the table would never freeze
-  const unsigned long long margin = t.cap / 32 < 4096ull ? t.cap / 32 : 4096ull;
-  if (*(volatile unsigned long long*)&t.hdr->committed + margin >= t.cap) atomicExch(&t.hdr->frozen, 1);
-  atomicExch((int*)&t.hdr->pad, 1);  // some insert was refused (ROUTE: cut the table at close)
+// Capacity reservations are aggregated per warp: the lanes that need one at
+// the same time take their count from the table's counter with one atomic by
+// a leader lane, so ~inserts / (lanes per event) global atomics replace one
+// same-address atomic per insert (which serialised at the L2 and dominated
+// FILL).  Grants never pass `cap`.  A reservation given back (the key turned
+// out to be present) goes to a per-CTA shared cache that later reservations
+// use first.  When the counter reaches the capacity the table freezes (FILL
+// stops grabbing tiles; the key set is final at the kernel boundary) and a
+// lane left without a reservation is refused without waiting — FILL defers the
+// record to the PROBE pass, ROUTE spills it to partition 0 and marks the table
+// for the overflow cut.  Never wait here: a lane spinning on a reservation
+// held by a lane of its own warp deadlocks at the loop's reconvergence point.
+struct CapCache {
+  int* avail;          // shared: reservations given back in this CTA
+  unsigned* commits;   // shared: keys this CTA inserted (added to hdr->committed at exit)
+  int* refused;        // shared: some insert of this CTA was refused (hdr->pad at exit)
+};
+
+__device__ __forceinline__ bool reserve_capacity(const GTable& t, const CapCache& cc) {
+  if (*(volatile int*)cc.avail > 0) {
+    if (atomicSub(cc.avail, 1) > 0) return true;
+    atomicAdd(cc.avail, 1);
+  }
+  const unsigned m = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  const unsigned n = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
+  unsigned long long g = ~0ull;
+  if (lane == leader && !*(volatile int*)&t.hdr->frozen) {
+    g = atomicAdd(&t.hdr->groups, (unsigned long long)n);
+    if (g + n >= t.cap) atomicExch(&t.hdr->frozen, 1);  // the counter reached the capacity
+  }
+  g = __shfl_sync(m, g, leader);
+  if (g != ~0ull && g + rank < t.cap) return true;
+  *(volatile int*)cc.refused = 1;  // published once per CTA (ROUTE: cut the table at close)
   return false;
 }
 
-__device__ __forceinline__ void commit_insert(const GTable& t) { atomicAdd(&t.hdr->committed, 1ull); }
+__device__ __forceinline__ void release_capacity(const CapCache& cc) { atomicAdd(cc.avail, 1); }
+__device__ __forceinline__ void commit_insert(const CapCache& cc) { atomicAdd(cc.commits, 1u); }
 
 __device__ __forceinline__ void ld_bucket(const uint64_t* keys, uint64_t b, uint64_t (&w)[4]) {
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(keys + b * 4);
@@ -96,13 +112,13 @@ __device__ __forceinline__ void ld_bucket(const uint64_t* keys, uint64_t b, uint
 
 // escape slot: the one key whose words all equal EMPTY
 template <int KW>
-__device__ __forceinline__ int64_t gt_escape(const GTable& t, bool insert, int& res) {
+__device__ __forceinline__ int64_t gt_escape(const GTable& t, bool insert, const CapCache& cc, int& res) {
   int64_t s = (int64_t)t.mask + 1;
   if (*(volatile int*)&t.hdr->esc) { res = R_HIT; return s; }
   if (!insert) { res = R_MISS; return -1; }
-  if (!reserve_capacity(t)) { res = R_REFUSED; return -1; }
-  if (atomicCAS(&t.hdr->esc, 0, 1) == 0) { commit_insert(t); res = R_INSERTED; return s; }
-  atomicAdd(&t.hdr->groups, ~0ull);
+  if (!reserve_capacity(t, cc)) { res = R_REFUSED; return -1; }
+  if (atomicCAS(&t.hdr->esc, 0, 1) == 0) { commit_insert(cc); res = R_INSERTED; return s; }
+  release_capacity(cc);
   res = R_HIT;
   return s;
 }
@@ -110,7 +126,7 @@ __device__ __forceinline__ int64_t gt_escape(const GTable& t, bool insert, int& 
 // Resolve key k whose first bucket b was already loaded into w[].
 template <int KW>
 __device__ __forceinline__ int64_t gt_resolve(const GTable& t, const uint64_t (&k)[KW], uint64_t b,
-                                              uint64_t (&w)[4], bool insert, int& res) {
+                                              uint64_t (&w)[4], bool insert, const CapCache& cc, int& res) {
   constexpr int BK = Bkt<KW>::N;
   bool reserved = false;
   int from = 0;
@@ -130,26 +146,26 @@ __device__ __forceinline__ int64_t gt_resolve(const GTable& t, const uint64_t (&
       else if (a0 == EMPTY && (KW == 1 || a1 == EMPTY)) emp = j;
     }
     if (hit >= 0) {
-      if (reserved) atomicAdd(&t.hdr->groups, ~0ull);
+      if (reserved) release_capacity(cc);
       res = R_HIT;
       return (int64_t)(b * BK + hit);
     }
     if (emp >= 0) {
       if (!insert) { res = R_MISS; return -1; }
       if (!reserved) {
-        if (!reserve_capacity(t)) { res = R_REFUSED; return -1; }
+        if (!reserve_capacity(t, cc)) { res = R_REFUSED; return -1; }
         reserved = true;
       }
       uint64_t* kp = t.keys + (b * BK + emp) * KW;
       if (KW == 1) {
         unsigned long long prev = atomicCAS((unsigned long long*)kp, EMPTY, k[0]);
-        if (prev == EMPTY) { commit_insert(t); res = R_INSERTED; return (int64_t)(b * BK + emp); }
-        if (prev == k[0]) { atomicAdd(&t.hdr->groups, ~0ull); res = R_HIT; return (int64_t)(b * BK + emp); }
+        if (prev == EMPTY) { commit_insert(cc); res = R_INSERTED; return (int64_t)(b * BK + emp); }
+        if (prev == k[0]) { release_capacity(cc); res = R_HIT; return (int64_t)(b * BK + emp); }
       } else {
         uint64_t x, y;
         cas128(kp, EMPTY, EMPTY, k[0], k[KW - 1], x, y);
-        if (x == EMPTY && y == EMPTY) { commit_insert(t); res = R_INSERTED; return (int64_t)(b * BK + emp); }
-        if (x == k[0] && y == k[KW - 1]) { atomicAdd(&t.hdr->groups, ~0ull); res = R_HIT; return (int64_t)(b * BK + emp); }
+        if (x == EMPTY && y == EMPTY) { commit_insert(cc); res = R_INSERTED; return (int64_t)(b * BK + emp); }
+        if (x == k[0] && y == k[KW - 1]) { release_capacity(cc); res = R_HIT; return (int64_t)(b * BK + emp); }
       }
       // another key took the slot: rescan this bucket after it
       ld_bucket(t.keys, b, w);
@@ -162,14 +178,6 @@ __device__ __forceinline__ int64_t gt_resolve(const GTable& t, const uint64_t (&
   }
 }
 
-template <int KW>
-__device__ __forceinline__ int64_t gtable_lookup(const GTable& t, const uint64_t (&k)[KW], bool insert, int& res) {
-  if (is_sentinel<KW>(k)) return gt_escape<KW>(t, insert, res);
-  uint64_t b = hash_key<KW>(k, t.seed) & t.bmask;
-  uint64_t w[4];
-  ld_bucket(t.keys, b, w);
-  return gt_resolve<KW>(t, k, b, w, insert, res);
-}
 
 // ---------------------------------------------------------------------------
 // blocked bloom filter of the frozen resident keys (the reference keeps a

@@ -124,6 +124,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   __shared__ unsigned long long s_grab, s_defer_base;
   __shared__ uint32_t s_ndefer;
   __shared__ uint32_t s_sbase, s_sused, s_scap;  // CTA-local page stash [s_sbase, s_sbase + s_scap)
+  __shared__ int s_avail;                         // table reservations given back in this CTA
+  __shared__ unsigned s_commits;                  // keys this CTA inserted
+  __shared__ int s_refused;
+  const CapCache cc{&s_avail, &s_commits, &s_refused};
   __shared__ unsigned long long s_cnt[ST_NSTATS];
 
   const int ns = a.sp.ns;
@@ -181,6 +185,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
 
   if (tid == 0) {
     s_ndefer = 0;
+    s_avail = 0;
+    s_commits = 0;
+    s_refused = 0;
     s_sbase = s_sused = s_scap = 0;
     s_ntouched[0] = s_ntouched[1] = 0;
     s_grab = grab();
@@ -251,8 +258,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       int64_t s = -1;
       if (part[r] != -2) c_rec++;
       if (part[r] == -1)
-        s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, res)
-                                   : gt_resolve<KW>(a.t, kc[r], bk[r] & a.t.bmask, bw[r], insert, res);
+        s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, cc, res)
+                                   : gt_resolve<KW>(a.t, kc[r], bk[r] & a.t.bmask, bw[r], insert, cc, res);
       __syncwarp();  // reconverge after the divergent probe before the updates
       if (part[r] == -1) {
         if (res == R_HIT || res == R_INSERTED) {
@@ -447,6 +454,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   }
   __syncthreads();
   if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
+  if (tid == 0 && s_commits) atomicAdd(&a.t.hdr->committed, (unsigned long long)s_commits);
+  if (tid == 0 && s_refused) atomicExch((int*)&a.t.hdr->pad, 1);
 }
 
 // ---------------------------------------------------------------------------
