@@ -449,6 +449,14 @@ unsigned long long* SC(Handle* h) { return h->scratch.as<unsigned long long>(); 
 
 int pool_ensure(Handle* h, uint64_t extra_pages) {
   uint64_t need = h->pool_bound + extra_pages;
+  if (need > h->pool_cap && h->pool_cap) {
+    // the running bound is loose (it sums every pass's worst case): before growing,
+    // tighten it to the pages actually allocated so far plus this pass's bound
+    uint32_t now = 0;
+    CU(cudaMemcpyAsync(&now, h->pool_ctr.p, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    need = std::min<uint64_t>(need, (uint64_t)std::min<uint32_t>(now, h->pool_cap) + extra_pages);
+  }
   if (need > 0xFFFFFFF0ull) return fail(AGGB_CAPACITY_EXCEEDED, "spill pool would exceed 2^32 pages");
   h->pool_bound = need;
   if (need <= h->pool_cap) return AGGB_OK;
@@ -584,6 +592,12 @@ int launch_pass(Handle* h, PassPlan& pp) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, blk, smem);
   int grid = std::max(1, occ) * h->sms;
+  if (pp.mode == MODE_GRACE || (pp.mode != MODE_FILL && pp.col.n == 0)) {
+    // small list passes: every CTA opens a page per partition it touches, so
+    // give each CTA at least ~4 tiles of records
+    const int64_t recs = pp.col.n + (pp.lin_count ? pp.lin_stride : 0);
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, (recs + 4LL * T - 1) / (4LL * T)));
+  }
   PassArgs a;
   memset(&a, 0, sizeof(a));
   a.sp = h->cs.ds;

@@ -191,18 +191,18 @@ struct Bloom {
   uint64_t seed;
 };
 
+// The filter is keyed off the table's own 64-bit hash h (k_pass / k_probe
+// derive bucket, spill partition and bloom probe from one hash): bucket from
+// bits 0..16 (the filter is off for tables large enough to use more), block
+// from bits 20..33, four bit positions from bits 34..53 (two per 32-bit half of
+// the block; 32-bit shifts only); the partition comes from the top bits.
+__device__ __forceinline__ uint32_t bloom_block(uint64_t h, uint32_t mask) { return (uint32_t)(h >> 20) & mask; }
 __device__ __forceinline__ uint64_t bloom_bits(uint64_t h) {
-  // four bits of the 64-bit block, two per 32-bit half (32-bit shifts only)
-  const uint32_t x = (uint32_t)(h >> 32);
+  const uint32_t x = (uint32_t)(h >> 34);
   const uint32_t lo = (1u << (x & 31)) | (1u << ((x >> 5) & 31));
   const uint32_t hi = (1u << ((x >> 10) & 31)) | (1u << ((x >> 15) & 31));
   return ((uint64_t)hi << 32) | lo;
 }
-
-// The filter is keyed off the table's own hash (k_pass derives bucket, spill
-// partition and bloom probe from one 64-bit hash): hb = h * golden, block =
-// (hb >> 8) & mask, bits = bloom_bits(hb).
-__device__ __forceinline__ uint64_t bloom_remix(uint64_t h) { return h * 0x9E3779B97F4A7C15ull; }
 
 template <int KW>
 __global__ void k_bloom_build(GTable t, uint64_t* bloom, uint32_t mask) {
@@ -212,8 +212,8 @@ __global__ void k_bloom_build(GTable t, uint64_t* bloom, uint32_t mask) {
 #pragma unroll
     for (int w = 0; w < KW; w++) k[w] = t.keys[i * KW + w];
     if (is_sentinel<KW>(k)) continue;
-    uint64_t hb = bloom_remix(hash_key<KW>(k, t.seed));
-    atomicOr((unsigned long long*)&bloom[(hb >> 8) & mask], (unsigned long long)bloom_bits(hb));
+    const uint64_t h = hash_key<KW>(k, t.seed);
+    atomicOr((unsigned long long*)&bloom[bloom_block(h, mask)], (unsigned long long)bloom_bits(h));
   }
 }
 

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
     // page-stash refill: phase A never overlaps phase B (the only consumer),
     // the atomic's latency hides behind this warp's phase A
-    const bool refill = spills && a.stash && tid == 0 && s_scap - min(s_sused, s_scap) < (uint32_t)a.stash / 2;
+    const bool refill = spills && a.stash && tid == 0 && s_sused >= s_scap;  // refill only when used up
     uint32_t ref_first = 0;
     if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
     // ---- [A] first-bucket loads for the current records
@@ -235,9 +235,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         const uint64_t h = hash_key<KW>(kc[r], a.t.seed);
         bk[r] = h;
         if (use_bloom) {
-          const uint64_t hb = bloom_remix(h);
-          const uint64_t bits = bloom_bits(hb);
-          if ((sbloom[(hb >> 8) & a.bloom.mask] & bits) != bits) {  // definitely not resident
+          const uint64_t bits = bloom_bits(h);
+          if ((sbloom[bloom_block(h, a.bloom.mask)] & bits) != bits) {  // definitely not resident
             part[r] = (int)reduce32(h, (uint32_t)P);
             continue;
           }
@@ -318,14 +317,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         pnew[p] = -1;
         if (e > room) {
           int need = (e - room + S - 1) / S;
-          uint32_t first;
-          const uint32_t off = atomicAdd(&s_sused, (uint32_t)need);
-          if (off + need <= s_scap) {
-            first = s_sbase + off;
-          } else {  // the stash cannot serve it: release the part taken (disjoint per taker)
-            for (uint32_t q = off; q < min(off + (uint32_t)need, s_scap); q++) a.pool.page_set[s_sbase + q] = -1;
-            first = atomicAdd(a.pool.next_page, (uint32_t)need);
+          // single pages come from the CTA's stash (a taker past its end takes
+          // nothing from it); runs of pages are contiguous: one global atomic
+          uint32_t first = 0xFFFFFFFFu;
+          if (need == 1) {
+            const uint32_t off = atomicAdd(&s_sused, 1u);
+            if (off < s_scap) first = s_sbase + off;
           }
+          if (first == 0xFFFFFFFFu) first = atomicAdd(a.pool.next_page, (uint32_t)need);
           if (first + need > a.pool.capacity) {
             atomicExch(a.pool.overflow, 1u);
             pcur[p] = -1;

@@ -53,8 +53,8 @@ __device__ __forceinline__ void probe_issue(const PassArgs& a, uint64_t k, uint6
   const uint64_t kk[1] = {k};
   b = hash_key<1>(kk, a.t.seed) & a.t.bmask;
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
-  x = __ldcg(p);
-  y = __ldcg(p + 1);
+  x = __ldca(p);  // L1: prefetched by the owner lane at classification
+  y = __ldca(p + 1);
 }
 
 // Spill layout: each CTA appends a partition's records to its own chain of
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
     if (tid == 0) {
       g_next = atomicAdd(a.tile_counter, 1ull);
       const int q = par ^ 1;
-      refill = a.stash && s_sc[q] - min(s_su[q], s_sc[q]) < (uint32_t)a.stash / 2;
+      refill = a.stash && s_su[q] >= s_sc[q];  // refill a used-up stash only: no page is dropped
       if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
     }
     // ---- [A] classify: one hash; partition from its high bits, bloom from a remix
@@ -160,10 +160,13 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       part[r] = kc[r] == EMPTY ? 0 : (int)reduce32(h, (uint32_t)P);
       bool posv = lc[r];
       if (nbw && kc[r] != EMPTY) {
-        const uint64_t hb = bloom_remix(h);
-        const uint64_t bits = bloom_bits(hb);
-        posv = posv && (sbloom[(uint32_t)(hb >> 8) & a.bloom.mask] & bits) == bits;
+        const uint64_t bits = bloom_bits(h);
+        posv = posv && (sbloom[bloom_block(h, a.bloom.mask)] & bits) == bits;
       }
+      // a positive is resolved by some lane of the warp shortly: pull its first
+      // bucket into L1 now (the frozen table is read-only for this kernel)
+      if (posv && kc[r] != EMPTY)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.t.keys + (h & a.t.bmask) * 4));
       seq[r] = posv ? 0u : ~0u;
     }
     // ---- prefetch the next tile
