@@ -278,7 +278,7 @@ PassCfg pass_kernel(int nwt, int prog) {
   if (KW == 2 && nwt == 4 && prog == 5) return pc<2, 4, 2, 512, ProgC5>();
   switch (nwt) {
     case 1: return pc<KW, 1, 4, 512, PD>();
-    case 2: return pc<KW, 2, 4, 512, PD>();
+    case 2: return pc<KW, 2, KW == 1 ? 4 : 2, 512, PD>();
     case 4: return pc<KW, 4, 2, 512, PD>();
     case 8: return pc<KW, 8, 1, 512, PD>();
     case 16: return pc<KW, 16, 1, 512, PD>();
@@ -587,6 +587,18 @@ int launch_pass(Handle* h, PassPlan& pp) {
     smem = smem_of(0);
   }
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
+  // SMEM pre-aggregation tier for inserting passes over one-word keys (pass.cuh)
+  int cache_log2 = 0;
+  if (!fast_probe && pp.mode == MODE_FILL && h->kw == 1 && !getenv("AGGB_NO_CACHE")) {
+    const size_t per = 12 + 8 * (size_t)h->cs.ds.ns;
+    const size_t room = std::min<size_t>(160 * 1024, 224 * 1024 - std::min<size_t>(smem + 16, 224 * 1024));
+    int L = 0;
+    while (L < 14 && ((size_t)1 << (L + 1)) * per <= room) L++;
+    if (L >= 8) {
+      cache_log2 = L;
+      smem += ((size_t)1 << L) * per + 16;
+    }
+  }
   CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int occ = 0;
@@ -634,6 +646,16 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.defer_count = SC(h) + 10;
   a.tile_counter = pp.counter;
   a.stats = SC(h);
+  a.cache_log2 = cache_log2;
+  // chunked reservations for large tables: unused chunks (< grid * chunk) stay under 1% of cap
+  {
+    const uint64_t cap = h->tab.cap;
+    const uint64_t chunk = std::min<uint64_t>(64, cap / (100ull * (uint64_t)grid));
+    if (chunk >= 32) {
+      a.cap_chunk = (uint32_t)chunk;
+      a.cap_chunked = cap - std::min<uint64_t>(cap, 2ull * (uint64_t)grid * chunk);
+    }
+  }
   if (pp.mode != MODE_FILL) {
     // upper bound of pages this pass can allocate
     int64_t recs = pp.col.n + (pp.lin_count ? (pp.lin_stride) : 0);

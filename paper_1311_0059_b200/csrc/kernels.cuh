@@ -31,11 +31,12 @@ enum { ST_SPILLED = 0, ST_HITS = 1, ST_INSERTS = 2, ST_DEFERRED = 3, ST_RECORDS 
        ST_NSTATS = 8 };
 
 struct TableHdr {
-  unsigned long long groups;     // capacity handed out to CTAs (chunks, may pass cap)
+  unsigned long long groups;     // exact-region reservations granted (may pass the region's size)
   int frozen;
   int esc;
   unsigned long long committed;  // keys actually inserted (each CTA adds its count at exit)
-  unsigned long long pad;
+  unsigned long long pad;        // some insert was refused
+  unsigned long long chunked;    // chunk-region reservations handed to CTAs
 };
 
 struct GTable {
@@ -73,10 +74,17 @@ struct Bkt {
 // record to the PROBE pass, ROUTE spills it to partition 0 and marks the table
 // for the overflow cut.  Never wait here: a lane spinning on a reservation
 // held by a lane of its own warp deadlocks at the loop's reconvergence point.
+// Large tables add a chunk region: capacity [0, cap_chunked) is handed to CTAs
+// `chunk` reservations at a time (one refilling thread per CTA), the rest
+// [cap_chunked, cap) through the exact per-warp path, so the table still fills
+// to within the CTAs' unused chunks (the host keeps that under 1% of cap).
 struct CapCache {
-  int* avail;          // shared: reservations given back in this CTA
+  int* avail;          // shared: reservations held by this CTA (given back or chunked)
   unsigned* commits;   // shared: keys this CTA inserted (added to hdr->committed at exit)
   int* refused;        // shared: some insert of this CTA was refused (hdr->pad at exit)
+  int* refilling;      // shared: a thread of this CTA is taking a chunk
+  uint32_t chunk;      // 0: no chunk region
+  unsigned long long cap_chunked;
 };
 
 __device__ __forceinline__ bool reserve_capacity(const GTable& t, const CapCache& cc) {
@@ -87,13 +95,32 @@ __device__ __forceinline__ bool reserve_capacity(const GTable& t, const CapCache
   const unsigned m = __activemask();
   const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
   const unsigned n = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
+  if (cc.chunk && *(volatile unsigned long long*)&t.hdr->chunked < cc.cap_chunked) {
+    // chunk region: the lanes here take one each; the leader also takes a chunk
+    // for its CTA when no other thread of the CTA is doing so
+    unsigned long long c = ~0ull;
+    if (lane == leader) {
+      const bool extra = atomicCAS(cc.refilling, 0, 1) == 0;
+      const unsigned long long want = n + (extra ? cc.chunk : 0u);
+      c = atomicAdd(&t.hdr->chunked, want);
+      if (c + want <= cc.cap_chunked) {
+        if (extra) atomicAdd(cc.avail, (int)cc.chunk);
+      } else {
+        c = ~0ull;  // region exhausted (its tail is left unused): the exact path decides
+      }
+      if (extra) atomicExch(cc.refilling, 0);
+    }
+    c = __shfl_sync(m, c, leader);
+    if (c != ~0ull) return true;
+  }
+  const unsigned long long exact = t.cap - cc.cap_chunked;  // size of the exact region
   unsigned long long g = ~0ull;
   if (lane == leader && !*(volatile int*)&t.hdr->frozen) {
     g = atomicAdd(&t.hdr->groups, (unsigned long long)n);
-    if (g + n >= t.cap) atomicExch(&t.hdr->frozen, 1);  // the counter reached the capacity
+    if (g + n >= exact) atomicExch(&t.hdr->frozen, 1);  // the counter reached the capacity
   }
   g = __shfl_sync(m, g, leader);
-  if (g != ~0ull && g + rank < t.cap) return true;
+  if (g != ~0ull && g + rank < exact) return true;
   *(volatile int*)cc.refused = 1;  // published once per CTA (ROUTE: cut the table at close)
   return false;
 }
@@ -229,6 +256,7 @@ __global__ void k_table_init(GTable t, int kw, DevSpec sp) {
     t.hdr->esc = 0;
     t.hdr->committed = 0;
     t.hdr->pad = 0;
+    t.hdr->chunked = 0;
   }
 }
 

@@ -42,6 +42,9 @@ struct PassArgs {
   unsigned long long* tile_counter;
   unsigned long long* stats;
   int32_t stash;                          // pages per CTA-local page-stash refill (0: global atomics only)
+  int32_t cache_log2;                     // FILL, one-word keys: SMEM pre-aggregation slots (0: off)
+  uint32_t cap_chunk;                     // table reservations per CTA chunk (0: exact path only)
+  unsigned long long cap_chunked;         // capacity handed out in chunks (kernels.cuh CapCache)
 };
 
 template <int KW, int NWT>
@@ -119,6 +122,16 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   uint32_t* rprev = rcnt + P;
   uint32_t* emitn = rprev + P;
   uint16_t* touched = (uint16_t*)(emitn + P);                // P: partitions touched by the tile
+  // SMEM pre-aggregation tier (FILL / ROUTE): per-CTA cache of resident keys.
+  // A key enters it only after its global lookup/insert succeeded (slot cgs);
+  // later records of that key update the cache's states in shared memory, which
+  // merge into the global slot at exit.  Hot (skewed) keys stop contending on
+  // one L2 address; the table's capacity semantics are untouched.
+  const int CH = (KW == 1 && a.cache_log2) ? 1 << a.cache_log2 : 0;
+  uint64_t* ckeys = (uint64_t*)(((uintptr_t)(touched + P) + 15) & ~(uintptr_t)15);  // CH
+  uint64_t* cst = ckeys + CH;                                                        // ns * CH
+  uint32_t* cgs = (uint32_t*)(cst + (size_t)a.sp.ns * CH);                           // CH
+  __shared__ int s_ccount;
   __shared__ uint32_t s_ntouched[2];  // by tile parity: A fills one while the other is reset
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_grab, s_defer_base;
@@ -126,8 +139,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   __shared__ uint32_t s_sbase, s_sused, s_scap;  // CTA-local page stash [s_sbase, s_sbase + s_scap)
   __shared__ int s_avail;                         // table reservations given back in this CTA
   __shared__ unsigned s_commits;                  // keys this CTA inserted
-  __shared__ int s_refused;
-  const CapCache cc{&s_avail, &s_commits, &s_refused};
+  __shared__ int s_refused, s_refilling;
+  const CapCache cc{&s_avail, &s_commits, &s_refused, &s_refilling, a.cap_chunk, a.cap_chunked};
   __shared__ unsigned long long s_cnt[ST_NSTATS];
 
   const int ns = a.sp.ns;
@@ -140,6 +153,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   }
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
   for (int i = tid; i < nbw; i += B) sbloom[i] = __ldcg((const unsigned long long*)a.bloom.words + i);
+  for (int i = tid; i < CH; i += B) {
+    ckeys[i] = EMPTY;
+    for (int j = 0; j < a.sp.ns; j++) cst[(size_t)j * CH + i] = state_identity(a.sp.op[j], a.sp.ty[j]);
+  }
+  if (tid == 0) s_ccount = 0;
   const int64_t n = a.col.n;
   const int64_t col_start =
       a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
@@ -188,6 +206,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     s_avail = 0;
     s_commits = 0;
     s_refused = 0;
+    s_refilling = 0;
     s_sbase = s_sused = s_scap = 0;
     s_ntouched[0] = s_ntouched[1] = 0;
     s_grab = grab();
@@ -234,6 +253,20 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         // spill partition from the high bits, bloom probe from a remix
         const uint64_t h = hash_key<KW>(kc[r], a.t.seed);
         bk[r] = h;
+        if (CH) {  // pre-aggregation tier: a cached key never leaves the SM
+          const int c0 = (int)(h >> 40) & (CH - 1);
+          int hit = -1;
+          for (int q = 0; q < 4; q++) {
+            const int c = (c0 + q) & (CH - 1);
+            const uint64_t ck = *(volatile uint64_t*)&ckeys[c];
+            if (ck == kc[r][0]) { hit = c; break; }
+            if (ck == EMPTY) break;
+          }
+          if (hit >= 0) {
+            part[r] = -3 - hit;
+            continue;
+          }
+        }
         if (use_bloom) {
           const uint64_t bits = bloom_bits(h);
           if ((sbloom[bloom_block(h, a.bloom.mask)] & bits) != bits) {  // definitely not resident
@@ -260,12 +293,31 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         s = is_sentinel<KW>(kc[r]) ? gt_escape<KW>(a.t, insert, cc, res)
                                    : gt_resolve<KW>(a.t, kc[r], bk[r] & a.t.bmask, bw[r], insert, cc, res);
       __syncwarp();  // reconverge after the divergent probe before the updates
+      if (part[r] <= -3) {  // cached key: shared-memory update
+        Upd<PG>::template sm<NWT>(cst, CH, -3 - part[r], kind, s_fd, ns, vc[r]);
+        c_hit++;
+        part[r] = -2;
+      }
       if (part[r] == -1) {
         if (res == R_HIT || res == R_INSERTED) {
           Upd<PG>::template g<NWT>(a.t.states, a.t.stride, (uint64_t)s, kind, s_fd, ns, vc[r]);
           c_hit += (res == R_HIT);
           c_ins += (res == R_INSERTED);
           part[r] = -2;
+          // resident now: cache the key for its later records (first come, no eviction)
+          if (CH && !is_sentinel<KW>(kc[r]) && *(volatile int*)&s_ccount < (CH * 3) / 4) {
+            const int c0 = (int)(bk[r] >> 40) & (CH - 1);
+            for (int q = 0; q < 4; q++) {
+              const int c = (c0 + q) & (CH - 1);
+              const unsigned long long prev = atomicCAS((unsigned long long*)&ckeys[c], EMPTY, kc[r][0]);
+              if (prev == EMPTY) {
+                cgs[c] = (uint32_t)s;
+                atomicAdd(&s_ccount, 1);
+                break;
+              }
+              if (prev == kc[r][0]) break;
+            }
+          }
         } else if (res == R_MISS) {
           part[r] = is_sentinel<KW>(kc[r]) ? 0 : (int)reduce32(bk[r], (uint32_t)P);
         } else if (a.mode == MODE_FILL) {
@@ -411,6 +463,17 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     }
   }
   __syncthreads();
+  // merge the pre-aggregation tier into the table (skip identity states: keys cached late)
+  for (int i = tid; i < CH; i += B) {
+    if (ckeys[i] == EMPTY) continue;
+    const uint64_t gs = cgs[i];
+    for (int j = 0; j < ns; j++) {
+      const uint64_t v = cst[(size_t)j * CH + i];
+      const uint32_t F = s_fd[j];
+      if (v == state_identity(F & 3, (F >> 2) & 3)) continue;
+      gupdate(a.t.states + (uint64_t)j * a.t.stride + gs, F & 3, (F >> 2) & 3, v);
+    }
+  }
   if (spills)
     for (uint32_t q = min(s_sused, s_scap) + tid; q < s_scap; q += B) a.pool.page_set[s_sbase + q] = -1;
   // drain the residuals (partial sectors, once per partition) and seal the pages
