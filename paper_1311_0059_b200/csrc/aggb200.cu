@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -352,6 +353,7 @@ struct Handle {
   // plan
   int64_t budget = 0;       // resident capacity (groups)
   bool unlimited = false;
+  bool l2_children = false; // spilled partitions aggregate in the budget-sized L2 table (drain)
   int P0 = 1;               // level-0 spill fan-out
   int child_slots_log2 = 11;
   int child_cap = 1024;
@@ -385,7 +387,7 @@ struct Handle {
   aggb_metrics met{};
   int64_t hash_sort_runs = 0;
   // recursion scratch
-  DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend;
+  DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend, l2stage, cut_tmp;
   int prog = 0;
   // blocked bloom filter of the frozen level-0 table (PROBE)
   DBuf bloom;
@@ -540,6 +542,7 @@ struct PassPlan {
   int mode;
   const aggb_input* in;      // columnar source (may be null)
   ColSrc col{};
+  int col_kind = 0;          // 0 raw payload, 1 native partial states
   bool use_start = false;    // start from tile counter A (after FILL)
   const uint64_t* lin = nullptr;
   int64_t lin_stride = 0;
@@ -562,7 +565,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   int G = pp.mode == MODE_FILL ? 1 : group_of(pp.ss.rw);
   int rw = pp.mode == MODE_FILL ? 1 : pp.ss.rw;
   // k_probe: 16-byte raw records from dense 8-byte columns (and the SoA deferral list)
-  const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 &&
+  const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 && pp.col_kind == 0 &&
                           pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 1 && pp.lin_kind == 0)) &&
                           dense8(pp.col, 1) && pp.ss.per_page == 512 &&
                           // page ids are 24-bit in k_probe's page map (conservative pool estimate)
@@ -617,6 +620,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.t = h->tab;
   a.col = pp.col;
   a.col_dense = dense8(pp.col, h->kw) ? 1 : 0;
+  a.col_kind = pp.col_kind;
   a.start_tiles = pp.use_start ? SC(h) + 8 : nullptr;
   a.start_T = T_fill;
   if (pp.lin) {
@@ -833,7 +837,19 @@ int plan(Handle* h) {
     P = std::max(P, plan_partitions(G * F, M));  // Formula 1 as the floor
   }
   int rw0 = h->kw + h->cs.nv;
-  h->P0 = std::min(P, std::min(MAX_PARTS, max_parts_for(rw0)));
+  const int cap_parts = std::min(MAX_PARTS, max_parts_for(rw0));
+  // Shared-memory children hold child_cap groups; when the fan-out that needs is
+  // more than one spill pass can write, every level would retire only
+  // cap_parts * child_cap groups (C5: ~20 levels).  Then each spilled partition
+  // is aggregated like the reference's child operator instead — with the full
+  // budget, in the L2-resident table (drain, l2 children) — and the fan-out
+  // only has to bring partitions under the budget.
+  h->l2_children = false;
+  if (P > cap_parts && !h->unlimited && !getenv("AGGB_NO_L2_CHILDREN")) {
+    h->l2_children = true;
+    P = std::max(2, (int)std::ceil(spill_groups / std::max(1.0, 0.5 * (double)h->budget)));
+  }
+  h->P0 = std::min(P, cap_parts);
   if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment
   return AGGB_OK;
 }
@@ -948,6 +964,8 @@ int ensure_defer(Handle* h, int64_t T) {
   return AGGB_OK;
 }
 
+int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss);
+
 int push_hybrid(Handle* h, const ColSrc& col) {
   int algo = h->cfg.algo;
   unsigned long long* ctrA = SC(h) + 8;
@@ -970,7 +988,28 @@ int push_hybrid(Handle* h, const ColSrc& col) {
     h->raw0_live = true;
     return AGGB_OK;
   }
-  // pre_partitioning / hash_sort: FILL then PROBE (kernel boundary = freeze point)
+  if (algo == AGGB_HASH_SORT) {  // FILL only: push_hash_sort handles freezes (cuts)
+    int nwt = nwt_for(std::max(1, col.nv));
+    PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+    TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk));
+    CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+    PassPlan f;
+    f.mode = MODE_FILL;
+    f.col = col;
+    f.counter = ctrA;
+    return launch_pass(h, f);
+  }
+  TRY(fill_probe(h, col, 0, h->raw0.ss));
+  h->raw0_live = true;
+  return AGGB_OK;
+}
+
+// FILL then PROBE (kernel boundary = freeze point) of a column source whose
+// records are of kind col_kind; misses spill to set ss.  pre_partitioning's
+// push, and the body of an L2-table child (drain).
+int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss) {
+  unsigned long long* ctrA = SC(h) + 8;
+  unsigned long long* ctrB = SC(h) + 9;
   int nwt = nwt_for(std::max(1, col.nv));
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
   TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk));
@@ -978,10 +1017,10 @@ int push_hybrid(Handle* h, const ColSrc& col) {
   PassPlan f;
   f.mode = MODE_FILL;
   f.col = col;
+  f.col_kind = col_kind;
   f.counter = ctrA;
   TRY(launch_pass(h, f));
-  if (algo == AGGB_HASH_SORT) return AGGB_OK;  // handled by push_hash_sort
-  // pre_partitioning: PROBE the remainder and the deferred records against the frozen table.
+  // PROBE the remainder and the deferred records against the frozen table.
   // The filter is rebuilt from the table as it stands after FILL (a kernel boundary, so
   // the key set is final once frozen); while the table is not frozen PROBE has no work.
   if (h->bloom_words) {
@@ -997,17 +1036,16 @@ int push_hybrid(Handle* h, const ColSrc& col) {
   PassPlan p;
   p.mode = MODE_PROBE;
   p.col = col;
+  p.col_kind = col_kind;
   p.use_start = true;
   p.lin = h->defer.as<uint64_t>();
   p.lin_stride = h->defer_cap;
   p.lin_count = SC(h) + 10;
-  p.lin_kind = 0;
+  p.lin_kind = col_kind;
   p.lin_words = col.nv;
-  p.ss = h->raw0.ss;
+  p.ss = ss;
   p.counter = ctrB;
-  TRY(launch_pass(h, p));
-  h->raw0_live = true;
-  return AGGB_OK;
+  return launch_pass(h, p);
 }
 
 
@@ -1016,13 +1054,12 @@ int push_hybrid(Handle* h, const ColSrc& col) {
 // shared-memory children), reset, and continue with the deferred records and
 // the rest of the batch.
 int cut_run(Handle* h) {
-  unsigned long long groups = 0;
-  CU(cudaMemcpyAsync(&groups, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
-  CU(cudaStreamSynchronize(h->st));
+  // the run holds at most the table's capacity (+ the escape group): a persistent
+  // buffer of that size, no read-back of the group count
   int words = h->kw + h->cs.ds.ns;
-  int64_t n = (int64_t)groups + 2;
-  DBuf tmp;
-  TRY(tmp.ensure((size_t)n * words * 8, nullptr));
+  int64_t n = (int64_t)h->tab.cap + 2;
+  DBuf& tmp = h->cut_tmp;
+  TRY(tmp.ensure((size_t)n * words * 8, &h->hw));
   OutBuf o;
   o.keys = tmp.as<uint64_t>();
   o.vals = tmp.as<uint64_t>() + (size_t)h->kw * n;
@@ -1041,8 +1078,6 @@ int cut_run(Handle* h) {
   g.ss = h->part0.ss;
   g.counter = SC(h) + 9;
   TRY(launch_pass(h, g));
-  CU(cudaStreamSynchronize(h->st));
-  tmp.release();
   h->part0_live = true;
   h->hash_sort_runs++;
   return table_reset(h);
@@ -1184,6 +1219,68 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
                                              h->cursor.as<uint32_t>() + (size_t)q * nparts, h->plist.as<uint2>());
       prof_end(h, pe);
       h->launches++;
+    }
+    if (h->l2_children && nsets == 1) {
+      // Children on the L2-resident table, one partition at a time, each the
+      // reference's child operator (hybrid.py:244-277): fresh seeds, the full
+      // budget, FILL then PROBE; what a child cannot hold spills to one shared
+      // next-level set.  This level's pages stay untouched until the next
+      // level starts (its spill is appended to the pool).
+      const int ikind = a.ss.kind, inw = a.ss.rw - h->kw;
+      std::vector<int64_t> irecs;
+      for (int p = 0; p < nparts; p++)
+        if (pages[p]) irecs.push_back((int64_t)recs[p]);
+      int64_t maxr = 0, out_need = 0;
+      for (int64_t r : irecs) {
+        maxr = std::max(maxr, r);
+        out_need += std::min<int64_t>(r, h->budget) + 2;
+      }
+      unsigned long long cnt = 0;
+      CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      TRY(ensure_out(h, (int64_t)cnt + out_need + 16));
+      TRY(h->l2stage.ensure((size_t)std::max<int64_t>(maxr, 1) * a.ss.rw * 8, &h->hw));
+      const int64_t total = std::accumulate(irecs.begin(), irecs.end(), (int64_t)0);
+      const int Pn = std::max(2, std::min(std::min(MAX_PARTS, max_parts_for(a.ss.rw)),
+                                          (int)std::ceil((double)total / std::max<int64_t>(1, h->budget))));
+      SetInfo nxt{make_set(h, Pn, inw, ikind, level_seed(h->cfg.seed, SALT_SPILL, depth + 1)), 0};
+      OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+      const uint64_t seed0 = h->tab.seed;
+      h->tab.seed = level_seed(h->cfg.seed, SALT_SLOT, depth + 1);
+      tr.mark(h->st, "drain: l2 children setup");
+      for (size_t i = 0; i < irecs.size(); i++) {
+        const int64_t qa = item_off[2 * i], qb = item_off[2 * i + 2];
+        TRY(table_reset(h));
+        CU(cudaMemsetAsync(SC(h) + 16, 0, 8, h->st));
+        const int gg = (int)std::min<int64_t>(qb - qa, (int64_t)h->sms * 8);
+        k_gather_pages<<<std::max(gg, 1), 256, 0, h->st>>>(pool_of(h), h->plist.as<uint2>() + qa, qb - qa, a.ss.rw,
+                                                          h->l2stage.as<uint64_t>(), irecs[i], SC(h) + 16);
+        h->launches++;
+        ColSrc c;
+        memset(&c, 0, sizeof(c));
+        c.n = irecs[i];
+        for (int w = 0; w < h->kw; w++) {
+          c.key[w] = (const uint8_t*)(h->l2stage.as<uint64_t>() + (size_t)w * irecs[i]);
+          c.kstride[w] = 8;
+          c.kty[w] = TY_I64;
+        }
+        c.nv = inw;
+        for (int w = 0; w < inw; w++) {
+          c.val[w] = (const uint8_t*)(h->l2stage.as<uint64_t>() + (size_t)(h->kw + w) * irecs[i]);
+          c.vstride[w] = 8;
+          c.vty[w] = (ikind == 0 && w < h->cs.ds.nv) ? h->cs.ds.vty[w] : TY_I64;
+        }
+        TRY(fill_probe(h, c, ikind, nxt.ss));
+        TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
+      }
+      h->tab.seed = seed0;
+      CU(cudaStreamSynchronize(h->st));
+      tr.mark(h->st, "drain: l2 children");
+      a = nxt;
+      a_live = true;
+      b_live = false;
+      depth++;
+      continue;
     }
     // child pass: output room + overflow room
     max_items_out = (int64_t)nonempty * (h->child_cap + 1);
@@ -1381,7 +1478,7 @@ void aggb_destroy(void* handle) {
   DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->pool_base, &h->page_part, &h->page_fill, &h->page_set,
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
-                  &h->item_off, &h->ovf, &h->pend, &h->bloom, &h->sort_keys, &h->sort_vals};
+                  &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals};
   for (DBuf* b : bufs) b->release();
   h->stage.release();
   for (auto& e : h->evs) {

@@ -653,6 +653,24 @@ __global__ void k_aos_to_soa(const uint64_t* in, int64_t n, int rw, uint64_t* ou
     for (int w = 0; w < rw; w++) out[(int64_t)w * n + i] = in[i * rw + w];
 }
 
+// Gather one item's records (AoS pages of rw words) into dense columns
+// (SoA, column stride `stride`) for an L2-table child; pages land in any order
+// (aggregation is order-free), each page's records contiguously.
+__global__ void k_gather_pages(PagePool pool, const uint2* plist, int64_t npages, int rw, uint64_t* out,
+                               int64_t stride, unsigned long long* count) {
+  __shared__ unsigned long long s_base;
+  for (int64_t q = blockIdx.x; q < npages; q += gridDim.x) {
+    const uint2 pe = plist[q];
+    if (threadIdx.x == 0) s_base = atomicAdd(count, (unsigned long long)pe.y);
+    __syncthreads();
+    const unsigned long long* src = (const unsigned long long*)page_ptr(pool, pe.x);
+    const int64_t base = (int64_t)s_base;
+    for (int i = threadIdx.x; i < (int)pe.y * rw; i += blockDim.x)
+      out[(int64_t)(i % rw) * stride + base + i / rw] = __ldcs(src + i);
+    __syncthreads();
+  }
+}
+
 __global__ void k_key_to_i32(const uint64_t* w, int32_t* out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)(uint32_t)(w[i] >> 32);

@@ -20,6 +20,7 @@ struct PassArgs {
   // source 1: columnar batch rows [start, n), start = min(n, *start_tiles * start_T)
   ColSrc col;
   int32_t col_dense;                      // all key/value columns 8-byte, stride 8
+  int32_t col_kind;                       // 0 raw payload, 1 native partial states
   const unsigned long long* start_tiles;  // nullable
   int64_t start_T;
   // source 2: SoA list (deferred / overflow records) described as dense columns
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   uint32_t c_hit = 0, c_ins = 0, c_rec = 0, c_sp = 0, c_def = 0;
   int par = 0;
   while (cur < total) {
-    const int kind = ((int64_t)cur < col_tiles) ? 0 : a.lin_kind;
+    const int kind = ((int64_t)cur < col_tiles) ? a.col_kind : a.lin_kind;
     // page-stash refill: phase A never overlaps phase B (the only consumer),
     // the atomic's latency hides behind this warp's phase A
     const bool refill = spills && a.stash && tid == 0 && s_sused >= s_scap;  // refill only when used up

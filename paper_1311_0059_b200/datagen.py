@@ -149,7 +149,10 @@ def scaled(cfg: Config, n: int, **over) -> Config:
         kw["key_range"] = max(1, int(round(cfg.key_range * f)))
     if cfg.zipf_k:
         kw["zipf_k"] = max(1, int(round(cfg.zipf_k * f)))
-    if cfg.budget_groups:
+    if cfg.budget_groups and (cfg.key_range or cfg.zipf_k):
+        # the budget keeps its ratio to the groups: it scales with a key universe
+        # that scales (C2); C5's composite key universe (4096 x 1024) is fixed, so
+        # its 2%-of-groups budget is too
         kw["budget_groups"] = max(1, int(round(cfg.budget_groups * f)))
     kw.update(over)
     return dataclasses.replace(cfg, **kw)
