@@ -1865,8 +1865,18 @@ int aggb_sort_finish(Handle* h) {
       int pe2 = prof_begin(h, 9);
       k_tile_hist<<<grid, 256, 0, h->st>>>(a.w[pw.first], 8 * pw.second, n, counts.as<uint32_t>(), ntiles);
       TRY(scan_u32(h, counts.as<uint32_t>(), ntiles * 256, offs.as<unsigned long long>(), tmp));
-      k_scatter<<<grid, SORT_BLOCK, 0, h->st>>>(a, b, pw.first, 8 * pw.second, n, offs.as<unsigned long long>(),
-                                                ntiles);
+      if (a.nw == 2) {  // key word + one payload word: tile-local rank + SMEM reorder
+        const int smem2 = SORT_TILE * 16;
+        CU(cudaFuncSetAttribute((const void*)k_scatter2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+        int occ2 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_scatter2, S2_BLOCK, smem2);
+        const int grid2 = (int)std::min<int64_t>(ntiles, (int64_t)std::max(1, occ2) * h->sms);
+        k_scatter2<<<grid2, S2_BLOCK, smem2, h->st>>>(a, b, pw.first, 8 * pw.second, n,
+                                                        offs.as<unsigned long long>(), ntiles);
+      } else {
+        k_scatter<<<grid, SORT_BLOCK, 0, h->st>>>(a, b, pw.first, 8 * pw.second, n, offs.as<unsigned long long>(),
+                                                  ntiles);
+      }
       prof_end(h, pe2);
       h->launches += 2;
       CU(cudaGetLastError());

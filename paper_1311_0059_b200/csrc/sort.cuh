@@ -218,6 +218,104 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_scatter(SortBuf src, SortBuf dst
   }
 }
 
+// ---- tile-local radix rank + SMEM reorder (two-word records) -----------------
+// Records of two 8-byte words (key word + one payload word: the C4 shape).  Warp
+// w owns tile items [512 w, 512 w + 512), slot j its items 512 w + 32 j + lane,
+// so (warp, slot, lane) order is index order and the ranks are stable:
+//   1. per slot, match_any ranks the lanes of each digit; a per-warp SMEM
+//      counter carries the digit's running count across slots (no block barrier);
+//   2. per digit, an exclusive prefix over warps and a scan over digits give
+//      every record its tile-local rank;
+//   3. records are reordered in SMEM by rank, then written out in rank order:
+//      consecutive threads write consecutive records of a digit run to
+//      consecutive addresses (coalesced), instead of one scattered write each.
+constexpr int S2_BLOCK = 512, S2_IPT = SORT_TILE / S2_BLOCK, S2_WARPS = S2_BLOCK / 32;
+
+__global__ void __launch_bounds__(S2_BLOCK, 2) k_scatter2(SortBuf src, SortBuf dst, int key_word, int shift, int64_t n,
+                                                       const unsigned long long* offs /* [256][ntiles] excl */,
+                                                       int64_t ntiles) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* sk = (uint64_t*)smem;               // SORT_TILE key words (rank order)
+  uint64_t* sv = sk + SORT_TILE;                // SORT_TILE payload words
+  __shared__ uint32_t wcnt[S2_WARPS][256];      // per-warp digit counts -> per-warp exclusive bases
+  __shared__ uint32_t dbase[256];               // tile-local exclusive base of each digit
+  __shared__ unsigned long long goff[256];      // global base of each digit for this tile
+  __shared__ uint32_t wsum[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int other = 1 - key_word;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+#pragma unroll
+    for (int q = lane; q < 256; q += 32) wcnt[wid][q] = 0;
+    __syncwarp();
+    const int64_t base = t * SORT_TILE + (int64_t)wid * (S2_IPT * 32);
+    uint64_t kk[S2_IPT], vv[S2_IPT];
+    uint32_t rk[S2_IPT];
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      const int64_t i = base + j * 32 + lane;
+      const bool live = i < n;
+      kk[j] = live ? src.w[key_word][i] : 0ull;
+      vv[j] = live ? src.w[other][i] : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      const bool live = base + j * 32 + lane < n;
+      const int d = live ? (int)((kk[j] >> shift) & 255) : 256 + lane;  // dead lanes: unique, not counted
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const unsigned run = live ? wcnt[wid][d] : 0u;
+      rk[j] = run + __popc(peers & ((1u << lane) - 1u));
+      __syncwarp();
+      if (live && lane == __ffs(peers) - 1) wcnt[wid][d] = run + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit (threads 0..255): exclusive prefix over warps; digit totals -> scan over digits
+    const int d0 = threadIdx.x;
+    uint32_t acc = 0, x = 0;
+    if (d0 < 256) {
+#pragma unroll
+      for (int w = 0; w < S2_WARPS; w++) {
+        const uint32_t c = wcnt[w][d0];
+        wcnt[w][d0] = acc;
+        acc += c;
+      }
+      x = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[wid] = x;
+      goff[d0] = offs[(int64_t)d0 * ntiles + t];
+    }
+    __syncthreads();
+    if (d0 < 256) {
+      uint32_t pre = 0;
+      for (int w = 0; w < wid; w++) pre += wsum[w];
+      dbase[d0] = pre + x - acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      if (base + j * 32 + lane >= n) continue;
+      const int d = (int)((kk[j] >> shift) & 255);
+      const uint32_t r = dbase[d] + wcnt[wid][d] + rk[j];
+      sk[r] = kk[j];
+      sv[r] = vv[j];
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)SORT_TILE, n - t * SORT_TILE);
+    for (int q = threadIdx.x; q < cnt; q += S2_BLOCK) {
+      const uint64_t k = sk[q];
+      const int d = (int)((k >> shift) & 255);
+      const unsigned long long pos = goff[d] + (q - dbase[d]);
+      dst.w[key_word][pos] = k;
+      dst.w[other][pos] = sv[q];
+    }
+    __syncthreads();
+  }
+}
+
 // ---- segmented reduction ----------------------------------------------------
 
 template <int KW>
