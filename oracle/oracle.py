@@ -379,14 +379,11 @@ def frames_for_budget(target_groups: float, group_bytes: float, G_total: float,
     raise ValueError("budget too large")
 
 
-def timed_port_run(algo: str, keys: list, vals: list, aggs, bind, budget_groups: int,
-                   threads: int = 1, frame_size: int = 32768, seed: int = 7):
-    """Run the C port over a sample, key-hash-sharded over `threads` independent
-    operator instances (the reference's concurrency model: independent
-    instances).  Each shard gets budget/threads groups.
-    Returns (seconds, groups, metrics of shard 0); frame packing is excluded."""
-    import time
-    from concurrent.futures import ThreadPoolExecutor
+def prepare_port(algo: str, keys: list, vals: list, aggs, bind, budget_groups: int,
+                 threads: int = 1, frame_size: int = 32768):
+    """Shard a sample by key hash over `threads` independent operator instances
+    (the reference's concurrency model) and pack each shard
+    into reference frames; each shard gets budget/threads groups.  Untimed."""
     sp = ospec(aggs)
     states = init_states(sp, vals, list(bind))
     kr = key_rows(keys)
@@ -394,24 +391,41 @@ def timed_port_run(algo: str, keys: list, vals: list, aggs, bind, budget_groups:
                          if np.asarray(keys[i]).dtype.itemsize == 8 else
                          (kr[:, i].astype(np.uint32)).astype(">u4").view(np.uint8).reshape(len(kr), 4)
                          for i in range(len(keys))], axis=1)
+    kb = np.ascontiguousarray(kb)
     h = hash_bytes(kb, 0x5eed) % np.uint64(threads) if threads > 1 else np.zeros(len(kb), np.uint64)
+    rowv = kb.view(np.dtype((np.void, kb.shape[1]))).ravel()  # one opaque item per key row
     jobs = []
     for t in range(threads):
         sel = np.flatnonzero(h == t)
-        g_t = len(np.unique(kb[sel], axis=0)) if len(sel) else 0
+        g_t = len(np.unique(rowv[sel])) if len(sel) else 0
         rec = 2 + kb.shape[1] + 8 * sp.state_width
         fr = pack_frames(kb[sel], states[sel], frame_size)
         M = frames_for_budget(max(1, budget_groups / threads), rec, max(g_t, 1), frame_size, algo)
         stats = (max(fr.shape[0], 1), len(sel), g_t * rec / frame_size, g_t)
         jobs.append((fr, M, stats))
+    return {"algo": algo, "sp": sp, "jobs": jobs, "kmax": kb.shape[1], "frame_size": frame_size}
+
+
+def run_prepared(prep, seed: int = 7):
+    """Time the C port over prepared shards, one thread per shard.
+    Returns (seconds, groups, metrics of shard 0)."""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
 
     def one(job):
         fr, M, stats = job
-        return run_port(algo, fr, sp, memory_frames=M, frame_size=frame_size, stats=stats,
-                        seed=seed, kmax=kb.shape[1])
+        return run_port(prep["algo"], fr, prep["sp"], memory_frames=M, frame_size=prep["frame_size"],
+                        stats=stats, seed=seed, kmax=prep["kmax"])
 
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        outs = list(ex.map(one, jobs))
+    with ThreadPoolExecutor(max_workers=len(prep["jobs"])) as ex:
+        outs = list(ex.map(one, prep["jobs"]))
     dt = time.perf_counter() - t0
     return dt, sum(len(o.klens) for o in outs), outs[0].metrics
+
+
+def timed_port_run(algo: str, keys: list, vals: list, aggs, bind, budget_groups: int,
+                   threads: int = 1, frame_size: int = 32768, seed: int = 7):
+    """prepare_port + run_prepared: (seconds, groups, metrics of shard 0);
+    frame packing is excluded from the time."""
+    return run_prepared(prepare_port(algo, keys, vals, aggs, bind, budget_groups, threads, frame_size), seed)
