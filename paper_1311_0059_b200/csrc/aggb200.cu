@@ -372,6 +372,7 @@ struct Handle {
   // deferral
   DBuf defer;
   int64_t defer_cap = 0;
+  int defer_words = 0;      // words per record the deferral buffer holds
   // scratch: [0..7] stats, [8] tile counter A, [9] tile counter B, [10] defer count, [11] ovf count,
   // [12] item counter, [13] out count
   DBuf scratch;
@@ -845,7 +846,8 @@ int plan(Handle* h) {
   // budget, in the L2-resident table (drain, l2 children) — and the fan-out
   // only has to bring partitions under the budget.
   h->l2_children = false;
-  if (P > cap_parts && !h->unlimited && !getenv("AGGB_NO_L2_CHILDREN")) {
+  const bool force_l2 = getenv("AGGB_FORCE_L2_CHILDREN") != nullptr;  // test hook
+  if ((P > cap_parts || force_l2) && !h->unlimited && !getenv("AGGB_NO_L2_CHILDREN")) {
     h->l2_children = true;
     P = std::max(2, (int)std::ceil(spill_groups / std::max(1.0, 0.5 * (double)h->budget)));
   }
@@ -955,12 +957,16 @@ int stage_input(Handle* h, const aggb_input* in, Staged& sg) {
   return AGGB_OK;
 }
 
-int ensure_defer(Handle* h, int64_t T) {
-  // in flight at a freeze: every CTA's current and prefetched tile (x2 headroom)
+int ensure_defer(Handle* h, int64_t T, int payload_words) {
+  // in flight at a freeze: every CTA's current and prefetched tile (x2 headroom);
+  // records of payload_words words (raw values, or partial states in L2 children)
   int64_t need = (int64_t)h->sms * 8 * T + 4096;
-  if (need <= h->defer_cap) return AGGB_OK;
-  TRY(h->defer.ensure((size_t)need * (h->kw + std::max(1, h->cs.nv)) * 8, &h->hw));
+  const int words = h->kw + std::max(1, payload_words);
+  if (need <= h->defer_cap && words <= h->defer_words) return AGGB_OK;
+  need = std::max(need, h->defer_cap);
+  TRY(h->defer.ensure((size_t)need * std::max(words, h->defer_words) * 8, &h->hw));
   h->defer_cap = need;
+  h->defer_words = std::max(words, h->defer_words);
   return AGGB_OK;
 }
 
@@ -991,7 +997,7 @@ int push_hybrid(Handle* h, const ColSrc& col) {
   if (algo == AGGB_HASH_SORT) {  // FILL only: push_hash_sort handles freezes (cuts)
     int nwt = nwt_for(std::max(1, col.nv));
     PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
-    TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk));
+    TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk, col.nv));
     CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
     PassPlan f;
     f.mode = MODE_FILL;
@@ -1012,7 +1018,7 @@ int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss) {
   unsigned long long* ctrB = SC(h) + 9;
   int nwt = nwt_for(std::max(1, col.nv));
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
-  TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk));
+  TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk, col.nv));
   CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
   PassPlan f;
   f.mode = MODE_FILL;
@@ -1087,7 +1093,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
   int nwt = nwt_for(std::max(1, col0.nv));
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
   int64_t T = (int64_t)pcfg.R * pcfg.blk;
-  TRY(ensure_defer(h, T));
+  TRY(ensure_defer(h, T, col0.nv));
   std::vector<ColSrc> queue{col0};
   std::vector<DBuf> temps;
   int rc = AGGB_OK;

@@ -90,6 +90,28 @@ def test_golden_tight_budget_chunked(algo, case):
         assert met["spilled_records"] > 0 or algo == "hash_sort"
 
 
+@pytest.mark.parametrize("algo", ["pre_partitioning", "hash_sort"])
+@pytest.mark.parametrize("case", ["C2s", "C3s15", "C5s", "C2grace"])
+def test_l2_table_children(algo, case, monkeypatch):
+    """Spilled partitions aggregated by budget-sized L2-table children (the mode
+    wide states switch to when shared-memory children would recurse): each
+    partition gathered, FILL + PROBE against the budget table with fresh seeds,
+    overflow to the next level.  Forced here on the golden inputs at a budget of
+    1/8 of the groups (the large C5 shape that selects it on its own is timed by
+    tools/all_configs.py)."""
+    monkeypatch.setenv("AGGB_FORCE_L2_CHILDREN", "1")
+    path = [p for p in GOLD if os.path.basename(p).startswith(case + "__")][0]
+    meta, gkeys, gvals = load_golden(path)
+    cfg, keys, vals = golden_inputs(meta)
+    budget = max(8, gkeys.shape[0] // 8)
+    from paper_1311_0059_b200.core import DatasetStats
+    st = DatasetStats(*meta["stats"])
+    res, met = run_gpu(algo, cfg, keys, vals, chunks=2, budget_groups=budget, stats=st, seed=5)
+    check_against(res, gkeys, gvals, cfg)
+    if algo == "pre_partitioning":
+        assert met["spilled_records"] > 0 and met["recursion_depth"] >= 1
+
+
 @pytest.mark.parametrize("algo", ALGOS_GPU)
 def test_unknown_cardinality_in_memory_plan(algo):
     """Stats claim few groups (the plan is in-memory) but there are many:
