@@ -471,11 +471,10 @@ __device__ __forceinline__ int stable_lookup(uint64_t* keys, int nslots, int cap
     // slots probed in aligned pairs, one 16-byte shared load per pair; the probe
     // sequence starts at the pair of the home slot (inserts and lookups agree)
     int s = (int)(hash_key<KW>(k, seed) & (uint64_t)mask) & ~1;
+    const uint32_t keys_sh = (uint32_t)__cvta_generic_to_shared(keys);
     for (;;) {
       uint64_t w0, w1;
-      asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
-                   : "=l"(w0), "=l"(w1)
-                   : "r"((uint32_t)__cvta_generic_to_shared(keys + s)));
+      asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "r"(keys_sh + 8u * (uint32_t)s));
       int at = -1;
       if (w0 == k[0]) at = s;
       else if (w1 == k[0]) at = s + 1;

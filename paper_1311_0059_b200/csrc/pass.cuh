@@ -564,8 +564,6 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
   __shared__ unsigned long long s_item;
   __shared__ unsigned long long s_cnt[ST_NSTATS];
   __shared__ uint32_t s_fd[MAX_STATES];
-  constexpr int CHP = 512;  // pages staged per chunk
-  __shared__ uint32_t s_pg[CHP], s_off[CHP], s_scr[33];
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
   uint32_t nrec = 0, novf = 0;
@@ -593,44 +591,41 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
       const int kind = ss.kind;
       const int nw = ss.rw - KW;
       const int rw = ss.rw;
-      // the item's records, concatenated over its pages, map onto the threads
-      // (CTA-private page chains leave most pages partly filled: a page-per-row
-      // mapping idled the high warps).  Pages are staged CHP at a time: ids and
-      // exclusive record offsets in shared memory, one forward cursor per thread.
-      for (int64_t c0 = qa; c0 < qb; c0 += CHP) {
-        const int np = (int)min((int64_t)CHP, qb - c0);
-        __syncthreads();  // the previous chunk's readers are done with s_pg / s_off
-        for (int q = tid; q < np; q += B) {
-          const uint2 pe = a.plist[c0 + q];
-          s_pg[q] = pe.x;
-          s_off[q] = pe.y;
-        }
-        __syncthreads();
-        const uint32_t tot = block_exscan(s_off, np, s_scr);
-        int cur = 0;
-        auto load_round = [&](uint32_t i0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
+      // Warp-per-page mapping: warp w takes pages qa + w, qa + w + NWARPS, ...;
+      // lane l handles slots l, l + 32, ... of the page (no page search, one
+      // base address per page; ~15 records per lane for the ~484-record pages
+      // CTA-private chains leave).  The next chunk of R records per lane is
+      // prefetched while the current one aggregates; the next page's list
+      // entry is loaded one page ahead.
+      const int lane = tid & 31, wid = tid >> 5, nwarps = B >> 5;
+      auto load_chunk = [&](const uint64_t* pbase, int fill, int s0, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT],
+                            bool (&live)[R]) {
 #pragma unroll
-          for (int r = 0; r < R; r++) {
-            const uint32_t i = i0 + (uint32_t)(r * B + tid);
-            live[r] = i < tot;
-            if (live[r]) {
-              while (cur + 1 < np && s_off[cur + 1] <= i) cur++;
-              const uint64_t* src = (const uint64_t*)page_ptr(a.pool, s_pg[cur]) + (size_t)(i - s_off[cur]) * rw;
+        for (int r = 0; r < R; r++) {
+          const int slot = s0 + r * 32 + lane;
+          live[r] = slot < fill;
+          if (live[r]) {
+            const unsigned long long* src = (const unsigned long long*)pbase + (size_t)slot * rw;
 #pragma unroll
-              for (int w = 0; w < KW; w++) k[r][w] = __ldcs((const unsigned long long*)src + w);
+            for (int w = 0; w < KW; w++) k[r][w] = __ldcs(src + w);
 #pragma unroll
-              for (int w = 0; w < NWT; w++)
-                v[r][w] = (w < nw) ? (uint64_t)__ldcs((const unsigned long long*)src + KW + w) : 0ull;
-            }
+            for (int w = 0; w < NWT; w++) v[r][w] = (w < nw) ? (uint64_t)__ldcs(src + KW + w) : 0ull;
           }
-        };
+        }
+      };
+      uint2 pe_next = (qa + wid < qb) ? a.plist[qa + wid] : make_uint2(0, 0);
+      for (int64_t q = qa + wid; q < qb; q += nwarps) {
+        const uint2 pe = pe_next;
+        if (q + nwarps < qb) pe_next = a.plist[q + nwarps];
+        const uint64_t* pbase = (const uint64_t*)page_ptr(a.pool, pe.x);
+        const int fill = (int)pe.y;
         uint64_t kc[R][KW], vc[R][NWT];
         bool lc[R];
-        load_round(0, kc, vc, lc);
-        for (uint32_t i0 = 0; i0 < tot; i0 += (uint32_t)(R * B)) {
+        load_chunk(pbase, fill, 0, kc, vc, lc);
+        for (int s0 = 0; s0 < fill; s0 += R * 32) {
           uint64_t kn[R][KW], vn[R][NWT];
           bool ln[R];
-          load_round(i0 + (uint32_t)(R * B), kn, vn, ln);
+          load_chunk(pbase, fill, s0 + R * 32, kn, vn, ln);
 #pragma unroll
           for (int r = 0; r < R; r++) {
             int res = R_MISS, s = -1;
