@@ -373,6 +373,8 @@ struct Handle {
   DBuf defer;
   int64_t defer_cap = 0;
   int defer_words = 0;      // words per record the deferral buffer holds
+  unsigned long long last_cap_chunked = 0;  // chunk-region size of the last inserting pass
+  unsigned long long reopen[2] = {0, 0};    // host staging for a hash_sort table reopen
   // scratch: [0..7] stats, [8] tile counter A, [9] tile counter B, [10] defer count, [11] ovf count,
   // [12] item counter, [13] out count
   DBuf scratch;
@@ -660,6 +662,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
       a.cap_chunk = (uint32_t)chunk;
       a.cap_chunked = cap - std::min<uint64_t>(cap, 2ull * (uint64_t)grid * chunk);
     }
+    h->last_cap_chunked = a.cap_chunked;
   }
   if (pp.mode != MODE_FILL) {
     // upper bound of pages this pass can allocate
@@ -862,7 +865,11 @@ int setup_table(Handle* h) {
   t.stride = (uint64_t)slots + 1;
   t.mask = (uint64_t)slots - 1;
   t.bmask = (uint64_t)(slots / (h->kw == 1 ? 4 : 2)) - 1;
-  t.cap = (uint64_t)h->budget;
+  // Budgeted tables grant exactly the budget.  An unlimited (in-memory) table's
+  // "budget" is only a size estimate: grant up to 3/4 of its slots, so the
+  // reservations stranded by racing duplicate inserts (returned to per-CTA
+  // caches) cannot freeze a table that still has room.
+  t.cap = h->unlimited ? (uint64_t)slots * 3 / 4 : (uint64_t)h->budget;
   t.seed = level_seed(h->cfg.seed, SALT_SLOT, h->cfg.level);
   TRY(h->tkeys.ensure((size_t)(t.stride + 1) * h->kw * 8, &h->hw));
   TRY(h->tstates.ensure((size_t)t.stride * std::max(1, h->cs.ds.ns) * 8, &h->hw));
@@ -1097,6 +1104,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
   std::vector<ColSrc> queue{col0};
   std::vector<DBuf> temps;
   int rc = AGGB_OK;
+  unsigned long long last_committed = ~0ull;
   while (!queue.empty() && rc == AGGB_OK) {
     ColSrc cur = queue.back();
     queue.pop_back();
@@ -1107,13 +1115,33 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
     f.col = cur;
     f.counter = SC(h) + 8;
     if ((rc = launch_pass(h, f))) break;
-    unsigned long long tiles = 0, nd = 0;
+    unsigned long long tiles = 0, nd = 0, committed = 0;
     int frozen = 0;
     CU(cudaMemcpyAsync(&tiles, SC(h) + 8, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(&nd, SC(h) + 10, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&committed, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    if (getenv("AGGB_TRACE"))
+      fprintf(stderr, "[aggb] hash_sort FILL: %lld records, tiles %llu, deferred %llu, frozen %d, keys %llu\n",
+              (long long)cur.n, tiles, nd, frozen, committed);
     if (!frozen && !nd) continue;
+    // A freeze with room left is premature: racing inserts of one key each took a
+    // reservation before their CAS, and the losers' reservations stayed in their
+    // CTAs.  The reference cuts a run only when the table is full, so reopen the
+    // table (grants = keys held) and feed the rest again instead of cutting.
+    if (frozen && committed + std::max<uint64_t>(64, h->tab.cap / 64) < h->tab.cap &&
+        (committed != last_committed || tiles > 0)) {
+      // the keys held count against the chunk region first (kernels.cuh CapCache)
+      const unsigned long long cc = h->last_cap_chunked;
+      h->reopen[0] = committed <= cc ? 0ull : committed - cc;  // exact-region grants
+      h->reopen[1] = committed <= cc ? committed : cc;          // chunk-region grants
+      CU(cudaMemcpyAsync(&h->tab.hdr->groups, &h->reopen[0], 8, cudaMemcpyHostToDevice, h->st));
+      CU(cudaMemcpyAsync(&h->tab.hdr->chunked, &h->reopen[1], 8, cudaMemcpyHostToDevice, h->st));
+      CU(cudaMemsetAsync(&h->tab.hdr->frozen, 0, 4, h->st));
+      frozen = 0;
+    }
+    last_committed = committed;
     int64_t start = std::min<int64_t>(cur.n, (int64_t)tiles * T);
     // keep the deferred records (the deferral buffer is reused by the next FILL)
     ColSrc dc;
