@@ -402,6 +402,11 @@ struct Handle {
   int64_t sort_n = 0, sort_cap = 0;
   // staging for host inputs (grow-only)
   DBuf stage;
+  // pipelined host pushes: copy stream, two staging buffers, their events
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  DBuf pstage[2];
+  bool pstage_busy[2] = {false, false};  // an aggregation reading pstage[b] may still run (ev_used[b])
   // per-kernel CUDA-event timing (aggb_profile)
   bool prof = false;
   struct Ev { int kid; cudaEvent_t a, b; };
@@ -1509,21 +1514,109 @@ void aggb_destroy(void* handle) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->cst) cudaStreamSynchronize(h->cst);
   DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->pool_base, &h->page_part, &h->page_fill, &h->page_set,
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals};
   for (DBuf* b : bufs) b->release();
   h->stage.release();
+  h->pstage[0].release();
+  h->pstage[1].release();
   for (auto& e : h->evs) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
   }
   for (auto e : h->free_events) cudaEventDestroy(e);
   if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  if (h->cst) {
+    cudaStreamDestroy(h->cst);
+    for (int b = 0; b < 2; b++) {
+      cudaEventDestroy(h->ev_copied[b]);
+      cudaEventDestroy(h->ev_used[b]);
+    }
+  }
   delete h;
 }
 
+
+int push_col(Handle* h, const ColSrc& col) {
+  if (h->cfg.algo == AGGB_SORT_BASED) return aggb_sort_push(h, col);
+  if (h->cfg.algo == AGGB_HASH_SORT) return push_hash_sort(h, col);
+  return push_hybrid(h, col);
+}
+
+// Host input larger than two chunks: chunk c+2's host-to-device copy (copy
+// stream) overlaps chunk c's aggregation; two staging buffers alternate, each
+// refilled only after the aggregation that read it.  Each chunk is a push of
+// its own (the operators accept any number of pushes).
+int64_t pipe_chunk() {
+  const char* e = getenv("AGGB_PIPE_CHUNK");  // tests exercise the pipeline on small inputs
+  return e ? std::max<int64_t>(1, atoll(e)) : 25000000;
+}
+
+int push_pipelined(Handle* h, const aggb_input* in) {
+  const int64_t PIPE_CHUNK = pipe_chunk();
+  if (!h->cst) {
+    CU(cudaStreamCreateWithFlags(&h->cst, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; b++) {
+      CU(cudaEventCreateWithFlags(&h->ev_copied[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&h->ev_used[b], cudaEventDisableTiming));
+    }
+  }
+  const int nk = h->kw, nv = h->spec.n_vals;
+  auto esz = [&](bool key, int w) { return (key ? h->spec.key_type[w] : h->spec.val_type[w]) == AGGB_I32 ? 4 : 8; };
+  auto strd = [&](bool key, int w) {
+    const int64_t st = key ? in->key_stride[w] : in->val_stride[w];
+    return st ? st : (int64_t)esz(key, w);
+  };
+  auto span = [&](bool key, int w, int64_t rows) { return (size_t)((rows - 1) * strd(key, w) + esz(key, w)); };
+  size_t per = 0;
+  for (int w = 0; w < nk; w++) per += (span(true, w, PIPE_CHUNK) + 255) & ~(size_t)255;
+  for (int w = 0; w < nv; w++) per += (span(false, w, PIPE_CHUNK) + 255) & ~(size_t)255;
+  for (int b = 0; b < 2; b++) TRY(h->pstage[b].ensure(per, &h->hw));
+  const int64_t n = in->n_rows, nch = (n + PIPE_CHUNK - 1) / PIPE_CHUNK;
+  std::vector<std::vector<const uint8_t*>> ptrs(nch);
+  auto copy = [&](int64_t c) -> int {
+    const int b = (int)(c & 1);
+    const int64_t r0 = c * PIPE_CHUNK, rows = std::min<int64_t>(PIPE_CHUNK, n - r0);
+    if (h->pstage_busy[b]) CU(cudaStreamWaitEvent(h->cst, h->ev_used[b], 0));  // also across pushes
+    size_t off = 0;
+    ptrs[c].clear();
+    for (int q = 0; q < nk + nv; q++) {
+      const bool key = q < nk;
+      const int w = key ? q : q - nk;
+      const uint8_t* src = (const uint8_t*)(key ? in->key[w] : in->val[w]) + r0 * strd(key, w);
+      uint8_t* dst = h->pstage[b].as<uint8_t>() + off;
+      CU(cudaMemcpyAsync(dst, src, span(key, w, rows), cudaMemcpyHostToDevice, h->cst));
+      ptrs[c].push_back(dst);
+      off += (span(key, w, PIPE_CHUNK) + 255) & ~(size_t)255;
+    }
+    CU(cudaEventRecord(h->ev_copied[b], h->cst));
+    return AGGB_OK;
+  };
+  TRY(copy(0));
+  if (nch > 1) TRY(copy(1));
+  for (int64_t c = 0; c < nch; c++) {
+    const int b = (int)(c & 1);
+    const int64_t rows = std::min<int64_t>(PIPE_CHUNK, n - c * PIPE_CHUNK);
+    CU(cudaStreamWaitEvent(h->st, h->ev_copied[b], 0));
+    aggb_input part = *in;
+    part.n_rows = rows;
+    part.on_host = 0;
+    const void* kp[AGGB_MAX_KEYS];
+    const void* vp[AGGB_MAX_VALS];
+    for (int w = 0; w < nk; w++) kp[w] = ptrs[c][w];
+    for (int w = 0; w < nv; w++) vp[w] = ptrs[c][nk + w];
+    ColSrc col = col_of(h, &part, kp, vp);
+    h->records += rows;
+    TRY(push_col(h, col));
+    CU(cudaEventRecord(h->ev_used[b], h->st));
+    h->pstage_busy[b] = true;
+    if (c + 2 < nch) TRY(copy(c + 2));
+  }
+  return AGGB_OK;
+}
 
 int aggb_push(void* handle, const aggb_input* in) {
   Handle* h = (Handle*)handle;
@@ -1532,6 +1625,12 @@ int aggb_push(void* handle, const aggb_input* in) {
   if (in->n_rows < 0) return fail(AGGB_INVALID_ARG, "negative row count");
   if (in->n_rows == 0) return AGGB_OK;
   cudaSetDevice(h->device);
+  if (in->on_host && in->n_rows > 2 * pipe_chunk() && !getenv("AGGB_NO_PIPELINE")) {
+    Trace tr;
+    const int s = push_pipelined(h, in);
+    tr.mark(h->st, "push (pipelined)");
+    return s;
+  }
   Staged sg;
   TRY(stage_input(h, in, sg));
   ColSrc col = col_of(h, in, sg.k, sg.v);

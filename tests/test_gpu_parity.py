@@ -113,6 +113,21 @@ def test_l2_table_children(algo, case, monkeypatch):
 
 
 @pytest.mark.parametrize("algo", ALGOS_GPU)
+def test_pipelined_host_push(algo, monkeypatch):
+    """Host input larger than two chunks is copied on a second stream while the
+    previous chunk aggregates (chunk size shrunk here to exercise it): same
+    results, in one push and across pushes reusing the staging buffers."""
+    monkeypatch.setenv("AGGB_PIPE_CHUNK", "23456")
+    path = [p for p in GOLD if os.path.basename(p).startswith("C2s__")][0]
+    meta, gkeys, gvals = load_golden(path)
+    cfg, keys, vals = golden_inputs(meta)
+    budget = max(8, gkeys.shape[0] // 8)
+    for chunks in (1, 2):
+        res, _ = run_gpu(algo, cfg, keys, vals, chunks=chunks, budget_groups=budget, seed=3)
+        check_against(res, gkeys, gvals, cfg)
+
+
+@pytest.mark.parametrize("algo", ALGOS_GPU)
 def test_unknown_cardinality_in_memory_plan(algo):
     """Stats claim few groups (the plan is in-memory) but there are many:
     the table overflows and the spill path must still give exact results."""
