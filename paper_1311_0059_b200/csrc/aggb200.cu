@@ -1222,9 +1222,11 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     std::vector<unsigned long long> recs(nparts);
     std::vector<uint32_t> pages(2 * (size_t)nparts, 0);
     uint32_t ovfl = 0;
+    unsigned long long cnt_now = 0;  // output rows so far (the page scatter does not change it)
     CU(cudaMemcpyAsync(recs.data(), h->part_records.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(pages.data(), h->part_pages.p, (size_t)nparts * 4 * nsets, cudaMemcpyDeviceToHost, h->st));
     CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&cnt_now, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
     if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
     std::vector<uint32_t> offs(2 * (size_t)nparts);
@@ -1323,10 +1325,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     }
     // child pass: output room + overflow room
     max_items_out = (int64_t)nonempty * (h->child_cap + 1);
-    unsigned long long cnt = 0;
-    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaStreamSynchronize(h->st));
-    TRY(ensure_out(h, (int64_t)cnt + max_items_out + 16));
+    TRY(ensure_out(h, (int64_t)cnt_now + max_items_out + 16));
     int64_t total_recs = 0;
     for (int p = 0; p < nparts; p++) total_recs += (int64_t)recs[p];
     int ovw = h->kw + h->cs.ds.ns;
@@ -1691,10 +1690,13 @@ int aggb_finish(void* handle, aggb_result* out) {
       TRY(aggb_sort_finish(h));
     } else {
       int frozen = 0, refused = 0;
-      unsigned long long groups = 0;
+      unsigned long long groups = 0, cnt0 = 0, sp0 = 0;
+      // one round trip for everything the level-0 close needs
       CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&refused, &h->tab.hdr->pad, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&groups, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&cnt0, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&sp0, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
       if (h->cfg.algo == AGGB_ORIGINAL_HH && refused) frozen = 1;  // partition 0 spilled: cut the table
       h->met.resident_groups = (int64_t)groups;
@@ -1735,15 +1737,14 @@ int aggb_finish(void* handle, aggb_result* out) {
       } else if (h->cfg.algo == AGGB_HASH_SORT && h->hash_sort_runs > 0) {
         TRY(cut_run(h));  // last run; the merge-with-fold is the drain below
       } else {
-        TRY(flush_table(h, h->cfg.emit_partials != 0, nullptr));
+        // the table holds at most `groups` keys (+ the escape group): size the
+        // output from the counts read above, flush without another round trip
+        TRY(ensure_out(h, (int64_t)cnt0 + (int64_t)groups + 2));
+        OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+        TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
       }
       tr.mark(h->st, "finish: level-0 flush");
-      {
-        unsigned long long sp0 = 0;
-        CU(cudaMemcpyAsync(&sp0, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToHost, h->st));
-        CU(cudaStreamSynchronize(h->st));
-        h->met.level0_spilled_records = (int64_t)sp0;
-      }
+      h->met.level0_spilled_records = (int64_t)sp0;
       TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
     }
     unsigned long long cnt = 0, st[ST_NSTATS];
