@@ -375,6 +375,9 @@ struct Handle {
   int defer_words = 0;      // words per record the deferral buffer holds
   unsigned long long last_cap_chunked = 0;  // chunk-region size of the last inserting pass
   unsigned long long reopen[2] = {0, 0};    // host staging for a hash_sort table reopen
+  unsigned long long tail_sc[16] = {};      // scratch counters read after the last child pass
+  uint32_t tail_ovfl = 0;
+  bool tail_valid = false;
   // scratch: [0..7] stats, [8] tile counter A, [9] tile counter B, [10] defer count, [11] ovf count,
   // [12] item counter, [13] out count
   DBuf scratch;
@@ -1366,11 +1369,17 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     prof_end(h, pe);
     h->launches++;
     CU(cudaGetLastError());
-    unsigned long long novf = 0;
-    CU(cudaMemcpyAsync(&novf, SC(h) + 11, 8, cudaMemcpyDeviceToHost, h->st));
+    // one round trip: the overflow count, and (if this was the last level) the
+    // counters aggb_finish reads next
+    CU(cudaMemcpyAsync(h->tail_sc, SC(h), sizeof(h->tail_sc), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&h->tail_ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    const unsigned long long novf = h->tail_sc[11];
     tr.mark(h->st, "drain: child");
-    if (!novf) return AGGB_OK;
+    if (!novf) {
+      h->tail_valid = true;
+      return AGGB_OK;
+    }
     // next level: grace-partition the overflow with fresh seeds (fresh per level, hybrid.py:181-184).
     // Every page of this level has been consumed by the children, so the pool
     // is recycled: the next level writes its pages from page 0 again.
@@ -1685,6 +1694,7 @@ int aggb_finish(void* handle, aggb_result* out) {
   if (!h || !out) return fail(AGGB_INVALID_ARG, "null argument");
   cudaSetDevice(h->device);
   Trace tr;
+  h->tail_valid = false;
   if (!h->finished) {
     if (h->cfg.algo == AGGB_SORT_BASED) {
       TRY(aggb_sort_finish(h));
@@ -1749,10 +1759,16 @@ int aggb_finish(void* handle, aggb_result* out) {
     }
     unsigned long long cnt = 0, st[ST_NSTATS];
     uint32_t ovfl = 0;
-    CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaStreamSynchronize(h->st));
+    if (h->tail_valid) {  // read by drain right after the last child pass
+      cnt = h->tail_sc[13];
+      memcpy(st, h->tail_sc, sizeof(st));
+      ovfl = h->tail_ovfl;
+    } else {
+      CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+    }
     if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
     if ((int64_t)cnt > h->out_cap) return fail(AGGB_CAPACITY_EXCEEDED, "output buffer overflow (%llu > %lld)", cnt, (long long)h->out_cap);
     // typed key columns
