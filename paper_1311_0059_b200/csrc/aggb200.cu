@@ -839,9 +839,11 @@ int plan(Handle* h) {
     h->unlimited = false;
   }
   h->child_cap = (int)std::max<int64_t>(1, std::min<int64_t>(ccap, h->budget));
-  // spill fan-out: every child partition should fit half a child table
+  // spill fan-out: every child partition should fill ~40% of a child table
+  // (C2, profiles/r01_notes.md: child 1.08 -> 0.94 ms from 0.5 to 0.4 of the
+  // table — lower load, shorter probes, a finer tail — for +0.04 ms of PROBE)
   double spill_groups = std::max(0.0, std::max(G_t, 1.0) - (double)h->budget);
-  int P = (int)std::ceil(spill_groups / std::max(1.0, 0.5 * h->child_cap));
+  int P = (int)std::ceil(spill_groups / std::max(1.0, 0.4 * h->child_cap));
   P = std::max(P, 1);
   if (c.budget_groups == 0 && M >= 3) {
     double bg = ref_group_bytes(c, h->cs.ref_width, G, G_t);
@@ -849,7 +851,10 @@ int plan(Handle* h) {
     P = std::max(P, plan_partitions(G * F, M));  // Formula 1 as the floor
   }
   int rw0 = h->kw + h->cs.nv;
-  const int cap_parts = std::min(MAX_PARTS, max_parts_for(rw0));
+  int cap_parts = std::min(MAX_PARTS, max_parts_for(rw0));
+  // k_probe (one-word keys, one value) keeps its 128 KB bloom only up to ~2.3K
+  // partitions of shared-memory state (probe_smem); beyond, PROBE runs 2x slower
+  if (h->kw == 1 && h->cs.nv == 1) cap_parts = std::min(cap_parts, 2200);
   // Shared-memory children hold child_cap groups; when the fan-out that needs is
   // more than one spill pass can write, every level would retire only
   // cap_parts * child_cap groups (C5: ~20 levels).  Then each spilled partition
@@ -862,8 +867,23 @@ int plan(Handle* h) {
     h->l2_children = true;
     P = std::max(2, (int)std::ceil(spill_groups / std::max(1.0, 0.5 * (double)h->budget)));
   }
+  // whole waves of children: with several partitions per resident child CTA,
+  // round the fan-out down to a multiple of the resident child grid (the load
+  // per partition grows by at most 1/3: <= ~0.53 of a table)
+  if (!h->l2_children && P > 0) {
+    const int nwt = nwt_for(std::max(1, h->cs.nv));
+    child_fn cf = h->kw == 1 ? child_kernel<1>(nwt, h->prog) : child_kernel<2>(nwt, h->prog);
+    const size_t csm = ((size_t)(1 << h->child_slots_log2) + 1) * (h->kw + h->cs.ds.ns) * 8;
+    int occ = 0;
+    if (cudaFuncSetAttribute((const void*)cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cf, BLOCK, csm) == cudaSuccess && occ > 0) {
+      const int cg = occ * h->sms;
+      if (P >= 3 * cg) P = P / cg * cg;
+    }
+    cudaGetLastError();
+  }
   h->P0 = std::min(P, cap_parts);
-  if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment
+  if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment override
   return AGGB_OK;
 }
 
