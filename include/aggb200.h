@@ -138,6 +138,8 @@ typedef struct {
   int64_t kernel_launches;             /* kernels launched since create/reset  */
   int64_t hbm_bytes_alg;               /* algorithmic bytes     */
   int64_t level0_spilled_records;      /* records spilled before recursion     */
+  int64_t child_subpasses;             /* most sub-passes a child took (fan-out
+                                          beyond one spill pass)               */
 } aggb_metrics;
 
 /* Operator.__init__ + open() (base.py:131-137, hash_sort.py:27-38,

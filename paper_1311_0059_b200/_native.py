@@ -80,7 +80,7 @@ class Metrics(ctypes.Structure):
         "records", "output_groups", "resident_groups", "spilled_records", "spilled_bytes",
         "spilled_partitions", "recursion_depth", "grace_levels", "fallbacks",
         "high_water_bytes", "budget_groups", "partitions_level0", "kernel_launches",
-        "hbm_bytes_alg", "level0_spilled_records")]
+        "hbm_bytes_alg", "level0_spilled_records", "child_subpasses")]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -108,7 +108,7 @@ uint64_t splitmix(uint64_t z) {
 }
 
 // role salts as in the reference (hybrid.py:57-60, hash_sort.py:32-33)
-enum { SALT_PART = 0x11, SALT_SLOT = 0x22, SALT_SPILL = 0x33, SALT_EXCH = 0x77 };
+enum { SALT_PART = 0x11, SALT_SLOT = 0x22, SALT_SPILL = 0x33, SALT_SUB = 0x44, SALT_EXCH = 0x77 };
 uint64_t level_seed(uint64_t seed, int salt, int level) {
   return splitmix(splitmix(seed) ^ ((uint64_t)salt + ((uint64_t)level << 8)));
 }
@@ -288,15 +288,30 @@ PassCfg pass_kernel(int nwt, int prog) {
 }
 
 // PROBE specialised for one-word keys and one dense 8-byte value column (probe.cuh)
-PassCfg probe_kernel(int prog) {
-  if (prog == 1) return PassCfg{k_probe<4, 512, ProgC1>, 4, 512};
-  if (prog == 2) return PassCfg{k_probe<4, 512, ProgC2>, 4, 512};
-  if (prog == 3) return PassCfg{k_probe<4, 512, ProgC3>, 4, 512};
-  return PassCfg{k_probe<4, 512, PD>, 4, 512};
+template <int PM, int R = 4, int BLK = 512>
+PassCfg probe_kernel_pm(int prog) {
+  if (prog == 1) return PassCfg{k_probe<R, BLK, ProgC1, PM>, R, BLK};
+  if (prog == 2) return PassCfg{k_probe<R, BLK, ProgC2, PM>, R, BLK};
+  if (prog == 3) return PassCfg{k_probe<R, BLK, ProgC3, PM>, R, BLK};
+  return PassCfg{k_probe<R, BLK, PD, PM>, R, BLK};
+}
+PassCfg probe_kernel(int prog, int pm) {
+  if (pm == PM_SCAN) {
+    const char* e = getenv("AGGB_SCAN_CFG");  // launch-shape experiments
+    if (e && !strcmp(e, "4x768")) return probe_kernel_pm<PM_SCAN, 4, 768>(prog);
+    if (e && !strcmp(e, "2x1024")) return probe_kernel_pm<PM_SCAN, 2, 1024>(prog);
+    if (e && !strcmp(e, "3x1024")) return probe_kernel_pm<PM_SCAN, 3, 1024>(prog);
+    if (e && !strcmp(e, "8x256")) return probe_kernel_pm<PM_SCAN, 8, 256>(prog);
+    return probe_kernel_pm<PM_SCAN>(prog);
+  }
+  if (pm == PM_RESOLVE) return probe_kernel_pm<PM_RESOLVE>(prog);
+  return probe_kernel_pm<PM_ONE>(prog);
 }
 
-size_t probe_smem(int P, int bloom_words, int blk) {
-  return (size_t)((bloom_words + 1) & ~1) * 8 + (size_t)(blk / 32) * PQ_RING * 16 + (size_t)P * (4 + 4 * 8) + 64;
+size_t probe_smem(int P, int bloom_words, int blk, int pm, bool pairs) {
+  const size_t ring = pm == PM_SCAN ? 0 : (size_t)(blk / 32) * PQ_RING * 16;
+  const size_t pk = (pairs && pm != PM_RESOLVE) ? (size_t)P * (16 + 4) + 16 : 0;  // parked record + tag
+  return (size_t)((bloom_words + 1) & ~1) * 8 + ring + (size_t)P * (4 + 4 * 8) + pk + 64;
 }
 
 template <int KW>
@@ -355,6 +370,8 @@ struct Handle {
   bool unlimited = false;
   bool l2_children = false; // spilled partitions aggregate in the budget-sized L2 table (drain)
   int P0 = 1;               // level-0 spill fan-out
+  int nsub0 = 1;            // sub-passes per level-1 child (fan-out beyond one spill pass)
+  int64_t fanout_need = 1;  // level-0 fan-out the child capacity asks for (P0 x nsub0)
   int child_slots_log2 = 11;
   int child_cap = 1024;
   // level-0 table
@@ -400,6 +417,8 @@ struct Handle {
   int64_t bloom_words = 0;
   uint64_t bloom_seed = 0;
   int64_t ovf_cap = 0;
+  // two-phase PROBE: candidate regions (bloom positives), open chains per (CTA, partition)
+  DBuf cand, chains;
   // sort path
   DBuf sort_keys, sort_vals;
   int64_t sort_n = 0, sort_cap = 0;
@@ -421,8 +440,8 @@ struct Handle {
 
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
-                        "k_exchange_pack", "k_segreduce", "k_bloom_build"};
-constexpr int NKINDS = 13;
+                        "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>"};
+constexpr int NKINDS = 14;
 
 int prof_begin(Handle* h, int kid) {
   if (!h->prof) return -1;
@@ -584,7 +603,9 @@ int launch_pass(Handle* h, PassPlan& pp) {
                                   (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
                           !getenv("AGGB_GENERIC_PROBE");
   const int T_fill = pcfg.R * pcfg.blk;  // tile size of the FILL pass (start_tiles counts its tiles)
-  if (fast_probe) pcfg = probe_kernel(h->prog);
+  // two-phase PROBE (probe.cuh): a streaming partition pass, then the bloom positives
+  const bool split = fast_probe && h->bloom_words && getenv("AGGB_SPLIT");
+  if (fast_probe) pcfg = probe_kernel(h->prog, split ? PM_SCAN : PM_ONE);
   pass_fn fn = pcfg.fn;
   int R = pcfg.R, blk = pcfg.blk;
   int T = R * blk;
@@ -594,8 +615,17 @@ int launch_pass(Handle* h, PassPlan& pp) {
     bl.mask = (uint32_t)h->bloom_words - 1;
     bl.seed = h->bloom_seed;
   }
-  auto smem_of = [&](int bw) { return fast_probe ? probe_smem(P, bw, blk) : pass_smem(P, G, rw, bw); };
+  // sector pairs pay off in the split scan only (C2: scan 1.83 -> 1.68 ms); in the
+  // one-pass kernel the deferred odd records lengthen the tile (2.15 -> 2.48 ms)
+  bool pairs = fast_probe && split && !getenv("AGGB_NO_PAIRS");
+  auto smem_of = [&](int bw) {
+    return fast_probe ? probe_smem(P, bw, blk, split ? PM_SCAN : PM_ONE, pairs) : pass_smem(P, G, rw, bw);
+  };
   size_t smem = smem_of(bl.words ? (int)h->bloom_words : 0);
+  if (smem > 226 * 1024 && pairs) {  // no room for sector pairs: the bloom filter matters more
+    pairs = false;
+    smem = smem_of(bl.words ? (int)h->bloom_words : 0);
+  }
   if (smem > 227 * 1024 && bl.words) {  // no room: probe without the filter
     bl.words = nullptr;
     smem = smem_of(0);
@@ -662,6 +692,8 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.tile_counter = pp.counter;
   a.stats = SC(h);
   a.cache_log2 = cache_log2;
+  a.dbg = getenv("AGGB_DBG") ? atoi(getenv("AGGB_DBG")) : 0;
+  a.pairs = pairs ? 1 : 0;
   // chunked reservations for large tables: unused chunks (< grid * chunk) stay under 1% of cap
   {
     const uint64_t cap = h->tab.cap;
@@ -683,9 +715,24 @@ int launch_pass(Handle* h, PassPlan& pp) {
     // window; each CTA may leave one unused refill behind
     const uint64_t per_cta = pages / (uint64_t)grid;
     a.stash = per_cta >= 64 ? 32 : 0;
-    pages += (uint64_t)grid * 2 * a.stash;
+    pages += (uint64_t)grid * 2 * a.stash * (split ? 2 : 1);
     TRY(pool_ensure(h, pages));
     a.pool = pool_of(h);
+  }
+  size_t smem_b = 0;
+  pass_fn fn_b = nullptr;
+  if (split) {
+    const int64_t recs = pp.col.n + (pp.lin_count ? pp.lin_stride : 0);
+    a.cand_stride = recs / NREG + 2 * T + 64;
+    TRY(h->cand.ensure((size_t)a.cand_stride * 2 * NREG * 8, &h->hw));
+    TRY(h->chains.ensure((size_t)grid * P * sizeof(uint2), &h->hw));
+    a.cand = h->cand.as<uint64_t>();
+    a.cand_count = SC(h) + 24;
+    a.chains = h->chains.as<uint2>();
+    CU(cudaMemsetAsync(a.cand_count, 0, NREG * 8, h->st));
+    fn_b = probe_kernel(h->prog, PM_RESOLVE).fn;
+    smem_b = probe_smem(P, 0, 512, PM_RESOLVE, false);
+    CU(cudaFuncSetAttribute((const void*)fn_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b));
   }
   CU(cudaMemsetAsync(pp.counter, 0, 8, h->st));
   int pe = prof_begin(h, pp.mode);
@@ -693,6 +740,16 @@ int launch_pass(Handle* h, PassPlan& pp) {
   prof_end(h, pe);
   h->launches++;
   CU(cudaGetLastError());
+  if (split) {
+    // phase 2 on the same grid: CTA c reopens CTA c's chains
+    a.tile_counter = SC(h) + 20;
+    CU(cudaMemsetAsync(a.tile_counter, 0, 8, h->st));
+    pe = prof_begin(h, 13);
+    fn_b<<<grid, 512, smem_b, h->st>>>(a);
+    prof_end(h, pe);
+    h->launches++;
+    CU(cudaGetLastError());
+  }
   return AGGB_OK;
 }
 
@@ -855,17 +912,25 @@ int plan(Handle* h) {
   // k_probe (one-word keys, one value) keeps its 128 KB bloom only up to ~2.3K
   // partitions of shared-memory state (probe_smem); beyond, PROBE runs 2x slower
   if (h->kw == 1 && h->cs.nv == 1) cap_parts = std::min(cap_parts, 2200);
+  if (getenv("AGGB_MAX_P0")) cap_parts = std::max(2, std::min(cap_parts, atoi(getenv("AGGB_MAX_P0"))));  // test hook
   // Shared-memory children hold child_cap groups; when the fan-out that needs is
   // more than one spill pass can write, every level would retire only
-  // cap_parts * child_cap groups (C5: ~20 levels).  Then each spilled partition
-  // is aggregated like the reference's child operator instead — with the full
-  // budget, in the L2-resident table (drain, l2 children) — and the fan-out
-  // only has to bring partitions under the budget.
+  // cap_parts * child_cap groups (C5: ~20 levels).  Then each child CTA takes
+  // its partition in nsub sub-passes: sub-pass s aggregates only the records
+  // whose sub-hash (an independent seed) falls in range s, in a fresh table,
+  // and flushes — the fan-out is P0 x nsub with one spill pass, at the price of
+  // re-reading a partition nsub times (C5 100M: 1,211 L2-table children,
+  // 134 ms -> SMEM sub-passes).  The L2-table child (the reference's child
+  // operator with the full budget) stays behind a test hook.
   h->l2_children = false;
+  h->nsub0 = 1;
   const bool force_l2 = getenv("AGGB_FORCE_L2_CHILDREN") != nullptr;  // test hook
-  if ((P > cap_parts || force_l2) && !h->unlimited && !getenv("AGGB_NO_L2_CHILDREN")) {
+  if (force_l2 && !h->unlimited) {
     h->l2_children = true;
     P = std::max(2, (int)std::ceil(spill_groups / std::max(1.0, 0.5 * (double)h->budget)));
+  } else if (P > cap_parts) {
+    h->nsub0 = (P + cap_parts - 1) / cap_parts;
+    P = (P + h->nsub0 - 1) / h->nsub0;
   }
   // whole waves of children: with several partitions per resident child CTA,
   // round the fan-out down to a multiple of the resident child grid (the load
@@ -884,6 +949,7 @@ int plan(Handle* h) {
   }
   h->P0 = std::min(P, cap_parts);
   if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment override
+  h->fanout_need = (int64_t)h->P0 * h->nsub0;
   return AGGB_OK;
 }
 
@@ -1216,6 +1282,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
 
 int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) {
   int depth = level;
+  int nsub = h->nsub0;  // sub-passes per child at this level (plan)
   Trace tr;
   for (int guard = 0; guard < 24; guard++) {
     if (!a_live && !b_live) return AGGB_OK;
@@ -1225,6 +1292,10 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     }
     int nparts = std::max(a.ss.nparts, b_live ? b.ss.nparts : 0);
     int nsets = b_live ? 2 : 1;
+    if (depth == level) {  // level-0 sets: a set with fewer partitions (wide partial states) needs more sub-passes
+      const int pmin = b_live ? std::min(a.ss.nparts, b.ss.nparts) : a.ss.nparts;
+      nsub = (int)std::max<int64_t>(h->nsub0, (h->fanout_need + pmin - 1) / std::max(1, pmin));
+    }
     TRY(h->part_records.ensure((size_t)nparts * 8, &h->hw));
     TRY(h->part_pages.ensure((size_t)nparts * 8, &h->hw));
     TRY(h->cursor.ensure((size_t)nparts * 8, &h->hw));
@@ -1347,7 +1418,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
       continue;
     }
     // child pass: output room + overflow room
-    max_items_out = (int64_t)nonempty * (h->child_cap + 1);
+    max_items_out = (int64_t)nonempty * nsub * (h->child_cap + 1);
     TRY(ensure_out(h, (int64_t)cnt_now + max_items_out + 16));
     int64_t total_recs = 0;
     for (int p = 0; p < nparts; p++) total_recs += (int64_t)recs[p];
@@ -1377,6 +1448,9 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     ca.slots_log2 = h->child_slots_log2;
     ca.cap = h->child_cap;
     ca.seed = level_seed(h->cfg.seed, SALT_SLOT, depth + 1);
+    ca.nsub = nsub;
+    ca.sub_seed = level_seed(h->cfg.seed, SALT_SUB, depth + 1);
+    h->met.child_subpasses = std::max<int64_t>(h->met.child_subpasses, nsub);
     ca.out = outbuf(h, h->cfg.emit_partials ? 1 : 0);
     ca.ovf = h->ovf.as<uint64_t>();
     ca.ovf_stride = h->ovf_cap;
@@ -1406,8 +1480,12 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     CU(cudaMemsetAsync(h->pool_ctr.p, 0, 8, h->st));
     h->pool_bound = 0;
     depth++;
-    int P = (int)std::min<int64_t>(max_parts_for(h->kw + h->cs.ds.ns),
-                                   std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.5 * h->child_cap))));
+    // novf records bound the groups from above; beyond one pass's fan-out the
+    // children take sub-passes (at most 4: the bound is loose)
+    const int64_t need = std::max<int64_t>(2, (int64_t)std::ceil(novf / std::max(1.0, 0.5 * h->child_cap)));
+    const int pmax = max_parts_for(h->kw + h->cs.ds.ns);
+    int P = (int)std::min<int64_t>(pmax, need);
+    nsub = (int)std::min<int64_t>(4, (need + pmax - 1) / pmax);
     SetInfo nxt{make_set(h, P, h->cs.ds.ns, 1, level_seed(h->cfg.seed, SALT_SPILL, depth)), 0};
     // move the overflow list into a staging copy (ovf is reused by the next child pass)
     DBuf tmp;

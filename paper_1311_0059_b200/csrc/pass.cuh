@@ -46,6 +46,13 @@ struct PassArgs {
   int32_t cache_log2;                     // FILL, one-word keys: SMEM pre-aggregation slots (0: off)
   uint32_t cap_chunk;                     // table reservations per CTA chunk (0: exact path only)
   unsigned long long cap_chunked;         // capacity handed out in chunks (kernels.cuh CapCache)
+  // two-phase PROBE (probe.cuh, k_probe PM_SCAN / PM_RESOLVE)
+  uint64_t* cand;                         // bloom positives: NREG regions of keys, then NREG of values
+  int64_t cand_stride;                    // records per region
+  unsigned long long* cand_count;         // [NREG]
+  uint2* chains;                          // per (CTA, partition): {records claimed, page of the last claim}
+  int32_t pairs;                          // k_probe: sector pairs on (shared memory permitting)
+  int32_t dbg;                            // experiments only (AGGB_DBG); 0 in production
 };
 
 template <int KW, int NWT>
@@ -535,6 +542,8 @@ struct ChildArgs {
   int32_t slots_log2;       // SMEM table slots
   int32_t cap;              // group capacity (<= budget)
   uint64_t seed;            // slot hash seed of this level
+  int32_t nsub;             // sub-passes per item (1: one table holds the partition)
+  uint64_t sub_seed;        // sub-pass hash seed (independent of the slot and spill seeds)
   OutBuf out;
   uint64_t* ovf;            // overflow list: native partial records, SoA KW + ns words
   int64_t ovf_stride;
@@ -568,8 +577,12 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
   uint32_t nrec = 0, novf = 0;
 
+  const int nsub = max(1, a.nsub);
+  int sub = nsub - 1;
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(a.item_counter, 1ull);
+    // an item runs nsub sub-passes, each in a fresh table (one flush each)
+    if (++sub == nsub) sub = 0;
+    if (tid == 0 && sub == 0) s_item = atomicAdd(a.item_counter, 1ull);
     for (int i = tid; i < stride; i += B) {
 #pragma unroll
       for (int w = 0; w < KW; w++) skeys[(size_t)i * KW + w] = EMPTY;
@@ -629,6 +642,7 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
 #pragma unroll
           for (int r = 0; r < R; r++) {
             int res = R_MISS, s = -1;
+            if (nsub > 1 && lc[r]) lc[r] = reduce32(hash_key<KW>(kc[r], a.sub_seed), (uint32_t)nsub) == (uint32_t)sub;
             if (lc[r]) {
               nrec++;
               s = stable_lookup<KW>(skeys, nslots, a.cap, kc[r], a.seed, true, s_groups, &s_frozen, &s_esc,

@@ -66,48 +66,114 @@ __device__ __forceinline__ void probe_issue(const PassArgs& a, uint64_t k, uint6
 // allocator is still in flight) is written after the tile's barrier, when
 // every allocation of the tile is visible.  8 map entries cover a tile: a map
 // entry is reused only 7 pages (3584 records) later, more than a tile holds.
-template <int R, int BLK, class PG>
+//
+// Phases (PM):
+//   PM_ONE     one pass: bloom positives resolved through the per-warp ring.
+//   PM_SCAN    two-phase PROBE, phase 1: a pure streaming partition pass.  Bloom
+//              positives (~15% on C2) are appended to NREG candidate regions
+//              (one atomic per warp and tile; warp w writes region w mod NREG,
+//              which bounds a region by a quarter of the records) and every
+//              other record spills.  No probe latency sits inside the tile
+//              loop.  The chains stay open: each CTA saves {cnt, last page}
+//              per partition.
+//   PM_RESOLVE phase 2 (same grid): CTA c reopens CTA c's chains, resolves the
+//              candidates 32 at a time through the ring (every lane busy),
+//              spills the misses (bloom false positives) into the same chains
+//              and seals them.
+constexpr int PM_ONE = 0, PM_SCAN = 1, PM_RESOLVE = 2;
+constexpr int NREG = 4;
+
+template <int R, int BLK, class PG, int PM>
 __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   constexpr int T = R * BLK, NWARP = BLK / 32;
   constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
   constexpr int NE = 8;                   // page-map entries per partition
   static_assert((NE - 1) * S >= T, "a page-map entry must outlive a tile");
+  static_assert(NWARP % NREG == 0, "candidate regions split the warps evenly");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int P = a.ss.nparts;
-  const int nbw = a.bloom.words ? (int)a.bloom.mask + 1 : 0;
+  const int nbw = (PM != PM_RESOLVE && a.bloom.words) ? (int)a.bloom.mask + 1 : 0;
   uint64_t* sbloom = (uint64_t*)smem;
-  ulonglong2* ring = (ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + wid * PQ_RING;  // this warp's ring (16-B aligned)
-  uint32_t* cnt = (uint32_t*)((ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + NWARP * PQ_RING);  // P
+  constexpr int RING = PM == PM_SCAN ? 0 : PQ_RING;                          // phase 1 has no ring
+  ulonglong2* ring = (ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + wid * RING;  // this warp's ring (16-B aligned)
+  uint32_t* cnt = (uint32_t*)((ulonglong2*)(sbloom + ((nbw + 1) & ~1)) + NWARP * RING);  // P
   uint32_t* ent = cnt + P;                                                                 // P * NE
+  // PM_SCAN sector pairs: records 2m and 2m+1 of a chain leave as one 32-byte
+  // store.  The even one parks in pk[p] (tag ptag[p] = m) and the odd one takes
+  // it; when the slot is busy the even one is written alone, and an odd one
+  // that does not find its partner parked (after the tile's barrier, every
+  // even record has parked or been written) is written alone too.
+  const bool PAIR = PM != PM_RESOLVE && a.pairs;
+  ulonglong2* pk = (ulonglong2*)(((uintptr_t)(ent + P * NE) + 15) & ~(uintptr_t)15);  // P (PAIR)
+  uint32_t* ptag = (uint32_t*)(pk + (PM != PM_RESOLVE ? P : 0));                        // P (PAIR)
+  constexpr uint32_t FREE = 0xFFFFFFFFu, BUSY = 0x80000000u;
   __shared__ uint32_t s_hm[NWARP][R];
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_grab[2];
   __shared__ uint32_t s_sb[2], s_su[2], s_sc[2];  // page stash by tile parity: base, used, capacity
   __shared__ unsigned long long s_cnt[ST_NSTATS];
+  __shared__ unsigned long long s_rt[NREG + 1];    // PM_RESOLVE: first tile of each candidate region
+  __shared__ unsigned long long s_rn[NREG];        // PM_RESOLVE: candidates per region
 
-  const int64_t n = a.col.n;
-  const int64_t col_start =
-      a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
+  const int64_t n = PM == PM_RESOLVE ? 0 : a.col.n;
+  const int64_t col_start = (PM != PM_RESOLVE && a.start_tiles)
+                                ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T)
+                                : 0;
   const int64_t col_tiles = (n - col_start + T - 1) / T;
-  const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
-  const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
-  if (total == 0) return;  // FILL took the whole batch: nothing to spill
+  const int64_t n_lin = (PM != PM_RESOLVE && a.lin_count) ? (int64_t)*a.lin_count : 0;
 
   const int ns = a.sp.ns;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
   for (int p = tid; p < P; p += BLK) cnt[p] = 0;
   for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
+  if (PAIR)
+    for (int p = tid; p < P; p += BLK) ptag[p] = FREE;
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
+  if (PM == PM_RESOLVE && tid == 0) {
+    unsigned long long acc = 0;
+    for (int g = 0; g < NREG; g++) {
+      s_rt[g] = acc;
+      s_rn[g] = a.cand_count[g];
+      acc += (s_rn[g] + T - 1) / T;
+    }
+    s_rt[NREG] = acc;
+  }
   for (int i = tid; i < nbw; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom.words + i);
+  __syncthreads();
+  if (PM == PM_RESOLVE) {  // reopen the chains phase 1 left in this CTA's name
+    for (int p = tid; p < P; p += BLK) {
+      const uint2 c = a.chains[(size_t)blockIdx.x * P + p];
+      cnt[p] = c.x;
+      if (c.x) {
+        const uint32_t j = (c.x - 1) >> SLOG;
+        ent[p * NE + (j & (NE - 1))] = (c.y << 8) | (j & 0xFFu);
+      }
+    }
+  }
+  const unsigned long long total =
+      PM == PM_RESOLVE ? s_rt[NREG] : (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
   uint64_t* const pool = (uint64_t*)a.pool.base;
 
   auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R], uint64_t (&v)[R], bool (&live)[R]) {
-    const int src = (int64_t)tile < col_tiles ? 0 : 1;
-    const int64_t base = src == 0 ? col_start + (int64_t)tile * T : ((int64_t)tile - col_tiles) * T;
-    const int64_t end = src == 0 ? n : n_lin;
-    const long long* kp = (const long long*)(src == 0 ? a.col.key[0] : a.lin.key[0]);
-    const long long* vp = (const long long*)(src == 0 ? a.col.val[0] : a.lin.val[0]);
+    int64_t base, end;
+    const long long *kp, *vp;
+    if constexpr (PM == PM_RESOLVE) {
+      int g = 0;
+#pragma unroll
+      for (int q = 1; q < NREG; q++)
+        if (tile >= s_rt[q]) g = q;
+      base = (int64_t)(tile - s_rt[g]) * T;
+      end = (int64_t)s_rn[g];
+      kp = (const long long*)a.cand + (size_t)g * a.cand_stride;
+      vp = kp + (size_t)NREG * a.cand_stride;
+    } else {
+      const int src = (int64_t)tile < col_tiles ? 0 : 1;
+      base = src == 0 ? col_start + (int64_t)tile * T : ((int64_t)tile - col_tiles) * T;
+      end = src == 0 ? n : n_lin;
+      kp = (const long long*)(src == 0 ? a.col.key[0] : a.lin.key[0]);
+      vp = (const long long*)(src == 0 ? a.col.val[0] : a.lin.val[0]);
+    }
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int64_t i = base + r * BLK + tid;
@@ -118,15 +184,46 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       }
     }
   };
+  auto put2 = [&](uint32_t pg, uint32_t slot_even, ulonglong2 e, uint64_t k, uint64_t v) {  // one full sector
+    if (pg < 0xFFFFFFu)
+      asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(pool + (((size_t)pg << SLOG) + slot_even) * 2),
+                   "l"(e.x), "l"(e.y), "l"(k), "l"(v)
+                   : "memory");
+  };
   auto put = [&](uint32_t pg, uint32_t slot, uint64_t k, uint64_t v) {
+    if (a.dbg == 1) return;
+    if (a.dbg == 2) {
+      __stcg((ulonglong2*)(pool + ((size_t)blockIdx.x * BLK + tid) * 2), make_ulonglong2(k, v));
+      return;
+    }
+    if (a.dbg == 3) {  // same scatter pattern, aliased into a small (L2-resident) window
+      if (pg < 0xFFFFFFu) __stcg((ulonglong2*)(pool + ((((size_t)pg & 63) << SLOG) + slot) * 2), make_ulonglong2(k, v));
+      return;
+    }
+    if (a.dbg == 4) {  // sector-complete: the record and its pair slot written back to back
+      if (pg < 0xFFFFFFu) {
+        ulonglong2* q = (ulonglong2*)(pool + (((size_t)pg << SLOG) + (slot & ~1u)) * 2);
+        __stcg(q, make_ulonglong2(k, v));
+        __stcg(q + 1, make_ulonglong2(k, v));
+      }
+      return;
+    }
+    if (a.dbg == 5) {  // one 32-byte store per PAIR of records (half the transactions)
+      if (pg < 0xFFFFFFu && (slot & 1)) {
+        ulonglong2* q = (ulonglong2*)(pool + (((size_t)pg << SLOG) + (slot & ~1u)) * 2);
+        __stcg(q, make_ulonglong2(k, v));
+        __stcg(q + 1, make_ulonglong2(k, v));
+      }
+      return;
+    }
     if (pg < 0xFFFFFFu) __stcg((ulonglong2*)(pool + (((size_t)pg << SLOG) + slot) * 2), make_ulonglong2(k, v));
   };
 
   // tiles are grabbed two ahead: s_grab[t & 1] holds the index of this CTA's tile t
   if (tid == 0) {
     s_sb[0] = s_sb[1] = s_su[0] = s_su[1] = s_sc[0] = s_sc[1] = 0;
-    s_grab[0] = atomicAdd(a.tile_counter, 1ull);
-    s_grab[1] = atomicAdd(a.tile_counter, 1ull);
+    s_grab[0] = total ? atomicAdd(a.tile_counter, 1ull) : 0ull;
+    s_grab[1] = total ? atomicAdd(a.tile_counter, 1ull) : 0ull;
   }
   __syncthreads();
   unsigned long long cur = s_grab[0], nxt = s_grab[1];
@@ -165,91 +262,150 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       }
       // a positive is resolved by some lane of the warp shortly: pull its first
       // bucket into L1 now (the frozen table is read-only for this kernel)
-      if (posv && kc[r] != EMPTY)
+      if (PM == PM_ONE && posv && kc[r] != EMPTY)
         asm volatile("prefetch.global.L1 [%0];" ::"l"(a.t.keys + (h & a.t.bmask) * 4));
       seq[r] = posv ? 0u : ~0u;
+    }
+    // ---- PM_SCAN: reserve this warp's candidate slots now (one atomic per warp
+    // and tile); the result is consumed after the claims, which hide its latency
+    uint32_t mk[R], ctot = 0;
+    unsigned long long cbase = 0;
+    if constexpr (PM == PM_SCAN) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        mk[r] = __ballot_sync(0xffffffffu, seq[r] == 0u);
+        ctot += __popc(mk[r]);
+      }
+      if (ctot && lane == 0) cbase = atomicAdd(&a.cand_count[wid & (NREG - 1)], (unsigned long long)ctot);
     }
     // ---- prefetch the next tile
     uint64_t kn[R], vn[R];
     bool ln[R];
     load_tile(nxt, kn, vn, ln);
-    // ---- resolve the bloom positives 32 at a time
-    uint32_t qt = 0, qh = 0;  // warp-uniform ring tail / head
-    auto round = [&](uint32_t cnt_in) {  // resolve ring entries [qh, qh + cnt_in)
-      __syncwarp();
-      bool hit = false;
-      if (lane < (int)cnt_in) {
-        const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
-        uint64_t b = 0;
-        ulonglong2 x = make_ulonglong2(0, 0), y = x;
-        if (e.x != EMPTY) probe_issue(a, e.x, b, x, y);
-        hit = probe_finish<PG>(a, e.x, e.y, b, x, y, s_fd, ns);
+    if constexpr (PM != PM_SCAN) {
+      // ---- resolve the bloom positives 32 at a time
+      uint32_t qt = 0, qh = 0;  // warp-uniform ring tail / head
+      auto round = [&](uint32_t cnt_in) {  // resolve ring entries [qh, qh + cnt_in)
+        __syncwarp();
+        bool hit = false;
+        if (lane < (int)cnt_in) {
+          const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
+          uint64_t b = 0;
+          ulonglong2 x = make_ulonglong2(0, 0), y = x;
+          if (e.x != EMPTY) probe_issue(a, e.x, b, x, y);
+          hit = probe_finish<PG>(a, e.x, e.y, b, x, y, s_fd, ns);
+        }
+        const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) s_hm[wid][qh >> 5] = hb;
+        __syncwarp();
+      };
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const bool posv = seq[r] == 0u;
+        const uint32_t m = __ballot_sync(0xffffffffu, posv);
+        if (posv) {
+          seq[r] = qt + __popc(m & lt_mask);
+          ring[seq[r] & (PQ_RING - 1)] = make_ulonglong2(kc[r], vc[r]);
+        }
+        qt += __popc(m);
+        if (qt - qh >= 32) {
+          round(32);
+          qh += 32;
+        }
       }
-      const uint32_t hb = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) s_hm[wid][qh >> 5] = hb;
+      if (qt != qh) round(qt - qh);
       __syncwarp();
-    };
+    }
+    // ---- claim chain positions (all R shared atomics in flight together), then
+    // allocate first slots, look the others' pages up, write
+    uint32_t pend = 0, pidx[R], pgv[R];
+    bool spill[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      const bool posv = seq[r] == 0u;
-      const uint32_t m = __ballot_sync(0xffffffffu, posv);
-      if (posv) {
-        seq[r] = qt + __popc(m & lt_mask);
-        ring[seq[r] & (PQ_RING - 1)] = make_ulonglong2(kc[r], vc[r]);
+      if (PM != PM_RESOLVE) c_rec += lc[r];
+      spill[r] = lc[r];
+      if (seq[r] != ~0u) {
+        if constexpr (PM == PM_SCAN) {
+          spill[r] = false;  // a candidate: phase 2 resolves it
+        } else {
+          const bool hit = (s_hm[wid][seq[r] >> 5] >> (seq[r] & 31)) & 1u;
+          c_hit += hit;
+          spill[r] = !hit;
+        }
       }
-      qt += __popc(m);
-      if (qt - qh >= 32) {
-        round(32);
-        qh += 32;
+      pidx[r] = spill[r] ? atomicAdd(&cnt[part[r]], 1u) : 0u;
+      c_sp += spill[r];
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      pgv[r] = 0xFFFFFFFFu;
+      if (!spill[r] || (pidx[r] & (S - 1))) continue;
+      // first record of page j: allocate it and publish it
+      const int p = part[r];
+      const uint32_t j = pidx[r] >> SLOG;
+      uint32_t pg;
+      const uint32_t off = atomicAdd(&s_su[par], 1u);
+      if (off < s_sc[par]) {
+        pg = s_sb[par] + off;
+      } else {
+        pg = atomicAdd(a.pool.next_page, 1u);
+        if (pg >= a.pool.capacity) {
+          atomicExch(a.pool.overflow, 1u);
+          pg = 0xFFFFFFu;
+        }
+      }
+      if (pg < 0xFFFFFFu) {
+        a.pool.page_part[pg] = p;
+        a.pool.page_set[pg] = a.ss.id;
+        a.pool.page_fill[pg] = S;
+      }
+      *(volatile uint32_t*)&ent[p * NE + (j & (NE - 1))] = (pg << 8) | (j & 0xFFu);
+      pgv[r] = pg;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if (!spill[r]) continue;
+      const uint32_t j = pidx[r] >> SLOG;
+      if (pidx[r] & (S - 1)) {
+        const uint32_t e = *(volatile uint32_t*)&ent[part[r] * NE + (j & (NE - 1))];
+        pgv[r] = ((e & 0xFFu) == (j & 0xFFu)) ? (e >> 8) : 0xFFFFFFFFu;
+      }
+      if (PAIR) {
+        const uint32_t idx = pidx[r], m = idx >> 1;
+        const int p = part[r];
+        if (!(idx & 1u)) {  // even: park for the partner, or go alone
+          // (no fence: the partner reads the slot only after the tile's barrier)
+          if (atomicCAS(&ptag[p], FREE, m | BUSY) == FREE) {
+            pk[p] = make_ulonglong2(kc[r], vc[r]);
+            *(volatile uint32_t*)&ptag[p] = m;
+          } else if (pgv[r] == 0xFFFFFFFFu) {
+            pend |= 1u << r;
+          } else {
+            put(pgv[r], idx & (S - 1), kc[r], vc[r]);
+          }
+        } else {
+          pend |= 1u << r;  // odd: decided after the barrier
+        }
+      } else {
+        if (pgv[r] == 0xFFFFFFFFu) pend |= 1u << r;
+        else put(pgv[r], pidx[r] & (S - 1), kc[r], vc[r]);
       }
     }
-    if (qt != qh) round(qt - qh);
-    __syncwarp();
-    // ---- claim chain positions and write the spilled records
-    uint32_t pend = 0, pidx[R];
+    if constexpr (PM == PM_SCAN) {
+      if (ctot) {
+        cbase = __shfl_sync(0xffffffffu, cbase, 0);
+        const int g = wid & (NREG - 1);
+        uint64_t* ck = a.cand + (size_t)g * a.cand_stride;
+        uint64_t* cv = a.cand + (size_t)(NREG + g) * a.cand_stride;
 #pragma unroll
-    for (int r = 0; r < R; r++) {
-      pidx[r] = 0;
-      c_rec += lc[r];
-      bool spill = lc[r];
-      if (seq[r] != ~0u) {
-        const bool hit = (s_hm[wid][seq[r] >> 5] >> (seq[r] & 31)) & 1u;
-        c_hit += hit;
-        spill = !hit;
-      }
-      if (!spill) continue;
-      c_sp++;
-      const int p = part[r];
-      const uint32_t idx = atomicAdd(&cnt[p], 1u);
-      const uint32_t j = idx >> SLOG, slot = idx & (S - 1);
-      uint32_t* ep = &ent[p * NE + (j & (NE - 1))];
-      uint32_t pg;
-      if (slot == 0) {  // first record of page j: allocate it and publish it
-        const uint32_t off = atomicAdd(&s_su[par], 1u);
-        if (off < s_sc[par]) {
-          pg = s_sb[par] + off;
-        } else {
-          pg = atomicAdd(a.pool.next_page, 1u);
-          if (pg >= a.pool.capacity) {
-            atomicExch(a.pool.overflow, 1u);
-            pg = 0xFFFFFFu;
+        for (int r = 0; r < R; r++) {
+          if (seq[r] == 0u) {
+            const unsigned long long i = cbase + __popc(mk[r] & lt_mask);
+            __stcg((unsigned long long*)ck + i, (unsigned long long)kc[r]);
+            __stcg((unsigned long long*)cv + i, (unsigned long long)vc[r]);
           }
+          cbase += __popc(mk[r]);
         }
-        if (pg < 0xFFFFFFu) {
-          a.pool.page_part[pg] = p;
-          a.pool.page_set[pg] = a.ss.id;
-          a.pool.page_fill[pg] = S;
-        }
-        *(volatile uint32_t*)ep = (pg << 8) | (j & 0xFFu);
-      } else {
-        const uint32_t e = *(volatile uint32_t*)ep;
-        pg = ((e & 0xFFu) == (j & 0xFFu)) ? (e >> 8) : 0xFFFFFFFFu;
-      }
-      if (pg == 0xFFFFFFFFu) {
-        pend |= 1u << r;
-        pidx[r] = idx;
-      } else {
-        put(pg, slot, kc[r], vc[r]);
       }
     }
     if (tid == 0) {
@@ -277,6 +433,18 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
         atomicExch(a.pool.overflow, 3u);  // cannot happen: the allocation precedes the barrier
         continue;
       }
+      if (PAIR && (idx & 1u)) {
+        const int p = part[r];
+        if (*(volatile uint32_t*)&ptag[p] == (idx >> 1)) {  // the partner parked before the barrier: take it
+          ulonglong2 pe;
+          asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(pe.x), "=l"(pe.y)
+                       : "r"((uint32_t)__cvta_generic_to_shared(&pk[p])));
+          *(volatile uint32_t*)&ptag[p] = FREE;  // after the read (in-order shared-memory pipe)
+          put2(e >> 8, idx & (S - 1) & ~1u, pe, kc[r], vc[r]);
+          continue;
+        }
+      }
       put(e >> 8, idx & (S - 1), kc[r], vc[r]);
     }
     cur = nxt;
@@ -290,14 +458,44 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
     }
   }
   __syncthreads();
-  // seal: the last page of every chain holds cnt mod S records; unused stash pages leave the set
-  for (int p = tid; p < P; p += BLK) {
-    const uint32_t c = cnt[p];
-    if (!c) continue;
-    const uint32_t j = (c - 1) >> SLOG;
-    const uint32_t e = ent[p * NE + (j & (NE - 1))];
-    if ((e >> 8) < 0xFFFFFFu) a.pool.page_fill[e >> 8] = (int32_t)(c - (j << SLOG));
+  if (PAIR) {
+    // a parked even record whose partner never came is the last of its chain
+    for (int p = tid; p < P; p += BLK) {
+      const uint32_t t = ptag[p];
+      if (t == FREE) continue;
+      const uint32_t idx = 2u * t, j = idx >> SLOG;
+      const uint32_t e = ent[p * NE + (j & (NE - 1))];
+      if ((t & BUSY) || idx + 1 != cnt[p] || (e & 0xFFu) != (j & 0xFFu)) {
+        atomicExch(a.pool.overflow, 3u);  // cannot happen
+        continue;
+      }
+      const ulonglong2 pe = pk[p];
+      put(e >> 8, idx & (S - 1), pe.x, pe.y);
+    }
   }
+  if constexpr (PM == PM_SCAN) {
+    // leave the chains open for phase 2: {records claimed, page of the last claim}
+    for (int p = tid; p < P; p += BLK) {
+      const uint32_t c = cnt[p];
+      uint32_t pg = 0xFFFFFFu;
+      if (c) {
+        const uint32_t j = (c - 1) >> SLOG;
+        const uint32_t e = ent[p * NE + (j & (NE - 1))];
+        if ((e & 0xFFu) == (j & 0xFFu)) pg = e >> 8;
+      }
+      a.chains[(size_t)blockIdx.x * P + p] = make_uint2(c, pg);
+    }
+  } else {
+    // seal: the last page of every chain holds cnt mod S records
+    for (int p = tid; p < P; p += BLK) {
+      const uint32_t c = cnt[p];
+      if (!c) continue;
+      const uint32_t j = (c - 1) >> SLOG;
+      const uint32_t e = ent[p * NE + (j & (NE - 1))];
+      if ((e >> 8) < 0xFFFFFFu) a.pool.page_fill[e >> 8] = (int32_t)(c - (j << SLOG));
+    }
+  }
+  // unused stash pages leave the set
   for (int q = 0; q < 2; q++)
     for (uint32_t x = min(s_su[q], s_sc[q]) + tid; x < s_sc[q]; x += BLK) a.pool.page_set[s_sb[q] + x] = -1;
   if (c_sp) atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
