@@ -440,8 +440,8 @@ struct Handle {
 
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
-                        "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>"};
-constexpr int NKINDS = 14;
+                        "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>", "k_split"};
+constexpr int NKINDS = 15;
 
 int prof_begin(Handle* h, int kid) {
   if (!h->prof) return -1;
@@ -793,7 +793,7 @@ OutBuf outbuf(Handle* h, int partial) {
   return o;
 }
 
-int flush_table(Handle* h, bool partial, OutBuf* dst) {
+int flush_table(Handle* h, bool partial, OutBuf* dst, bool clear = false) {
   int64_t cap_needed;
   OutBuf o;
   if (dst) {
@@ -808,11 +808,17 @@ int flush_table(Handle* h, bool partial, OutBuf* dst) {
   }
   int grid = h->sms * 4;
   int pe = prof_begin(h, 5);
-  if (h->kw == 1) k_flush_table<1><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
-  else k_flush_table<2><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+  if (clear) {
+    if (h->kw == 1) k_flush_table<1, true><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+    else k_flush_table<2, true><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+  } else {
+    if (h->kw == 1) k_flush_table<1><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+    else k_flush_table<2><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
+  }
   prof_end(h, pe);
   h->launches++;
   CU(cudaGetLastError());
+  if (clear) CU(cudaMemsetAsync(h->tab.hdr, 0, sizeof(TableHdr), h->st));
   return AGGB_OK;
 }
 
@@ -1190,6 +1196,65 @@ int cut_run(Handle* h) {
   return table_reset(h);
 }
 
+// hash_sort when the table fills about as fast as records arrive (little
+// aggregation per run: C5 cuts every ~84K records): instead of a host round
+// trip per cut, the rest of the batch is cut blind — chunks of `cap` records
+// (at most cap distinct keys, so the table never refuses: its capacity check is
+// lifted to the physical limit while the chunk bounds the groups it can hold),
+// each aggregated, flushed as a partial run into an accumulation buffer and
+// cleared on the way (k_flush_table<CLEAR>); every K runs the buffer is
+// hash-partitioned into part0 (GRACE) like cut_run does.  Results are those of
+// cutting when full; the runs are only cut earlier than full.
+int hash_sort_blind(Handle* h, const ColSrc& rest) {
+  const int64_t c = std::max<int64_t>(1, (int64_t)h->tab.cap);
+  const int words = h->kw + h->cs.ds.ns;
+  const int64_t K = std::max<int64_t>(1, std::min<int64_t>((rest.n + c - 1) / c, (int64_t)(8 << 20) / (c + 2)));
+  const int64_t acc_cap = K * (c + 2);
+  TRY(h->cut_tmp.ensure((size_t)acc_cap * words * 8, &h->hw));
+  OutBuf o;
+  o.keys = h->cut_tmp.as<uint64_t>();
+  o.vals = h->cut_tmp.as<uint64_t>() + (size_t)h->kw * acc_cap;
+  o.cap = acc_cap;
+  o.count = SC(h) + 11;
+  o.partial = 1;
+  CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+  CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+  const uint64_t cap0 = h->tab.cap;
+  h->tab.cap = (h->tab.mask + 1) * 3 / 4;  // no refusals: the chunk bounds the keys
+  int rc = AGGB_OK;
+  int64_t in_acc = 0;
+  for (int64_t off = 0; off < rest.n && rc == AGGB_OK; off += c) {
+    ColSrc ch = rest;
+    ch.n = std::min<int64_t>(c, rest.n - off);
+    for (int w = 0; w < h->kw; w++) ch.key[w] = rest.key[w] + off * rest.kstride[w];
+    for (int w = 0; w < rest.nv; w++) ch.val[w] = rest.val[w] + off * rest.vstride[w];
+    PassPlan f;
+    f.mode = MODE_FILL;
+    f.col = ch;
+    f.counter = SC(h) + 8;
+    if ((rc = launch_pass(h, f))) break;
+    if ((rc = flush_table(h, true, &o, true))) break;
+    h->hash_sort_runs++;
+    if (++in_acc == K || off + c >= rest.n) {
+      PassPlan g;
+      g.mode = MODE_GRACE;
+      g.lin = h->cut_tmp.as<uint64_t>();
+      g.lin_stride = acc_cap;
+      g.lin_count = SC(h) + 11;
+      g.lin_kind = 1;
+      g.lin_words = h->cs.ds.ns;
+      g.ss = h->part0.ss;
+      g.counter = SC(h) + 9;
+      if ((rc = launch_pass(h, g))) break;
+      CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+      h->part0_live = true;
+      in_acc = 0;
+    }
+  }
+  h->tab.cap = cap0;
+  return rc;
+}
+
 int push_hash_sort(Handle* h, const ColSrc& col0) {
   int nwt = nwt_for(std::max(1, col0.nv));
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
@@ -1267,7 +1332,13 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
       rest.n = cur.n - start;
       for (int w = 0; w < h->kw; w++) rest.key[w] = cur.key[w] + start * cur.kstride[w];
       for (int w = 0; w < cur.nv; w++) rest.val[w] = cur.val[w] + start * cur.vstride[w];
-      queue.push_back(rest);
+      // the table filled early in the batch (at least 8 more cuts ahead, each a
+      // host round trip and a GRACE pass of its own): cut the rest blind
+      if (frozen && rest.n > 8 * std::max<int64_t>(start, (int64_t)h->tab.cap) && !getenv("AGGB_HS_NO_BLIND")) {
+        if ((rc = hash_sort_blind(h, rest))) break;
+      } else {
+        queue.push_back(rest);
+      }
     }
     if (nd) queue.push_back(dc);  // deferred records first
   }
@@ -1283,6 +1354,7 @@ int push_hash_sort(Handle* h, const ColSrc& col0) {
 int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) {
   int depth = level;
   int nsub = h->nsub0;  // sub-passes per child at this level (plan)
+  bool split_done = false;
   Trace tr;
   for (int guard = 0; guard < 24; guard++) {
     if (!a_live && !b_live) return AGGB_OK;
@@ -1292,7 +1364,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     }
     int nparts = std::max(a.ss.nparts, b_live ? b.ss.nparts : 0);
     int nsets = b_live ? 2 : 1;
-    if (depth == level) {  // level-0 sets: a set with fewer partitions (wide partial states) needs more sub-passes
+    if (depth == level && !split_done) {  // level-0 sets: a set with fewer partitions (wide partial states) needs more sub-passes
       const int pmin = b_live ? std::min(a.ss.nparts, b.ss.nparts) : a.ss.nparts;
       nsub = (int)std::max<int64_t>(h->nsub0, (h->fanout_need + pmin - 1) / std::max(1, pmin));
     }
@@ -1415,6 +1487,45 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
       a_live = true;
       b_live = false;
       depth++;
+      continue;
+    }
+    // Partitions that would need >= 3 child sub-passes get one more grace level
+    // instead (k_split: the partition is read twice and written once, where
+    // sub-passes would read it nsub times); the children then take the
+    // page-aligned sub-partitions in one pass each.
+    if (nsub >= 3 && nsets == 1 && !getenv("AGGB_NO_SPLIT_LEVEL")) {
+      const int S = std::min(nsub, 1024);
+      int64_t total_in = 0;
+      for (int p = 0; p < nparts; p++) total_in += (int64_t)recs[p];
+      SetInfo sp{make_set(h, nonempty * S, a.ss.rw - h->kw, a.ss.kind, level_seed(h->cfg.seed, SALT_SPILL, depth + 17)),
+                 0};
+      TRY(pool_ensure(h, (uint64_t)(total_in / std::max(1, sp.ss.per_page)) + (uint64_t)nonempty * S + 16));
+      CU(cudaMemsetAsync(SC(h) + 12, 0, 8, h->st));
+      SplitArgs sa;
+      memset(&sa, 0, sizeof(sa));
+      sa.pool = pool_of(h);
+      sa.in = a.ss;
+      sa.plist = h->plist.as<uint2>();
+      sa.item_off = h->item_off.as<int64_t>();
+      sa.nitems = nonempty;
+      sa.S = S;
+      sa.sub_seed = level_seed(h->cfg.seed, SALT_SUB, depth + 1);
+      sa.out = sp.ss;
+      sa.item_counter = SC(h) + 12;
+      int pe = prof_begin(h, 14);
+      if (h->kw == 1) k_split<1><<<h->sms * 4, 512, 0, h->st>>>(sa);
+      else k_split<2><<<h->sms * 4, 512, 0, h->st>>>(sa);
+      prof_end(h, pe);
+      h->launches++;
+      CU(cudaGetLastError());
+      h->met.grace_levels++;
+      h->met.spilled_partitions -= nonempty;  // the sub-partitions are counted next
+      tr.mark(h->st, "drain: split level");
+      a = sp;
+      a_live = true;
+      b_live = false;
+      nsub = 1;
+      split_done = true;
       continue;
     }
     // child pass: output room + overflow room

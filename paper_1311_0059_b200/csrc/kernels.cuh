@@ -400,7 +400,10 @@ __device__ __forceinline__ void emit_group(const DevSpec& sp, const OutBuf& o, i
   }
 }
 
-template <int KW>
+// CLEAR: also reset every slot it emits (keys EMPTY, states at identity), so
+// a table cut by hash_sort is empty again without a full k_table_init pass
+// (the header is reset separately, after the kernel)
+template <int KW, bool CLEAR = false>
 __global__ void k_flush_table(GTable t, DevSpec sp, OutBuf o) {
   int lane = threadIdx.x & 31;
   uint64_t n = t.stride;
@@ -423,6 +426,11 @@ __global__ void k_flush_table(GTable t, DevSpec sp, OutBuf o) {
       uint64_t st[MAX_STATES];
       for (int j = 0; j < sp.ns; j++) st[j] = t.states[(uint64_t)j * n + s];
       emit_group<KW>(sp, o, (int64_t)(wbase + __popc(m & ((1u << lane) - 1))), k, st);
+      if (CLEAR) {
+#pragma unroll
+        for (int w = 0; w < KW; w++) t.keys[s * KW + w] = EMPTY;
+        for (int j = 0; j < sp.ns; j++) t.states[(uint64_t)j * n + s] = state_identity(sp.op[j], sp.ty[j]);
+      }
     }
   }
 }

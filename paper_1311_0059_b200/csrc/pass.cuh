@@ -737,3 +737,106 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
 }
 
 }  // namespace aggb
+
+namespace aggb {
+
+// ---------------------------------------------------------------------------
+// k_split: one more grace level for partitions too large for a child table
+// (hybrid.py:281-318 grace partitioning, fresh seed per level).  A CTA takes a
+// spilled partition (item) and re-partitions it into S sub-partitions:
+//   1. count the item's records per sub-partition (keys only),
+//   2. reserve whole pages per sub-partition (one global atomic each), so a
+//      sub-partition is a page-aligned run the children read like any other,
+//   3. scatter: lanes with the same sub-partition claim consecutive slots
+//      (match_any + one shared atomic), so a warp's record writes coalesce.
+// The item is read twice; a child would otherwise read it once per sub-pass.
+// ---------------------------------------------------------------------------
+
+struct SplitArgs {
+  PagePool pool;
+  SpillSet in;              // input set (one live set)
+  const uint2* plist;       // {page id, records} grouped by item
+  const int64_t* item_off;  // [2 * nitems + 1] (child layout: set 0 range, set 1 range)
+  int32_t nitems;
+  int32_t S;                // sub-partitions per item (<= 1024)
+  uint64_t sub_seed;
+  SpillSet out;             // output set: partition = item * S + sub
+  unsigned long long* item_counter;
+};
+
+template <int KW>
+__global__ void __launch_bounds__(512) k_split(SplitArgs a) {
+  __shared__ uint32_t s_hist[1024], s_base[1024], s_cur[1024];
+  __shared__ unsigned long long s_item;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
+  const int S = a.S, rw = a.in.rw, per = a.out.per_page;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.item_counter, 1ull);
+    for (int s = tid; s < S; s += blockDim.x) s_hist[s] = s_cur[s] = 0;
+    __syncthreads();
+    const unsigned long long item = s_item;
+    if (item >= (unsigned long long)a.nitems) break;
+    const int64_t qa = a.item_off[2 * item], qb = a.item_off[2 * item + 2];
+    // 1. histogram
+    for (int64_t q = qa + wid; q < qb; q += nwarps) {
+      const uint2 pe = a.plist[q];
+      const uint64_t* pb = (const uint64_t*)page_ptr(a.pool, pe.x);
+      for (int slot = lane; slot < (int)pe.y; slot += 32) {
+        uint64_t k[KW];
+#pragma unroll
+        for (int w = 0; w < KW; w++) k[w] = __ldcg(pb + (size_t)slot * rw + w);
+        atomicAdd(&s_hist[reduce32(hash_key<KW>(k, a.sub_seed), (uint32_t)S)], 1u);
+      }
+    }
+    __syncthreads();
+    // 2. whole pages per sub-partition
+    for (int s = tid; s < S; s += blockDim.x) {
+      const uint32_t n = s_hist[s];
+      const uint32_t np = (n + per - 1) / per;
+      uint32_t b = 0xFFFFFFFFu;
+      if (np) {
+        b = atomicAdd(a.pool.next_page, np);
+        if (b + np > a.pool.capacity) {
+          atomicExch(a.pool.overflow, 1u);
+          b = 0xFFFFFFFFu;
+        } else {
+          const int part = (int)(item * (unsigned long long)S + s);
+          for (uint32_t x = 0; x < np; x++) {
+            a.pool.page_part[b + x] = part;
+            a.pool.page_set[b + x] = a.out.id;
+            a.pool.page_fill[b + x] = (int32_t)min((uint32_t)per, n - x * per);
+          }
+        }
+      }
+      s_base[s] = b;
+    }
+    __syncthreads();
+    // 3. scatter
+    for (int64_t q = qa + wid; q < qb; q += nwarps) {
+      const uint2 pe = a.plist[q];
+      const uint64_t* pb = (const uint64_t*)page_ptr(a.pool, pe.x);
+      for (int s0 = 0; s0 < (int)pe.y; s0 += 32) {
+        const int slot = s0 + lane;
+        const bool live = slot < (int)pe.y;
+        uint64_t k[KW];
+#pragma unroll
+        for (int w = 0; w < KW; w++) k[w] = live ? __ldcs(pb + (size_t)slot * rw + w) : 0ull;
+        const uint32_t sub = live ? reduce32(hash_key<KW>(k, a.sub_seed), (uint32_t)S) : 0xFFFFFFFFu;
+        const uint32_t grp = __match_any_sync(0xffffffffu, sub);
+        const int leader = __ffs(grp) - 1;
+        uint32_t at = 0;
+        if (live && lane == leader) at = atomicAdd(&s_cur[sub], (uint32_t)__popc(grp));
+        at = __shfl_sync(0xffffffffu, at, leader) + __popc(grp & ((1u << lane) - 1u));
+        if (!live || s_base[sub] == 0xFFFFFFFFu) continue;
+        uint64_t* dst = (uint64_t*)page_ptr(a.pool, s_base[sub] + at / per) + (size_t)(at % per) * rw;
+        const uint64_t* src = pb + (size_t)slot * rw;
+#pragma unroll
+        for (int w = 0; w < KW; w++) __stcg((unsigned long long*)dst + w, (unsigned long long)k[w]);
+        for (int w = KW; w < rw; w++) __stcg((unsigned long long*)dst + w, __ldcs((const unsigned long long*)src + w));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace aggb

@@ -115,12 +115,16 @@ def test_l2_table_children(algo, case, monkeypatch):
 @pytest.mark.parametrize("algo", ["pre_partitioning", "original_hh", "hash_sort"])
 @pytest.mark.parametrize("case", ["C2s", "C3s15", "C5s", "C2grace"])
 @pytest.mark.parametrize("max_p0", [2, 3])
-def test_child_subpasses(algo, case, max_p0, monkeypatch):
+@pytest.mark.parametrize("mode", ["split", "subpass"])
+def test_child_subpasses(algo, case, max_p0, mode, monkeypatch):
     """Spill fan-out beyond what one pass can write (C5's wide states): the
-    level-0 fan-out is capped (test hook; C5 at full size hits the real cap) and
-    each child takes its partition in sub-passes, each aggregating one sub-hash
-    range in a fresh shared-memory table."""
+    level-0 fan-out is capped (test hook; C5 at full size hits the real cap).
+    Partitions needing >= 3 child tables get one more grace level (k_split:
+    page-aligned sub-partitions); with that off ("subpass") each child takes
+    its partition in sub-passes, one sub-hash range per fresh table."""
     monkeypatch.setenv("AGGB_MAX_P0", str(max_p0))
+    if mode == "subpass":
+        monkeypatch.setenv("AGGB_NO_SPLIT_LEVEL", "1")
     path = [p for p in GOLD if os.path.basename(p).startswith(case + "__")][0]
     meta, gkeys, gvals = load_golden(path)
     cfg, keys, vals = golden_inputs(meta)
@@ -130,7 +134,7 @@ def test_child_subpasses(algo, case, max_p0, monkeypatch):
     res, met = run_gpu(algo, cfg, keys, vals, chunks=2, budget_groups=budget, stats=st, seed=7)
     check_against(res, gkeys, gvals, cfg)
     if algo == "pre_partitioning" and case in ("C2grace", "C5s"):
-        assert met["child_subpasses"] > 1
+        assert met["child_subpasses"] > 1 or met["grace_levels"] >= 1
 
 
 @pytest.mark.parametrize("algo", ALGOS_GPU)
