@@ -371,6 +371,7 @@ struct Handle {
   bool l2_children = false; // spilled partitions aggregate in the budget-sized L2 table (drain)
   int P0 = 1;               // level-0 spill fan-out
   int nsub0 = 1;            // sub-passes per level-1 child (fan-out beyond one spill pass)
+  bool l2_capped = false;   // in-memory plan run budgeted at an L2-sized table
   int64_t fanout_need = 1;  // level-0 fan-out the child capacity asks for (P0 x nsub0)
   int child_slots_log2 = 11;
   int child_cap = 1024;
@@ -603,6 +604,15 @@ int launch_pass(Handle* h, PassPlan& pp) {
                                   (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
                           !getenv("AGGB_GENERIC_PROBE");
   const int T_fill = pcfg.R * pcfg.blk;  // tile size of the FILL pass (start_tiles counts its tiles)
+  // k_probe_w: two-word keys + 4 payload words (C5 rows), raw records
+  const bool wide_probe = !fast_probe && pp.mode == MODE_PROBE && h->kw == 2 && pp.col.nv == 4 && pp.ss.rw == 6 &&
+                          pp.col_kind == 0 && pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 4 && pp.lin_kind == 0)) &&
+                          pp.ss.per_page == 170 &&
+                          h->pool_bound + (uint64_t)(pp.col.n + pp.lin_stride) / 64 +
+                                  (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
+                          !getenv("AGGB_GENERIC_PROBE");
+  if (wide_probe)
+    pcfg = h->prog == 5 ? PassCfg{k_probe_w<2, 4, 2, 512, ProgC5>, 2, 512} : PassCfg{k_probe_w<2, 4, 2, 512, PD>, 2, 512};
   // two-phase PROBE (probe.cuh): a streaming partition pass, then the bloom positives
   const bool split = fast_probe && h->bloom_words && getenv("AGGB_SPLIT");
   if (fast_probe) pcfg = probe_kernel(h->prog, split ? PM_SCAN : PM_ONE);
@@ -619,6 +629,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   // one-pass kernel the deferred odd records lengthen the tile (2.15 -> 2.48 ms)
   bool pairs = fast_probe && split && !getenv("AGGB_NO_PAIRS");
   auto smem_of = [&](int bw) {
+    if (wide_probe) return (size_t)((bw + 1) & ~1) * 8 + (size_t)P * (4 + 8 * 4) + 64;
     return fast_probe ? probe_smem(P, bw, blk, split ? PM_SCAN : PM_ONE, pairs) : pass_smem(P, G, rw, bw);
   };
   size_t smem = smem_of(bl.words ? (int)h->bloom_words : 0);
@@ -900,6 +911,25 @@ int plan(Handle* h) {
     }
     h->budget = std::max<int64_t>(1, plan_table_cap(frames, p, bg, c.slot_ratio, bloom));
     h->unlimited = false;
+  }
+  // Experiment (AGGB_L2_CAP): run an in-memory plan whose table would not fit
+  // in L2 budgeted at an L2-sized table, the groups beyond it taking the spill
+  // path.  Measured slower on C3 (Zipf s=1, 200M): FILL into the HBM table with
+  // its SMEM tier for hot keys 15.2 ms vs 30.2 ms capped (k_probe has no SMEM
+  // tier: the hot keys' REDs serialize), hash_sort 62 ms capped.  Off.
+  h->l2_capped = false;
+  if (h->unlimited && algo != AGGB_SORT_BASED && algo != AGGB_ORIGINAL_HH && getenv("AGGB_L2_CAP")) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    cudaGetLastError();
+    const double per_group = 2.0 * 8.0 * (h->kw + std::max(1, ns));  // 2 slots per group, key + states
+    const int64_t l2cap = (int64_t)(0.4 * std::max(l2, 32 << 20) / per_group);
+    if (h->budget > 2 * l2cap) {
+      h->budget = l2cap;
+      h->unlimited = false;
+      h->l2_capped = true;
+    }
   }
   h->child_cap = (int)std::max<int64_t>(1, std::min<int64_t>(ccap, h->budget));
   // spill fan-out: every child partition should fill ~40% of a child table

@@ -504,4 +504,239 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
 }
 
+
+// ---------------------------------------------------------------------------
+// k_probe_w: the PROBE pass for wider records — two-word keys and several
+// payload words read from strided, typed columns (C5's 64-byte rows: int64 ||
+// int32 key, 4 values; 48-byte spill records).  Same page chains, claims and
+// page map as k_probe.  Bloom positives are rare here (the table holds ~2% of
+// the groups), so they are resolved inline; a record's words leave as 16-byte
+// stores (a 48-byte record covers 1.5 sectors, so partial sectors are few).
+// ---------------------------------------------------------------------------
+constexpr int gcd_c(int x, int y) { return y ? gcd_c(y, x % y) : x; }
+
+template <int KW, int NW, int R, int BLK, class PG>
+__global__ void __launch_bounds__(BLK, 1) k_probe_w(PassArgs a) {
+  constexpr int RW = KW + NW;
+  constexpr int GRP = 4 / gcd_c(RW, 4);
+  constexpr int S = (8192 / (RW * 8)) / GRP * GRP;  // records per page, as make_set
+  constexpr int T = R * BLK;
+  constexpr int NE = 8;
+  static_assert((NE - 1) * S >= T, "a page-map entry must outlive a tile");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int P = a.ss.nparts;
+  const int nbw = a.bloom.words ? (int)a.bloom.mask + 1 : 0;
+  uint64_t* sbloom = (uint64_t*)smem;
+  uint32_t* cnt = (uint32_t*)(sbloom + ((nbw + 1) & ~1));  // P
+  uint32_t* ent = cnt + P;                                  // P * NE
+  __shared__ uint32_t s_fd[MAX_STATES];
+  __shared__ unsigned long long s_grab[2];
+  __shared__ uint32_t s_sb[2], s_su[2], s_sc[2];
+  __shared__ unsigned long long s_cnt[ST_NSTATS];
+  __shared__ int s_dummy[4];
+  const CapCache cc{&s_dummy[0], (unsigned*)&s_dummy[1], &s_dummy[2], &s_dummy[3], 0u, 0ull};
+
+  const int64_t n = a.col.n;
+  const int64_t col_start =
+      a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
+  const int64_t col_tiles = (n - col_start + T - 1) / T;
+  const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
+  const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
+  if (total == 0) return;
+
+  const int ns = a.sp.ns;
+  if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
+  for (int p = tid; p < P; p += BLK) cnt[p] = 0;
+  for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
+  if (tid < ST_NSTATS) s_cnt[tid] = 0;
+  for (int i = tid; i < nbw; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom.words + i);
+  uint64_t* const pool = (uint64_t*)a.pool.base;
+
+  auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R][KW], uint64_t (&v)[R][NW], bool (&live)[R]) {
+    const bool lin = (int64_t)tile >= col_tiles;
+    const int64_t base = lin ? ((int64_t)tile - col_tiles) * T : col_start + (int64_t)tile * T;
+    const int64_t end = lin ? n_lin : n;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int64_t i = base + r * BLK + tid;
+      live[r] = (tile < total) && (i < end);
+      if (live[r]) {
+        col_key<KW>(lin ? a.lin : a.col, i, k[r]);
+        col_vals<NW>(lin ? a.lin : a.col, i, v[r]);
+      }
+    }
+  };
+  auto put = [&](uint32_t pg, uint32_t slot, const uint64_t (&k)[KW], const uint64_t (&v)[NW]) {
+    if (pg >= 0xFFFFFFu) return;
+    uint64_t* d = pool + ((size_t)pg * (8192 / 8) + (size_t)slot * RW);
+    uint64_t w[RW];
+#pragma unroll
+    for (int q = 0; q < KW; q++) w[q] = k[q];
+#pragma unroll
+    for (int q = 0; q < NW; q++) w[KW + q] = v[q];
+    if constexpr (RW % 2 == 0) {
+#pragma unroll
+      for (int q = 0; q < RW; q += 2) __stcg((ulonglong2*)(d + q), make_ulonglong2(w[q], w[q + 1]));
+    } else {
+#pragma unroll
+      for (int q = 0; q < RW; q++) __stcg((unsigned long long*)d + q, (unsigned long long)w[q]);
+    }
+  };
+
+  if (tid == 0) {
+    s_sb[0] = s_sb[1] = s_su[0] = s_su[1] = s_sc[0] = s_sc[1] = 0;
+    s_grab[0] = atomicAdd(a.tile_counter, 1ull);
+    s_grab[1] = atomicAdd(a.tile_counter, 1ull);
+  }
+  __syncthreads();
+  unsigned long long cur = s_grab[0], nxt = s_grab[1];
+  uint64_t kc[R][KW], vc[R][NW];
+  bool lc[R];
+  load_tile(cur, kc, vc, lc);
+
+  uint32_t c_hit = 0, c_rec = 0, c_sp = 0;
+  int par = 0;
+  while (cur < total) {
+    unsigned long long g_next = 0;
+    uint32_t ref_first = 0;
+    bool refill = false;
+    if (tid == 0) {
+      g_next = atomicAdd(a.tile_counter, 1ull);
+      const int q = par ^ 1;
+      refill = a.stash && s_su[q] >= s_sc[q];
+      if (refill) ref_first = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
+    }
+    uint64_t kn[R][KW], vn[R][NW];
+    bool ln[R];
+    load_tile(nxt, kn, vn, ln);
+    uint32_t pend = 0, pidx[R];
+    int part[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      pidx[r] = 0;
+      part[r] = 0;
+      if (!lc[r]) continue;
+      c_rec++;
+      const bool sent = is_sentinel<KW>(kc[r]);
+      const uint64_t h = hash_key<KW>(kc[r], a.t.seed);
+      part[r] = sent ? 0 : (int)reduce32(h, (uint32_t)P);
+      bool posv = true;
+      if (nbw && !sent) {
+        const uint64_t bits = bloom_bits(h);
+        posv = (sbloom[bloom_block(h, a.bloom.mask)] & bits) == bits;
+      }
+      if (posv) {  // rare: resolve inline against the frozen table
+        int res = R_MISS;
+        int64_t sl;
+        if (sent) {
+          sl = gt_escape<KW>(a.t, false, cc, res);
+        } else {
+          const uint64_t b = h & a.t.bmask;
+          uint64_t w[4];
+          ld_bucket(a.t.keys, b, w);
+          sl = gt_resolve<KW>(a.t, kc[r], b, w, false, cc, res);
+        }
+        if (res == R_HIT) {
+          Upd<PG>::template g<NW>(a.t.states, a.t.stride, (uint64_t)sl, 0, s_fd, ns, vc[r]);
+          c_hit++;
+          continue;
+        }
+      }
+      c_sp++;
+      const int p = part[r];
+      const uint32_t idx = atomicAdd(&cnt[p], 1u);
+      const uint32_t j = idx / S, slot = idx - j * S;
+      uint32_t* ep = &ent[p * NE + (j & (NE - 1))];
+      uint32_t pg;
+      if (slot == 0) {
+        const uint32_t off = atomicAdd(&s_su[par], 1u);
+        if (off < s_sc[par]) {
+          pg = s_sb[par] + off;
+        } else {
+          pg = atomicAdd(a.pool.next_page, 1u);
+          if (pg >= a.pool.capacity) {
+            atomicExch(a.pool.overflow, 1u);
+            pg = 0xFFFFFFu;
+          }
+        }
+        if (pg < 0xFFFFFFu) {
+          a.pool.page_part[pg] = p;
+          a.pool.page_set[pg] = a.ss.id;
+          a.pool.page_fill[pg] = S;
+        }
+        *(volatile uint32_t*)ep = (pg << 8) | (j & 0xFFu);
+      } else {
+        const uint32_t e = *(volatile uint32_t*)ep;
+        pg = ((e & 0xFFu) == (j & 0xFFu)) ? (e >> 8) : 0xFFFFFFFFu;
+      }
+      if (pg == 0xFFFFFFFFu) {
+        pend |= 1u << r;
+        pidx[r] = idx;
+      } else {
+        put(pg, slot, kc[r], vc[r]);
+      }
+    }
+    if (tid == 0) {
+      s_grab[par] = g_next;
+      if (refill) {
+        const int q = par ^ 1;
+        for (uint32_t x = min(s_su[q], s_sc[q]); x < s_sc[q]; x++) a.pool.page_set[s_sb[q] + x] = -1;
+        const bool fits = ref_first + (uint32_t)a.stash <= a.pool.capacity;
+        if (!fits)
+          for (uint32_t x = ref_first; x < min(ref_first + (uint32_t)a.stash, a.pool.capacity); x++)
+            a.pool.page_set[x] = -1;
+        s_sb[q] = ref_first;
+        s_sc[q] = fits ? (uint32_t)a.stash : 0u;
+        s_su[q] = 0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if (!((pend >> r) & 1u)) continue;
+      const uint32_t idx = pidx[r], j = idx / S;
+      const uint32_t e = ent[part[r] * NE + (j & (NE - 1))];
+      if ((e & 0xFFu) != (j & 0xFFu)) {
+        atomicExch(a.pool.overflow, 3u);  // cannot happen: the allocation precedes the barrier
+        continue;
+      }
+      put(e >> 8, idx - j * S, kc[r], vc[r]);
+    }
+    cur = nxt;
+    nxt = s_grab[par];
+    par ^= 1;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      lc[r] = ln[r];
+#pragma unroll
+      for (int q = 0; q < KW; q++) kc[r][q] = kn[r][q];
+#pragma unroll
+      for (int q = 0; q < NW; q++) vc[r][q] = vn[r][q];
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < P; p += BLK) {
+    const uint32_t c = cnt[p];
+    if (!c) continue;
+    const uint32_t j = (c - 1) / S;
+    const uint32_t e = ent[p * NE + (j & (NE - 1))];
+    if ((e >> 8) < 0xFFFFFFu) a.pool.page_fill[e >> 8] = (int32_t)(c - j * S);
+  }
+  for (int q = 0; q < 2; q++)
+    for (uint32_t x = min(s_su[q], s_sc[q]) + tid; x < s_sc[q]; x += BLK) a.pool.page_set[s_sb[q] + x] = -1;
+  if (c_sp) atomicExch(&a.t.hdr->frozen, 1);
+  uint32_t cs[3] = {c_sp, c_hit, c_rec};
+  const int ids[3] = {ST_SPILLED, ST_HITS, ST_RECORDS};
+#pragma unroll
+  for (int q = 0; q < 3; q++) {
+    uint32_t x = cs[q];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(&s_cnt[ids[q]], (unsigned long long)x);
+  }
+  __syncthreads();
+  if (tid < ST_NSTATS && s_cnt[tid]) atomicAdd(&a.stats[tid], s_cnt[tid]);
+}
+
 }  // namespace aggb
