@@ -1543,8 +1543,14 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
       sa.out = sp.ss;
       sa.item_counter = SC(h) + 12;
       int pe = prof_begin(h, 14);
-      if (h->kw == 1) k_split<1><<<h->sms * 4, 512, 0, h->st>>>(sa);
-      else k_split<2><<<h->sms * 4, 512, 0, h->st>>>(sa);
+      void (*sf)(SplitArgs) = h->kw == 1 ? k_split<1, 0> : k_split<2, 0>;
+      const int rwi = a.ss.rw;
+      if (h->kw == 1 && rwi == 2) sf = k_split<1, 2>;
+      if (h->kw == 1 && rwi == 3) sf = k_split<1, 3>;
+      if (h->kw == 1 && rwi == 5) sf = k_split<1, 5>;
+      if (h->kw == 2 && rwi == 6) sf = k_split<2, 6>;
+      if (h->kw == 2 && rwi == 15) sf = k_split<2, 15>;
+      sf<<<h->sms * 4, 512, 0, h->st>>>(sa);
       prof_end(h, pe);
       h->launches++;
       CU(cudaGetLastError());

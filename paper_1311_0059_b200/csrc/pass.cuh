@@ -764,12 +764,14 @@ struct SplitArgs {
   unsigned long long* item_counter;
 };
 
-template <int KW>
+// RWC: record width known at compile time (registers), 0: any width (per-word copies)
+template <int KW, int RWC>
 __global__ void __launch_bounds__(512) k_split(SplitArgs a) {
   __shared__ uint32_t s_hist[1024], s_base[1024], s_cur[1024];
   __shared__ unsigned long long s_item;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nwarps = blockDim.x >> 5;
-  const int S = a.S, rw = a.in.rw, per = a.out.per_page;
+  const int S = a.S, rw = RWC ? RWC : a.in.rw, per = a.out.per_page;
+  constexpr int NR = RWC ? RWC : KW;  // words held in registers
   for (;;) {
     if (tid == 0) s_item = atomicAdd(a.item_counter, 1ull);
     for (int s = tid; s < S; s += blockDim.x) s_hist[s] = s_cur[s] = 0;
@@ -818,9 +820,26 @@ __global__ void __launch_bounds__(512) k_split(SplitArgs a) {
       for (int s0 = 0; s0 < (int)pe.y; s0 += 32) {
         const int slot = s0 + lane;
         const bool live = slot < (int)pe.y;
+        // the whole record in registers (16-byte loads when records are 16-byte
+        // aligned: streaming per-word loads re-fetched each line from L2)
+        uint64_t rec[NR];
+        const uint64_t* src = pb + (size_t)slot * rw;
+        if (live) {
+          if constexpr (NR % 2 == 0) {
+#pragma unroll
+            for (int w = 0; w < NR; w += 2) {
+              const ulonglong2 x = __ldcs((const ulonglong2*)(src + w));
+              rec[w] = x.x;
+              rec[w + 1] = x.y;
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < NR; w++) rec[w] = __ldcs((const unsigned long long*)src + w);
+          }
+        }
         uint64_t k[KW];
 #pragma unroll
-        for (int w = 0; w < KW; w++) k[w] = live ? __ldcs(pb + (size_t)slot * rw + w) : 0ull;
+        for (int w = 0; w < KW; w++) k[w] = live ? rec[w] : 0ull;
         const uint32_t sub = live ? reduce32(hash_key<KW>(k, a.sub_seed), (uint32_t)S) : 0xFFFFFFFFu;
         const uint32_t grp = __match_any_sync(0xffffffffu, sub);
         const int leader = __ffs(grp) - 1;
@@ -829,10 +848,15 @@ __global__ void __launch_bounds__(512) k_split(SplitArgs a) {
         at = __shfl_sync(0xffffffffu, at, leader) + __popc(grp & ((1u << lane) - 1u));
         if (!live || s_base[sub] == 0xFFFFFFFFu) continue;
         uint64_t* dst = (uint64_t*)page_ptr(a.pool, s_base[sub] + at / per) + (size_t)(at % per) * rw;
-        const uint64_t* src = pb + (size_t)slot * rw;
+        if constexpr (NR % 2 == 0) {
 #pragma unroll
-        for (int w = 0; w < KW; w++) __stcg((unsigned long long*)dst + w, (unsigned long long)k[w]);
-        for (int w = KW; w < rw; w++) __stcg((unsigned long long*)dst + w, __ldcs((const unsigned long long*)src + w));
+          for (int w = 0; w < NR; w += 2) __stcg((ulonglong2*)(dst + w), make_ulonglong2(rec[w], rec[w + 1]));
+        } else {
+#pragma unroll
+          for (int w = 0; w < NR; w++) __stcg((unsigned long long*)dst + w, (unsigned long long)rec[w]);
+        }
+        for (int w = NR; w < rw; w++)  // RWC == 0: the payload words beyond the key
+          __stcg((unsigned long long*)dst + w, __ldcg((const unsigned long long*)src + w));
       }
     }
     __syncthreads();
