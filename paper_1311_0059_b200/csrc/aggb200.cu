@@ -703,7 +703,6 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.tile_counter = pp.counter;
   a.stats = SC(h);
   a.cache_log2 = cache_log2;
-  a.dbg = getenv("AGGB_DBG") ? atoi(getenv("AGGB_DBG")) : 0;
   a.pairs = pairs ? 1 : 0;
   // chunked reservations for large tables: unused chunks (< grid * chunk) stay under 1% of cap
   {

@@ -52,7 +52,6 @@ struct PassArgs {
   unsigned long long* cand_count;         // [NREG]
   uint2* chains;                          // per (CTA, partition): {records claimed, page of the last claim}
   int32_t pairs;                          // k_probe: sector pairs on (shared memory permitting)
-  int32_t dbg;                            // experiments only (AGGB_DBG); 0 in production
 };
 
 template <int KW, int NWT>

@@ -191,31 +191,6 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
                    : "memory");
   };
   auto put = [&](uint32_t pg, uint32_t slot, uint64_t k, uint64_t v) {
-    if (a.dbg == 1) return;
-    if (a.dbg == 2) {
-      __stcg((ulonglong2*)(pool + ((size_t)blockIdx.x * BLK + tid) * 2), make_ulonglong2(k, v));
-      return;
-    }
-    if (a.dbg == 3) {  // same scatter pattern, aliased into a small (L2-resident) window
-      if (pg < 0xFFFFFFu) __stcg((ulonglong2*)(pool + ((((size_t)pg & 63) << SLOG) + slot) * 2), make_ulonglong2(k, v));
-      return;
-    }
-    if (a.dbg == 4) {  // sector-complete: the record and its pair slot written back to back
-      if (pg < 0xFFFFFFu) {
-        ulonglong2* q = (ulonglong2*)(pool + (((size_t)pg << SLOG) + (slot & ~1u)) * 2);
-        __stcg(q, make_ulonglong2(k, v));
-        __stcg(q + 1, make_ulonglong2(k, v));
-      }
-      return;
-    }
-    if (a.dbg == 5) {  // one 32-byte store per PAIR of records (half the transactions)
-      if (pg < 0xFFFFFFu && (slot & 1)) {
-        ulonglong2* q = (ulonglong2*)(pool + (((size_t)pg << SLOG) + (slot & ~1u)) * 2);
-        __stcg(q, make_ulonglong2(k, v));
-        __stcg(q + 1, make_ulonglong2(k, v));
-      }
-      return;
-    }
     if (pg < 0xFFFFFFu) __stcg((ulonglong2*)(pool + (((size_t)pg << SLOG) + slot) * 2), make_ulonglong2(k, v));
   };
 
