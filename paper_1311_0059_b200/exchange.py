@@ -60,6 +60,7 @@ class Exchanger:
                              agg, key_types, val_types, device=device.index, stream=stream,
                              budget_groups=kw.pop("budget_groups", -1), **kw)
         self.rec_bytes = int(local.L.aggb_exchange_record_bytes(local.h))
+        self.stream = stream
         self._send = None
         self.last_counts = None
 
@@ -74,7 +75,14 @@ class Exchanger:
         N.check(L.aggb_exchange_pack(self.local.h, self.world, ctypes.c_void_p(self._send.data_ptr()),
                                      counts), "aggb_exchange_pack")
         send_counts = [int(c) for c in counts]
-        recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
+        # the collectives are ordered on the handles' stream: the pack kernel
+        # before them, the merge after them (NCCL waits on / signals the
+        # current stream; a side stream would race the receive buffer)
+        if self.stream is not None and self.device.type == "cuda":
+            with torch.cuda.stream(self.stream):
+                recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
+        else:
+            recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
         self.last_counts = (send_counts, recv_counts)
         self.merge.reset()
         total = sum(recv_counts)
