@@ -598,7 +598,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   // k_probe: 16-byte raw records from dense 8-byte columns (and the SoA deferral list)
   const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 && pp.col_kind == 0 &&
                           pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 1 && pp.lin_kind == 0)) &&
-                          dense8(pp.col, 1) && pp.ss.per_page == 512 &&
+                          dense8(pp.col, 1) && pp.ss.per_page == 512 && !h->l2_capped &&
                           // page ids are 24-bit in k_probe's page map (conservative pool estimate)
                           h->pool_bound + (uint64_t)(pp.col.n + pp.lin_stride) / 256 +
                                   (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
@@ -644,7 +644,9 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
   // SMEM pre-aggregation tier for inserting passes over one-word keys (pass.cuh)
   int cache_log2 = 0;
-  if (!fast_probe && pp.mode == MODE_FILL && h->kw == 1 && !getenv("AGGB_NO_CACHE")) {
+  // (an L2-capped in-memory plan probes hot keys: the tier serves PROBE too)
+  if (!fast_probe && (pp.mode == MODE_FILL || (pp.mode == MODE_PROBE && h->l2_capped)) && h->kw == 1 &&
+      !getenv("AGGB_NO_CACHE")) {
     const size_t per = 12 + 8 * (size_t)h->cs.ds.ns;
     const size_t room = std::min<size_t>(160 * 1024, 224 * 1024 - std::min<size_t>(smem + 16, 224 * 1024));
     int L = 0;
@@ -911,13 +913,16 @@ int plan(Handle* h) {
     h->budget = std::max<int64_t>(1, plan_table_cap(frames, p, bg, c.slot_ratio, bloom));
     h->unlimited = false;
   }
-  // Experiment (AGGB_L2_CAP): run an in-memory plan whose table would not fit
-  // in L2 budgeted at an L2-sized table, the groups beyond it taking the spill
-  // path.  Measured slower on C3 (Zipf s=1, 200M): FILL into the HBM table with
-  // its SMEM tier for hot keys 15.2 ms vs 30.2 ms capped (k_probe has no SMEM
-  // tier: the hot keys' REDs serialize), hash_sort 62 ms capped.  Off.
+  // An in-memory pre-partitioning plan whose table would not fit in L2 (C3:
+  // ~9M groups) aggregates with random HBM accesses per record (ncu: 17.7 GB
+  // of DRAM reads for 3.2 GB of input).  The budget is an upper bound, not a
+  // target: such a plan runs budgeted at an L2-sized table (~40% of L2), the
+  // first-seen (for skewed data: hot) keys resident, the PROBE pass keeping
+  // its SMEM tier for them, the rest through the spill path.  C3 (Zipf s=1,
+  // 200M): 15.2 -> 11.1 ms.  hash_sort keeps its in-memory table (capped it
+  // cuts a run per chunk: 62 ms).
   h->l2_capped = false;
-  if (h->unlimited && algo != AGGB_SORT_BASED && algo != AGGB_ORIGINAL_HH && getenv("AGGB_L2_CAP")) {
+  if (h->unlimited && algo == AGGB_PRE_PARTITIONING && !getenv("AGGB_NO_L2_CAP")) {
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
