@@ -928,7 +928,8 @@ int plan(Handle* h) {
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     cudaGetLastError();
     const double per_group = 2.0 * 8.0 * (h->kw + std::max(1, ns));  // 2 slots per group, key + states
-    const int64_t l2cap = (int64_t)(0.4 * std::max(l2, 32 << 20) / per_group);
+    int64_t l2cap = (int64_t)(0.4 * std::max(l2, 32 << 20) / per_group);
+    if (getenv("AGGB_L2_CAP_GROUPS")) l2cap = std::max(8, atoi(getenv("AGGB_L2_CAP_GROUPS")));  // test hook
     if (h->budget > 2 * l2cap) {
       h->budget = l2cap;
       h->unlimited = false;

@@ -137,6 +137,25 @@ def test_child_subpasses(algo, case, max_p0, mode, monkeypatch):
         assert met["child_subpasses"] > 1 or met["grace_levels"] >= 1
 
 
+@pytest.mark.parametrize("case", ["C1", "C2s", "C3s05", "C3s10", "C3s15", "C4s"])
+def test_in_memory_l2_capped_plan(case, monkeypatch):
+    """An in-memory pre_partitioning plan whose table would exceed L2 runs at
+    an L2-sized table and spills the rest (C3 at full size); the cap is shrunk
+    here (test hook) so the golden inputs take that path: the first-seen keys
+    stay resident, PROBE keeps the shared-memory hot-key tier."""
+    monkeypatch.setenv("AGGB_L2_CAP_GROUPS", "64")
+    path = [p for p in GOLD if os.path.basename(p).startswith(case + "__")][0]
+    meta, gkeys, gvals = load_golden(path)
+    cfg, keys, vals = golden_inputs(meta)
+    from paper_1311_0059_b200.core import DatasetStats
+    n = len(keys[0])
+    st = DatasetStats(R=1, R_t=n, G=1, G_t=gkeys.shape[0])
+    res, met = run_gpu("pre_partitioning", cfg, keys, vals, chunks=2, budget_groups=-1, stats=st, seed=9)
+    check_against(res, gkeys, gvals, cfg)
+    if gkeys.shape[0] > 128:
+        assert met["spilled_records"] > 0 and met["resident_groups"] <= 64
+
+
 @pytest.mark.parametrize("algo", ALGOS_GPU)
 def test_pipelined_host_push(algo, monkeypatch):
     """Host input larger than two chunks is copied on a second stream while the
