@@ -6,6 +6,7 @@
 // becomes a resident-table capacity in groups; Formula-1 partition counts are a
 // lower bound on the spill fan-out, which is raised until every child
 // partition fits a shared-memory table.
+#include <cuda.h>  // driver-API types for the VMM page pool (entry points via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -98,6 +99,125 @@ struct DBuf {
   }
   template <class T>
   T* as() const { return (T*)p; }
+};
+
+// Spill page pool memory: one virtual address range reserved for the device's
+// whole memory, physical memory mapped onto its end as the pool grows (CUDA
+// VMM).  Growth never copies and never holds old + new at once: a pool that
+// doubles to 60+ GB (C5 hash_sort at 500M records) only maps the difference.
+struct VPool {
+  CUdeviceptr va = 0;
+  size_t reserved = 0, mapped = 0, gran = 0;
+  int dev = -1;
+  std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks;
+  struct Api {
+    CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*afree)(CUdeviceptr, size_t);
+    CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*release)(CUmemGenericAllocationHandle);
+    CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*unmap)(CUdeviceptr, size_t);
+    CUresult (*access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+    bool ok = false;
+  };
+  static const Api& api() {
+    static Api a = [] {
+      Api x;
+      memset(&x, 0, sizeof(x));
+      cudaDriverEntryPointQueryResult q;
+      bool ok = true;
+      auto get = [&](const char* name, void** fn) {
+        if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+            !*fn)
+          ok = false;
+      };
+      get("cuMemAddressReserve", (void**)&x.reserve);
+      get("cuMemAddressFree", (void**)&x.afree);
+      get("cuMemCreate", (void**)&x.create);
+      get("cuMemRelease", (void**)&x.release);
+      get("cuMemMap", (void**)&x.map);
+      get("cuMemUnmap", (void**)&x.unmap);
+      get("cuMemSetAccess", (void**)&x.access);
+      get("cuMemGetAllocationGranularity", (void**)&x.granularity);
+      cudaGetLastError();
+      x.ok = ok;
+      return x;
+    }();
+    return a;
+  }
+  CUmemAllocationProp prop() const {
+    CUmemAllocationProp pr;
+    memset(&pr, 0, sizeof(pr));
+    pr.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    pr.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    pr.location.id = dev;
+    return pr;
+  }
+  // make [va, va + need) usable, [va, va + want) if memory allows (headroom
+  // keeps growth steps few)
+  int grow(size_t need, size_t want, size_t* hw) {
+    if (need <= mapped) return AGGB_OK;
+    const Api& A = api();
+    if (!A.ok) return fail(AGGB_CUDA_ERROR, "CUDA VMM entry points unavailable");
+    if (!va) {
+      cudaGetDevice(&dev);
+      CUmemAllocationProp pr = prop();
+      if (A.granularity(&gran, &pr, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) gran = 2u << 20;
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      reserved = ((std::max(tot, need) + gran - 1) / gran) * gran;
+      if (A.reserve(&va, reserved, gran, 0, 0) != CUDA_SUCCESS) {
+        va = 0;
+        return fail(AGGB_CUDA_ERROR, "cuMemAddressReserve(%zu) failed", reserved);
+      }
+    }
+    if (need > reserved) return fail(AGGB_CAPACITY_EXCEEDED, "spill pool of %zu bytes exceeds device memory", need);
+    want = std::min(reserved, std::max(std::max(want, need), mapped + ((size_t)512 << 20)));
+    size_t sz = ((want - mapped + gran - 1) / gran) * gran;
+    sz = std::min(sz, reserved - mapped);
+    CUmemAllocationProp pr = prop();
+    CUmemGenericAllocationHandle hd;
+    if (A.create(&hd, sz, &pr, 0) != CUDA_SUCCESS) {
+      // no room for the headroom: map just what is needed
+      sz = ((need - mapped + gran - 1) / gran) * gran;
+      if (A.create(&hd, sz, &pr, 0) != CUDA_SUCCESS)
+        return fail(AGGB_CUDA_ERROR, "cuMemCreate(%zu): out of memory (pool %zu mapped)", sz, mapped);
+    }
+    if (A.map(va + mapped, sz, 0, hd, 0) != CUDA_SUCCESS) {
+      A.release(hd);
+      return fail(AGGB_CUDA_ERROR, "cuMemMap failed");
+    }
+    CUmemAccessDesc ad;
+    memset(&ad, 0, sizeof(ad));
+    ad.location = pr.location;
+    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (A.access(va + mapped, sz, &ad, 1) != CUDA_SUCCESS) {
+      A.unmap(va + mapped, sz);
+      A.release(hd);
+      return fail(AGGB_CUDA_ERROR, "cuMemSetAccess failed");
+    }
+    chunks.push_back({hd, sz});
+    mapped += sz;
+    if (hw) *hw += sz;
+    return AGGB_OK;
+  }
+  void release() {
+    if (!va) return;
+    const Api& A = api();
+    size_t off = 0;
+    for (auto& c : chunks) {
+      A.unmap(va + off, c.second);
+      A.release(c.first);
+      off += c.second;
+    }
+    A.afree(va, reserved);
+    chunks.clear();
+    va = 0;
+    reserved = mapped = 0;
+  }
+  template <class T>
+  T* as() const { return (T*)va; }
 };
 
 uint64_t splitmix(uint64_t z) {
@@ -380,7 +500,8 @@ struct Handle {
   DBuf tkeys, tstates, thdr;
   bool has_table = false;
   // page pool
-  DBuf pool_base, page_part, page_fill, page_set, pool_ctr;  // pool_ctr: [0]=next_page [1]=overflow
+  VPool pool_base;
+  DBuf page_part, page_fill, page_set, pool_ctr;  // pool_ctr: [0]=next_page [1]=overflow
   uint32_t pool_cap = 0;
   uint64_t pool_bound = 0;  // upper bound of pages used since reset
   // spill sets
@@ -501,26 +622,27 @@ int pool_ensure(Handle* h, uint64_t extra_pages) {
     CU(cudaStreamSynchronize(h->st));
     used = std::min<uint32_t>(used, h->pool_cap);
   }
-  DBuf np, nf, ns, nb;
+  // page memory grows in place (VPool: mapped onto a reserved range, pages stay
+  // where they are); the 12 bytes of metadata per page are copied over
+  CU(cudaStreamSynchronize(h->st));
+  TRY(h->pool_base.grow(need * (size_t)PAGE_BYTES, cap * (size_t)PAGE_BYTES, &h->hw));
+  cap = std::min<uint64_t>(h->pool_base.mapped / PAGE_BYTES, 0xFFFFFFF0ull);
+  DBuf np, nf, ns;
   TRY(np.ensure(cap * 4, &h->hw));
   TRY(nf.ensure(cap * 4, &h->hw));
   TRY(ns.ensure(cap * 4, &h->hw));
-  TRY(nb.ensure(cap * (size_t)PAGE_BYTES, &h->hw));
   if (used) {
     CU(cudaMemcpyAsync(np.p, h->page_part.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
     CU(cudaMemcpyAsync(nf.p, h->page_fill.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
     CU(cudaMemcpyAsync(ns.p, h->page_set.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, h->st));
-    CU(cudaMemcpyAsync(nb.p, h->pool_base.p, (size_t)used * PAGE_BYTES, cudaMemcpyDeviceToDevice, h->st));
   }
   CU(cudaStreamSynchronize(h->st));
   h->page_part.release();
   h->page_fill.release();
   h->page_set.release();
-  h->pool_base.release();
   h->page_part = np;
   h->page_fill = nf;
   h->page_set = ns;
-  h->pool_base = nb;
   h->pool_cap = (uint32_t)cap;
   return AGGB_OK;
 }
@@ -1528,7 +1650,29 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     // instead (k_split: the partition is read twice and written once, where
     // sub-passes would read it nsub times); the children then take the
     // page-aligned sub-partitions in one pass each.
-    if (nsub >= 3 && nsets == 1 && !getenv("AGGB_NO_SPLIT_LEVEL")) {
+    // The split writes the whole set once more while its input stays live: when
+    // the pages it needs cannot be mapped from free memory (C5 hash_sort at 500M
+    // records: ~60 GB of partial-state runs), the children take sub-passes.
+    bool split_fits = true;
+    if (nsub >= 3 && nsets == 1) {
+      int64_t tin = 0;
+      for (int p = 0; p < nparts; p++) tin += (int64_t)recs[p];
+      const int per = std::max(1, make_set(h, 1, a.ss.rw - h->kw, a.ss.kind, 0).per_page);
+      uint32_t used = 0;
+      CU(cudaMemcpyAsync(&used, h->pool_ctr.p, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      const uint64_t pages = (uint64_t)std::min<uint32_t>(used, h->pool_cap) + (uint64_t)(tin / per) +
+                             (uint64_t)nonempty * std::min(nsub, 1024) + 16;
+      const size_t bytes = (size_t)pages * PAGE_BYTES;
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if (bytes > h->pool_base.mapped && bytes - h->pool_base.mapped > (size_t)(0.9 * (double)fr)) split_fits = false;
+      if (getenv("AGGB_TRACE"))
+        fprintf(stderr, "[aggb] split level: %llu pages (%.1f GB), mapped %.1f GB, free %.1f GB -> %s\n",
+                (unsigned long long)pages, bytes / 1e9, h->pool_base.mapped / 1e9, fr / 1e9,
+                split_fits ? "split" : "sub-passes");
+    }
+    if (nsub >= 3 && nsets == 1 && split_fits && !getenv("AGGB_NO_SPLIT_LEVEL")) {
       const int S = std::min(nsub, 1024);
       int64_t total_in = 0;
       for (int p = 0; p < nparts; p++) total_in += (int64_t)recs[p];
@@ -1575,9 +1719,21 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     int64_t total_recs = 0;
     for (int p = 0; p < nparts; p++) total_recs += (int64_t)recs[p];
     int ovw = h->kw + h->cs.ds.ns;
-    if (total_recs + 16 > h->ovf_cap) {
-      TRY(h->ovf.ensure((size_t)(total_recs + 16) * ovw * 8, &h->hw));
-      h->ovf_cap = total_recs + 16;
+    // the overflow list holds every record in the worst case, or what half of
+    // the free memory holds when that is less (C5 hash_sort at 500M records:
+    // 59 GB worst case, ~0 in fact); a longer list fails loudly below
+    int64_t ovf_want = total_recs + 16;
+    if (ovf_want > h->ovf_cap) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      const int64_t fit = (int64_t)(0.5 * (double)(fr + h->ovf.bytes) / (ovw * 8 * 1.25));
+      ovf_want = std::max<int64_t>(std::min<int64_t>(ovf_want, fit), std::min<int64_t>(ovf_want, 1 << 20));
+    }
+    if (ovf_want > h->ovf_cap) {
+      h->ovf.release();
+      h->ovf_cap = 0;
+      TRY(h->ovf.ensure((size_t)ovf_want * ovw * 8, &h->hw));
+      h->ovf_cap = ovf_want;
     }
     CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
     CU(cudaMemsetAsync(SC(h) + 12, 0, 8, h->st));
@@ -1622,6 +1778,9 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     CU(cudaStreamSynchronize(h->st));
     const unsigned long long novf = h->tail_sc[11];
     tr.mark(h->st, "drain: child");
+    if (novf > (unsigned long long)h->ovf_cap)
+      return fail(AGGB_CAPACITY_EXCEEDED, "child overflow of %llu records exceeds its %lld-record list", novf,
+                  (long long)h->ovf_cap);
     if (!novf) {
       h->tail_valid = true;
       return AGGB_OK;
@@ -1773,11 +1932,12 @@ void aggb_destroy(void* handle) {
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->cst) cudaStreamSynchronize(h->cst);
-  DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->pool_base, &h->page_part, &h->page_fill, &h->page_set,
+  DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->page_part, &h->page_fill, &h->page_set,
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals};
   for (DBuf* b : bufs) b->release();
+  h->pool_base.release();
   h->stage.release();
   h->pstage[0].release();
   h->pstage[1].release();

@@ -656,10 +656,12 @@ __global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
             } else if (lc[r]) {  // not resident: the next recursion level
               unsigned long long d = atomicAdd(a.ovf_count, 1ull);
               novf++;
+              if (d < (unsigned long long)a.ovf_stride) {  // past the list: counted, reported by the host
 #pragma unroll
-              for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
-              for (int j = 0; j < ns; j++)
-                a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
+                for (int w = 0; w < KW; w++) a.ovf[w * a.ovf_stride + d] = kc[r][w];
+                for (int j = 0; j < ns; j++)
+                  a.ovf[(KW + j) * a.ovf_stride + d] = contrib_fd<NWT>(s_fd[j], kind, j, vc[r]);
+              }
             }
             __syncwarp();
           }

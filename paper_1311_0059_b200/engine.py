@@ -123,10 +123,21 @@ class GroupBy:
         for i, t in enumerate(self.val_types):
             sp.val_type[i] = t
         sp.input_kind = N.INPUT_STATES if input_kind == "states" else N.INPUT_RAW
+        if stream is None:
+            # stream-ordered with the caller's torch work by default: device
+            # columns produced on torch's current stream are complete before
+            # this handle reads them (a private non-blocking stream would not
+            # wait for them)
+            import torch
+            if torch.cuda.is_available():
+                stream = torch.cuda.current_stream(device)
         self._stream = stream
         sptr = None
         if stream is not None:
             sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+            if sptr == 0:
+                sptr = 1  # torch's default stream is the legacy stream: cudaStreamLegacy
+
         h = ctypes.c_void_p()
         N.check(self.L.aggb_create(device, ctypes.byref(cfg), ctypes.byref(sp),
                                    ctypes.c_void_p(sptr) if sptr else None, ctypes.byref(h)),

@@ -6,8 +6,10 @@ source lines with the most stall samples.
 """
 import csv,sys,subprocess
 rep=sys.argv[1]
+IDX=int(sys.argv[3]) if len(sys.argv)>3 else 0  # which captured launch
+sel=['--launch-skip',str(IDX),'--launch-count','1']
 raw=subprocess.run(['ncu','-i',rep,'--page','raw','--csv'],capture_output=True,text=True).stdout
-r=list(csv.reader(raw.splitlines())); h=r[0]; v=r[2]
+r=list(csv.reader(raw.splitlines())); h=r[0]; v=r[2+IDX]
 def g(k):
     return v[h.index(k)] if k in h else None
 print('dur', g('gpu__time_duration.sum'), 'inst', g('smsp__inst_executed.sum'), 'ipc', g('sm__inst_executed.avg.per_cycle_active'))
@@ -21,7 +23,7 @@ for i,k in enumerate(h):
     try: x=float(v[i].replace(',','')); out.append((x,k[33:])); tot+=x
     except: pass
 print(' '.join(f'{k}:{100*x/tot:.1f}%' for x,k in sorted(out,reverse=True)[:9]))
-src=subprocess.run(['ncu','-i',rep,'--page','source','--csv','--print-source=cuda,sass'],capture_output=True,text=True).stdout
+src=subprocess.run(['ncu','-i',rep,'--page','source','--csv','--print-source=cuda,sass']+sel,capture_output=True,text=True).stdout
 rows=list(csv.reader(src.splitlines()))
 f=None; agg=[]
 for x in rows:
