@@ -615,7 +615,7 @@ int pool_ensure(Handle* h, uint64_t extra_pages) {
   h->pool_bound = need;
   if (need <= h->pool_cap) return AGGB_OK;
   // grow: one contiguous allocation; used pages and metadata are copied over
-  uint64_t cap = std::max<uint64_t>(need + need / 4, 4096);
+  uint64_t cap = std::max<uint64_t>(need + (need > (2u << 20) ? need / 16 : need / 4), 4096);  // less slack past 16 GB
   uint32_t used = 0;
   if (h->pool_cap) {
     CU(cudaMemcpyAsync(&used, h->pool_ctr.p, 4, cudaMemcpyDeviceToHost, h->st));
@@ -1365,7 +1365,11 @@ int cut_run(Handle* h) {
 int hash_sort_blind(Handle* h, const ColSrc& rest) {
   const int64_t c = std::max<int64_t>(1, (int64_t)h->tab.cap);
   const int words = h->kw + h->cs.ds.ns;
-  const int64_t K = std::max<int64_t>(1, std::min<int64_t>((rest.n + c - 1) / c, (int64_t)(8 << 20) / (c + 2)));
+  // runs accumulate to ~1/8 of the batch (8M to 64M records) per GRACE pass:
+  // every pass leaves a partly filled page per (CTA, partition), so fewer passes
+  // fragment the pool less (C5 at 500M records: 60 passes left ~16 GB of slack)
+  const int64_t acc_recs = std::max<int64_t>(8 << 20, std::min<int64_t>(64 << 20, rest.n / 8));
+  const int64_t K = std::max<int64_t>(1, std::min<int64_t>((rest.n + c - 1) / c, acc_recs / (c + 2)));
   const int64_t acc_cap = K * (c + 2);
   TRY(h->cut_tmp.ensure((size_t)acc_cap * words * 8, &h->hw));
   OutBuf o;
@@ -1666,6 +1670,10 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
       const size_t bytes = (size_t)pages * PAGE_BYTES;
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
+      if (bytes > h->pool_base.mapped && bytes - h->pool_base.mapped > (size_t)(0.9 * (double)fr) && h->cut_tmp.p) {
+        h->cut_tmp.release();  // hash_sort's run accumulation buffer is idle until the next push
+        cudaMemGetInfo(&fr, &tot);
+      }
       if (bytes > h->pool_base.mapped && bytes - h->pool_base.mapped > (size_t)(0.9 * (double)fr)) split_fits = false;
       if (getenv("AGGB_TRACE"))
         fprintf(stderr, "[aggb] split level: %llu pages (%.1f GB), mapped %.1f GB, free %.1f GB -> %s\n",

@@ -7,16 +7,26 @@ from paper_1311_0059_b200 import datagen as D
 from paper_1311_0059_b200.engine import GroupBy
 from paper_1311_0059_b200.core import DatasetStats
 
-runs = [("C1", "pre_partitioning", 0), ("C1", "hash_sort", 0), ("C2", "original_hh", 0),
-        ("C3", "pre_partitioning", 0), ("C3", "hash_sort", 0),
-        ("C4", "sort_based", 200_000_000), ("C4", "hash_sort", 200_000_000),
-        ("C5", "pre_partitioning", 100_000_000), ("C5", "hash_sort", 100_000_000)]
+# every config at its BASELINE.json size (C3 at each Zipf exponent); the
+# AGGB_SCALED=1 environment keeps the older scaled C4 (200M) / C5 (100M) runs
+FULL = not os.environ.get("AGGB_SCALED")
+runs = [("C1", "pre_partitioning", 0, None), ("C1", "hash_sort", 0, None),
+        ("C2", "pre_partitioning", 0, None), ("C2", "original_hh", 0, None),
+        ("C3", "pre_partitioning", 0, 0.5), ("C3", "pre_partitioning", 0, 1.0),
+        ("C3", "pre_partitioning", 0, 1.5), ("C3", "hash_sort", 0, 0.5), ("C3", "hash_sort", 0, 1.0),
+        ("C3", "hash_sort", 0, 1.5),
+        ("C4", "sort_based", 0 if FULL else 200_000_000, None), ("C4", "hash_sort", 0 if FULL else 200_000_000, None),
+        ("C5", "pre_partitioning", 0 if FULL else 100_000_000, None),
+        ("C5", "hash_sort", 0 if FULL else 100_000_000, None)]
 only = sys.argv[1:]
 dev = torch.device("cuda", 0)
-for name, algo, nrec in runs:
+import dataclasses
+for name, algo, nrec, zs in runs:
     if only and name not in only:
         continue
     cfg = D.CONFIGS[name]
+    if zs is not None:
+        cfg = dataclasses.replace(cfg, zipf_s=zs)
     if nrec:
         cfg = D.scaled(cfg, nrec)
     keys, vals = bench.make_inputs(cfg, 0, cfg.n, dev)
@@ -38,7 +48,7 @@ for name, algo, nrec in runs:
         m = g.metrics()
         kk, vv = g.result_torch()
         cnt = vv[0].sum().item()  # COUNT column
-        print(json.dumps({"cfg": name, "algo": algo, "n": cfg.n, "ms": round(ms, 2),
+        print(json.dumps({"cfg": name, "algo": algo, "s": zs, "n": cfg.n, "ms": round(ms, 2),
                           "Grec_s": round(cfg.n / ms / 1e6, 2), "groups": res.n_groups,
                           "count_sum_ok": int(cnt) == cfg.n, "spilled": m["spilled_records"],
                           "depth": m["recursion_depth"], "kernels": ks}), flush=True)
@@ -46,4 +56,5 @@ for name, algo, nrec in runs:
     except Exception as e:
         print(json.dumps({"cfg": name, "algo": algo, "error": f"{type(e).__name__}: {e}"}), flush=True)
     del keys, vals
+    bench.make_inputs.rows = None  # C5's 64-byte rows (32 GB at full size)
     torch.cuda.empty_cache()
