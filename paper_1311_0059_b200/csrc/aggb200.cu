@@ -384,13 +384,19 @@ struct PassCfg {
   int R, blk;
 };
 
-template <int KW, int NWT, int R, int BLK, class PG>
-PassCfg pc() { return PassCfg{k_pass<KW, NWT, R, BLK, 1, PG>, R, BLK}; }
+template <int KW, int NWT, int R, int BLK, class PG, int NH = 0>
+PassCfg pc() { return PassCfg{k_pass<KW, NWT, R, BLK, 1, PG, NH>, R, BLK}; }
+
+constexpr int NHOT = 1;  // k_pass heavy-hitter tier on (pass.cuh HotOps; up to HOT_MAX keys)
 
 template <int KW>
-PassCfg pass_kernel(int nwt, int prog) {
+PassCfg pass_kernel(int nwt, int prog, bool hot = false) {
   // 512 threads x 4 records, up to 128 registers, 1 CTA/SM: the 1024 x 2 shape
   // spilled at its 64-register cap (profiles/r01_notes.md)
+  if (KW == 1 && nwt == 1 && hot) {
+    if (prog == 1) return pc<1, 1, 4, 512, ProgC1, NHOT>();
+    if (prog == 3) return pc<1, 1, 4, 512, ProgC3, NHOT>();
+  }
   if (KW == 1 && nwt == 1) {
     if (prog == 1) return pc<1, 1, 4, 512, ProgC1>();
     if (prog == 2) return pc<1, 1, 4, 512, ProgC2>();
@@ -533,6 +539,9 @@ struct Handle {
   int64_t hash_sort_runs = 0;
   // recursion scratch
   DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend, l2stage, cut_tmp;
+  DBuf hot;                 // heavy-hitter keys of the current push (k_hot_sample)
+  bool hot_ready = false;
+  bool hot_no_tier = false;  // the hot keys cover most records: no SMEM pre-aggregation tier
   int prog = 0;
   // blocked bloom filter of the frozen level-0 table (PROBE)
   DBuf bloom;
@@ -713,7 +722,8 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (pp.mode != MODE_FILL) payload = std::max(payload, pp.ss.rw - h->kw);
   int nwt = nwt_for(std::max(payload, 1));
   if (nwt > 32) return fail(AGGB_SPEC_ERROR, "record payload of %d words exceeds 32", payload);
-  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+  bool hot = h->hot_ready && h->kw == 1 && nwt == 1 && (pp.mode == MODE_FILL || pp.mode == MODE_PROBE);
+  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog, hot) : pass_kernel<2>(nwt, h->prog);
   int P = pp.mode == MODE_FILL ? 1 : pp.ss.nparts;
   int G = pp.mode == MODE_FILL ? 1 : group_of(pp.ss.rw);
   int rw = pp.mode == MODE_FILL ? 1 : pp.ss.rw;
@@ -766,9 +776,16 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
   // SMEM pre-aggregation tier for inserting passes over one-word keys (pass.cuh)
   int cache_log2 = 0;
+  if (hot && smem + hot_smem<ProgC1>(blk) + 16 <= 200 * 1024) {
+    smem += hot_smem<ProgC1>(blk) + 16;  // ProgC1 and ProgC3 both hold 2 fields
+  } else if (hot) {                      // no room next to the partitions: the plain pass
+    hot = false;
+    pcfg = pass_kernel<1>(nwt, h->prog, false);
+    fn = pcfg.fn;
+  }
   // (an L2-capped in-memory plan probes hot keys: the tier serves PROBE too)
   if (!fast_probe && (pp.mode == MODE_FILL || (pp.mode == MODE_PROBE && h->l2_capped)) && h->kw == 1 &&
-      !getenv("AGGB_NO_CACHE")) {
+      !getenv("AGGB_NO_CACHE") && !(hot && h->hot_no_tier)) {
     const size_t per = 12 + 8 * (size_t)h->cs.ds.ns;
     const size_t room = std::min<size_t>(160 * 1024, 224 * 1024 - std::min<size_t>(smem + 16, 224 * 1024));
     int L = 0;
@@ -828,6 +845,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.stats = SC(h);
   a.cache_log2 = cache_log2;
   a.pairs = pairs ? 1 : 0;
+  a.hot = hot ? h->hot.as<uint64_t>() : nullptr;
   // chunked reservations for large tables: unused chunks (< grid * chunk) stay under 1% of cap
   {
     const uint64_t cap = h->tab.cap;
@@ -1966,8 +1984,39 @@ void aggb_destroy(void* handle) {
 }
 
 
+// Heavy hitters of this push (pass.cuh k_hot_sample): in-memory and L2-capped
+// plans of one-word keys with the COUNT/SUM programs (C1, C3, C4).  Budgeted
+// plans keep the reference's arrival-order residency untouched (the tier only
+// takes keys already resolved resident, but its sample is not needed there).
+int hot_sample(Handle* h, const ColSrc& col) {
+  h->hot_ready = false;
+  const bool eligible = h->kw == 1 && col.nv == 1 && (h->prog == 1 || h->prog == 3) &&
+                        (h->unlimited || h->l2_capped) && (h->cfg.algo == AGGB_PRE_PARTITIONING ||
+                                                           h->cfg.algo == AGGB_HASH_SORT) &&
+                        col.n >= (1 << 16) && !getenv("AGGB_NO_HOT");
+  if (!eligible) return AGGB_OK;
+  TRY(h->hot.ensure((HOT_MAX + 2) * 8, &h->hw));
+  const int64_t sample = std::min<int64_t>(col.n, 1 << 17);
+  const uint32_t min_count = (uint32_t)std::max<int64_t>(8, sample / 256);  // >= 0.4% of the records
+  k_hot_sample<<<1, 1024, 0, h->st>>>(col, col.n, sample, min_count, h->hot.as<uint64_t>());
+  h->launches++;
+  CU(cudaGetLastError());
+  uint64_t nh[2] = {0, 0};  // no heavy hitters (uniform keys): the plain pass, no tier cost
+  CU(cudaMemcpyAsync(nh, h->hot.as<uint64_t>() + HOT_MAX, 16, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  h->hot_ready = nh[0] > 0;
+  // When the hot keys carry most of the records (Zipf s = 1.5: ~74%), the keys
+  // just below them are still hot enough to serialise the SMEM tier's CAS loops
+  // (f64 ADD), while L2 REDs do not stall the issuing warp: the pass runs
+  // without the SMEM tier (C3 s = 1.5 FILL 14.0 -> 5.2 ms; at s = 1.0, 16%
+  // covered, the tier stays: 9.06 vs 9.63 ms without it).
+  h->hot_no_tier = h->hot_ready && nh[1] * 10 >= (uint64_t)sample * 4;
+  return AGGB_OK;
+}
+
 int push_col(Handle* h, const ColSrc& col) {
   if (h->cfg.algo == AGGB_SORT_BASED) return aggb_sort_push(h, col);
+  TRY(hot_sample(h, col));
   if (h->cfg.algo == AGGB_HASH_SORT) return push_hash_sort(h, col);
   return push_hybrid(h, col);
 }
@@ -2063,9 +2112,7 @@ int aggb_push(void* handle, const aggb_input* in) {
   h->records += in->n_rows;
   int s;
   Trace tr;
-  if (h->cfg.algo == AGGB_SORT_BASED) s = aggb_sort_push(h, col);
-  else if (h->cfg.algo == AGGB_HASH_SORT) s = push_hash_sort(h, col);
-  else s = push_hybrid(h, col);
+  s = push_col(h, col);
   tr.mark(h->st, "push");
   if (!sg.owned.empty()) {
     cudaStreamSynchronize(h->st);

@@ -52,7 +52,118 @@ struct PassArgs {
   unsigned long long* cand_count;         // [NREG]
   uint2* chains;                          // per (CTA, partition): {records claimed, page of the last claim}
   int32_t pairs;                          // k_probe: sector pairs on (shared memory permitting)
+  const uint64_t* hot;                    // heavy-hitter keys (k_hot_sample): hot[0..7] keys, hot[8] count
 };
+
+// ---------------------------------------------------------------------------
+// Heavy-hitter tier (k_pass NH > 0; in-memory and L2-capped plans of one-word
+// keys).  Under Zipf s = 1.5 (C3) the hottest key is ~38% of the records and
+// the next few several percent each: in the SMEM pre-aggregation tier every CTA
+// serialises on a handful of shared addresses (f64 ADD is a CAS loop there;
+// ncu: 60% of the FILL's stalls).  k_hot_sample finds up to 8 keys above 0.4% of
+// a strided sample.  k_pass gives every thread a private accumulator column per
+// hot key in shared memory (no atomics, no contention), reached through a
+// 64-entry directory indexed by the record's table hash; a record takes it once
+// its key is known resident in this CTA (slot resolved through the table, as
+// for the SMEM tier).  At exit the columns are warp-reduced and merged into
+// the table with one L2 update per warp and field.
+// ---------------------------------------------------------------------------
+constexpr int HOT_MAX = 8;
+constexpr int HOT_DIR = 64;  // directory entries (power of two)
+template <class PG>
+struct HotOps {
+  static constexpr int N = 1;
+  static __device__ __forceinline__ uint32_t desc(int) { return 0; }
+  template <int NWT>
+  static __device__ __forceinline__ void add(uint64_t*, int, int, const uint64_t (&)[NWT]) {}
+};
+template <uint32_t... F>
+struct HotOps<PS<F...>> {
+  static constexpr int N = sizeof...(F);
+  static __device__ __forceinline__ uint32_t desc(int j) {
+    constexpr uint32_t fd[N] = {F...};
+    return fd[j];
+  }
+  // col: this thread's column of hot key q (field j at col[j * stride])
+  template <int NWT>
+  static __device__ __forceinline__ void add(uint64_t* col, int stride, int kind, const uint64_t (&v)[NWT]) {
+    constexpr uint32_t fd[N] = {F...};
+#pragma unroll
+    for (int j = 0; j < N; j++)
+      col[j * stride] = merge_word(col[j * stride], contrib_fd<NWT>(fd[j], kind, j, v), fd[j] & 3, (fd[j] >> 2) & 3);
+  }
+};
+// dynamic shared memory of the tier: directory keys, directory hot index, slots, accumulators
+template <class PG>
+constexpr size_t hot_smem(int blk) {
+  return HOT_DIR * 8 + HOT_DIR * 4 + HOT_MAX * 8 + (size_t)HOT_MAX * HotOps<PG>::N * blk * 8;
+}
+
+// one CTA: count the keys of a strided sample in a shared-memory table, then
+// pick up to 8 keys seen at least min_count times, most frequent first
+constexpr int HOT_SLOTS = 2048;
+__global__ void __launch_bounds__(1024) k_hot_sample(ColSrc c, int64_t n, int64_t sample, uint32_t min_count,
+                                                     uint64_t* out) {
+  __shared__ unsigned long long sk[HOT_SLOTS];
+  __shared__ uint32_t sc[HOT_SLOTS];
+  __shared__ unsigned long long s_best[32];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < HOT_SLOTS; i += blockDim.x) {
+    sk[i] = EMPTY;
+    sc[i] = 0;
+  }
+  __syncthreads();
+  const int64_t step = sample > 0 ? (n / sample > 1 ? n / sample : 1) : 1;
+  for (int64_t q = tid; q < sample; q += blockDim.x) {
+    const int64_t i = q * step;
+    if (i >= n) break;
+    uint64_t k[1];
+    col_key<1>(c, i, k);
+    if (k[0] == EMPTY) continue;
+    uint32_t b = (uint32_t)fmix64(k[0]) & (HOT_SLOTS - 1);
+    for (int t = 0; t < 16; t++, b = (b + 1) & (HOT_SLOTS - 1)) {
+      unsigned long long prev = sk[b];
+      if (prev == EMPTY) prev = atomicCAS(&sk[b], EMPTY, (unsigned long long)k[0]);
+      if (prev == EMPTY || prev == k[0]) {
+        atomicAdd(&sc[b], 1u);
+        break;
+      }
+    }
+  }
+  if (tid == 0) out[HOT_MAX + 1] = 0;
+  __syncthreads();
+  int found = 0;
+  for (int r = 0; r < HOT_MAX; r++) {
+    unsigned long long best = 0;  // count << 32 | slot
+    for (int i = tid; i < HOT_SLOTS; i += blockDim.x)
+      if (sc[i] >= min_count) best = max(best, ((unsigned long long)sc[i] << 32) | (unsigned)i);
+    for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((tid & 31) == 0) s_best[tid >> 5] = best;
+    __syncthreads();
+    if (tid < 32) {
+      best = tid < (int)(blockDim.x >> 5) ? s_best[tid] : 0ull;
+      for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (tid == 0) {
+        if (best >> 32) {
+          out[HOT_MAX + 1] += best >> 32;  // sample records the hot keys cover
+          out[found] = sk[(uint32_t)best];
+          sc[(uint32_t)best] = 0;
+        }
+        s_best[0] = best;
+      }
+    }
+    __syncthreads();
+    const bool any = (s_best[0] >> 32) != 0;
+    __syncthreads();
+    if (!any) break;
+    found++;
+  }
+  if (tid == 0) {
+    for (int r = found; r < HOT_MAX; r++) out[r] = EMPTY;
+    out[HOT_MAX] = (uint64_t)found;
+  }
+}
+
 
 template <int KW, int NWT>
 __device__ __forceinline__ void load_rec(const ColSrc& c, bool dense, int nv, int64_t i, uint64_t (&k)[KW],
@@ -103,7 +214,7 @@ __device__ __forceinline__ void put_rec(uint64_t* dst, const uint64_t (&k)[KW], 
 // never evicts a half-written sector (which ECC DRAM would read-modify-write).
 // ---------------------------------------------------------------------------
 
-template <int KW, int NWT, int R, int BLK, int MINB, class PG>
+template <int KW, int NWT, int R, int BLK, int MINB, class PG, int NH = 0>
 __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = BLK, tid = threadIdx.x;
@@ -165,6 +276,36 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     for (int j = 0; j < a.sp.ns; j++) cst[(size_t)j * CH + i] = state_identity(a.sp.op[j], a.sp.ty[j]);
   }
   if (tid == 0) s_ccount = 0;
+  // heavy-hitter tier (NH > 0): directory, resolved slots, per-thread accumulator columns
+  using HO = HotOps<PG>;
+  uint64_t* hdk = (uint64_t*)(((uintptr_t)(cgs + CH) + 15) & ~(uintptr_t)15);  // HOT_DIR keys
+  int32_t* hdi = (int32_t*)(hdk + HOT_DIR);                                     // HOT_DIR hot index
+  long long* hsl = (long long*)(hdi + HOT_DIR);                                 // HOT_MAX slots
+  uint64_t* hacc = (uint64_t*)(hsl + HOT_MAX);                                  // [HOT_MAX][N][BLK]
+  if constexpr (NH > 0) {
+    for (int i = tid; i < HOT_DIR; i += B) {
+      hdk[i] = EMPTY;
+      hdi[i] = -1;
+    }
+    if (tid < HOT_MAX) hsl[tid] = -1;
+    for (int q = 0; q < HOT_MAX; q++)
+      for (int j = 0; j < HO::N; j++) {
+        const uint32_t F = HO::desc(j);
+        hacc[((size_t)q * HO::N + j) * BLK + tid] = state_identity(F & 3, (F >> 2) & 3);
+      }
+    __syncthreads();
+    if (tid == 0) {  // hot keys into the directory (a colliding later key is left out)
+      const int nh = a.hot[HOT_MAX] < (uint64_t)HOT_MAX ? (int)a.hot[HOT_MAX] : HOT_MAX;
+      for (int q = 0; q < nh; q++) {
+        const uint64_t k[1] = {a.hot[q]};
+        const int d = (int)(hash_key<1>(k, a.t.seed) >> 58) & (HOT_DIR - 1);
+        if (hdi[d] < 0) {
+          hdk[d] = k[0];
+          hdi[d] = q;
+        }
+      }
+    }
+  }
   const int64_t n = a.col.n;
   const int64_t col_start =
       a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
@@ -260,6 +401,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         // spill partition from the high bits, bloom probe from a remix
         const uint64_t h = hash_key<KW>(kc[r], a.t.seed);
         bk[r] = h;
+        if constexpr (NH > 0) {  // heavy hitter with a resolved slot: this thread's column
+          const int d = (int)(h >> 58) & (HOT_DIR - 1);
+          if (hdk[d] == kc[r][0]) {
+            const int q = hdi[d];
+            if (*(volatile long long*)&hsl[q] >= 0) {
+              HO::template add<NWT>(hacc + (size_t)q * HO::N * BLK + tid, BLK, kind, vc[r]);
+              c_rec++;
+              c_hit++;
+              part[r] = -2;
+              continue;
+            }
+          }
+        }
         if (CH) {  // pre-aggregation tier: a cached key never leaves the SM
           const int c0 = (int)(h >> 40) & (CH - 1);
           int hit = -1;
@@ -311,6 +465,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
           c_hit += (res == R_HIT);
           c_ins += (res == R_INSERTED);
           part[r] = -2;
+          if constexpr (NH > 0) {
+            const int d = (int)(bk[r] >> 58) & (HOT_DIR - 1);
+            if (hdk[d] == kc[r][0] && !is_sentinel<KW>(kc[r])) *(volatile long long*)&hsl[hdi[d]] = s;
+          }
           // resident now: cache the key for its later records (first come, no eviction)
           if (CH && !is_sentinel<KW>(kc[r]) && *(volatile int*)&s_ccount < (CH * 3) / 4) {
             const int c0 = (int)(bk[r] >> 40) & (CH - 1);
@@ -470,6 +628,21 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
     }
   }
   __syncthreads();
+  if constexpr (NH > 0) {  // heavy-hitter columns: warp-reduced, one L2 update per warp and field
+    for (int q = 0; q < HOT_MAX; q++) {
+      const long long sl = hsl[q];
+      if (sl < 0) continue;  // CTA-uniform (after the barrier above)
+#pragma unroll
+      for (int j = 0; j < HO::N; j++) {
+        const uint32_t F = HO::desc(j);
+        uint64_t v = hacc[((size_t)q * HO::N + j) * BLK + tid];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = merge_word(v, __shfl_xor_sync(0xffffffffu, v, o), F & 3, (F >> 2) & 3);
+        if ((tid & 31) == 0 && v != state_identity(F & 3, (F >> 2) & 3))
+          gupdate(a.t.states + (uint64_t)j * a.t.stride + (uint64_t)sl, F & 3, (F >> 2) & 3, v);
+      }
+    }
+  }
   // merge the pre-aggregation tier into the table (skip identity states: keys cached late)
   for (int i = tid; i < CH; i += B) {
     if (ckeys[i] == EMPTY) continue;

@@ -13,8 +13,12 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--algo", default="pre_partitioning")
 ap.add_argument("--records", type=int, default=0)
 ap.add_argument("--runs", type=int, default=2)
+ap.add_argument("--zipf-s", type=float, default=0.0)
 a = ap.parse_args()
 cfg = D.CONFIGS[a.config]
+if a.zipf_s:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, zipf_s=a.zipf_s)
 if a.records:
     cfg = D.scaled(cfg, a.records)
 dev = torch.device("cuda", 0)

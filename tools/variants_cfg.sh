@@ -1,8 +1,9 @@
 #!/bin/bash
 # Time one config/algo under several env settings: variants_cfg.sh CFG ALGO RECORDS "ENV=.." ...
 cfg=$1; algo=$2; recs=$3; shift 3
+zs=${ZIPF_S:-0}
 for v in "$@"; do
-  env $v timeout 300 python tools/prof_run.py --config $cfg --algo $algo --records $recs > gpurun_out/var.log 2>&1
+  env $v timeout 300 python tools/prof_run.py --config $cfg --algo $algo --records $recs --zipf-s $zs > gpurun_out/var.log 2>&1
   python - "$v" <<'PY'
 import json, sys
 t = open('gpurun_out/var.log').read()
