@@ -415,7 +415,9 @@ PassCfg pass_kernel(int nwt, int prog, bool hot = false) {
 
 // PROBE specialised for one-word keys and one dense 8-byte value column (probe.cuh)
 template <int PM, int R = 4, int BLK = 512>
-PassCfg probe_kernel_pm(int prog) {
+PassCfg probe_kernel_pm(int prog, bool hot = false) {
+  if (PM == PM_ONE && hot && prog == 1) return PassCfg{k_probe<R, BLK, ProgC1, PM, 1>, R, BLK};
+  if (PM == PM_ONE && hot && prog == 3) return PassCfg{k_probe<R, BLK, ProgC3, PM, 1>, R, BLK};
   if (prog == 1) return PassCfg{k_probe<R, BLK, ProgC1, PM>, R, BLK};
   if (prog == 2) return PassCfg{k_probe<R, BLK, ProgC2, PM>, R, BLK};
   if (prog == 3) return PassCfg{k_probe<R, BLK, ProgC3, PM>, R, BLK};
@@ -730,7 +732,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   // k_probe: 16-byte raw records from dense 8-byte columns (and the SoA deferral list)
   const bool fast_probe = pp.mode == MODE_PROBE && h->kw == 1 && pp.col.nv == 1 && pp.ss.rw == 2 && pp.col_kind == 0 &&
                           pp.ss.kind == 0 && (!pp.lin || (pp.lin_words == 1 && pp.lin_kind == 0)) &&
-                          dense8(pp.col, 1) && pp.ss.per_page == 512 && !h->l2_capped &&
+                          dense8(pp.col, 1) && pp.ss.per_page == 512 && (!h->l2_capped || !getenv("AGGB_L2CAP_WIDE")) &&
                           // page ids are 24-bit in k_probe's page map (conservative pool estimate)
                           h->pool_bound + (uint64_t)(pp.col.n + pp.lin_stride) / 256 +
                                   (uint64_t)h->sms * (2ull * pp.ss.nparts + 128) < 0xFFFFF0ull &&
@@ -747,7 +749,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
     pcfg = h->prog == 5 ? PassCfg{k_probe_w<2, 4, 2, 512, ProgC5>, 2, 512} : PassCfg{k_probe_w<2, 4, 2, 512, PD>, 2, 512};
   // two-phase PROBE (probe.cuh): a streaming partition pass, then the bloom positives
   const bool split = fast_probe && h->bloom_words && getenv("AGGB_SPLIT");
-  if (fast_probe) pcfg = probe_kernel(h->prog, split ? PM_SCAN : PM_ONE);
+  if (fast_probe) pcfg = split ? probe_kernel(h->prog, PM_SCAN) : probe_kernel_pm<PM_ONE>(h->prog, hot);
   pass_fn fn = pcfg.fn;
   int R = pcfg.R, blk = pcfg.blk;
   int T = R * blk;
@@ -776,11 +778,12 @@ int launch_pass(Handle* h, PassPlan& pp) {
   if (smem > 227 * 1024) return fail(AGGB_SPEC_ERROR, "pass needs %zu bytes of shared memory", smem);
   // SMEM pre-aggregation tier for inserting passes over one-word keys (pass.cuh)
   int cache_log2 = 0;
-  if (hot && smem + hot_smem<ProgC1>(blk) + 16 <= 200 * 1024) {
+  if (wide_probe || (fast_probe && split)) hot = false;  // k_probe_w / the split PROBE: no heavy-hitter tier
+  if (hot && smem + hot_smem<ProgC1>(blk) + 16 <= (fast_probe ? 220 : 200) * 1024) {
     smem += hot_smem<ProgC1>(blk) + 16;  // ProgC1 and ProgC3 both hold 2 fields
   } else if (hot) {                      // no room next to the partitions: the plain pass
     hot = false;
-    pcfg = pass_kernel<1>(nwt, h->prog, false);
+    pcfg = fast_probe ? probe_kernel_pm<PM_ONE>(h->prog, false) : pass_kernel<1>(nwt, h->prog, false);
     fn = pcfg.fn;
   }
   // (an L2-capped in-memory plan probes hot keys: the tier serves PROBE too)
@@ -1069,6 +1072,11 @@ int plan(Handle* h) {
     cudaGetLastError();
     const double per_group = 2.0 * 8.0 * (h->kw + std::max(1, ns));  // 2 slots per group, key + states
     int64_t l2cap = (int64_t)(0.4 * std::max(l2, 32 << 20) / per_group);
+    // one-word keys with one value column PROBE through k_probe: its SMEM bloom
+    // (8 bits per resident key in 64 KB) rejects the records to spill, and the
+    // heavy-hitter columns fit beside it.  C3 s = 0.5: generic PROBE of a 1M-group
+    // table 12.9 ms -> k_probe 4.3 ms (profiles/r01_notes.md, session 3)
+    if (h->kw == 1 && h->cs.nv == 1 && !getenv("AGGB_L2CAP_WIDE")) l2cap = std::min<int64_t>(l2cap, 65536);
     if (getenv("AGGB_L2_CAP_GROUPS")) l2cap = std::max(8, atoi(getenv("AGGB_L2_CAP_GROUPS")));  // test hook
     if (h->budget > 2 * l2cap) {
       h->budget = l2cap;
@@ -1092,7 +1100,7 @@ int plan(Handle* h) {
   int cap_parts = std::min(MAX_PARTS, max_parts_for(rw0));
   // k_probe (one-word keys, one value) keeps its 128 KB bloom only up to ~2.3K
   // partitions of shared-memory state (probe_smem); beyond, PROBE runs 2x slower
-  if (h->kw == 1 && h->cs.nv == 1) cap_parts = std::min(cap_parts, 2200);
+  if (h->kw == 1 && h->cs.nv == 1) cap_parts = std::min(cap_parts, h->l2_capped ? 1536 : 2200);  // + hot columns
   if (getenv("AGGB_MAX_P0")) cap_parts = std::max(2, std::min(cap_parts, atoi(getenv("AGGB_MAX_P0"))));  // test hook
   // Shared-memory children hold child_cap groups; when the fan-out that needs is
   // more than one spill pass can write, every level would retire only
@@ -1756,10 +1764,10 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
       ovf_want = std::max<int64_t>(std::min<int64_t>(ovf_want, fit), std::min<int64_t>(ovf_want, 1 << 20));
     }
     if (ovf_want > h->ovf_cap) {
-      h->ovf.release();
+      if ((size_t)ovf_want * ovw * 8 > h->ovf.bytes) h->ovf.release();  // no copy needed: reallocate
       h->ovf_cap = 0;
       TRY(h->ovf.ensure((size_t)ovf_want * ovw * 8, &h->hw));
-      h->ovf_cap = ovf_want;
+      h->ovf_cap = (int64_t)(h->ovf.bytes / ((size_t)ovw * 8));  // the buffer's headroom counts
     }
     CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
     CU(cudaMemsetAsync(SC(h) + 12, 0, 8, h->st));

@@ -25,7 +25,7 @@ constexpr int PQ_RING = 64;  // per-warp ring of bloom-positive records (two rou
 // Resolve key k (value v) against the frozen table: aggregate with L2 atomics if
 // resident.  The first bucket (b, x, y) was loaded by the caller.
 template <class PG>
-__device__ __forceinline__ bool probe_finish(const PassArgs& a, uint64_t k, uint64_t v, uint64_t b, ulonglong2 x,
+__device__ __forceinline__ int64_t probe_finish(const PassArgs& a, uint64_t k, uint64_t v, uint64_t b, ulonglong2 x,
                                              ulonglong2 y, const uint32_t* s_fd, int ns) {
   int64_t s = -1;
   if (k == EMPTY) {  // escape slot: the key whose word equals the sentinel
@@ -43,18 +43,20 @@ __device__ __forceinline__ bool probe_finish(const PassArgs& a, uint64_t k, uint
       y = __ldcg(p + 1);
     }
   }
-  if (s < 0) return false;
+  if (s < 0) return -1;
   const uint64_t vv[1] = {v};
   Upd<PG>::template g<1>(a.t.states, a.t.stride, (uint64_t)s, 0, s_fd, ns, vv);
-  return true;
+  return s;
 }
 
-__device__ __forceinline__ void probe_issue(const PassArgs& a, uint64_t k, uint64_t& b, ulonglong2& x, ulonglong2& y) {
+__device__ __forceinline__ uint64_t probe_issue(const PassArgs& a, uint64_t k, uint64_t& b, ulonglong2& x, ulonglong2& y) {
   const uint64_t kk[1] = {k};
-  b = hash_key<1>(kk, a.t.seed) & a.t.bmask;
+  const uint64_t hh = hash_key<1>(kk, a.t.seed);
+  b = hh & a.t.bmask;
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
   x = __ldca(p);  // L1: prefetched by the owner lane at classification
   y = __ldca(p + 1);
+  return hh;
 }
 
 // Spill layout: each CTA appends a partition's records to its own chain of
@@ -83,7 +85,7 @@ __device__ __forceinline__ void probe_issue(const PassArgs& a, uint64_t k, uint6
 constexpr int PM_ONE = 0, PM_SCAN = 1, PM_RESOLVE = 2;
 constexpr int NREG = 4;
 
-template <int R, int BLK, class PG, int PM>
+template <int R, int BLK, class PG, int PM, int NH = 0>
 __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   constexpr int T = R * BLK, NWARP = BLK / 32;
   constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
@@ -115,6 +117,36 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
   __shared__ unsigned long long s_cnt[ST_NSTATS];
   __shared__ unsigned long long s_rt[NREG + 1];    // PM_RESOLVE: first tile of each candidate region
   __shared__ unsigned long long s_rn[NREG];        // PM_RESOLVE: candidates per region
+  // heavy-hitter tier (NH > 0, pass.cuh): directory, resolved slots, per-thread columns
+  using HO = HotOps<PG>;
+  uint64_t* hdk = (uint64_t*)(((uintptr_t)(PAIR ? (void*)(ptag + P) : (void*)(ent + P * NE)) + 15) & ~(uintptr_t)15);
+  int32_t* hdi = (int32_t*)(hdk + HOT_DIR);
+  long long* hsl = (long long*)(hdi + HOT_DIR);
+  uint64_t* hacc = (uint64_t*)(hsl + HOT_MAX);
+  if constexpr (NH > 0) {
+    for (int i = tid; i < HOT_DIR; i += BLK) {
+      hdk[i] = EMPTY;
+      hdi[i] = -1;
+    }
+    if (tid < HOT_MAX) hsl[tid] = -1;
+    for (int q = 0; q < HOT_MAX; q++)
+      for (int j = 0; j < HO::N; j++) {
+        const uint32_t F = HO::desc(j);
+        hacc[((size_t)q * HO::N + j) * BLK + tid] = state_identity(F & 3, (F >> 2) & 3);
+      }
+    __syncthreads();
+    if (tid == 0) {
+      const int nh = a.hot[HOT_MAX] < (uint64_t)HOT_MAX ? (int)a.hot[HOT_MAX] : HOT_MAX;
+      for (int q = 0; q < nh; q++) {
+        const uint64_t k[1] = {a.hot[q]};
+        const int d = (int)(hash_key<1>(k, a.t.seed) >> 58) & (HOT_DIR - 1);
+        if (hdi[d] < 0) {
+          hdk[d] = k[0];
+          hdi[d] = q;
+        }
+      }
+    }
+  }
 
   const int64_t n = PM == PM_RESOLVE ? 0 : a.col.n;
   const int64_t col_start = (PM != PM_RESOLVE && a.start_tiles)
@@ -230,6 +262,19 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
       const uint64_t kk[1] = {kc[r]};
       const uint64_t h = hash_key<1>(kk, a.t.seed);
       part[r] = kc[r] == EMPTY ? 0 : (int)reduce32(h, (uint32_t)P);
+      if constexpr (NH > 0) {  // heavy hitter with a resolved slot: this thread's column
+        const int d = (int)(h >> 58) & (HOT_DIR - 1);
+        if (lc[r] && hdk[d] == kc[r] && kc[r] != EMPTY) {
+          const int q = hdi[d];
+          if (*(volatile long long*)&hsl[q] >= 0) {
+            const uint64_t vv[1] = {vc[r]};
+            HO::template add<1>(hacc + (size_t)q * HO::N * BLK + tid, BLK, 0, vv);
+            c_rec++;
+            c_hit++;
+            lc[r] = false;
+          }
+        }
+      }
       bool posv = lc[r];
       if (nbw && kc[r] != EMPTY) {
         const uint64_t bits = bloom_bits(h);
@@ -265,10 +310,15 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
         bool hit = false;
         if (lane < (int)cnt_in) {
           const ulonglong2 e = ring[(qh + lane) & (PQ_RING - 1)];
-          uint64_t b = 0;
+          uint64_t b = 0, hh = 0;
           ulonglong2 x = make_ulonglong2(0, 0), y = x;
-          if (e.x != EMPTY) probe_issue(a, e.x, b, x, y);
-          hit = probe_finish<PG>(a, e.x, e.y, b, x, y, s_fd, ns);
+          if (e.x != EMPTY) hh = probe_issue(a, e.x, b, x, y);
+          const int64_t sl = probe_finish<PG>(a, e.x, e.y, b, x, y, s_fd, ns);
+          hit = sl >= 0;
+          if constexpr (NH > 0) {  // a resolved heavy hitter: this CTA's columns take it from now on
+            const int d = (int)(hh >> 58) & (HOT_DIR - 1);
+            if (hit && e.x != EMPTY && hdk[d] == e.x) *(volatile long long*)&hsl[hdi[d]] = sl;
+          }
         }
         const uint32_t hb = __ballot_sync(0xffffffffu, hit);
         if (lane == 0) s_hm[wid][qh >> 5] = hb;
@@ -425,6 +475,21 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
     }
   }
   __syncthreads();
+  if constexpr (NH > 0) {  // heavy-hitter columns: warp-reduced, one L2 update per warp and field
+    for (int q = 0; q < HOT_MAX; q++) {
+      const long long sl = hsl[q];
+      if (sl < 0) continue;  // CTA-uniform (after the barrier above)
+#pragma unroll
+      for (int j = 0; j < HO::N; j++) {
+        const uint32_t F = HO::desc(j);
+        uint64_t v = hacc[((size_t)q * HO::N + j) * BLK + tid];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = merge_word(v, __shfl_xor_sync(0xffffffffu, v, o), F & 3, (F >> 2) & 3);
+        if (lane == 0 && v != state_identity(F & 3, (F >> 2) & 3))
+          gupdate(a.t.states + (uint64_t)j * a.t.stride + (uint64_t)sl, F & 3, (F >> 2) & 3, v);
+      }
+    }
+  }
   if (PAIR) {
     // a parked even record whose partner never came is the last of its chain
     for (int p = tid; p < P; p += BLK) {
