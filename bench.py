@@ -204,16 +204,30 @@ def run_ours(args, rank, world, device):
                          G_t=min(G_est, n))
     stream = torch.cuda.Stream(device=device)
     agg = spec_of(cfg)
+    # N > 1: exchange partial groups after a local combine, or raw rows first
+    # when the combine would not shrink what is sent
+    xmode = None
+    if world > 1:
+        from paper_1311_0059_b200.exchange import choose_exchange
+        n_cols = len(keys) + len(vals)
+        part_b = 8 * (len(keys) + len(spec_of(cfg).fns) + 1)  # key words + states (upper bound)
+        xmode = args.exchange if args.exchange != "auto" else choose_exchange(n, G_est, 8 * n_cols, part_b)
     g = GroupBy(args.algo, agg, types_of(keys), types_of(vals), budget_groups=budget_of(cfg, n),
                 stats=stats, seed=1234, device=device.index, stream=stream,
-                emit_partials=world > 1)
-    xg = None
-    if world > 1:
+                emit_partials=xmode == "partial")
+    xg = xr = None
+    if xmode == "partial":
         from paper_1311_0059_b200.exchange import Exchanger
         xg = Exchanger(g, agg, types_of(keys), types_of(vals), device, stream, rank, world,
                        stats=stats, seed=1234, budget_groups=budget_of(cfg, n))
+    elif xmode == "raw":
+        from paper_1311_0059_b200.exchange import RawExchanger
+        xr = RawExchanger(g, device, stream)
 
     def step():
+        if xr is not None:
+            xr.run(keys, vals)
+            return
         g.reset()
         g.push(keys, vals)
         g.finish()
@@ -251,8 +265,8 @@ def run_ours(args, rank, world, device):
         g.profile(False)
     met = g.metrics()
     res_groups = met["output_groups"]
-    if xg is not None:
-        res_groups = xg.merge.metrics()["output_groups"]
+    if xg is not None or xr is not None:
+        res_groups = (xg.merge if xg is not None else g).metrics()["output_groups"]
         t = torch.tensor([res_groups], dtype=torch.int64, device=device)
         torch.distributed.all_reduce(t)
         res_groups = int(t.item())
@@ -261,7 +275,7 @@ def run_ours(args, rank, world, device):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     out = dict(ms=ms, kernels=ks, metrics=met, launches=launches, clocks=clk.summary(),
-               n=n, cfg=cfg, groups=res_groups)
+               n=n, cfg=cfg, groups=res_groups, xmode=xmode)
 
     # e2e through the C ABI with pinned host buffers (H2D + D2H inside the timed
     # region); at N > 1 every rank pushes its shard from host memory, the
@@ -271,20 +285,29 @@ def run_ours(args, rank, world, device):
         hv = [v.cpu().pin_memory() for v in vals]
         ge = GroupBy(args.algo, agg, types_of(keys), types_of(vals),
                      budget_groups=budget_of(cfg, n), stats=stats, seed=1234,
-                     device=device.index, stream=stream, emit_partials=world > 1)
-        xe = None
-        if world > 1:
+                     device=device.index, stream=stream, emit_partials=xmode == "partial")
+        xe = xre = None
+        if xmode == "partial":
             from paper_1311_0059_b200.exchange import Exchanger
             xe = Exchanger(ge, agg, types_of(keys), types_of(vals), device, stream, rank, world,
                            stats=stats, seed=1234, budget_groups=budget_of(cfg, n))
+        elif xmode == "raw":
+            from paper_1311_0059_b200.exchange import RawExchanger
+            xre = RawExchanger(ge, device, stream)
         outk = outv = None
 
         def estep():
             nonlocal outk, outv
-            ge.reset()
-            ge.push([k.numpy() for k in hk], [v.numpy() for v in hv])
-            res = ge.finish()
             hres = ge
+            if xre is not None:  # raw-first: the shard goes to the device, then to its ranks
+                with torch.cuda.stream(stream):
+                    dk = [k.to(device, non_blocking=True) for k in hk]
+                    dv = [v.to(device, non_blocking=True) for v in hv]
+                res = xre.run(dk, dv)
+            else:
+                ge.reset()
+                ge.push([k.numpy() for k in hk], [v.numpy() for v in hv])
+                res = ge.finish()
             if xe is not None:
                 res = xe.run()
                 hres = xe.merge
@@ -453,6 +476,8 @@ def main():
     ap.add_argument("--records", type=int, default=0, help="records per GPU (default: config N)")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=("auto", "partial", "raw"),
+                    help="N > 1: partial groups after a local combine, or raw rows first")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
     ap.add_argument("--also", default="original_hh", help="extra algorithms to time (comma list)")
@@ -502,7 +527,8 @@ def main():
                        "budget_groups": cfg.budget_groups or "in-memory",
                        "groups_out": out["groups"],
                        "l2": f"inputs {n * (kb + vb) / 1e9:.2f} GB/GPU > 126 MB L2; no flush",
-                       "parallelism": f"dp{world} (shard + hash exchange)" if world > 1 else "1 GPU"},
+                       "parallelism": f"dp{world} (shard + hash exchange of {out.get('xmode')} records)"
+                       if world > 1 else "1 GPU"},
             "roofline": roof,
             "kernels": table,
             "gpu_launches": out["launches"],

@@ -178,6 +178,18 @@ int64_t aggb_exchange_record_bytes(void* handle);
 int aggb_exchange_pack(void* handle, int nranks, void* send, int64_t* counts);
 int aggb_push_partials(void* handle, const void* recv, int64_t n_records);
 
+/* Raw-first exchange (new; "choose raw vs partial
+ * adaptively").  When local aggregation would collapse little (C4: ~0.5N
+ * distinct keys, 16 B raw < 24 B partial per record), ranks exchange input rows
+ * before aggregating.  aggb_exchange_pack_raw packs the device columns of `in`
+ * by dest = hash(key, exchange seed) % nranks (the seed aggb_exchange_pack
+ * uses) into `send`: records of aggb_exchange_raw_record_bytes() bytes, one
+ * 8-byte slot per key column then per value column (4-byte columns in the low
+ * half).  The receiver pushes what it got with aggb_push, each column a
+ * strided view (stride = record bytes, offset = 8 x column index). */
+int64_t aggb_exchange_raw_record_bytes(void* handle);
+int aggb_exchange_pack_raw(void* handle, const aggb_input* in, int nranks, void* send, int64_t* counts);
+
 /* Metrics snapshot (Metrics.as_dict, core.py:378-380). */
 int aggb_metrics_get(void* handle, aggb_metrics* out);
 

@@ -2520,6 +2520,49 @@ int64_t aggb_exchange_record_bytes(void* handle) {
   return h ? (int64_t)(h->kw + h->cs.ds.ns) * 8 : 0;
 }
 
+int64_t aggb_exchange_raw_record_bytes(void* handle) {
+  Handle* h = (Handle*)handle;
+  return h ? (int64_t)(h->spec.n_keys + h->spec.n_vals) * 8 : -1;
+}
+
+int aggb_exchange_pack_raw(void* handle, const aggb_input* in, int nranks, void* send, int64_t* counts) {
+  Handle* h = (Handle*)handle;
+  if (!h || !in || !counts || nranks < 1 || nranks > 256) return fail(AGGB_INVALID_ARG, "bad exchange arguments");
+  if (in->on_host) return fail(AGGB_INVALID_ARG, "exchange_pack_raw takes device columns");
+  cudaSetDevice(h->device);
+  for (int i = 0; i < nranks; i++) counts[i] = 0;
+  if (in->n_rows <= 0) return AGGB_OK;
+  if (!send) return fail(AGGB_INVALID_ARG, "null send buffer");
+  ColSrc col = col_of(h, in, in->key, in->val);
+  // the partial exchange's seed: either mode sends a key to the same rank
+  const uint64_t seed = level_seed(h->cfg.seed, SALT_EXCH, 0);
+  DBuf c;
+  TRY(c.ensure(2 * 256 * 8, nullptr));
+  unsigned long long* cnt = c.as<unsigned long long>();
+  CU(cudaMemsetAsync(cnt, 0, 256 * 8, h->st));
+  const int grid = (int)std::min<int64_t>((col.n + 255) / 256, (int64_t)h->sms * 8);
+  int pe = prof_begin(h, 10);
+  if (h->kw == 1) k_exch_raw_count<1><<<grid, 256, 0, h->st>>>(col, seed, nranks, cnt);
+  else k_exch_raw_count<2><<<grid, 256, 0, h->st>>>(col, seed, nranks, cnt);
+  std::vector<unsigned long long> hc(nranks), off(nranks);
+  CU(cudaMemcpyAsync(hc.data(), cnt, nranks * 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  unsigned long long acc = 0;
+  for (int i = 0; i < nranks; i++) {
+    off[i] = acc;
+    acc += hc[i];
+    counts[i] = (int64_t)hc[i];
+  }
+  CU(cudaMemcpyAsync(cnt + 256, off.data(), nranks * 8, cudaMemcpyHostToDevice, h->st));
+  if (h->kw == 1) k_exch_raw_scatter<1><<<grid, 256, 0, h->st>>>(col, seed, nranks, cnt + 256, (uint64_t*)send);
+  else k_exch_raw_scatter<2><<<grid, 256, 0, h->st>>>(col, seed, nranks, cnt + 256, (uint64_t*)send);
+  prof_end(h, pe);
+  h->launches += 2;
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->st));
+  return AGGB_OK;
+}
+
 int aggb_exchange_pack(void* handle, int nranks, void* send, int64_t* counts) {
   Handle* h = (Handle*)handle;
   if (!h || !counts || nranks < 1 || nranks > 256) return fail(AGGB_INVALID_ARG, "bad exchange arguments");

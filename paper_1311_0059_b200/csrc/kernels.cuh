@@ -654,6 +654,45 @@ __global__ void k_exch_scatter(const uint64_t* keys, const uint64_t* states, int
   }
 }
 
+// raw-first exchange (C4-like inputs, little local collapse): input rows are
+// packed by destination before any aggregation, one 8-byte slot per key and
+// value column (4-byte columns in the slot's low half), so the receiver pushes
+// the buffer as strided columns of the same types
+template <int KW>
+__global__ void k_exch_raw_count(ColSrc c, uint64_t seed, int nranks, unsigned long long* counts) {
+  __shared__ unsigned int sh[256];
+  for (int i = threadIdx.x; i < nranks; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+    col_key<KW>(c, i, k);
+    atomicAdd(&sh[reduce32(hash_key<KW>(k, seed), (uint32_t)nranks)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nranks; i += blockDim.x)
+    if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
+}
+
+__device__ __forceinline__ uint64_t raw_slot(const uint8_t* base, int64_t stride, int ty, int64_t i) {
+  const uint8_t* p = base + i * stride;
+  return ty == TY_I32 ? (uint64_t)(uint32_t)*(const int32_t*)p : *(const uint64_t*)p;
+}
+
+template <int KW>
+__global__ void k_exch_raw_scatter(ColSrc c, uint64_t seed, int nranks, unsigned long long* cursor, uint64_t* send) {
+  const int rw = KW + c.nv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+    col_key<KW>(c, i, k);
+    const unsigned d = reduce32(hash_key<KW>(k, seed), (uint32_t)nranks);
+    const unsigned long long at = atomicAdd(&cursor[d], 1ull);
+    uint64_t* dst = send + at * rw;
+#pragma unroll
+    for (int w = 0; w < KW; w++) dst[w] = raw_slot(c.key[w], c.kstride[w], c.kty[w], i);
+    for (int w = 0; w < c.nv; w++) dst[KW + w] = raw_slot(c.val[w], c.vstride[w], c.vty[w], i);
+  }
+}
+
 // AoS partial records -> SoA (the pass kernels' list layout)
 __global__ void k_aos_to_soa(const uint64_t* in, int64_t n, int rw, uint64_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -205,6 +205,39 @@ class GroupBy:
                 "aggb_exchange_pack")
         return buf, [int(c) for c in counts], rb
 
+    def pack_raw(self, keys: list, vals: list, nranks: int, out=None):
+        """Pack input rows (device columns) by destination rank before any
+        aggregation -> (uint8 tensor, counts, record bytes); raw-first exchange."""
+        import torch
+        inp = N.Input()
+        n = len(keys[0])
+        keep = []
+        for i, k in enumerate(keys):
+            p, s, oh, ref = _ptr_stride(k)
+            keep.append(ref)
+            inp.key[i], inp.key_stride[i] = p, s
+        for i, v in enumerate(vals):
+            p, s, oh, ref = _ptr_stride(v)
+            keep.append(ref)
+            inp.val[i], inp.val_stride[i] = p, s
+        inp.n_rows = n
+        rb = int(self.L.aggb_exchange_raw_record_bytes(self.h))
+        if out is None or out.numel() < max(n, 1) * rb:
+            out = torch.empty(max(n, 1) * rb, dtype=torch.uint8, device=keys[0].device)
+        counts = (ctypes.c_int64 * nranks)()
+        N.check(self.L.aggb_exchange_pack_raw(self.h, ctypes.byref(inp), nranks,
+                                              ctypes.c_void_p(out.data_ptr()), counts),
+                "aggb_exchange_pack_raw")
+        return out, [int(c) for c in counts], rb
+
+    def push_packed_raw(self, buf, n: int) -> None:
+        """Aggregate rows in the aggb_exchange_pack_raw layout (device buffer)."""
+        rb = (len(self.key_types) + len(self.val_types)) * 8
+        base = buf.data_ptr() if hasattr(buf, "data_ptr") else int(buf)
+        nk = len(self.key_types)
+        self.push_raw(n, [base + 8 * i for i in range(nk)], [rb] * nk,
+                      [base + 8 * (nk + j) for j in range(len(self.val_types))], [rb] * len(self.val_types))
+
     def finish(self) -> N.Result:
         res = N.Result()
         N.check(self.L.aggb_finish(self.h, ctypes.byref(res)), "aggb_finish")

@@ -91,3 +91,71 @@ def test_two_rank_exchange_gives_global_groupby():
     uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
     assert np.array_equal(allk[order], uk[:, 0].view(np.int64))
     assert np.array_equal(allv[order], want)
+
+
+class _NumpyRawHandle:
+    """Stand-in for GroupBy in the raw-first exchange (CPU): rows packed by
+    destination as int64 [key, value] slots, then one group-by on receipt."""
+
+    def __init__(self):
+        self.rows = []
+
+    def pack_raw(self, keys, vals, nranks, out=None):
+        k = keys[0].numpy()
+        v = vals[0].numpy()
+        dest = (k.view(np.uint64) * np.uint64(0x9E3779B97F4A7C15) >> np.uint64(40)).astype(np.int64) % nranks
+        order = np.argsort(dest, kind="stable")
+        packed = np.stack([k[order], v[order]], axis=1)
+        return (torch.from_numpy(packed.view(np.uint8).reshape(-1).copy()),
+                np.bincount(dest, minlength=nranks).tolist(), 16)
+
+    def reset(self):
+        self.rows = []
+
+    def push_packed_raw(self, buf, n):
+        self.rows.append(buf.numpy().view(np.int64).reshape(-1, 2)[:n])
+
+    def finish(self):
+        r = np.concatenate(self.rows) if self.rows else np.zeros((0, 2), np.int64)
+        return _partials(r[:, 0], r[:, 1])
+
+
+def _raw_worker(rank, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_1311_0059_b200 import datagen as D
+    from paper_1311_0059_b200.exchange import RawExchanger
+    cfg = D.scaled(D.CONFIGS["C4"], 40_000)
+    n = cfg.n // WORLD
+    keys, vals = D.generate(cfg, rank * n, n)
+    x = RawExchanger(_NumpyRawHandle(), torch.device("cpu"), None)
+    res = x.run([torch.from_numpy(keys[0])], [torch.from_numpy(vals[0])])
+    out_q.put((rank, res, x.last_counts))
+    dist.destroy_process_group()
+
+
+def test_two_rank_raw_exchange_gives_global_groupby():
+    """Raw-first exchange (C4 shape) over gloo: every rank aggregates only what it
+    received; the union of the ranks' groups is the global group-by."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_raw_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(WORLD)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    a, b = res[0][1], res[1][1]
+    assert len(np.intersect1d(a[:, 0], b[:, 0])) == 0
+    sent0, recv0 = res[0][2]
+    sent1, recv1 = res[1][2]
+    assert recv0[1] == sent1[0] and recv1[0] == sent0[1]
+    from paper_1311_0059_b200 import datagen as D
+    cfg = D.scaled(D.CONFIGS["C4"], 40_000)
+    keys, vals = D.generate(cfg)
+    want = _partials(keys[0], vals[0])
+    got = np.concatenate([a, b])
+    got = got[np.argsort(got[:, 0])]
+    assert np.array_equal(got, want)

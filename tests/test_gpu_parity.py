@@ -324,3 +324,80 @@ def test_exchange_pack_merge_simulated_ranks(world):
     uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
     assert np.array_equal(allk[order], uk[:, 0].view(np.int64))
     assert np.array_equal(allv[order], want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_raw_exchange_simulated_ranks(world):
+    """Raw-first exchange (C4 shape: little local collapse) on one device: each
+    shard's input rows are packed by destination before any aggregation, each
+    destination aggregates what it received once; the union is the global
+    group-by with disjoint key sets, and the partial exchange routes every key
+    to the same rank."""
+    import torch
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C4"], 400_000)
+    keys, vals = D.generate(cfg)
+    agg = _agg(cfg)
+    dk = [torch.from_numpy(k).cuda() for k in keys]
+    dv = [torch.from_numpy(v).cuda() for v in vals]
+    n = -(-cfg.n // world)
+    segs = [[] for _ in range(world)]
+    for r in range(world):
+        with E.GroupBy("hash_sort", agg, ["i64"], ["i64"], seed=42) as g:
+            buf, counts, rb = g.pack_raw([k[r * n:(r + 1) * n] for k in dk],
+                                         [v[r * n:(r + 1) * n] for v in dv], world)
+            assert rb == 16 and sum(counts) == len(dk[0][r * n:(r + 1) * n])
+            off = 0
+            for d in range(world):
+                segs[d].append(buf[off * rb:(off + counts[d]) * rb].clone())
+                off += counts[d]
+    outk, outv = [], []
+    for d in range(world):
+        recv = torch.cat(segs[d])
+        with E.GroupBy("hash_sort", agg, ["i64"], ["i64"], seed=42) as m:
+            m.push_packed_raw(recv, recv.numel() // 16)
+            res = m.result()
+        outk.append(res.keys[0])
+        outv.append(res.as_float64())
+        # the partial exchange of the same keys lands on the same rank
+        with E.GroupBy("hash_sort", agg, ["i64"], ["i64"], seed=42, emit_partials=True) as p:
+            p.push([torch.from_numpy(res.keys[0]).cuda()], [torch.ones(len(res.keys[0]), dtype=torch.int64).cuda()])
+            p.finish()
+            _, pc, _ = p.pack(world)
+            assert pc[d] == len(res.keys[0]) and sum(pc) == pc[d]
+    for a in range(world):
+        for b in range(a + 1, world):
+            assert len(np.intersect1d(outk[a], outk[b])) == 0
+    allk = np.concatenate(outk)
+    allv = np.concatenate(outv)
+    order = np.argsort(allk)
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert np.array_equal(allk[order], uk[:, 0].view(np.int64))
+    assert np.array_equal(allv[order], want)
+
+
+def test_raw_exchange_wide_rows():
+    """Raw packing of C5's strided 64-byte rows (int64 || int32 key, two int64 and
+    two fp64 values): one destination gets every row back unchanged."""
+    import torch
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    E = _engine()
+    cfg = D.scaled(D.CONFIGS["C5"], 50_000)
+    keys, vals = D.generate(cfg)
+    rows = torch.from_numpy(D.wide_rows(keys, vals)).cuda()
+    kcols = [rows[:, 0:8].contiguous().view(torch.int64)[:, 0], rows[:, 8:12].contiguous().view(torch.int32)[:, 0]]
+    vcols = [rows[:, 16 + 8 * j:24 + 8 * j].contiguous().view(torch.float64 if j >= 2 else torch.int64)[:, 0]
+             for j in range(4)]
+    agg = _agg(cfg)
+    with E.GroupBy("pre_partitioning", agg, ["i64", "i32"], ["i64", "i64", "f64", "f64"],
+                   budget_groups=2000, seed=7) as g:
+        buf, counts, rb = g.pack_raw(kcols, vcols, 1)
+        assert rb == 48 and counts == [cfg.n]
+        g.push_packed_raw(buf, cfg.n)
+        res = g.result().sorted_by_key()
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs), bind=list(cfg.bind))
+    assert res.n_groups == len(uk)
+    assert_values_match(res.as_float64(), want, float_out_cols(cfg))

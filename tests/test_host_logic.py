@@ -85,3 +85,14 @@ def test_zipf_generator_shape():
     keys, _ = D.generate(cfg)
     _, counts = np.unique(keys[0], return_counts=True)
     assert counts.max() > 0.3 * len(keys[0])  # s = 1.5: the top key takes ~38%
+
+
+def test_choose_exchange_rule():
+    """partial groups when local aggregation shrinks the bytes
+    to send, raw rows otherwise (C2 partial at any N; C4 raw at 8 GPUs)."""
+    from paper_1311_0059_b200.exchange import choose_exchange, expected_distinct
+    assert abs(expected_distinct(1e9, 627_500_000) / 1e9 - 0.5) < 0.01  # C4: ~0.5N distinct
+    assert choose_exchange(100_000_000, 1_000_000, 16, 40) == "partial"  # C2 per GPU
+    assert choose_exchange(125_000_000, 627_500_000, 16, 24) == "raw"    # C4 at 8 GPUs
+    assert choose_exchange(1_000_000, 10_000, 16, 24) == "partial"       # C1
+    assert choose_exchange(0, 10, 16, 24) == "partial"
