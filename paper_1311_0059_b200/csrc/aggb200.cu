@@ -849,6 +849,15 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.cache_log2 = cache_log2;
   a.pairs = pairs ? 1 : 0;
   a.hot = hot ? h->hot.as<uint64_t>() : nullptr;
+  if (wide_probe) {  // C5's row layout read as three 16-byte loads per row
+    const ColSrc& c = pp.col;
+    const int64_t st = c.kstride[0];
+    bool ok = c.kty[0] == TY_I64 && c.kty[1] == TY_I32 && c.key[1] == c.key[0] + 8 && st % 16 == 0 &&
+              c.kstride[1] == st && ((uintptr_t)c.key[0] & 15) == 0 && c.nv == 4;
+    for (int w = 0; ok && w < 4; w++)
+      ok = c.val[w] == c.key[0] + 16 + 8 * w && c.vstride[w] == st && c.vty[w] != TY_I32;
+    a.rows64 = ok ? 1 : 0;
+  }
   // chunked reservations for large tables: unused chunks (< grid * chunk) stay under 1% of cap
   {
     const uint64_t cap = h->tab.cap;

@@ -53,6 +53,7 @@ struct PassArgs {
   uint2* chains;                          // per (CTA, partition): {records claimed, page of the last claim}
   int32_t pairs;                          // k_probe: sector pairs on (shared memory permitting)
   const uint64_t* hot;                    // heavy-hitter keys (k_hot_sample): hot[0..7] keys, hot[8] count
+  int32_t rows64;                         // k_probe_w: columns are C5's 64-byte rows (k0 i64 | k1 i32 | v0..v3 at +16)
 };
 
 // ---------------------------------------------------------------------------
