@@ -1085,7 +1085,8 @@ int plan(Handle* h) {
     // (8 bits per resident key in 64 KB) rejects the records to spill, and the
     // heavy-hitter columns fit beside it.  C3 s = 0.5: generic PROBE of a 1M-group
     // table 12.9 ms -> k_probe 4.3 ms (profiles/r01_notes.md, session 3)
-    if (h->kw == 1 && h->cs.nv == 1 && !getenv("AGGB_L2CAP_WIDE")) l2cap = std::min<int64_t>(l2cap, 65536);
+    if (algo == AGGB_PRE_PARTITIONING && h->kw == 1 && h->cs.nv == 1 && !getenv("AGGB_L2CAP_WIDE"))
+      l2cap = std::min<int64_t>(l2cap, 65536);
     if (getenv("AGGB_L2_CAP_GROUPS")) l2cap = std::max(8, atoi(getenv("AGGB_L2_CAP_GROUPS")));  // test hook
     if (h->budget > 2 * l2cap) {
       h->budget = l2cap;
