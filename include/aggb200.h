@@ -190,6 +190,11 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records);
 int64_t aggb_exchange_raw_record_bytes(void* handle);
 int aggb_exchange_pack_raw(void* handle, const aggb_input* in, int nranks, void* send, int64_t* counts);
 
+/* Bytes of the spill page pool mapped from pinned host memory (new; SURVEY.md
+ * §8(f) f3): the pool is one reserved address range, HBM first, host memory once
+ * HBM is exhausted (runs larger than HBM, the RunWriter/RunReader analog). */
+int64_t aggb_pool_host_bytes(void* handle);
+
 /* Metrics snapshot (Metrics.as_dict, core.py:378-380). */
 int aggb_metrics_get(void* handle, aggb_metrics* out);
 

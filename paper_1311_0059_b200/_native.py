@@ -35,7 +35,7 @@ MAX_FNS, MAX_VALS, MAX_KEYS = 32, 32, 2
 # every symbol the header declares (checked by tests/test_abi.py)
 EXPORTS = ("aggb_create", "aggb_push", "aggb_finish", "aggb_copy_result",
            "aggb_exchange_record_bytes", "aggb_exchange_pack", "aggb_push_partials",
-           "aggb_exchange_raw_record_bytes", "aggb_exchange_pack_raw",
+           "aggb_exchange_raw_record_bytes", "aggb_exchange_pack_raw", "aggb_pool_host_bytes",
            "aggb_metrics_get", "aggb_reset", "aggb_destroy", "aggb_last_error",
            "aggb_generate", "aggb_l2_flush", "aggb_version", "aggb_profile",
            "aggb_kernel_stats")
@@ -111,6 +111,8 @@ def load(path: str = LIB_PATH):
     L.aggb_push_partials.argtypes = [vp, vp, i64]
     L.aggb_exchange_raw_record_bytes.argtypes = [vp]
     L.aggb_exchange_raw_record_bytes.restype = i64
+    L.aggb_pool_host_bytes.argtypes = [vp]
+    L.aggb_pool_host_bytes.restype = i64
     L.aggb_exchange_pack_raw.argtypes = [vp, ctypes.POINTER(Input), i32, vp, ctypes.POINTER(i64)]
     L.aggb_metrics_get.argtypes = [vp, ctypes.POINTER(Metrics)]
     L.aggb_reset.argtypes = [vp]

@@ -101,13 +101,15 @@ struct DBuf {
   T* as() const { return (T*)p; }
 };
 
-// Spill page pool memory: one virtual address range reserved for the device's
-// whole memory, physical memory mapped onto its end as the pool grows (CUDA
-// VMM).  Growth never copies and never holds old + new at once: a pool that
+// Spill page pool memory: one virtual address range reserved for twice the
+// device's memory, physical memory mapped onto its end as the pool grows (CUDA
+// VMM): HBM first, then pinned host memory once HBM is exhausted (SURVEY §8(f)
+// f3, the external RunWriter/RunReader analog: runs larger than HBM).  Growth never copies and never holds old + new at once: a pool that
 // doubles to 60+ GB (C5 hash_sort at 500M records) only maps the difference.
 struct VPool {
   CUdeviceptr va = 0;
   size_t reserved = 0, mapped = 0, gran = 0;
+  size_t dev_mapped = 0, host_mapped = 0, dev_limit = ~(size_t)0;
   int dev = -1;
   std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> chunks;
   struct Api {
@@ -146,6 +148,14 @@ struct VPool {
     }();
     return a;
   }
+  CUmemAllocationProp host_prop() const {
+    CUmemAllocationProp pr;
+    memset(&pr, 0, sizeof(pr));
+    pr.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    pr.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+    pr.location.id = 0;
+    return pr;
+  }
   CUmemAllocationProp prop() const {
     CUmemAllocationProp pr;
     memset(&pr, 0, sizeof(pr));
@@ -162,44 +172,70 @@ struct VPool {
     if (!A.ok) return fail(AGGB_CUDA_ERROR, "CUDA VMM entry points unavailable");
     if (!va) {
       cudaGetDevice(&dev);
-      CUmemAllocationProp pr = prop();
+      CUmemAllocationProp pr = prop(), ph = host_prop();
+      size_t gh = 0;
       if (A.granularity(&gran, &pr, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) gran = 2u << 20;
+      if (A.granularity(&gh, &ph, CU_MEM_ALLOC_GRANULARITY_MINIMUM) == CUDA_SUCCESS && gh > gran && gh % gran == 0)
+        gran = gh;
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      reserved = ((std::max(tot, need) + gran - 1) / gran) * gran;
+      // the device's memory, then as much again of pinned host memory
+      reserved = ((std::max(2 * tot, need) + gran - 1) / gran) * gran;
       if (A.reserve(&va, reserved, gran, 0, 0) != CUDA_SUCCESS) {
         va = 0;
         return fail(AGGB_CUDA_ERROR, "cuMemAddressReserve(%zu) failed", reserved);
       }
+      const char* e = getenv("AGGB_POOL_DEVICE_LIMIT_MB");  // test hook: overflow to host early
+      dev_limit = e ? (size_t)atoll(e) << 20 : ~(size_t)0;
     }
-    if (need > reserved) return fail(AGGB_CAPACITY_EXCEEDED, "spill pool of %zu bytes exceeds device memory", need);
+    if (need > reserved) return fail(AGGB_CAPACITY_EXCEEDED, "spill pool of %zu bytes exceeds its address range", need);
     want = std::min(reserved, std::max(std::max(want, need), mapped + ((size_t)512 << 20)));
-    size_t sz = ((want - mapped + gran - 1) / gran) * gran;
-    sz = std::min(sz, reserved - mapped);
-    CUmemAllocationProp pr = prop();
-    CUmemGenericAllocationHandle hd;
-    if (A.create(&hd, sz, &pr, 0) != CUDA_SUCCESS) {
-      // no room for the headroom: map just what is needed
-      sz = ((need - mapped + gran - 1) / gran) * gran;
-      if (A.create(&hd, sz, &pr, 0) != CUDA_SUCCESS)
-        return fail(AGGB_CUDA_ERROR, "cuMemCreate(%zu): out of memory (pool %zu mapped)", sz, mapped);
+    auto up = [&](size_t x) { return ((x + gran - 1) / gran) * gran; };
+    while (mapped < need) {
+      CUmemGenericAllocationHandle hd;
+      size_t sz = 0;
+      bool host = false;
+      CUmemAllocationProp pr = prop();
+      if (dev_mapped < dev_limit) {
+        const size_t room = dev_limit == ~(size_t)0 ? ~(size_t)0 : ((dev_limit - dev_mapped) / gran) * gran;
+        const size_t tries[2] = {std::min(up(want - mapped), reserved - mapped), up(need - mapped)};
+        for (size_t t : tries) {
+          t = std::min(t, room);
+          if (t && A.create(&hd, t, &pr, 0) == CUDA_SUCCESS) {
+            sz = t;
+            break;
+          }
+        }
+      }
+      if (!sz) {
+        // HBM exhausted (or capped): pinned host memory mapped into the same
+        // range; the kernels reach those pages over the host link unchanged
+        pr = host_prop();
+        sz = std::min(up(need - mapped), reserved - mapped);
+        if (A.create(&hd, sz, &pr, 0) != CUDA_SUCCESS)
+          return fail(AGGB_CUDA_ERROR, "cuMemCreate(%zu): out of device and host memory (pool %zu mapped)", sz,
+                      mapped);
+        host = true;
+      }
+      if (A.map(va + mapped, sz, 0, hd, 0) != CUDA_SUCCESS) {
+        A.release(hd);
+        return fail(AGGB_CUDA_ERROR, "cuMemMap failed");
+      }
+      CUmemAccessDesc ad;
+      memset(&ad, 0, sizeof(ad));
+      ad.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+      ad.location.id = dev;
+      ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+      if (A.access(va + mapped, sz, &ad, 1) != CUDA_SUCCESS) {
+        A.unmap(va + mapped, sz);
+        A.release(hd);
+        return fail(AGGB_CUDA_ERROR, "cuMemSetAccess failed");
+      }
+      chunks.push_back({hd, sz});
+      mapped += sz;
+      (host ? host_mapped : dev_mapped) += sz;
+      if (hw && !host) *hw += sz;
     }
-    if (A.map(va + mapped, sz, 0, hd, 0) != CUDA_SUCCESS) {
-      A.release(hd);
-      return fail(AGGB_CUDA_ERROR, "cuMemMap failed");
-    }
-    CUmemAccessDesc ad;
-    memset(&ad, 0, sizeof(ad));
-    ad.location = pr.location;
-    ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    if (A.access(va + mapped, sz, &ad, 1) != CUDA_SUCCESS) {
-      A.unmap(va + mapped, sz);
-      A.release(hd);
-      return fail(AGGB_CUDA_ERROR, "cuMemSetAccess failed");
-    }
-    chunks.push_back({hd, sz});
-    mapped += sz;
-    if (hw) *hw += sz;
     return AGGB_OK;
   }
   void release() {
@@ -214,7 +250,7 @@ struct VPool {
     A.afree(va, reserved);
     chunks.clear();
     va = 0;
-    reserved = mapped = 0;
+    reserved = mapped = dev_mapped = host_mapped = 0;
   }
   template <class T>
   T* as() const { return (T*)va; }
@@ -2528,6 +2564,11 @@ extern "C" {
 int64_t aggb_exchange_record_bytes(void* handle) {
   Handle* h = (Handle*)handle;
   return h ? (int64_t)(h->kw + h->cs.ds.ns) * 8 : 0;
+}
+
+int64_t aggb_pool_host_bytes(void* handle) {
+  Handle* h = (Handle*)handle;
+  return h ? (int64_t)h->pool_base.host_mapped : -1;
 }
 
 int64_t aggb_exchange_raw_record_bytes(void* handle) {

@@ -276,7 +276,9 @@ class GroupBy:
     def metrics(self) -> dict:
         m = N.Metrics()
         N.check(self.L.aggb_metrics_get(self.h, ctypes.byref(m)), "aggb_metrics_get")
-        return m.as_dict()
+        d = m.as_dict()
+        d["pool_host_bytes"] = int(self.L.aggb_pool_host_bytes(self.h))
+        return d
 
     def profile(self, enable: bool = True) -> None:
         N.check(self.L.aggb_profile(self.h, int(enable)), "aggb_profile")

@@ -401,3 +401,23 @@ def test_raw_exchange_wide_rows():
     uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs), bind=list(cfg.bind))
     assert res.n_groups == len(uk)
     assert_values_match(res.as_float64(), want, float_out_cols(cfg))
+
+
+@pytest.mark.parametrize("algo", ["pre_partitioning", "hash_sort"])
+def test_spill_pool_overflows_to_host_memory(algo, monkeypatch):
+    """Runs larger than HBM: once the device part of the spill
+    pool is exhausted — capped at 16 MB here by a test hook — its range is
+    extended with pinned host memory and the kernels spill into and re-read those
+    pages unchanged; results stay exact."""
+    from paper_1311_0059_b200 import datagen as D
+    from oracle import oracle as O
+    monkeypatch.setenv("AGGB_POOL_DEVICE_LIMIT_MB", "16")
+    cfg = D.scaled(D.CONFIGS["C2"], 4_000_000)
+    keys, vals = D.generate(cfg)
+    res, met = run_gpu(algo, cfg, keys, vals, budget_groups=cfg.budget_groups, seed=9)
+    assert met["spilled_records"] * 16 > 32 << 20  # well past the device part
+    assert met["pool_host_bytes"] > 0
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert res.n_groups == len(uk)
+    assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+    assert np.array_equal(res.as_float64(), want)
