@@ -580,6 +580,8 @@ struct Handle {
   DBuf hot;                 // heavy-hitter keys of the current push (k_hot_sample)
   bool hot_ready = false;
   bool hot_no_tier = false;  // the hot keys cover most records: no SMEM pre-aggregation tier
+  int64_t skew_cap = 0;      // L2-capped plans: the capacity a heavily skewed push may use
+  bool first_push = true;
   int prog = 0;
   // blocked bloom filter of the frozen level-0 table (PROBE)
   DBuf bloom;
@@ -1110,6 +1112,7 @@ int plan(Handle* h) {
   // 200M): 15.2 -> 11.1 ms.  hash_sort keeps its in-memory table (capped it
   // cuts a run per chunk: 62 ms).
   h->l2_capped = false;
+  h->skew_cap = 0;
   if (h->unlimited && algo == AGGB_PRE_PARTITIONING && !getenv("AGGB_NO_L2_CAP")) {
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
@@ -1121,13 +1124,22 @@ int plan(Handle* h) {
     // (8 bits per resident key in 64 KB) rejects the records to spill, and the
     // heavy-hitter columns fit beside it.  C3 s = 0.5: generic PROBE of a 1M-group
     // table 12.9 ms -> k_probe 4.3 ms (profiles/r01_notes.md, session 3)
+    const int64_t l2full = l2cap;
     if (algo == AGGB_PRE_PARTITIONING && h->kw == 1 && h->cs.nv == 1 && !getenv("AGGB_L2CAP_WIDE"))
       l2cap = std::min<int64_t>(l2cap, 65536);
-    if (getenv("AGGB_L2_CAP_GROUPS")) l2cap = std::max(8, atoi(getenv("AGGB_L2_CAP_GROUPS")));  // test hook
+    // heavily skewed pushes (most records on a few hot keys: C3 s = 1.5, 434K
+    // groups) keep the full L2-sized table: they fit it and never reach PROBE
+    h->skew_cap = l2full > l2cap ? l2full : 0;
+    if (getenv("AGGB_L2_CAP_GROUPS")) {  // test hook: this cap, no skew exception
+      l2cap = std::max(8, atoi(getenv("AGGB_L2_CAP_GROUPS")));
+      h->skew_cap = 0;
+    }
     if (h->budget > 2 * l2cap) {
       h->budget = l2cap;
       h->unlimited = false;
       h->l2_capped = true;
+    } else {
+      h->skew_cap = 0;
     }
   }
   h->child_cap = (int)std::max<int64_t>(1, std::min<int64_t>(ccap, h->budget));
@@ -1189,7 +1201,7 @@ int plan(Handle* h) {
 }
 
 int setup_table(Handle* h) {
-  int64_t slots = next_pow2(std::max<int64_t>(64, 2 * h->budget));
+  int64_t slots = next_pow2(std::max<int64_t>(64, 2 * std::max<int64_t>(h->budget, h->skew_cap)));
   GTable& t = h->tab;
   t.stride = (uint64_t)slots + 1;
   t.mask = (uint64_t)slots - 1;
@@ -1228,6 +1240,8 @@ int begin_run(Handle* h) {
   h->records = 0;
   h->launches = 0;
   h->finished = false;
+  h->first_push = true;
+  if (h->has_table && h->skew_cap) h->tab.cap = (uint64_t)h->budget;
   h->hash_sort_runs = 0;
   h->sort_n = 0;
   memset(&h->met, 0, sizeof(h->met));
@@ -2065,6 +2079,10 @@ int hot_sample(Handle* h, const ColSrc& col) {
   // without the SMEM tier (C3 s = 1.5 FILL 14.0 -> 5.2 ms; at s = 1.0, 16%
   // covered, the tier stays: 9.06 vs 9.63 ms without it).
   h->hot_no_tier = h->hot_ready && nh[1] * 10 >= (uint64_t)sample * 4;
+  if (h->skew_cap && h->first_push) {  // the table was sized for skew_cap; grant it to skewed runs
+    h->tab.cap = h->hot_no_tier ? (uint64_t)h->skew_cap : (uint64_t)h->budget;
+    h->first_push = false;
+  }
   return AGGB_OK;
 }
 
