@@ -96,3 +96,45 @@ def test_choose_exchange_rule():
     assert choose_exchange(125_000_000, 627_500_000, 16, 24) == "raw"    # C4 at 8 GPUs
     assert choose_exchange(1_000_000, 10_000, 16, 24) == "partial"       # C1
     assert choose_exchange(0, 10, 16, 24) == "partial"
+
+
+# measured on B200 (profiles/r01_all_configs_full.jsonl, session 3), ms
+_MEASURED = {
+    "C2": (dict(n=1e8, groups=1e6, rec_bytes=16, state_bytes=40, out_bytes=40, budget_groups=125000,
+                key_bits=20), {"pre_partitioning": 3.44, "original_hh": 5.51}),
+    "C3s05": (dict(n=2e8, groups=1e7, state_bytes=24, out_bytes=32, key_bits=24),
+              {"pre_partitioning": 9.09, "hash_sort": 26.7}),
+    "C3s1": (dict(n=2e8, groups=8.9e6, state_bytes=24, out_bytes=32, key_bits=24, hot_share=0.16),
+             {"pre_partitioning": 8.46, "hash_sort": 15.8}),
+    "C4": (dict(n=1e9, groups=5e8, key_bits=30), {"sort_based": 101.6, "hash_sort": 356.6,
+                                                  "pre_partitioning": 104.7}),
+    "C5": (dict(n=5e8, groups=4194304, rec_bytes=64, state_bytes=120, out_bytes=144, budget_groups=83886,
+                key_bits=44, spill_rec_bytes=48), {"pre_partitioning": 58.7, "hash_sort": 914.0}),
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(_MEASURED))
+def test_gpu_cost_model_orders_like_the_measurements(cfg):
+    """the GPU byte/time model ranks the config's algorithms
+    in the measured order and lands within 3x of every measured time (~25% for
+    the streaming schedules)."""
+    from paper_1311_0059_b200.operators.gpu_cost import Workload, model, select_algorithm_gpu
+    kw, meas = _MEASURED[cfg]
+    w = Workload(**kw)
+    pred = {a: model(a, w).ms for a in meas}
+    best_meas = min(meas, key=meas.get)
+    assert min(pred, key=pred.get) == best_meas
+    assert select_algorithm_gpu(w, algos=tuple(meas)) == best_meas
+    for a, m in meas.items():
+        assert m / 3 <= pred[a] <= 3 * m, (a, pred[a], m)
+        if a in ("pre_partitioning", "original_hh", "sort_based"):
+            assert abs(pred[a] - m) <= 0.3 * m, (a, pred[a], m)
+
+
+def test_gpu_cost_model_bytes_follow_the_survey_formulas():
+    """C2 pre-partitioning: 16 B read per record, the 7/8 spill written and re-read
+    at 16 B, 40 B out per group (4.44 GB)."""
+    from paper_1311_0059_b200.operators.gpu_cost import Workload, model
+    r = model("pre_partitioning", Workload(1e8, 1e6, 16, 40, 40, 125000, 20))
+    assert abs((r.bytes_read + r.bytes_written) / 1e9 - 4.44) < 0.01
+    assert abs(r.spill_bytes / 1e9 - 1.4) < 0.01
