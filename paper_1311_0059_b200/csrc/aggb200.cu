@@ -1008,7 +1008,7 @@ int flush_table(Handle* h, bool partial, OutBuf* dst, bool clear = false) {
     TRY(ensure_out(h, cap_needed));
     o = outbuf(h, partial ? 1 : 0);
   }
-  int grid = h->sms * 4;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (int64_t)((h->tab.stride + 2047) / 2048)));
   int pe = prof_begin(h, 5);
   if (clear) {
     if (h->kw == 1) k_flush_table<1, true><<<grid, 256, 0, h->st>>>(h->tab, h->cs.ds, o);
