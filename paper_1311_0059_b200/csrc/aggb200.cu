@@ -578,6 +578,9 @@ struct Handle {
   // recursion scratch
   DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend, l2stage, cut_tmp;
   DBuf hot;                 // heavy-hitter keys of the current push (k_hot_sample)
+  DBuf dd_spilled, dd_tmp;  // dynamic destaging: destaged-partition flags, eviction lists
+  std::vector<uint8_t> dd_host;
+  int64_t dd_evictions = 0;
   bool hot_ready = false;
   bool hot_no_tier = false;  // the hot keys cover most records: no SMEM pre-aggregation tier
   int64_t skew_cap = 0;      // L2-capped plans: the capacity a heavily skewed push may use
@@ -887,6 +890,7 @@ int launch_pass(Handle* h, PassPlan& pp) {
   a.cache_log2 = cache_log2;
   a.pairs = pairs ? 1 : 0;
   a.hot = hot ? h->hot.as<uint64_t>() : nullptr;
+  a.dd_spilled = pp.mode == MODE_DD ? h->dd_spilled.as<uint8_t>() : nullptr;
   if (wide_probe) {  // C5's row layout read as three 16-byte loads per row
     const ColSrc& c = pp.col;
     const int64_t st = c.kstride[0];
@@ -1253,11 +1257,21 @@ int begin_run(Handle* h) {
     h->raw0 = {make_set(h, h->P0 + 1, h->cs.nv, 0, level_seed(seed, SALT_SPILL, lv)), 0};
     h->part0 = {make_set(h, h->P0 + 1, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
   } else {
-    h->raw0 = {make_set(h, h->P0, h->cs.nv, 0, level_seed(seed, SALT_SPILL, lv)), 0};
     int pp = std::min(h->P0, max_parts_for(h->kw + h->cs.ds.ns));
+    // dynamic destaging: a destaged partition's raw records and its evicted
+    // groups must land in the same partition of both sets
+    h->raw0 = {make_set(h, algo == AGGB_DYNAMIC_DESTAGING ? pp : h->P0, h->cs.nv, 0,
+                        level_seed(seed, SALT_SPILL, lv)), 0};
     h->part0 = {make_set(h, pp, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
   }
   h->raw0_live = h->part0_live = false;
+  if (algo == AGGB_DYNAMIC_DESTAGING) {
+    const int P = h->part0.ss.nparts;
+    TRY(h->dd_spilled.ensure((size_t)P + 16, &h->hw));
+    CU(cudaMemsetAsync(h->dd_spilled.p, 0, (size_t)P + 16, h->st));
+    h->dd_host.assign((size_t)P, 0);
+    h->dd_evictions = 0;
+  }
   if (h->has_table) TRY(table_reset(h));
   return AGGB_OK;
 }
@@ -1948,9 +1962,8 @@ int aggb_create(int device, const aggb_config* cfg, const aggb_spec* spec, void*
   h->kw = h->cs.kw;
   h->prog = detect_prog(h->cs.ds, h->kw);
   if (getenv("AGGB_NO_SPECIALIZE")) h->prog = 0;
-  if (h->cfg.algo == AGGB_SHARED_HASH || h->cfg.algo == AGGB_DYNAMIC_DESTAGING) {
-    // same primitives; both run the pre-partitioning schedule on the GPU
-  }
+  // shared_hash runs the pre-partitioning schedule on the GPU; dynamic_destaging
+  // has its own (push_dd: destage the largest partitions when the table runs dry)
   s = plan(h);
   if (s) {
     delete h;
@@ -2052,6 +2065,171 @@ void aggb_destroy(void* handle) {
 }
 
 
+// ---------------------------------------------------------------------------
+// dynamic destaging (hybrid.py:974-1149, DynamicDestaging): every partition
+// aggregates in the shared table until it runs dry; then the largest resident
+// partitions are destaged — their groups cut to a partial run (part0) and their
+// later records spilled raw (raw0) — and the pass resumes.  The partitions are
+// the spill sets' fine partitions (children fit them); one destaging round
+// evicts largest-first until 1/dd_rounds() of the table is free, the share one of
+// the reference's coarse partitions holds.
+// ---------------------------------------------------------------------------
+int dd_rounds() {  // share of the table one destaging round frees: 1/DD_ROUNDS
+  const char* e = getenv("AGGB_DD_ROUNDS");
+  return e ? std::max(1, atoi(e)) : 4;  // C2 100M: 16 -> 34.5 ms, 8 -> 22.0, 4 -> 15.7 (same spill), 2 -> 13.5 (+5% spill)
+}
+
+int dd_evict(Handle* h) {
+  const int P = h->part0.ss.nparts;
+  const int words = h->kw + h->cs.ds.ns;
+  const int64_t n = (int64_t)h->tab.cap + 2;
+  TRY(h->dd_tmp.ensure((size_t)3 * n * words * 8 + 64 + (size_t)P * 8, &h->hw));
+  uint64_t* all = h->dd_tmp.as<uint64_t>();
+  uint64_t* ev = all + (size_t)n * words;
+  uint64_t* kept = ev + (size_t)n * words;
+  unsigned long long* hist = (unsigned long long*)(kept + (size_t)n * words);
+  unsigned long long* cnts = SC(h) + 40;  // [40] all, [41] evicted, [42] kept
+  OutBuf o;
+  o.keys = all;
+  o.vals = all + (size_t)h->kw * n;
+  o.cap = n;
+  o.count = cnts;
+  o.partial = 1;
+  CU(cudaMemsetAsync(cnts, 0, 24, h->st));
+  CU(cudaMemsetAsync(hist, 0, (size_t)P * 8, h->st));
+  TRY(flush_table(h, true, &o));
+  const uint64_t seed = h->part0.ss.seed;
+  const int grid = h->sms * 4;
+  if (h->kw == 1) k_dd_hist<1><<<grid, 256, 0, h->st>>>(all, n, cnts, seed, P, hist);
+  else k_dd_hist<2><<<grid, 256, 0, h->st>>>(all, n, cnts, seed, P, hist);
+  std::vector<unsigned long long> hh(P);
+  unsigned long long total = 0;
+  CU(cudaMemcpyAsync(hh.data(), hist, (size_t)P * 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(&total, cnts, 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  // largest resident partitions first, until a round's share of the table is free
+  std::vector<int> order;
+  for (int p = 0; p < P; p++)
+    if (!h->dd_host[p] && hh[p]) order.push_back(p);
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return hh[x] > hh[y] || (hh[x] == hh[y] && x < y); });
+  const unsigned long long want = std::max<unsigned long long>(1, (unsigned long long)h->tab.cap / dd_rounds());
+  unsigned long long freed = 0;
+  std::vector<uint8_t> evict(P, 0);
+  for (int p : order) {
+    if (freed >= want) break;
+    evict[p] = 1;
+    h->dd_host[p] = 1;
+    freed += hh[p];
+    h->dd_evictions++;
+  }
+  if (order.empty()) {  // nothing resident left to destage: every later record spills raw
+    for (int p = 0; p < P; p++) h->dd_host[p] = 1;
+  }
+  uint8_t* flags = h->dd_spilled.as<uint8_t>();
+  CU(cudaMemcpyAsync(flags, h->dd_host.data(), (size_t)P, cudaMemcpyHostToDevice, h->st));
+  // split the flushed groups: evicted -> the partial set, kept -> back into the table
+  if (h->kw == 1) k_dd_split<1><<<grid, 256, 0, h->st>>>(all, n, cnts, words, seed, P, flags, ev, kept, cnts + 1);
+  else k_dd_split<2><<<grid, 256, 0, h->st>>>(all, n, cnts, words, seed, P, flags, ev, kept, cnts + 1);
+  h->launches += 3;
+  CU(cudaGetLastError());
+  PassPlan g;
+  g.mode = MODE_GRACE;
+  g.lin = ev;
+  g.lin_stride = n;
+  g.lin_count = cnts + 1;
+  g.lin_kind = 1;
+  g.lin_words = h->cs.ds.ns;
+  g.ss = h->part0.ss;
+  g.counter = SC(h) + 9;
+  TRY(launch_pass(h, g));
+  h->part0_live = true;
+  TRY(table_reset(h));
+  PassPlan f;  // the kept groups: merge ops into the fresh table (they fit: fewer than before)
+  f.mode = MODE_FILL;
+  f.lin = kept;
+  f.lin_stride = n;
+  f.lin_count = cnts + 2;
+  f.lin_kind = 1;
+  f.lin_words = h->cs.ds.ns;
+  f.counter = SC(h) + 8;
+  CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+  TRY(launch_pass(h, f));
+  return AGGB_OK;
+}
+
+int push_dd(Handle* h, const ColSrc& col0) {
+  const int nwt = nwt_for(std::max(1, col0.nv));
+  PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
+  const int64_t T = (int64_t)pcfg.R * pcfg.blk;
+  TRY(ensure_defer(h, T, col0.nv));
+  std::vector<ColSrc> queue{col0};
+  std::vector<DBuf> temps;
+  int rc = AGGB_OK;
+  int guard = 0;
+  while (!queue.empty() && rc == AGGB_OK) {
+    ColSrc cur = queue.back();
+    queue.pop_back();
+    if (cur.n <= 0) continue;
+    CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+    PassPlan f;
+    f.mode = MODE_DD;
+    f.col = cur;
+    f.ss = h->raw0.ss;
+    f.counter = SC(h) + 8;
+    if ((rc = launch_pass(h, f))) break;
+    h->raw0_live = true;
+    unsigned long long tiles = 0, nd = 0;
+    int frozen = 0;
+    CU(cudaMemcpyAsync(&tiles, SC(h) + 8, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&nd, SC(h) + 10, 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    if (!frozen && !nd) continue;
+    if (++guard > h->part0.ss.nparts + 64) {  // every round destages at least one partition
+      rc = fail(AGGB_CAPACITY_EXCEEDED, "dynamic destaging made no progress");
+      break;
+    }
+    const int64_t start = std::min<int64_t>(cur.n, (int64_t)tiles * T);
+    ColSrc dc;
+    memset(&dc, 0, sizeof(dc));
+    if (nd) {  // keep the refused records (the deferral buffer is reused)
+      DBuf tmp;
+      const int words = h->kw + cur.nv;
+      if ((rc = tmp.ensure((size_t)nd * words * 8, nullptr))) break;
+      for (int w = 0; w < words; w++)
+        CU(cudaMemcpyAsync(tmp.as<uint64_t>() + w * nd, h->defer.as<uint64_t>() + w * h->defer_cap, nd * 8,
+                           cudaMemcpyDeviceToDevice, h->st));
+      dc.n = (int64_t)nd;
+      for (int w = 0; w < h->kw; w++) {
+        dc.key[w] = (const uint8_t*)(tmp.as<uint64_t>() + w * nd);
+        dc.kstride[w] = 8;
+        dc.kty[w] = TY_I64;
+      }
+      dc.nv = cur.nv;
+      for (int w = 0; w < cur.nv; w++) {
+        dc.val[w] = (const uint8_t*)(tmp.as<uint64_t>() + (h->kw + w) * nd);
+        dc.vstride[w] = 8;
+        dc.vty[w] = (h->cs.ds.vty[w] == TY_F64) ? TY_F64 : TY_I64;
+      }
+      temps.push_back(tmp);
+    }
+    if ((rc = dd_evict(h))) break;  // the pool ran dry: destage the largest partitions
+    if (start < cur.n) {
+      ColSrc rest = cur;
+      rest.n = cur.n - start;
+      for (int w = 0; w < h->kw; w++) rest.key[w] = cur.key[w] + start * cur.kstride[w];
+      for (int w = 0; w < cur.nv; w++) rest.val[w] = cur.val[w] + start * cur.vstride[w];
+      queue.push_back(rest);
+    }
+    if (nd) queue.push_back(dc);  // refused records first
+  }
+  cudaStreamSynchronize(h->st);
+  for (auto& t : temps) t.release();
+  h->met.spilled_partitions = 0;
+  for (uint8_t x : h->dd_host) h->met.spilled_partitions += x;
+  return rc;
+}
+
 // Heavy hitters of this push (pass.cuh k_hot_sample): in-memory and L2-capped
 // plans of one-word keys with the COUNT/SUM programs (C1, C3, C4).  Budgeted
 // plans keep the reference's arrival-order residency untouched (the tier only
@@ -2088,6 +2266,7 @@ int hot_sample(Handle* h, const ColSrc& col) {
 
 int push_col(Handle* h, const ColSrc& col) {
   if (h->cfg.algo == AGGB_SORT_BASED) return aggb_sort_push(h, col);
+  if (h->cfg.algo == AGGB_DYNAMIC_DESTAGING) return push_dd(h, col);
   TRY(hot_sample(h, col));
   if (h->cfg.algo == AGGB_HASH_SORT) return push_hash_sort(h, col);
   return push_hybrid(h, col);

@@ -25,7 +25,7 @@
 
 namespace aggb {
 
-enum { MODE_FILL = 0, MODE_PROBE = 1, MODE_ROUTE = 2, MODE_GRACE = 3 };
+enum { MODE_FILL = 0, MODE_PROBE = 1, MODE_ROUTE = 2, MODE_GRACE = 3, MODE_DD = 4 };
 enum { R_HIT = 0, R_INSERTED = 1, R_MISS = 2, R_REFUSED = 3 };
 enum { ST_SPILLED = 0, ST_HITS = 1, ST_INSERTS = 2, ST_DEFERRED = 3, ST_RECORDS = 4, ST_OVERFLOW = 5,
        ST_NSTATS = 8 };
@@ -775,6 +775,36 @@ __global__ void k_exch_raw_scatter(ColSrc c, uint64_t seed, int nranks, unsigned
 #pragma unroll
     for (int w = 0; w < KW; w++) dst[w] = raw_slot(c.key[w], c.kstride[w], c.kty[w], i);
     for (int w = 0; w < c.nv; w++) dst[KW + w] = raw_slot(c.val[w], c.vstride[w], c.vty[w], i);
+  }
+}
+
+// dynamic destaging (hybrid.py:974-1149): groups of a flushed table (SoA
+// partial list, `n` records, column stride `cap`) counted per partition, and
+// split into the evicted partitions' groups and the kept ones
+template <int KW>
+__global__ void k_dd_hist(const uint64_t* keys, int64_t cap, const unsigned long long* n, uint64_t seed, int P,
+                          unsigned long long* hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = keys[w * cap + i];
+    const int p = (int)reduce32(hash_key<KW>(k, seed), (uint32_t)P);  // GRACE's partition
+    atomicAdd(&hist[p], 1ull);
+  }
+}
+
+template <int KW>
+__global__ void k_dd_split(const uint64_t* src, int64_t cap, const unsigned long long* n, int words, uint64_t seed,
+                           int P, const uint8_t* evict, uint64_t* ev, uint64_t* kept, unsigned long long* counts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)*n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k[KW];
+#pragma unroll
+    for (int w = 0; w < KW; w++) k[w] = src[w * cap + i];
+    const int p = (int)reduce32(hash_key<KW>(k, seed), (uint32_t)P);
+    const int e = evict[p] ? 0 : 1;
+    uint64_t* dst = e == 0 ? ev : kept;
+    const unsigned long long at = atomicAdd(&counts[e], 1ull);
+    for (int w = 0; w < words; w++) dst[w * cap + at] = src[w * cap + i];
   }
 }
 

@@ -54,6 +54,7 @@ struct PassArgs {
   int32_t pairs;                          // k_probe: sector pairs on (shared memory permitting)
   const uint64_t* hot;                    // heavy-hitter keys (k_hot_sample): hot[0..7] keys, hot[8] count
   int32_t rows64;                         // k_probe_w: columns are C5's 64-byte rows (k0 i64 | k1 i32 | v0..v3 at +16)
+  const uint8_t* dd_spilled;              // MODE_DD: partitions destaged so far (their records spill raw)
 };
 
 // ---------------------------------------------------------------------------
@@ -313,12 +314,12 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
   const int64_t col_tiles = (n - col_start + T - 1) / T;
   const int64_t n_lin = a.lin_count ? (int64_t)*a.lin_count : 0;
   const unsigned long long total = (unsigned long long)(col_tiles + (n_lin + T - 1) / T);
-  const bool use_table = (a.mode == MODE_FILL || a.mode == MODE_PROBE || a.mode == MODE_ROUTE);
+  const bool use_table = (a.mode == MODE_FILL || a.mode == MODE_PROBE || a.mode == MODE_ROUTE || a.mode == MODE_DD);
   const bool insert = (a.mode != MODE_PROBE);
   const int nvc = a.col.nv, nvl = a.lin.nv;
 
   auto grab = [&]() -> unsigned long long {
-    if (a.mode == MODE_FILL && *(volatile int*)&a.t.hdr->frozen) return ~0ull;
+    if ((a.mode == MODE_FILL || a.mode == MODE_DD) && *(volatile int*)&a.t.hdr->frozen) return ~0ull;
     return atomicAdd(a.tile_counter, 1ull);
   };
   auto load_tile = [&](unsigned long long tile, uint64_t (&k)[R][KW], uint64_t (&v)[R][NWT], bool (&live)[R]) {
@@ -396,6 +397,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
         }
       } else if (a.mode == MODE_GRACE) {
         part[r] = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);
+      } else if (a.mode == MODE_DD) {  // destaged partitions spill raw, the others aggregate
+        const int pp = (int)reduce32(hash_key<KW>(kc[r], a.ss.seed), (uint32_t)P);  // GRACE's partition
+        if (a.dd_spilled[pp]) part[r] = pp;
       }
       if (use_table && part[r] == -1 && !is_sentinel<KW>(kc[r])) {
         // one 64-bit hash per record at this level: bucket from the low bits,
@@ -486,7 +490,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
           }
         } else if (res == R_MISS) {
           part[r] = is_sentinel<KW>(kc[r]) ? 0 : (int)reduce32(bk[r], (uint32_t)P);
-        } else if (a.mode == MODE_FILL) {
+        } else if (a.mode == MODE_FILL || a.mode == MODE_DD) {
           tag[r] = 0x80000000u | atomicAdd(&s_ndefer, 1u);
           c_def++;
           part[r] = -2;

@@ -16,7 +16,7 @@ from conftest import (assert_values_match, float_out_cols, golden_files, golden_
 
 pytestmark = pytest.mark.gpu
 
-ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort", "sort_based")
+ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort", "sort_based", "dynamic_destaging")
 
 
 def _engine():
@@ -421,3 +421,24 @@ def test_spill_pool_overflows_to_host_memory(algo, monkeypatch):
     assert res.n_groups == len(uk)
     assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
     assert np.array_equal(res.as_float64(), want)
+
+
+def test_dynamic_destaging_destages_partitions():
+    """dynamic_destaging (hybrid.py:974-1149): when the shared table runs dry the
+    largest resident partitions are destaged — their groups cut to a partial
+    run, their later records spilled raw — and the rest keep aggregating in
+    memory; the merged result is exact."""
+    from paper_1311_0059_b200 import datagen as D
+    from paper_1311_0059_b200.core import DatasetStats
+    from oracle import oracle as O
+    cfg = D.scaled(D.CONFIGS["C2"], 2_000_000)
+    keys, vals = D.generate(cfg)
+    st = DatasetStats(R=1, R_t=cfg.n, G=1, G_t=cfg.key_range)
+    res, met = run_gpu("dynamic_destaging", cfg, keys, vals, chunks=3, budget_groups=cfg.budget_groups,
+                       stats=st, seed=5)
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    assert res.n_groups == len(uk)
+    assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+    assert np.array_equal(res.as_float64(), want)
+    assert met["spilled_partitions"] > 0 and met["spilled_records"] > 0
+    assert 0 < met["resident_groups"] <= cfg.budget_groups
