@@ -581,6 +581,7 @@ struct Handle {
   DBuf dd_spilled, dd_tmp;  // dynamic destaging: destaged-partition flags, eviction lists
   std::vector<uint8_t> dd_host;
   int64_t dd_evictions = 0;
+  int sh_stage = 0;  // shared_hash: overflows seen (0: shared table, 1: original_hh shape, 2: pure routing)
   bool hot_ready = false;
   bool hot_no_tier = false;  // the hot keys cover most records: no SMEM pre-aggregation tier
   int64_t skew_cap = 0;      // L2-capped plans: the capacity a heavily skewed push may use
@@ -1260,13 +1261,15 @@ int begin_run(Handle* h) {
     int pp = std::min(h->P0, max_parts_for(h->kw + h->cs.ds.ns));
     // dynamic destaging: a destaged partition's raw records and its evicted
     // groups must land in the same partition of both sets
-    h->raw0 = {make_set(h, algo == AGGB_DYNAMIC_DESTAGING ? pp : h->P0, h->cs.nv, 0,
+    const bool dd = algo == AGGB_DYNAMIC_DESTAGING || algo == AGGB_SHARED_HASH;
+    h->raw0 = {make_set(h, dd ? pp : h->P0, h->cs.nv, 0,
                         level_seed(seed, SALT_SPILL, lv)), 0};
     h->part0 = {make_set(h, pp, h->cs.ds.ns, 1, level_seed(seed, SALT_SPILL, lv)), 0};
   }
   h->raw0_live = h->part0_live = false;
-  if (algo == AGGB_DYNAMIC_DESTAGING) {
+  if (algo == AGGB_DYNAMIC_DESTAGING || algo == AGGB_SHARED_HASH) {
     const int P = h->part0.ss.nparts;
+    h->sh_stage = 0;
     TRY(h->dd_spilled.ensure((size_t)P + 16, &h->hw));
     CU(cudaMemsetAsync(h->dd_spilled.p, 0, (size_t)P + 16, h->st));
     h->dd_host.assign((size_t)P, 0);
@@ -1962,8 +1965,8 @@ int aggb_create(int device, const aggb_config* cfg, const aggb_spec* spec, void*
   h->kw = h->cs.kw;
   h->prog = detect_prog(h->cs.ds, h->kw);
   if (getenv("AGGB_NO_SPECIALIZE")) h->prog = 0;
-  // shared_hash runs the pre-partitioning schedule on the GPU; dynamic_destaging
-  // has its own (push_dd: destage the largest partitions when the table runs dry)
+  // dynamic_destaging and shared_hash share push_dd (MODE_DD passes); they differ
+  // in what an overflow destages (dd_evict)
   s = plan(h);
   if (s) {
     delete h;
@@ -2112,15 +2115,31 @@ int dd_evict(Handle* h) {
   for (int p = 0; p < P; p++)
     if (!h->dd_host[p] && hh[p]) order.push_back(p);
   std::sort(order.begin(), order.end(), [&](int x, int y) { return hh[x] > hh[y] || (hh[x] == hh[y] && x < y); });
-  const unsigned long long want = std::max<unsigned long long>(1, (unsigned long long)h->tab.cap / dd_rounds());
-  unsigned long long freed = 0;
   std::vector<uint8_t> evict(P, 0);
-  for (int p : order) {
-    if (freed >= want) break;
-    evict[p] = 1;
-    h->dd_host[p] = 1;
-    freed += hh[p];
-    h->dd_evictions++;
+  if (h->cfg.algo == AGGB_SHARED_HASH) {
+    // shared_hash (hybrid.py:579-915): the first overflow cuts every partition but
+    // partition 0 (the resident share r_res of the hash range, as original_hh
+    // plans it) to runs; a second overflow cuts partition 0 too: pure routing
+    const double G_t = std::max(1.0, h->cfg.stats_G_t);
+    const double r_res = h->cfg.stats_G_t > 0 ? std::min(1.0, 0.9 * (double)h->budget / G_t) : 0.5;
+    const int k0 = h->sh_stage == 0 ? std::max(1, std::min(P - 1, (int)std::lround(r_res * P))) : 0;
+    for (int p = k0; p < P; p++)
+      if (!h->dd_host[p]) {
+        evict[p] = 1;
+        h->dd_host[p] = 1;
+        h->dd_evictions++;
+      }
+    h->sh_stage++;
+  } else {
+    const unsigned long long want = std::max<unsigned long long>(1, (unsigned long long)h->tab.cap / dd_rounds());
+    unsigned long long freed = 0;
+    for (int p : order) {
+      if (freed >= want) break;
+      evict[p] = 1;
+      h->dd_host[p] = 1;
+      freed += hh[p];
+      h->dd_evictions++;
+    }
   }
   if (order.empty()) {  // nothing resident left to destage: every later record spills raw
     for (int p = 0; p < P; p++) h->dd_host[p] = 1;
@@ -2266,7 +2285,7 @@ int hot_sample(Handle* h, const ColSrc& col) {
 
 int push_col(Handle* h, const ColSrc& col) {
   if (h->cfg.algo == AGGB_SORT_BASED) return aggb_sort_push(h, col);
-  if (h->cfg.algo == AGGB_DYNAMIC_DESTAGING) return push_dd(h, col);
+  if (h->cfg.algo == AGGB_DYNAMIC_DESTAGING || h->cfg.algo == AGGB_SHARED_HASH) return push_dd(h, col);
   TRY(hot_sample(h, col));
   if (h->cfg.algo == AGGB_HASH_SORT) return push_hash_sort(h, col);
   return push_hybrid(h, col);

@@ -16,7 +16,7 @@ from conftest import (assert_values_match, float_out_cols, golden_files, golden_
 
 pytestmark = pytest.mark.gpu
 
-ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort", "sort_based", "dynamic_destaging")
+ALGOS_GPU = ("pre_partitioning", "original_hh", "hash_sort", "sort_based", "dynamic_destaging", "shared_hash")
 
 
 def _engine():
@@ -442,3 +442,23 @@ def test_dynamic_destaging_destages_partitions():
     assert np.array_equal(res.as_float64(), want)
     assert met["spilled_partitions"] > 0 and met["spilled_records"] > 0
     assert 0 < met["resident_groups"] <= cfg.budget_groups
+
+
+def test_shared_hash_two_overflow_stages():
+    """shared_hash (hybrid.py:579-915): one table shared by every partition until
+    the first overflow, which cuts all partitions but partition 0 to runs (the
+    original_hh shape); a second overflow cuts partition 0 too.  Exact results."""
+    from paper_1311_0059_b200 import datagen as D
+    from paper_1311_0059_b200.core import DatasetStats
+    from oracle import oracle as O
+    cfg = D.scaled(D.CONFIGS["C2"], 2_000_000)
+    keys, vals = D.generate(cfg)
+    uk, want, _ = O.groupby_numpy(keys, vals, O.ospec(cfg.aggs))
+    for g_t in (cfg.key_range, cfg.key_range // 20):  # right estimate, and a 20x underestimate
+        st = DatasetStats(R=1, R_t=cfg.n, G=1, G_t=g_t)
+        res, met = run_gpu("shared_hash", cfg, keys, vals, chunks=2, budget_groups=cfg.budget_groups, stats=st,
+                           seed=6)
+        assert res.n_groups == len(uk)
+        assert np.array_equal(res.keys[0], uk[:, 0].view(np.int64))
+        assert np.array_equal(res.as_float64(), want)
+        assert met["spilled_partitions"] > 0 and met["resident_groups"] <= cfg.budget_groups

@@ -15,7 +15,7 @@ for n, kr, bg in [(200_000, 20_000, 2500), (4_000_000, 40_000, 5000), (100_000_0
     else:
         dk = [torch.from_numpy(k).cuda() for k in keys]; dv = [torch.from_numpy(v).cuda() for v in vals]
     agg = AggSpec.from_names(list(cfg.aggs))
-    for algo in ("dynamic_destaging", "pre_partitioning"):
+    for algo in ("dynamic_destaging", "shared_hash", "pre_partitioning"):
         with GroupBy(algo, agg, ["i64"], ["i64"], budget_groups=bg, seed=3, stats=DatasetStats(R=1, R_t=n, G=1, G_t=kr)) as g:
             for it in range(2):
                 g.reset(); torch.cuda.synchronize(); t0 = time.time()
