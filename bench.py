@@ -480,7 +480,8 @@ def main():
                     help="N > 1: partial groups after a local combine, or raw rows first")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=50_000_000)
-    ap.add_argument("--also", default="original_hh", help="extra algorithms to time (comma list)")
+    ap.add_argument("--also", default="original_hh,shared_hash,dynamic_destaging",
+                    help="extra algorithms to time (comma list)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
