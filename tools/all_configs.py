@@ -12,6 +12,7 @@ from paper_1311_0059_b200.core import DatasetStats
 FULL = not os.environ.get("AGGB_SCALED")
 runs = [("C1", "pre_partitioning", 0, None), ("C1", "hash_sort", 0, None),
         ("C2", "pre_partitioning", 0, None), ("C2", "original_hh", 0, None),
+        ("C2", "shared_hash", 0, None), ("C2", "dynamic_destaging", 0, None),
         ("C3", "pre_partitioning", 0, 0.5), ("C3", "pre_partitioning", 0, 1.0),
         ("C3", "pre_partitioning", 0, 1.5), ("C3", "hash_sort", 0, 0.5), ("C3", "hash_sort", 0, 1.0),
         ("C3", "hash_sort", 0, 1.5),
