@@ -1152,7 +1152,10 @@ int plan(Handle* h) {
   // (C2, profiles/r01_notes.md: child 1.08 -> 0.94 ms from 0.5 to 0.4 of the
   // table — lower load, shorter probes, a finer tail — for +0.04 ms of PROBE)
   double spill_groups = std::max(0.0, std::max(G_t, 1.0) - (double)h->budget);
-  int P = (int)std::ceil(spill_groups / std::max(1.0, 0.4 * h->child_cap));
+  // (C5 at 100M: 0.55 cut the child 6.33 -> 5.46 ms, but at 500M records per
+  // item the gain is gone: 16.5 vs 16.9 ms; 0.4 stays)
+  const double load = getenv("AGGB_CHILD_LOAD") ? atof(getenv("AGGB_CHILD_LOAD")) : 0.4;  // experiment knob
+  int P = (int)std::ceil(spill_groups / std::max(1.0, load * h->child_cap));
   P = std::max(P, 1);
   if (c.budget_groups == 0 && M >= 3) {
     double bg = ref_group_bytes(c, h->cs.ref_width, G, G_t);
