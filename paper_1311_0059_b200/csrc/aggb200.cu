@@ -578,6 +578,7 @@ struct Handle {
   // recursion scratch
   DBuf part_records, part_pages, cursor, plist, item_off, ovf, pend, l2stage, cut_tmp;
   DBuf hot;                 // heavy-hitter keys of the current push (k_hot_sample)
+  DBuf sort_hist;           // sort path: byte histograms of the appended keys
   DBuf dd_spilled, dd_tmp;  // dynamic destaging: destaged-partition flags, eviction lists
   std::vector<uint8_t> dd_host;
   int64_t dd_evictions = 0;
@@ -2634,9 +2635,12 @@ int aggb_sort_push(Handle* h, const ColSrc& col) {
     h->sort_cap = cap;
   }
   SortBuf a = sortbuf(h, h->sort_keys, h->sort_cap);
+  TRY(h->sort_hist.ensure(16 * 256 * 8, &h->hw));
+  if (h->sort_n == 0) CU(cudaMemsetAsync(h->sort_hist.p, 0, 16 * 256 * 8, h->st));
   int pe = prof_begin(h, 9);
-  if (h->kw == 1) k_sort_append<1, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n);
-  else k_sort_append<2, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n);
+  unsigned long long* hist = h->sort_hist.as<unsigned long long>();
+  if (h->kw == 1) k_sort_append<1, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n, hist);
+  else k_sort_append<2, 1><<<h->sms * 8, 256, 0, h->st>>>(col, col.nv, a, h->sort_n, hist);
   prof_end(h, pe);
   h->launches++;
   CU(cudaGetLastError());
@@ -2722,18 +2726,9 @@ int aggb_sort_finish(Handle* h) {
     CU(cudaStreamSynchronize(h->st));
     if (bad) return fail(AGGB_ORDER_ERROR, "input declared sorted but a key decreased");
   } else {
-    DBuf hist, keyptrs;
-    TRY(hist.ensure(16 * 256 * 8, nullptr));
-    TRY(keyptrs.ensure(2 * 8, nullptr));
-    CU(cudaMemsetAsync(hist.p, 0, 16 * 256 * 8, h->st));
-    const uint64_t* kp[2] = {a.w[0], h->kw > 1 ? a.w[1] : a.w[0]};
-    CU(cudaMemcpyAsync(keyptrs.p, kp, sizeof(kp), cudaMemcpyHostToDevice, h->st));
-    int pe = prof_begin(h, 9);
-    k_digit_hist8<<<h->sms * 4, 256, 0, h->st>>>(keyptrs.as<const uint64_t*>(), h->kw, n,
-                                                 hist.as<unsigned long long>());
-    prof_end(h, pe);
+    // byte histograms of every key, gathered by k_sort_append as the keys came in
     std::vector<unsigned long long> hh(16 * 256);
-    CU(cudaMemcpyAsync(hh.data(), hist.p, 16 * 256 * 8, cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(hh.data(), h->sort_hist.p, 16 * 256 * 8, cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
     // LSD order: least significant word last in the key, lowest byte first
     std::vector<std::pair<int, int>> passes;

@@ -1,9 +1,10 @@
 // sort.cuh — the sort path (sort_based.py:24-211): LSD radix sort of the
 // records by key words, then a segmented reduction over runs of equal keys.
 //
-//   k_digit_hist8    one read of all keys: 256-bin histograms of every byte
-//                    position (decides which digit passes are needed: a byte
-//                    that is equal in every key needs no pass)
+//   k_sort_append    copies pushed columns into the sort buffers and gathers
+//                    256-bin histograms of every key byte on the way (decides
+//                    which digit passes are needed: a byte equal in every key
+//                    needs no pass)
 //   k_tile_hist      per-tile digit counts for one pass   -> counts[d][tile]
 //   k_scan_*         3-phase exclusive scan of the digit-major counts
 //   k_scatter        stable scatter of one pass (warp match_any ranking)
@@ -26,23 +27,6 @@ struct SortBuf {
   uint64_t* w[MAX_STATES + 2];  // word columns (KW key words first)
   int nw;
 };
-
-// 256-bin histograms for 8 * KW byte positions (digit index = word * 8 + byte)
-__global__ void k_digit_hist8(const uint64_t* const* keys, int kw, int64_t n, unsigned long long* hist /* [16][256] */) {
-  __shared__ unsigned int sh[16][256];
-  for (int i = threadIdx.x; i < 16 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    for (int w = 0; w < kw; w++) {
-      uint64_t k = keys[w][i];
-#pragma unroll
-      for (int b = 0; b < 8; b++) atomicAdd(&sh[w * 8 + b][(k >> (8 * b)) & 255], 1u);
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kw * 8 * 256; i += blockDim.x)
-    if ((&sh[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&sh[0][0])[i]);
-}
 
 __global__ void k_tile_hist(const uint64_t* key, int shift, int64_t n, uint32_t* counts /* [256][ntiles] */,
                             int64_t ntiles) {
@@ -472,18 +456,30 @@ __global__ void k_check_sorted(const SortBuf s, int64_t n, int* bad) {
 
 // append a columnar batch to the sort buffer as words (keys, payload words)
 template <int KW, int NWT>
-__global__ void k_sort_append(ColSrc c, int nv, SortBuf s, int64_t at) {
+__global__ void k_sort_append(ColSrc c, int nv, SortBuf s, int64_t at, unsigned long long* hist /* [16][256] */) {
+  // the byte histograms are gathered here while the keys pass through registers
+  // (a separate histogram pass re-read every key at finish: 4 ms per 1B records)
+  __shared__ unsigned int sh[KW * 8][256];
+  for (int i = threadIdx.x; i < KW * 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.n; i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k[KW];
     col_key<KW>(c, i, k);
 #pragma unroll
-    for (int w = 0; w < KW; w++) s.w[w][at + i] = k[w];
+    for (int w = 0; w < KW; w++) {
+      s.w[w][at + i] = k[w];
+#pragma unroll
+      for (int b = 0; b < 8; b++) atomicAdd(&sh[w * 8 + b][(k[w] >> (8 * b)) & 255], 1u);
+    }
     for (int w = 0; w < nv; w++) {
       const uint8_t* p = c.val[w] + i * c.vstride[w];
       s.w[KW + w][at + i] =
           (c.vty[w] == TY_I32) ? (uint64_t)(long long)*(const int*)p : (uint64_t)*(const long long*)p;
     }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < KW * 8 * 256; i += blockDim.x)
+    if ((&sh[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&sh[0][0])[i]);
 }
 
 }  // namespace aggb
