@@ -42,8 +42,10 @@ struct TableHdr {
 struct GTable {
   uint64_t* keys;    // (nslots + 2) * KW words; slots grouped in 32-byte buckets
                      // (4 one-word keys or 2 two-word keys), escape slot last
-  uint64_t* states;  // ns * stride, field-major
+  uint64_t* states;  // ns * stride words: state j of slot s at states[j * fstride + s * sstride]
   uint64_t stride;   // nslots + 1 (slot nslots = escape slot of the sentinel key)
+  uint64_t fstride;  // field-major (SoA, fstride = stride, sstride = 1) for L2-resident tables;
+  uint64_t sstride;  // slot-major (AoS, fstride = 1, sstride = ns) for tables beyond L2 (one sector per slot)
   uint64_t mask;     // nslots - 1
   uint64_t bmask;    // nbuckets - 1
   uint64_t cap;      // group capacity (budget)
@@ -260,7 +262,22 @@ __global__ void k_table_init(GTable t, int kw, DevSpec sp) {
     if (tail && t0 == 0) p[cnt - 1] = v;
   };
   fill(t.keys, n * (uint64_t)kw, EMPTY);
-  for (int j = 0; j < sp.ns; j++) fill(t.states + (uint64_t)j * n, n, state_identity(sp.op[j], sp.ty[j]));
+  if (t.sstride == 1) {
+    for (int j = 0; j < sp.ns; j++) fill(t.states + (uint64_t)j * n, n, state_identity(sp.op[j], sp.ty[j]));
+  } else {  // slot-major: the identities repeat with period ns
+    uint64_t id[MAX_STATES];
+    bool zero = true;
+    for (int j = 0; j < sp.ns; j++) {
+      id[j] = state_identity(sp.op[j], sp.ty[j]);
+      zero = zero && id[j] == 0;
+    }
+    const uint64_t words = n * (uint64_t)sp.ns;
+    if (zero) {
+      fill(t.states, words, 0ull);
+    } else {
+      for (uint64_t i = t0; i < words; i += gt) t.states[i] = id[i % (uint64_t)sp.ns];
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     t.hdr->groups = 0;
     t.hdr->frozen = 0;
@@ -501,17 +518,17 @@ __global__ void __launch_bounds__(256) k_flush_table(GTable t, DevSpec sp, OutBu
         if (sp.ns <= 4 && sp.nout <= 4) {
           uint64_t st4[4];
 #pragma unroll
-          for (int q = 0; q < 4; q++) st4[q] = q < sp.ns ? t.states[(uint64_t)q * n + s] : 0ull;
+          for (int q = 0; q < 4; q++) st4[q] = q < sp.ns ? t.states[(uint64_t)q * t.fstride + s * t.sstride] : 0ull;
           emit_group4<KW>(sp, o, idx, k, st4);
         } else {
           uint64_t st[MAX_STATES];
-          for (int q = 0; q < sp.ns; q++) st[q] = t.states[(uint64_t)q * n + s];
+          for (int q = 0; q < sp.ns; q++) st[q] = t.states[(uint64_t)q * t.fstride + s * t.sstride];
           emit_group<KW>(sp, o, idx, k, st);
         }
         if (CLEAR) {
 #pragma unroll
           for (int w = 0; w < KW; w++) t.keys[s * KW + w] = EMPTY;
-          for (int q = 0; q < sp.ns; q++) t.states[(uint64_t)q * n + s] = state_identity(sp.op[q], sp.ty[q]);
+          for (int q = 0; q < sp.ns; q++) t.states[(uint64_t)q * t.fstride + s * t.sstride] = state_identity(sp.op[q], sp.ty[q]);
         }
       }
       at += __popc(m[j]);

@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       }
       if (part[r] == -1) {
         if (res == R_HIT || res == R_INSERTED) {
-          Upd<PG>::template g<NWT>(a.t.states, a.t.stride, (uint64_t)s, kind, s_fd, ns, vc[r]);
+          Upd<PG>::template g<NWT>(a.t.states, a.t.fstride, (uint64_t)s * a.t.sstride, kind, s_fd, ns, vc[r]);
           c_hit += (res == R_HIT);
           c_ins += (res == R_INSERTED);
           part[r] = -2;
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = merge_word(v, __shfl_xor_sync(0xffffffffu, v, o), F & 3, (F >> 2) & 3);
         if ((tid & 31) == 0 && v != state_identity(F & 3, (F >> 2) & 3))
-          gupdate(a.t.states + (uint64_t)j * a.t.stride + (uint64_t)sl, F & 3, (F >> 2) & 3, v);
+          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)sl * a.t.sstride, F & 3, (F >> 2) & 3, v);
       }
     }
   }
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_pass(PassArgs a) {
       const uint64_t v = cst[(size_t)j * CH + i];
       const uint32_t F = s_fd[j];
       if (v == state_identity(F & 3, (F >> 2) & 3)) continue;
-      gupdate(a.t.states + (uint64_t)j * a.t.stride + gs, F & 3, (F >> 2) & 3, v);
+      gupdate(a.t.states + (uint64_t)j * a.t.fstride + gs * a.t.sstride, F & 3, (F >> 2) & 3, v);
     }
   }
   if (spills)

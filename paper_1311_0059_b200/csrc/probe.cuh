@@ -45,7 +45,7 @@ __device__ __forceinline__ int64_t probe_finish(const PassArgs& a, uint64_t k, u
   }
   if (s < 0) return -1;
   const uint64_t vv[1] = {v};
-  Upd<PG>::template g<1>(a.t.states, a.t.stride, (uint64_t)s, 0, s_fd, ns, vv);
+  Upd<PG>::template g<1>(a.t.states, a.t.fstride, (uint64_t)s * a.t.sstride, 0, s_fd, ns, vv);
   return s;
 }
 
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe(PassArgs a) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) v = merge_word(v, __shfl_xor_sync(0xffffffffu, v, o), F & 3, (F >> 2) & 3);
         if (lane == 0 && v != state_identity(F & 3, (F >> 2) & 3))
-          gupdate(a.t.states + (uint64_t)j * a.t.stride + (uint64_t)sl, F & 3, (F >> 2) & 3, v);
+          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)sl * a.t.sstride, F & 3, (F >> 2) & 3, v);
       }
     }
   }
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_w(PassArgs a) {
           sl = gt_resolve<KW>(a.t, kc[r], b, w, false, cc, res);
         }
         if (res == R_HIT) {
-          Upd<PG>::template g<NW>(a.t.states, a.t.stride, (uint64_t)sl, 0, s_fd, ns, vc[r]);
+          Upd<PG>::template g<NW>(a.t.states, a.t.fstride, (uint64_t)sl * a.t.sstride, 0, s_fd, ns, vc[r]);
           c_hit++;
           continue;
         }
