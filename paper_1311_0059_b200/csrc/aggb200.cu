@@ -1218,8 +1218,9 @@ int setup_table(Handle* h) {
   // updates touch one sector of states instead of one per field (C4 / C3
   // hash_sort: random HBM sectors per record 3 -> 2)
   const int ns_t = std::max(1, h->cs.ds.ns);
-  const bool aos = h->unlimited && (double)slots * (8.0 * h->kw + 8.0 * ns_t) > 0.5 * 126e6 && ns_t <= 4 &&
-                   !getenv("AGGB_SOA_STATES");
+  const bool aos = ((h->unlimited && (double)slots * (8.0 * h->kw + 8.0 * ns_t) > 0.5 * 126e6) ||
+                    getenv("AGGB_AOS_ALL")) &&
+                   ns_t <= 4 && !getenv("AGGB_SOA_STATES");
   t.fstride = aos ? 1 : (uint64_t)slots + 1;
   t.sstride = aos ? (uint64_t)ns_t : 1;
   t.bmask = (uint64_t)(slots / (h->kw == 1 ? 4 : 2)) - 1;
