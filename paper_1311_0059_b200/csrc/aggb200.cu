@@ -493,9 +493,11 @@ child_fn child_kernel(int nwt, int prog) {
     case 1: return k_child<KW, 1, 2, PD>;
     case 2: return k_child<KW, 2, 2, PD>;
     case 4: return k_child<KW, 4, 2, PD>;
-    case 8: return k_child<KW, 8, 1, PD>;
-    case 16: return k_child<KW, 16, 1, PD>;
-    default: return k_child<KW, 32, 1, PD>;
+    // wide payloads (partial-state merges of wide specs: C5 hash_sort runs) take
+    // up to 128 registers at one CTA per SM: at 64 they spilled 200-1,360 bytes
+    case 8: return getenv("AGGB_CHILD_MINB2") ? k_child<KW, 8, 1, PD> : k_child<KW, 8, 1, PD, 1>;
+    case 16: return getenv("AGGB_CHILD_MINB2") ? k_child<KW, 16, 1, PD> : k_child<KW, 16, 1, PD, 1>;
+    default: return getenv("AGGB_CHILD_MINB2") ? k_child<KW, 32, 1, PD> : k_child<KW, 32, 1, PD, 1>;
   }
 }
 

@@ -737,8 +737,8 @@ struct ChildArgs {
 // (the child's budget: the reference's TABLE_FULL + freeze) waits until no
 // insert is in flight — the key set is then final — and re-probes: resident
 // keys aggregate in place, the rest go to the overflow list (next level).
-template <int KW, int NWT, int R, class PG>
-__global__ void __launch_bounds__(512, 2) k_child(ChildArgs a) {
+template <int KW, int NWT, int R, class PG, int MINB = 2>
+__global__ void __launch_bounds__(512, MINB) k_child(ChildArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x;
   const int nslots = 1 << a.slots_log2;
