@@ -47,6 +47,8 @@ class GpuCostParams:
     rand_sector_ns: float = 0.095  # per random table sector beyond L2 (fit: C4 hash_sort FILL)
     split_fanout: int = 2200       # partitions one spill pass writes (k_probe SMEM)
     item_us: float = 0.07          # per child item (table init + flush), C4 fit
+    destage_round_ms: float = 1.0  # dynamic_destaging: one destaging round (C2 fit)
+    shared_stage_ms: float = 3.5   # shared_hash: one overflow stage (C2 fit)
     cut_us: float = 60.0           # hash_sort: launches and flush per table cut (C5: ~1,190 cuts / 100M)
 
 
@@ -128,7 +130,14 @@ def model(algo: str, w: Workload, pm: GpuCostParams | None = None, child_groups:
             r.add("split", 2 * part, part, pm)
         r.add("child", part, out, pm)
         return r
-    # pre_partitioning / original_hh (and the ids that run their schedule)
+    # pre_partitioning / original_hh / the destaging schedules (same bytes; the
+    # destaging ids add host-driven rounds: flush, per-partition histogram,
+    # eviction, re-insert — fitted on C2: shared_hash 10.3 ms, dynamic_destaging 16 ms)
+    extra = 0.0
+    if algo == "dynamic_destaging" and w.groups > budget:
+        extra = math.ceil(4 * math.log2(w.groups / budget + 1)) * pm.destage_round_ms
+    elif algo == "shared_hash" and w.groups > budget:
+        extra = 2 * pm.shared_stage_ms
     if algo == "pre_partitioning" and budget == math.inf and w.groups * 2 * w.state_bytes > 0.4 * pm.l2_bytes \
             and w.hot_share < 0.4:
         budget = 65536  # in-memory plans beyond L2 run at an L2-sized table (k_probe + bloom)
@@ -146,11 +155,11 @@ def model(algo: str, w: Workload, pm: GpuCostParams | None = None, child_groups:
     # children: one CTA per (sub-)partition; small items pay their table init and
     # flush (C4 pre-partitioning at 1B: 1.57M items of ~640 records, child 65 ms)
     items = max(1.0, (w.groups - resident) / (0.4 * child_groups))
-    r.add("child", spill, out, pm, items * pm.item_us * 1e-3)
+    r.add("child", spill, out, pm, items * pm.item_us * 1e-3 + extra)
     return r
 
 
-ALGOS = ("pre_partitioning", "original_hh", "hash_sort", "sort_based")
+ALGOS = ("pre_partitioning", "original_hh", "shared_hash", "dynamic_destaging", "hash_sort", "sort_based")
 
 
 def select_algorithm_gpu(w: Workload, pm: GpuCostParams | None = None, algos=ALGOS) -> str:

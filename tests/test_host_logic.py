@@ -101,7 +101,8 @@ def test_choose_exchange_rule():
 # measured on B200 (profiles/r01_all_configs_full.jsonl, session 3), ms
 _MEASURED = {
     "C2": (dict(n=1e8, groups=1e6, rec_bytes=16, state_bytes=40, out_bytes=40, budget_groups=125000,
-                key_bits=20), {"pre_partitioning": 3.44, "original_hh": 5.51}),
+                key_bits=20), {"pre_partitioning": 3.44, "original_hh": 5.51, "shared_hash": 10.3,
+                               "dynamic_destaging": 16.2}),
     "C3s05": (dict(n=2e8, groups=1e7, state_bytes=24, out_bytes=32, key_bits=24),
               {"pre_partitioning": 9.09, "hash_sort": 26.7}),
     "C3s1": (dict(n=2e8, groups=8.9e6, state_bytes=24, out_bytes=32, key_bits=24, hot_share=0.16),
