@@ -123,9 +123,11 @@ def _check(cfg, algo):
     return met
 
 
-CASES = [("C2", "pre_partitioning", {}), ("C2", "original_hh", {}),
+CASES = [("C2", "pre_partitioning", {}), ("C2", "original_hh", {}), ("C2", "shared_hash", {}),
+         ("C2", "dynamic_destaging", {}),
          ("C3", "pre_partitioning", {"zipf_s": 0.5}), ("C3", "pre_partitioning", {"zipf_s": 1.0}),
-         ("C3", "pre_partitioning", {"zipf_s": 1.5}), ("C3", "hash_sort", {"zipf_s": 1.0}),
+         ("C3", "pre_partitioning", {"zipf_s": 1.5}), ("C3", "hash_sort", {"zipf_s": 0.5}),
+         ("C3", "hash_sort", {"zipf_s": 1.0}), ("C3", "hash_sort", {"zipf_s": 1.5}),
          ("C4", "sort_based", {}), ("C4", "hash_sort", {}),
          ("C5", "pre_partitioning", {}), ("C5", "hash_sort", {})]
 
