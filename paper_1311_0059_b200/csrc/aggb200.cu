@@ -590,6 +590,7 @@ struct Handle {
   bool hot_no_tier = false;  // the hot keys cover most records: no SMEM pre-aggregation tier
   int64_t skew_cap = 0;      // L2-capped plans: the capacity a heavily skewed push may use
   bool aos_planned = false;  // slot-major states planned (in-memory table beyond L2)
+  bool l0_deferred = false;  // level-0 metrics ride on the tail's read (finish without a round trip)
   bool first_push = true;
   int prog = 0;
   // blocked bloom filter of the frozen level-0 table (PROBE)
@@ -2464,9 +2465,28 @@ int aggb_finish(void* handle, aggb_result* out) {
     if (h->cfg.algo == AGGB_SORT_BASED) {
       TRY(aggb_sort_finish(h));
     } else {
+      const int algo0 = h->cfg.algo;
+      // No level-0 decision of these schedules depends on the device counters:
+      // flush without a round trip (the table holds at most tab.cap groups + the
+      // escape group, and nothing has been emitted yet); the two metrics the
+      // close reports travel to scratch slots 14/15 and come back with the
+      // tail's read (C2: one host round trip less per step)
+      const bool no_rt = (algo0 == AGGB_PRE_PARTITIONING || algo0 == AGGB_SHARED_HASH ||
+                          algo0 == AGGB_DYNAMIC_DESTAGING) && !getenv("AGGB_L0_ROUNDTRIP");
+      if (no_rt) {
+        CU(cudaMemcpyAsync(SC(h) + 14, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToDevice, h->st));
+        CU(cudaMemcpyAsync(SC(h) + 15, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToDevice, h->st));
+        TRY(ensure_out(h, (int64_t)h->tab.cap + 4));
+        OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+        TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
+        tr.mark(h->st, "finish: level-0 flush");
+        h->l0_deferred = true;
+        TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
+      }
       int frozen = 0, refused = 0;
       unsigned long long groups = 0, cnt0 = 0, sp0 = 0;
       // one round trip for everything the level-0 close needs
+      if (!no_rt) {
       CU(cudaMemcpyAsync(&frozen, &h->tab.hdr->frozen, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&refused, &h->tab.hdr->pad, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&groups, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToHost, h->st));
@@ -2521,18 +2541,28 @@ int aggb_finish(void* handle, aggb_result* out) {
       tr.mark(h->st, "finish: level-0 flush");
       h->met.level0_spilled_records = (int64_t)sp0;
       TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
+      }
     }
     unsigned long long cnt = 0, st[ST_NSTATS];
     uint32_t ovfl = 0;
+    unsigned long long l0[2] = {0, 0};  // deferred level-0 metrics (scratch 14, 15)
     if (h->tail_valid) {  // read by drain right after the last child pass
       cnt = h->tail_sc[13];
       memcpy(st, h->tail_sc, sizeof(st));
       ovfl = h->tail_ovfl;
+      l0[0] = h->tail_sc[14];
+      l0[1] = h->tail_sc[15];
     } else {
       CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(l0, SC(h) + 14, 16, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
+    }
+    if (h->l0_deferred) {
+      h->met.resident_groups = (int64_t)l0[0];
+      h->met.level0_spilled_records = (int64_t)l0[1];
+      h->l0_deferred = false;
     }
     if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
     if ((int64_t)cnt > h->out_cap) return fail(AGGB_CAPACITY_EXCEEDED, "output buffer overflow (%llu > %lld)", cnt, (long long)h->out_cap);
