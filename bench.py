@@ -452,8 +452,13 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "records/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sample / v * 1e3, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "algorithm": args.algo,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "int64" if cfg.value != "u01" else "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "algorithm": args.algo, "records_per_gpu": cfg.n,
+                       "global_records": cfg.n * world, "aggregates": list(cfg.aggs),
+                       "key_universe": cfg.key_range or cfg.zipf_k or cfg.k0_range * cfg.k1_range,
+                       "budget_groups": cfg.budget_groups or "in-memory",
+                       "parallelism": "host cores of rank 0",
                        "records_per_step": sample, "note": "bounded sample of the workload"},
             "cpu_baseline": {"value": round(v, 1), "unit": "records/s", "cores": threads,
                              "kind": "port",
