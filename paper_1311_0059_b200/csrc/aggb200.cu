@@ -101,6 +101,34 @@ struct DBuf {
   T* as() const { return (T*)p; }
 };
 
+// Pinned host staging for the planning round trips: the D2H copies queue
+// without the driver's pageable bounce (one blocking copy each) and complete
+// behind a single stream synchronize.
+struct HPin {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return AGGB_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    size_t nb = std::max(need + need / 4, (size_t)4096);
+    cudaError_t e = cudaHostAlloc(&p, nb, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return fail(AGGB_CUDA_ERROR, "cudaHostAlloc(%zu): %s", nb, cudaGetErrorString(e));
+    }
+    bytes = nb;
+    return AGGB_OK;
+  }
+  ~HPin() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* as() const { return (T*)p; }
+};
+
 // Spill page pool memory: one virtual address range reserved for twice the
 // device's memory, physical memory mapped onto its end as the pool grows (CUDA
 // VMM): HBM first, then pinned host memory once HBM is exhausted (SURVEY §8(f)
@@ -564,6 +592,7 @@ struct Handle {
   unsigned long long tail_sc[16] = {};      // scratch counters read after the last child pass
   uint32_t tail_ovfl = 0;
   bool tail_valid = false;
+  HPin hpin;  // pinned staging of the drain's planning reads
   // scratch: [0..7] stats, [8] tile counter A, [9] tile counter B, [10] defer count, [11] ovf count,
   // [12] item counter, [13] out count
   DBuf scratch;
@@ -1676,11 +1705,20 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     std::vector<uint32_t> pages(2 * (size_t)nparts, 0);
     uint32_t ovfl = 0;
     unsigned long long cnt_now = 0;  // output rows so far (the page scatter does not change it)
-    CU(cudaMemcpyAsync(recs.data(), h->part_records.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(pages.data(), h->part_pages.p, (size_t)nparts * 4 * nsets, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(&cnt_now, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
-    CU(cudaStreamSynchronize(h->st));
+    {
+      const size_t o_pages = (size_t)nparts * 8, o_cnt = o_pages + (size_t)nparts * 8, o_ovfl = o_cnt + 8;
+      TRY(h->hpin.ensure(o_ovfl + 8));
+      uint8_t* hp = h->hpin.as<uint8_t>();
+      CU(cudaMemcpyAsync(hp, h->part_records.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(hp + o_pages, h->part_pages.p, (size_t)nparts * 4 * nsets, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(hp + o_cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaMemcpyAsync(hp + o_ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+      CU(cudaStreamSynchronize(h->st));
+      memcpy(recs.data(), hp, (size_t)nparts * 8);
+      memcpy(pages.data(), hp + o_pages, (size_t)nparts * 4 * nsets);
+      memcpy(&cnt_now, hp + o_cnt, 8);
+      memcpy(&ovfl, hp + o_ovfl, 4);
+    }
     if (ovfl) return fail(AGGB_CAPACITY_EXCEEDED, "spill page pool overflowed");
     std::vector<uint32_t> offs(2 * (size_t)nparts);
     std::vector<int64_t> item_off;
@@ -1907,9 +1945,13 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     CU(cudaGetLastError());
     // one round trip: the overflow count, and (if this was the last level) the
     // counters aggb_finish reads next
-    CU(cudaMemcpyAsync(h->tail_sc, SC(h), sizeof(h->tail_sc), cudaMemcpyDeviceToHost, h->st));
-    CU(cudaMemcpyAsync(&h->tail_ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+    TRY(h->hpin.ensure(sizeof(h->tail_sc) + 8));
+    CU(cudaMemcpyAsync(h->hpin.p, SC(h), sizeof(h->tail_sc), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaMemcpyAsync(h->hpin.as<uint8_t>() + sizeof(h->tail_sc), h->pool_ctr.as<uint32_t>() + 1, 4,
+                       cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    memcpy(h->tail_sc, h->hpin.p, sizeof(h->tail_sc));
+    memcpy(&h->tail_ovfl, h->hpin.as<uint8_t>() + sizeof(h->tail_sc), 4);
     const unsigned long long novf = h->tail_sc[11];
     tr.mark(h->st, "drain: child");
     if (novf > (unsigned long long)h->ovf_cap)
