@@ -1707,7 +1707,7 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     unsigned long long cnt_now = 0;  // output rows so far (the page scatter does not change it)
     {
       const size_t o_pages = (size_t)nparts * 8, o_cnt = o_pages + (size_t)nparts * 8, o_ovfl = o_cnt + 8;
-      TRY(h->hpin.ensure(o_ovfl + 8));
+      TRY(h->hpin.ensure(o_ovfl + 8 + (size_t)nparts * 8 + ((size_t)2 * nparts + 1) * 8));  // + the plan's H2D
       uint8_t* hp = h->hpin.as<uint8_t>();
       CU(cudaMemcpyAsync(hp, h->part_records.p, (size_t)nparts * 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(hp + o_pages, h->part_pages.p, (size_t)nparts * 4 * nsets, cudaMemcpyDeviceToHost, h->st));
@@ -1742,8 +1742,16 @@ int drain(Handle* h, SetInfo a, bool a_live, SetInfo b, bool b_live, int level) 
     h->met.recursion_depth = std::max<int64_t>(h->met.recursion_depth, depth + 1);
     TRY(h->plist.ensure((size_t)tot * 8, &h->hw));
     TRY(h->item_off.ensure(item_off.size() * 8, &h->hw));
-    CU(cudaMemcpyAsync(h->cursor.p, offs.data(), (size_t)nparts * 4 * nsets, cudaMemcpyHostToDevice, h->st));
-    CU(cudaMemcpyAsync(h->item_off.p, item_off.data(), item_off.size() * 8, cudaMemcpyHostToDevice, h->st));
+    {
+      // staged behind the planning reads in the pinned buffer; its next host
+      // write comes after the child's synchronize, its next device write is
+      // stream-ordered after these copies
+      uint8_t* hp = h->hpin.as<uint8_t>() + (size_t)nparts * 16 + 16;
+      memcpy(hp, offs.data(), (size_t)nparts * 4 * nsets);
+      memcpy(hp + (size_t)nparts * 8, item_off.data(), item_off.size() * 8);
+      CU(cudaMemcpyAsync(h->cursor.p, hp, (size_t)nparts * 4 * nsets, cudaMemcpyHostToDevice, h->st));
+      CU(cudaMemcpyAsync(h->item_off.p, hp + (size_t)nparts * 8, item_off.size() * 8, cudaMemcpyHostToDevice, h->st));
+    }
     tr.mark(h->st, "drain: page hist + D2H");
     for (int q = 0; q < nsets; q++) {
       int pe = prof_begin(h, 7);
