@@ -375,14 +375,15 @@ def roofline(out, args, peak):
     steps = args.steps
     groups = {}
     # level-0 pass (FILL + PROBE / ROUTE): reads the batch, writes the spill
-    l0 = [k for k in ks if k.startswith("k_pass<") and "GRACE" not in k]
+    l0 = [k for k in ks if (k.startswith("k_pass<") and "GRACE" not in k) or k.startswith("k_probe_wc")]
     if l0:
         ms = sum(ks[k][1] for k in l0) / steps
         nl = sum(ks[k][0] for k in l0) / steps
         groups["level0_pass"] = (ms, nl, in_b * n + spill_rec * S)
-    if "k_child" in ks:
-        ms = ks["k_child"][1] / steps
-        nl = ks["k_child"][0] / steps
+    ch = [k for k in ("k_child", "k_child_wc") if k in ks]
+    if ch:
+        ms = sum(ks[k][1] for k in ch) / steps
+        nl = sum(ks[k][0] for k in ch) / steps
         groups["child_aggregate"] = (ms, nl, spill_rec * S + out_b * max(G - R, 0))
     if not groups:
         return None, {}

@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libaggb200.so")
+LIB_PATH = os.environ.get("AGGB_LIB_OVERRIDE") or os.path.join(HERE, "lib", "libaggb200.so")  # (experiment builds)
 HEADER = os.path.join(os.path.dirname(HERE), "include", "aggb200.h")
 
 AGGB_OK = 0

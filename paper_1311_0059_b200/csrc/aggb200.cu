@@ -23,6 +23,7 @@
 #include "pass.cuh"
 #include "probe.cuh"
 #include "sort.cuh"
+#include "wc.cuh"
 
 using namespace aggb;
 
@@ -629,6 +630,17 @@ struct Handle {
   int64_t ovf_cap = 0;
   // two-phase PROBE: candidate regions (bloom positives), open chains per (CTA, partition)
   DBuf cand, chains;
+  // write-combined level-0 PROBE + one-wave compact children (wc.cuh): planned
+  // for budgeted pre-partitioning of one-word keys and one int64 column with an
+  // integer COUNT/SUM(/MIN/MAX) spec; children find their pages through device
+  // page lists (no host round trip), a partition they cannot hold goes to drain
+  bool wc = false;
+  bool wc_used = false;       // some PROBE of this run went through k_probe_wc
+  uint32_t wc_nblk = 0;       // bloom blocks (64-bit)
+  int wc_table_bytes = 0;     // child shared-memory table
+  uint32_t wc_plist_cap = 0;  // page-list entries per partition
+  int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
+  DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_pos, wc_pos_count;
   // sort path
   DBuf sort_keys, sort_vals;
   int64_t sort_n = 0, sort_cap = 0;
@@ -644,14 +656,15 @@ struct Handle {
   struct Ev { int kid; cudaEvent_t a, b; };
   std::vector<Ev> evs;
   std::vector<cudaEvent_t> free_events;
-  double kms[16] = {0};
-  int64_t kcount[16] = {0};
+  double kms[24] = {0};
+  int64_t kcount[24] = {0};
 };
 
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
-                        "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>", "k_split"};
-constexpr int NKINDS = 15;
+                        "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>", "k_split",
+                        "k_probe_wc<scan>", "k_probe_wc<resolve>", "k_child_wc"};
+constexpr int NKINDS = 18;
 
 int prof_begin(Handle* h, int kid) {
   if (!h->prof) return -1;
@@ -1096,6 +1109,7 @@ ColSrc col_of(Handle* h, const aggb_input* in, const void* const* kptr, const vo
 // planning
 // ---------------------------------------------------------------------------
 
+void wc_plan(Handle* h, double spill_groups);
 int plan(Handle* h) {
   const aggb_config& c = h->cfg;
   int M = c.memory_frames;
@@ -1240,7 +1254,49 @@ int plan(Handle* h) {
   h->P0 = std::min(P, cap_parts);
   if (getenv("AGGB_P0")) h->P0 = atoi(getenv("AGGB_P0"));  // experiment override
   h->fanout_need = (int64_t)h->P0 * h->nsub0;
+  wc_plan(h, spill_groups);
   return AGGB_OK;
+}
+
+// The write-combined level-0 path (wc.cuh) for budgeted pre-partitioning of
+// one-word keys and one int64 value column with an integer COUNT/SUM/MIN/MAX
+// spec.  Its children are one CTA per SM with a compact table (u32 states) in
+// shared memory, run in whole waves: the fan-out is the smallest multiple of
+// the SM count that leaves every child table at most ~40% full, and it must
+// leave the level-0 pass room for its bloom filter (>= 2 bits per resident key).
+// scan: 4 records per thread per tile, double-buffered stages (per-tile
+// overhead halved: C2 scan 1.64 -> 1.36 ms against 2 per thread x 3 stages);
+// resolve (no bloom in shared memory): 2 x 3
+constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_RR = 2, WC_RNS = 3, WC_LINES = 2, WC_CBLK = 1024, WC_CRL = 4;
+using WcL = WcLayout<WC_BLK, WC_R, WC_NS, WC_LINES>;
+using WcLR = WcLayout<WC_BLK, WC_RR, WC_RNS, WC_LINES>;
+void wc_plan(Handle* h, double spill_groups) {
+  h->wc = false;
+  const aggb_config& c = h->cfg;
+  if (c.algo != AGGB_PRE_PARTITIONING || h->kw != 1 || h->cs.nv != 1 || (h->prog != 1 && h->prog != 2) ||
+      h->unlimited || h->l2_capped || c.level != 0 || h->cs.ds.vty[0] != TY_I64 || getenv("AGGB_NO_WC") ||
+      getenv("AGGB_FORCE_L2_CHILDREN"))
+    return;
+  const int words = 2 + (h->prog == 2 ? 4 : 2);  // key, count word, one u32 per other field
+  const int tbytes = 220 * 1024;
+  const int nslots = ((tbytes / 4 - 2) / words - 1) / 4 * 4;
+  const int sms = std::max(1, h->sms);
+  int P = (int)std::ceil(std::max(1.0, spill_groups) / (0.4 * nslots));
+  P = (P + sms - 1) / sms * sms;
+  if (getenv("AGGB_WC_P0")) P = std::max(1, atoi(getenv("AGGB_WC_P0")));  // experiment override
+  const size_t fixed = WcL::bytes(P, 0) + 1024;
+  if (fixed >= 227 * 1024) return;
+  const int64_t want = std::max<int64_t>(64, (int64_t)(8 * h->budget) / 64);  // ~8 bits per resident key
+  const int64_t room = (int64_t)((227 * 1024 - fixed) / 8);
+  const int64_t nblk = std::min(want, room);
+  if (nblk < std::max<int64_t>(16, (int64_t)(2 * h->budget) / 64)) return;
+  h->wc = true;
+  h->wc_nblk = (uint32_t)nblk;
+  h->wc_table_bytes = tbytes;
+  h->P0 = P;
+  h->nsub0 = 1;
+  h->fanout_need = P;
+  h->l2_children = false;
 }
 
 int setup_table(Handle* h) {
@@ -1328,6 +1384,21 @@ int begin_run(Handle* h) {
     h->dd_evictions = 0;
   }
   if (h->has_table) TRY(table_reset(h));
+  h->wc_used = false;
+  if (h->wc) {
+    const size_t P = (size_t)h->P0;
+    TRY(h->wc_pn.ensure(P * 4, &h->hw));
+    TRY(h->wc_recs.ensure(P * 8, &h->hw));
+    TRY(h->wc_failed.ensure(P * 4, &h->hw));
+    TRY(h->wc_vinfo.ensure(8, &h->hw));
+    TRY(h->wc_fail.ensure(8, &h->hw));
+    TRY(h->wc_bloom.ensure((size_t)h->wc_nblk * 8, &h->hw));
+    CU(cudaMemsetAsync(h->wc_pn.p, 0, P * 4, h->st));
+    CU(cudaMemsetAsync(h->wc_recs.p, 0, P * 8, h->st));
+    CU(cudaMemsetAsync(h->wc_failed.p, 0, P * 4, h->st));
+    CU(cudaMemsetAsync(h->wc_vinfo.p, 0, 8, h->st));
+    CU(cudaMemsetAsync(h->wc_fail.p, 0, 8, h->st));
+  }
   return AGGB_OK;
 }
 
@@ -1391,6 +1462,106 @@ int ensure_defer(Handle* h, int64_t T, int payload_words) {
 
 int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss);
 
+// k_probe_wc reads the key and value columns with 16-byte bulk copies
+bool wc_eligible(Handle* h, const ColSrc& col) {
+  return col.nv == 1 && dense8(col, 1) && col.kty[0] == TY_I64 && col.vty[0] == TY_I64 &&
+         ((uintptr_t)col.key[0] & 15) == 0 && ((uintptr_t)col.val[0] & 15) == 0 && !h->hot_ready &&
+         h->pool_bound + (uint64_t)(col.n + h->defer_cap) / 256 + (uint64_t)h->sms * (4ull * h->P0 + 128) < 0xFFFFF0ull;
+}
+
+// PROBE through k_probe_wc (partition half) + k_resolve_wc (the bloom positives)
+int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
+  const int P = ss.nparts;
+  const int grid = h->sms;
+  const int64_t T = WcL::T;
+  // the filter of the table as FILL left it (a kernel boundary: the key set is final once frozen)
+  CU(cudaMemsetAsync(h->wc_bloom.p, 0, (size_t)h->wc_nblk * 8, h->st));
+  int pe = prof_begin(h, 12);
+  k_bloom_build_wc<<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->wc_bloom.as<uint64_t>(), h->wc_nblk);
+  prof_end(h, pe);
+  h->launches++;
+  const int64_t nlin_cap = h->defer_cap;
+  // bloom positives: one region per CTA, room for every record it may read
+  const int64_t tiles = (col.n + T - 1) / T + (nlin_cap + T - 1) / T;
+  const int64_t stride = ((tiles + grid - 1) / grid + 1) * T;
+  TRY(h->wc_pos.ensure((size_t)stride * grid * 16, &h->hw));
+  TRY(h->wc_pos_count.ensure((size_t)grid * 8, &h->hw));
+  // page lists: every record of the run so far, at twice the mean pages per partition
+  const int64_t recs_run = h->records + col.n + nlin_cap;
+  const uint32_t need_cap = (uint32_t)std::min<int64_t>(
+      0x7FFFFFFF, 2 * (recs_run / 512 / std::max(1, P)) + 4 * (int64_t)grid + 64);
+  if (need_cap > h->wc_plist_cap) {
+    DBuf nb;
+    TRY(nb.ensure((size_t)P * need_cap * 4, &h->hw));
+    if (h->wc_used && h->wc_plist_cap)
+      CU(cudaMemcpy2DAsync(nb.p, (size_t)need_cap * 4, h->wc_plist.p, (size_t)h->wc_plist_cap * 4,
+                           (size_t)h->wc_plist_cap * 4, (size_t)P, cudaMemcpyDeviceToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    h->wc_plist.release();
+    h->wc_plist = nb;
+    nb.p = nullptr;
+    h->wc_plist_cap = need_cap;
+  }
+  // pages: the records, plus each (CTA, partition) chain's last page, plus stashes
+  const int stash = 32;
+  const uint64_t pages = (uint64_t)((col.n + nlin_cap) / 512) + 2ull * grid * P + 4ull * grid * stash + 64;
+  TRY(pool_ensure(h, pages));
+  WcArgs a;
+  memset(&a, 0, sizeof(a));
+  a.sp = h->cs.ds;
+  a.t = h->tab;
+  a.key = (const unsigned long long*)col.key[0];
+  a.val = (const unsigned long long*)col.val[0];
+  a.n = col.n;
+  a.start_tiles = SC(h) + 8;
+  a.start_T = 0;
+  {
+    int nwt = nwt_for(std::max(1, col.nv));
+    PassCfg pcfg = pass_kernel<1>(nwt, h->prog);
+    a.start_T = (int64_t)pcfg.R * pcfg.blk;  // FILL's tile
+  }
+  a.lkey = (const unsigned long long*)h->defer.as<uint64_t>();
+  a.lval = (const unsigned long long*)(h->defer.as<uint64_t>() + h->defer_cap);
+  a.lcount = SC(h) + 10;
+  a.bloom = h->wc_bloom.as<uint64_t>();
+  a.nblk = h->wc_nblk;
+  a.pool = pool_of(h);
+  a.ss = ss;
+  a.plist = h->wc_plist.as<uint32_t>();
+  a.plist_n = h->wc_pn.as<uint32_t>();
+  a.plist_cap = h->wc_plist_cap;
+  a.part_recs = h->wc_recs.as<unsigned long long>();
+  a.tile_counter = SC(h) + 20;
+  a.stats = SC(h);
+  a.vinfo = h->wc_vinfo.as<unsigned int>();
+  a.fail = h->wc_fail.as<uint32_t>();
+  a.stash = stash;
+  a.pos = h->wc_pos.as<uint64_t>();
+  a.pos_stride = stride;
+  a.pos_count = h->wc_pos_count.as<unsigned long long>();
+  a.pos_regions = grid;
+  a.dbg = getenv("AGGB_WC_DBG") ? atoi(getenv("AGGB_WC_DBG")) : 0;
+  a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
+  auto fs = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>
+                         : k_probe_wc<ProgC1, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>;
+  auto fr = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_RR, WC_RNS, WC_LINES, WC_RESOLVE>
+                         : k_probe_wc<ProgC1, WC_BLK, WC_RR, WC_RNS, WC_LINES, WC_RESOLVE>;
+  const size_t smem = WcL::bytes(P, h->wc_nblk), rsmem = WcLR::bytes(P, 0);
+  CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CU(cudaFuncSetAttribute((const void*)fr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+  pe = prof_begin(h, 15);
+  fs<<<grid, WC_BLK, smem, h->st>>>(a);
+  prof_end(h, pe);
+  CU(cudaGetLastError());
+  pe = prof_begin(h, 16);
+  fr<<<grid, WC_BLK, rsmem, h->st>>>(a);
+  prof_end(h, pe);
+  CU(cudaGetLastError());
+  h->launches += 2;
+  h->wc_used = true;
+  return AGGB_OK;
+}
+
 int push_hybrid(Handle* h, const ColSrc& col) {
   int algo = h->cfg.algo;
   unsigned long long* ctrA = SC(h) + 8;
@@ -1445,6 +1616,8 @@ int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss) {
   f.col_kind = col_kind;
   f.counter = ctrA;
   TRY(launch_pass(h, f));
+  // PROBE the remainder and the deferred records against the frozen table.
+  if (h->wc && col_kind == 0 && ss.id == h->raw0.ss.id && wc_eligible(h, col)) return wc_probe(h, col, ss);
   // PROBE the remainder and the deferred records against the frozen table.
   // The filter is rebuilt from the table as it stands after FILL (a kernel boundary, so
   // the key set is final once frozen); while the table is not frozen PROBE has no work.
@@ -2505,6 +2678,50 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   return AGGB_OK;
 }
 
+// the children of the write-combined level 0 (k_child_wc): one wave per SM
+// count of partitions, pages found through the device page lists
+int wc_children(Handle* h) {
+  CwArgs ca;
+  memset(&ca, 0, sizeof(ca));
+  ca.sp = h->cs.ds;
+  ca.pool = pool_of(h);
+  ca.plist = h->wc_plist.as<uint32_t>();
+  ca.plist_n = h->wc_pn.as<uint32_t>();
+  ca.plist_cap = h->wc_plist_cap;
+  ca.part_recs = h->wc_recs.as<unsigned long long>();
+  ca.vinfo = h->wc_vinfo.as<unsigned int>();
+  ca.P = h->raw0.ss.nparts;
+  ca.table_bytes = h->wc_table_bytes;
+  if (getenv("AGGB_WC_CHILD_KB"))  // test hook: small child tables send partitions to the fallback
+    ca.table_bytes = std::max(4, std::min(h->wc_table_bytes / 1024, atoi(getenv("AGGB_WC_CHILD_KB")))) * 1024;
+  ca.seed = level_seed(h->cfg.seed, SALT_SLOT, h->cfg.level + 1);
+  ca.out = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+  ca.failed = h->wc_failed.as<uint32_t>();
+  ca.fail = h->wc_fail.as<uint32_t>();
+  ca.stats = SC(h);
+  auto fc = h->prog == 2 ? k_child_wc<CpC2, WC_CBLK, WC_CRL> : k_child_wc<CpC1, WC_CBLK, WC_CRL>;
+  CU(cudaFuncSetAttribute((const void*)fc, cudaFuncAttributeMaxDynamicSharedMemorySize, h->wc_table_bytes));
+  int pe = prof_begin(h, 17);
+  fc<<<std::min(h->sms, ca.P), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
+  prof_end(h, pe);
+  CU(cudaGetLastError());
+  h->launches++;
+  return AGGB_OK;
+}
+
+// a partition k_child_wc could not hold (more groups than its table, rows past
+// the output estimate, an overflowed page list): retire the completed ones'
+// pages and let drain recurse on the rest
+int wc_fallback(Handle* h) {
+  k_wc_retire<<<std::max(1, std::min(h->raw0.ss.nparts, h->sms * 4)), 256, 0, h->st>>>(
+      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, h->wc_failed.as<uint32_t>(),
+      h->raw0.ss.nparts, h->page_set.as<int32_t>());
+  CU(cudaGetLastError());
+  h->launches++;
+  h->tail_valid = false;
+  return drain(h, h->raw0, true, h->part0, h->part0_live, h->cfg.level);
+}
+
 int aggb_finish(void* handle, aggb_result* out) {
   Handle* h = (Handle*)handle;
   if (!h || !out) return fail(AGGB_INVALID_ARG, "null argument");
@@ -2526,12 +2743,20 @@ int aggb_finish(void* handle, aggb_result* out) {
       if (no_rt) {
         CU(cudaMemcpyAsync(SC(h) + 14, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToDevice, h->st));
         CU(cudaMemcpyAsync(SC(h) + 15, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToDevice, h->st));
-        TRY(ensure_out(h, (int64_t)h->tab.cap + 4));
+        // (k_child_wc: rows for the expected groups; a partition past them falls back to drain)
+        const int64_t wc_rows =
+            h->wc_used ? (int64_t)std::min<double>((double)h->records, std::max(2.0 * h->cfg.stats_G_t, 1.0e6)) : 0;
+        TRY(ensure_out(h, (int64_t)h->tab.cap + 4 + wc_rows));
         OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
         TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
         tr.mark(h->st, "finish: level-0 flush");
         h->l0_deferred = true;
-        TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
+        if (h->wc_used) {
+          TRY(wc_children(h));
+          tr.mark(h->st, "finish: wc children");
+        } else {
+          TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
+        }
       }
       int frozen = 0, refused = 0;
       unsigned long long groups = 0, cnt0 = 0, sp0 = 0;
@@ -2603,11 +2828,26 @@ int aggb_finish(void* handle, aggb_result* out) {
       l0[0] = h->tail_sc[14];
       l0[1] = h->tail_sc[15];
     } else {
+      uint32_t wcf = 0;
       CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(l0, SC(h) + 14, 16, cudaMemcpyDeviceToHost, h->st));
+      if (h->wc_used) CU(cudaMemcpyAsync(&wcf, h->wc_fail.p, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
+      if (wcf & 2u) return fail(AGGB_CUDA_ERROR, "k_probe_wc: page map inconsistency (internal error)");
+      if (h->wc_used) {
+        h->met.recursion_depth = std::max<int64_t>(h->met.recursion_depth, st[ST_SPILLED] ? 1 : 0);
+        h->met.spilled_partitions += st[ST_SPILLED] ? h->raw0.ss.nparts : 0;
+      }
+      if (wcf) {  // some partition did not fit k_child_wc: the generic recursion takes it
+        TRY(wc_fallback(h));
+        h->wc_fallbacks++;
+        CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
+        CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaStreamSynchronize(h->st));
+      }
     }
     if (h->l0_deferred) {
       h->met.resident_groups = (int64_t)l0[0];

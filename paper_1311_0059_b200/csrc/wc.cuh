@@ -75,6 +75,51 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(m))
                : "memory");
 }
+// one 128-byte (or any 16-byte multiple) shared -> global bulk copy by the TMA engine
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+// bring a global range into L2 ahead of its bulk copy into shared memory (no
+// shared memory held: the stages then wait on L2, not DRAM, latency)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// generic-proxy shared-memory writes before async-proxy (bulk copy) reads of them
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// shared memory through 32-bit addresses (a generic pointer costs an address-space
+// conversion per access, and the compiler wraps generic atomics in a warp
+// aggregation it cannot prove unnecessary)
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint64_t x, uint64_t y) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint16_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+  return r;
+}
+// one 32-byte table bucket with a single 256-bit load (LDG.E.ENL2.256: one L1TEX
+// wavefront per lane instead of two for a pair of 16-byte loads)
+__device__ __forceinline__ void ld_bucket32(const uint64_t* p, ulonglong2& x, ulonglong2& y) {
+  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(x.x), "=l"(x.y), "=l"(y.x), "=l"(y.y)
+               : "l"(p));
+}
 __device__ __forceinline__ void st_v2(void* p, ulonglong2 v) {
   asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v.x), "l"(v.y) : "memory");
 }
@@ -125,46 +170,59 @@ struct WcArgs {
   unsigned long long* part_recs;          // [P] records spilled per partition
   unsigned long long* tile_counter;
   unsigned long long* stats;              // ST_* counters
-  long long* vrange;                      // [0] min, [1] max of the spilled values (int64 columns)
+  unsigned int* vinfo;                    // [0] some probed value is outside int32, [1] max |v| (int64 columns)
   uint32_t* fail;                         // page list overflow / page map error
   int32_t stash;                          // pages per CTA stash refill
+  // bloom positives: WC_SCAN writes CTA c's keys to pos[c * pos_stride ...] and
+  // values pos_regions * pos_stride words further, their number to pos_count[c];
+  // WC_RESOLVE reads them
+  uint64_t* pos;
+  int64_t pos_stride;
+  unsigned long long* pos_count;
+  int32_t pos_regions;
+  int32_t pf;   // L2 prefetch of the batch tiles ahead
+  int32_t dbg;  // measurement hook (WC_RESOLVE): 1 no spills, 2 no REDs/spills, 3 no probe (wrong results)
 };
 
-template <int BLK, int NS, int LINES>
+template <int BLK, int R, int NS, int LINES>
 struct WcLayout {
-  static constexpr int T = BLK;  // records per tile: one per thread
+  static constexpr int T = BLK * R;
   static constexpr int RING = LINES * 8;
   static constexpr int NE = 8;
-  // bytes: stages, ring, bloom + bit patterns, cnt + lb + page maps
+  // bytes: stages, ring, bloom + bit patterns, cnt + lb + page maps, positive index list
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
   static __host__ __device__ size_t ring_bytes(int P) { return (size_t)P * RING * 16; }
   static __host__ __device__ size_t meta_bytes(int P) { return ((size_t)P * (2 + NE) * 4 + 15) & ~(size_t)15; }
   static __host__ __device__ size_t bytes(int P, uint32_t nblk) {
-    return stage_bytes() + ring_bytes(P) + (size_t)(nblk + WC_NPAT) * 8 + meta_bytes(P);
+    return stage_bytes() + ring_bytes(P) + (size_t)(nblk + WC_NPAT) * 8 + meta_bytes(P) + (size_t)T * 2;
   }
 };
 
-// One CTA per SM, one record per thread per tile.  Per tile:
-//   [A] wait for the stage; resolve the lane's carried bloom positive (its
-//       bucket arrived during the last tile): hit -> REDs, miss -> spill; then
-//       the lane's new record: hash -> bloom -> positive (issue its bucket
-//       loads, carry it) or spill (claim x in its partition's chain; window
-//       records into the ring, others held in registers);
-//   barrier 1 (stage consumed -> its next tile is issued; claims visible);
-//   [B] every complete line of every window is copied out (8 lanes x 16 B per
-//       line); held records of complete lines go straight to their page, those
-//       of the open line are parked for the next tile; windows move on;
-//   barrier 2 (the ring lines are out before the next tile writes the ring).
-template <class PG, int BLK, int NS, int LINES>
+// k_probe_wc<MODE>: level-0 PROBE in two launches of one kernel.
+//   WC_SCAN    the batch: hash -> bloom.  A positive (resident key or filter
+//              false positive) is copied, coalesced, to this CTA's positive
+//              region (SoA); any other record spills.
+//   WC_RESOLVE the positive regions: every record probes the frozen table (its
+//              first bucket loads are issued for all R records at once): a hit
+//              aggregates with L2 REDs, a miss (filter false positive) spills.
+// A spill claims chain position x of its partition (one shared atomic): inside
+// the partition's window -> the ring (the claimer of a line's 8th slot owns the
+// line), beyond -> held in registers.  Per tile: [A] classify + claims;
+// barrier 1; [B] owned lines leave as 128-byte bulk copies (UBLKCP), held
+// records of complete lines go straight to their page, those of the open line
+// are parked for the next tile, windows move on; barrier 2 (ring, positive
+// list and stage free again; the stage's next tile is issued).
+constexpr int WC_SCAN = 0, WC_RESOLVE = 1;
+constexpr int WC_PF = 6;  // k_probe_wc: L2 prefetch distance in tiles (rounds of the grid)
+template <class PG, int BLK, int R, int NS, int LINES, int MODE>
 __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
-  using L = WcLayout<BLK, NS, LINES>;
+  using L = WcLayout<BLK, R, NS, LINES>;
   constexpr int T = L::T, RING = L::RING, NE = L::NE;
   constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
-  constexpr int NWARP = BLK / 32;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
   const int P = a.ss.nparts;
-  const uint32_t nblk = a.nblk;
+  const uint32_t nblk = MODE == WC_SCAN ? a.nblk : 0u;
   unsigned long long* stg = (unsigned long long*)smem;
   ulonglong2* ring = (ulonglong2*)(smem + L::stage_bytes());
   uint64_t* sbloom = (uint64_t*)(smem + L::stage_bytes() + L::ring_bytes(P));
@@ -172,18 +230,36 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   uint32_t* cnt = (uint32_t*)(spat + WC_NPAT);
   uint32_t* lb = cnt + P;
   uint32_t* ent = lb + P;
+  uint16_t* plist_t = (uint16_t*)((unsigned char*)cnt + L::meta_bytes(P));  // this tile's positives (stage indices)
+  // 32-bit shared addresses of the same arrays (the hot loop's accesses)
+  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_bloom = smem_u32(sbloom),
+                 a_pat = smem_u32(spat), a_cnt = smem_u32(cnt), a_lb = smem_u32(lb), a_pl = smem_u32(plist_t);
   __shared__ __align__(8) uint64_t mbar[NS];
   __shared__ int s_tcnt[NS];
+  __shared__ uint32_t s_npos;
   __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv;
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_cnt[ST_NSTATS];
+  __shared__ unsigned long long s_maxch;
 
+  // inputs.  WC_SCAN: the batch rows [col_start, n), then FILL's deferral list.
+  // WC_RESOLVE: region g holds pos_count[g] positives; tile = g * maxch + chunk.
   const int64_t n = a.n;
-  const int64_t col_start =
-      a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
-  const int64_t col_tiles = (n - col_start + T - 1) / T;
-  const int64_t nlin = a.lcount ? (int64_t)*a.lcount : 0;
-  const unsigned long long total = (unsigned long long)(col_tiles + (nlin + T - 1) / T);
+  int64_t col_start = 0, col_tiles = 0, nlin = 0;
+  unsigned long long total = 0, maxch = 0;
+  if constexpr (MODE == WC_SCAN) {
+    col_start = a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
+    col_tiles = (n - col_start + T - 1) / T;
+    nlin = a.lcount ? (int64_t)*a.lcount : 0;
+    total = (unsigned long long)(col_tiles + (nlin + T - 1) / T);
+  } else {
+    if (tid == 0) s_maxch = 0;
+    __syncthreads();
+    for (int g = tid; g < a.pos_regions; g += BLK) atomicMax(&s_maxch, (a.pos_count[g] + T - 1) / T);
+    __syncthreads();
+    maxch = s_maxch;
+    total = maxch * (unsigned long long)a.pos_regions;
+  }
 
   const int ns = a.sp.ns;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
@@ -191,32 +267,47 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   for (int p = tid; p < P; p += BLK) cnt[p] = lb[p] = 0;
   for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
   for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom + i);
-  for (int i = tid; i < WC_NPAT; i += BLK) spat[i] = wc_pattern((uint32_t)i);
+  if (MODE == WC_SCAN)
+    for (int i = tid; i < WC_NPAT; i += BLK) spat[i] = wc_pattern((uint32_t)i);
   if (tid == 0) {
+    s_npos = 0;
     s_sb = s_su = s_sc = s_nb = s_nv = 0;
     for (int s = 0; s < NS; s++) mbar_init(&mbar[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
 
-  // producer (thread 0): tiles round-robin over the CTAs (uniform work per tile;
-  // no returning global atomic on the barrier's path)
+  // producer (thread 0): tiles round-robin over the CTAs (no returning global
+  // atomic on the barrier's path); WC_RESOLVE skips the empty chunks of short regions
   unsigned long long next_tile = blockIdx.x;
   auto issue = [&](int s) {
-    const unsigned long long tile = next_tile;
-    next_tile += gridDim.x;
     int c = 0;
     const unsigned long long *kp = nullptr, *vp = nullptr;
-    if (tile < (unsigned long long)col_tiles) {
-      const int64_t b = col_start + (int64_t)tile * T;
-      c = (int)(n - b < (int64_t)T ? n - b : (int64_t)T);
-      kp = a.key + b;
-      vp = a.val + b;
-    } else if (tile < total) {
-      const int64_t b = (int64_t)(tile - col_tiles) * T;
-      c = (int)(nlin - b < (int64_t)T ? nlin - b : (int64_t)T);
-      kp = a.lkey + b;
-      vp = a.lval + b;
+    while (next_tile < total) {
+      const unsigned long long tile = next_tile;
+      next_tile += gridDim.x;
+      if constexpr (MODE == WC_SCAN) {
+        if (tile < (unsigned long long)col_tiles) {
+          const int64_t b = col_start + (int64_t)tile * T;
+          c = (int)(n - b < (int64_t)T ? n - b : (int64_t)T);
+          kp = a.key + b;
+          vp = a.val + b;
+        } else {
+          const int64_t b = (int64_t)(tile - col_tiles) * T;
+          c = (int)(nlin - b < (int64_t)T ? nlin - b : (int64_t)T);
+          kp = a.lkey + b;
+          vp = a.lval + b;
+        }
+      } else {
+        const unsigned long long g = tile / maxch;
+        const int64_t b = (int64_t)(tile - g * maxch) * T;
+        const int64_t np = (int64_t)a.pos_count[g];
+        if (b >= np) continue;
+        c = (int)(np - b < (int64_t)T ? np - b : (int64_t)T);
+        kp = (const unsigned long long*)a.pos + (size_t)g * a.pos_stride + b;
+        vp = kp + (size_t)a.pos_regions * a.pos_stride;
+      }
+      break;
     }
     s_tcnt[s] = c;
     unsigned long long* sk = stg + (size_t)s * 2 * T;
@@ -232,6 +323,17 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       bulk_g2s(sv, vp, (uint32_t)c2 * 8u, &mbar[s]);
     } else {
       mbar_arrive(&mbar[s]);
+    }
+    if constexpr (MODE == WC_SCAN) {  // the tile WC_PF rounds ahead into L2
+      const unsigned long long pt = next_tile + (unsigned long long)(WC_PF - 1) * gridDim.x;
+      if (a.pf && pt < (unsigned long long)col_tiles) {
+        const int64_t b = col_start + (int64_t)pt * T;
+        const uint32_t cb = (uint32_t)((n - b < (int64_t)T ? n - b : (int64_t)T) & ~1ll) * 8u;
+        if (cb) {
+          bulk_prefetch_l2(a.key + b, cb);
+          bulk_prefetch_l2(a.val + b, cb);
+        }
+      }
     }
   };
   if (tid == 0)
@@ -270,34 +372,43 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     ent[p * NE + (j & (NE - 1))] = (pg << 8) | (j & 0xFFu);
   };
 
-  // the lane's bloom positive in flight (bucket loads issued, resolved next tile)
-  bool cf = false;
-  uint64_t ck = 0, cv = 0;
-  uint32_t cb = 0;
-  int cp = 0;
-  ulonglong2 cx = make_ulonglong2(0, 0), cy = cx;
-  // records beyond their window: pending (after barrier 1) / parked (open line, next tile)
-  uint32_t opend = 0, opark = 0;
-  uint32_t ox[2] = {0, 0};
-  int op[2] = {0, 0};
-  uint64_t okk[2] = {0, 0}, ovv[2] = {0, 0};
-  long long vlo = LLONG_MAX, vhi = LLONG_MIN;
-  uint32_t c_hit = 0, c_rec = 0, c_sp = 0;
-  uint32_t nb_pending = 0;  // thread 0: next stash base in flight
+  uint32_t opend = 0, opark = 0, lf = 0;
+  uint32_t xs[R];
+  int ps[R];
+  uint64_t hk[R], hv[R];  // held records (beyond the window)
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    xs[r] = 0;
+    ps[r] = 0;
+    hk[r] = hv[r] = 0;
+  }
+  uint32_t vbad = 0, vabs = 0;  // value range of the probed records (compact children)
+  uint32_t c_rec = 0, c_sp = 0, c_hit = 0;
+  unsigned long long pcur = 0;  // WC_SCAN: positives written to this CTA's region
+  uint32_t nb_pending = 0;      // thread 0: next stash base in flight
   bool nb_busy = false;
 
   auto spill = [&](uint64_t k, uint64_t v, int p, int q) {
     c_sp++;
-    const uint32_t x = atomicAdd(&cnt[p], 1u);
+    if (MODE == WC_SCAN && a.dbg == 4) {
+      vabs ^= (uint32_t)(k ^ v) + p;
+      return;
+    }
+    const uint32_t x = atoms_add(a_cnt + 4u * (uint32_t)p, 1u);
+    if (MODE == WC_SCAN && a.dbg == 5) {
+      vabs ^= x;
+      return;
+    }
     if (__builtin_expect((x & (S - 1)) == 0, 0)) alloc_page(p, x >> SLOG);
-    if (__builtin_expect(x < lb[p] + RING, 1)) {
-      ring[p * RING + (x & (RING - 1))] = make_ulonglong2(k, v);
+    xs[q] = x;
+    ps[q] = p;
+    if (__builtin_expect(x < lds32(a_lb + 4u * (uint32_t)p) + RING, 1)) {
+      sts128(a_ring + 16u * ((uint32_t)p * RING + (x & (RING - 1))), k, v);
+      lf |= (uint32_t)((x & 7u) == 7u && (MODE != WC_SCAN || a.dbg != 6)) << q;  // this thread sends the line after barrier 1
     } else {
       opend |= 1u << q;
-      ox[q] = x;
-      op[q] = p;
-      okk[q] = k;
-      ovv[q] = v;
+      hk[q] = k;
+      hv[q] = v;
     }
   };
 
@@ -312,71 +423,119 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     // ---- [A1] parked open-line records of the last tile into the ring
     if (__builtin_expect(opark != 0, 0)) {
 #pragma unroll
-      for (int q = 0; q < 2; q++)
-        if ((opark >> q) & 1u) ring[op[q] * RING + (ox[q] & (RING - 1))] = make_ulonglong2(okk[q], ovv[q]);
+      for (int r = 0; r < R; r++)
+        if ((opark >> r) & 1u) ring[ps[r] * RING + (xs[r] & (RING - 1))] = make_ulonglong2(hk[r], hv[r]);
       opark = 0;
     }
-    // ---- [A2] the carried positive
-    if (cf) {
-      int64_t sl = -1;
-      if (ck == EMPTY) {
-        if (*(volatile int*)&a.t.hdr->esc) sl = (int64_t)a.t.mask + 1;
-      } else {
-        uint64_t b = cb;
-        ulonglong2 x = cx, y = cy;
-        for (;;) {
-          if (x.x == ck) { sl = (int64_t)(b * 4); break; }
-          if (x.y == ck) { sl = (int64_t)(b * 4 + 1); break; }
-          if (y.x == ck) { sl = (int64_t)(b * 4 + 2); break; }
-          if (y.y == ck) { sl = (int64_t)(b * 4 + 3); break; }
-          if ((x.x == EMPTY) | (x.y == EMPTY) | (y.x == EMPTY) | (y.y == EMPTY)) break;
-          b = (b + 1) & a.t.bmask;
-          const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(a.t.keys + b * 4);
-          x = __ldcg(pp);
-          y = __ldcg(pp + 1);
-        }
-      }
-      if (sl >= 0) {
-        const uint64_t vv[1] = {cv};
-        Upd<PG>::template g<1>(a.t.states, a.t.fstride, (uint64_t)sl * a.t.sstride, 0, s_fd, ns, vv);
-        c_hit++;
-      } else {
-        spill(ck, cv, cp, 0);
-      }
-      cf = false;
+    // ---- [A2] this tile's records
+    const unsigned long long* sk = stg + (size_t)s * 2 * T;
+    const unsigned long long* sv = sk + T;
+    const uint32_t a_sk = a_stg + (uint32_t)s * 2u * T * 8u, a_sv = a_sk + T * 8u;
+    uint64_t k3[R], v3[R], h3[R];
+    bool val3[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {  // loads and hashes of all R records first (ILP)
+      const int idx = r * BLK + tid;
+      val3[r] = idx < c;
+      k3[r] = lds64(a_sk + 8u * (uint32_t)idx);
+      v3[r] = lds64(a_sv + 8u * (uint32_t)idx);
+      const uint64_t kk[1] = {k3[r]};
+      h3[r] = hash_key<1>(kk, a.t.seed);
     }
-    // ---- [A3] the lane's record of this tile
-    if (tid < c) {
-      const unsigned long long* sk = stg + (size_t)s * 2 * T;
-      const uint64_t k = sk[tid], v = sk[T + tid];
-      c_rec++;
-      vlo = min(vlo, (long long)v);
-      vhi = max(vhi, (long long)v);
-      const uint64_t kk[1] = {k};
-      const uint64_t h = hash_key<1>(kk, a.t.seed);
-      const int p = k == EMPTY ? 0 : (int)reduce32(h, (uint32_t)P);
-      const uint64_t bits = spat[wc_pat_index(h)];
-      const bool pos = k == EMPTY || (sbloom[wc_bloom_block(h, nblk)] & bits) == bits;
-      if (pos) {
-        cf = true;
-        ck = k;
-        cv = v;
-        cp = p;
-        if (k != EMPTY) {
-          cb = (uint32_t)(h & a.t.bmask);
-          const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(a.t.keys + (uint64_t)cb * 4);
-          cx = __ldcg(pp);
-          cy = __ldcg(pp + 1);
+    if constexpr (MODE == WC_SCAN) {
+      bool pos3[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint64_t bits = lds64(a_pat + 8u * wc_pat_index(h3[r]));
+        const uint64_t blk = lds64(a_bloom + 8u * wc_bloom_block(h3[r], nblk));
+        pos3[r] = val3[r] & ((k3[r] == EMPTY) | ((blk & bits) == bits));
+      }
+#pragma unroll
+      for (int r = 0; r < R; r++) c_rec += (uint32_t)val3[r];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint64_t v = val3[r] ? v3[r] : 0ull;
+        vbad |= (uint32_t)((v + 0x80000000ull) >> 32);
+        vabs = max(vabs, (uint32_t)abs((int)(uint32_t)v));
+        // positives: the tile's list (one shared atomic per warp)
+        const uint32_t m = __ballot_sync(0xffffffffu, pos3[r]);
+        if (m) {
+          uint32_t base = 0;
+          if (lane == 0) base = atoms_add(smem_u32(&s_npos), (uint32_t)__popc(m));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (pos3[r]) sts16(a_pl + 2u * (base + __popc(m & ((1u << lane) - 1u))), (uint16_t)(r * BLK + tid));
         }
+        if (val3[r] & !pos3[r]) spill(k3[r], v3[r], (int)reduce32(h3[r], (uint32_t)P), r);
+      }
+    } else {
+      // probe the frozen table: all R first buckets in flight together
+      if (a.dbg == 3) {
+#pragma unroll
+        for (int r = 0; r < R; r++) vabs += (uint32_t)(k3[r] ^ v3[r] ^ h3[r]) & (val3[r] ? 1u : 0u);
       } else {
-        spill(k, v, p, 1);
+      // the first two buckets (64 B) of every record are loaded together: a miss
+      // must reach an empty slot and a displaced key the next bucket, and a warp
+      // waits for its slowest lane (one more dependent L2 round trip per tile)
+      uint64_t bb[R];
+      ulonglong2 bx[R][4];
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        bb[r] = h3[r] & a.t.bmask;
+        if (val3[r] && k3[r] != EMPTY) {
+          ld_bucket32(a.t.keys + bb[r] * 4, bx[r][0], bx[r][1]);
+          ld_bucket32(a.t.keys + ((bb[r] + 1) & a.t.bmask) * 4, bx[r][2], bx[r][3]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if (!val3[r]) continue;
+        const uint64_t k = k3[r];
+        int64_t sl = -1;
+        if (k == EMPTY) {
+          if (*(volatile int*)&a.t.hdr->esc) sl = (int64_t)a.t.mask + 1;
+        } else {
+          // the two loaded buckets, branch-free; a longer chain (rare) continues below
+          const ulonglong2 x0 = bx[r][0], y0 = bx[r][1], x1 = bx[r][2], y1 = bx[r][3];
+          const uint32_t hm = (uint32_t)(x0.x == k) | ((uint32_t)(x0.y == k) << 1) | ((uint32_t)(y0.x == k) << 2) |
+                              ((uint32_t)(y0.y == k) << 3) | ((uint32_t)(x1.x == k) << 4) | ((uint32_t)(x1.y == k) << 5) |
+                              ((uint32_t)(y1.x == k) << 6) | ((uint32_t)(y1.y == k) << 7);
+          const uint32_t em = (uint32_t)(x0.x == EMPTY) | ((uint32_t)(x0.y == EMPTY) << 1) |
+                              ((uint32_t)(y0.x == EMPTY) << 2) | ((uint32_t)(y0.y == EMPTY) << 3) |
+                              ((uint32_t)(x1.x == EMPTY) << 4) | ((uint32_t)(x1.y == EMPTY) << 5) |
+                              ((uint32_t)(y1.x == EMPTY) << 6) | ((uint32_t)(y1.y == EMPTY) << 7);
+          // (a key sits before the first empty slot of its chain)
+          const uint32_t hbit = hm & -hm, ebit = em & -em;
+          if (hm && (!em || hbit < ebit)) {
+            const int i = __ffs(hm) - 1;
+            sl = (int64_t)(((bb[r] + (uint32_t)(i >> 2)) & a.t.bmask) * 4 + (uint32_t)(i & 3));
+          } else if (!em) {  // both buckets full and no match: walk on
+            uint64_t b = (bb[r] + 2) & a.t.bmask;
+            for (;;) {
+              ulonglong2 x, y;
+              ld_bucket32(a.t.keys + b * 4, x, y);
+              if (x.x == k) { sl = (int64_t)(b * 4); break; }
+              if (x.y == k) { sl = (int64_t)(b * 4 + 1); break; }
+              if (y.x == k) { sl = (int64_t)(b * 4 + 2); break; }
+              if (y.y == k) { sl = (int64_t)(b * 4 + 3); break; }
+              if ((x.x == EMPTY) | (x.y == EMPTY) | (y.x == EMPTY) | (y.y == EMPTY)) break;
+              b = (b + 1) & a.t.bmask;
+            }
+          }
+        }
+        if (sl >= 0) {
+          const uint64_t vv[1] = {v3[r]};
+          if (a.dbg < 2) Upd<PG>::template g<1>(a.t.states, a.t.fstride, (uint64_t)sl * a.t.sstride, 0, s_fd, ns, vv);
+          c_hit++;
+        } else if (a.dbg == 0) {
+          spill(k, v3[r], k == EMPTY ? 0 : (int)reduce32(h3[r], (uint32_t)P), r);
+        }
+      }
       }
     }
     const bool more = c != 0;
-    const bool pending = cf || opend != 0;
-    __syncthreads();  // ---- barrier 1: claims, ring writes and page maps are visible; the stage is consumed
+    fence_proxy_async_smem();  // ring writes before the bulk copies that read them
+    __syncthreads();           // ---- barrier 1
     if (tid == 0) {
-      issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
       if (nb_busy) {
         s_nb = nb_pending;
         s_nv = 1;
@@ -392,63 +551,60 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
         s_nv = 0;
       }
     }
-    // ---- [B1] complete lines of the windows: lane l of warp w looks at partition
-    // l * NWARP + w; the warp copies its lines 4 at a time, 8 lanes (16 B each) per line
-    {
-      const int p = lane * NWARP + wid;
-      uint32_t l0 = 0, nl = 0;
-      if (p < P) {
-        const uint32_t w = lb[p], ce = cnt[p];
-        l0 = w >> 3;
-        nl = (min(ce, w + RING) >> 3) - l0;
-        lb[p] = ce & ~7u;  // the window moves to the open line (read again after barrier 2)
-      }
+    // ---- [B1] owned lines: 128-byte bulk copies (TMA engine)
+    if (lf) {
 #pragma unroll
-      for (int i = 0; i < LINES; i++) {
-        uint32_t m = __ballot_sync(0xffffffffu, nl > (uint32_t)i);
-        while (m) {
-          uint32_t mm = m;
-          int src = -1;
-#pragma unroll
-          for (int g = 0; g < 4; g++) {  // group g = lane >> 3 takes the g-th set bit
-            const int b = __ffs(mm) - 1;
-            if (g == (lane >> 3)) src = b;
-            if (mm) mm &= mm - 1;
-          }
-          m = mm;
-          const int sp = __shfl_sync(0xffffffffu, p, src < 0 ? 0 : src);
-          const uint32_t sl = __shfl_sync(0xffffffffu, l0, src < 0 ? 0 : src) + (uint32_t)i;
-          if (src >= 0) {
-            const uint32_t x = (sl << 3) | (lane & 7);
-            const ulonglong2 rec = ring[sp * RING + (x & (RING - 1))];
-            const uint32_t pg = page_of(sp, x >> SLOG);
-            if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), rec);
-          }
-        }
+      for (int r = 0; r < R; r++) {
+        if (!((lf >> r) & 1u)) continue;
+        const uint32_t x0 = xs[r] & ~7u;
+        const uint32_t pg = page_of(ps[r], x0 >> SLOG);
+        if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[ps[r] * RING + (x0 & (RING - 1))], 128u);
       }
+      bulk_commit();
     }
-    // ---- [B2] held records: complete lines go straight to their page, the open line waits
+    if constexpr (MODE == WC_SCAN) {
+      // ---- [B2] the tile's positives to this CTA's region (SoA), coalesced
+      const uint32_t npos = s_npos;
+      unsigned long long* pk = (unsigned long long*)a.pos + (size_t)blockIdx.x * a.pos_stride + pcur;
+      unsigned long long* pv = pk + (size_t)a.pos_regions * a.pos_stride;
+      for (uint32_t i = tid; i < npos; i += BLK) {
+        const uint32_t idx = plist_t[i];
+        __stcg(pk + i, sk[idx]);
+        __stcg(pv + i, sv[idx]);
+      }
+      pcur += npos;
+    }
+    // ---- [B3] held records: complete lines straight to their page, the open line waits
     if (__builtin_expect(opend != 0, 0)) {
 #pragma unroll
-      for (int q = 0; q < 2; q++) {
-        if (!((opend >> q) & 1u)) continue;
-        const uint32_t cend = cnt[op[q]];
-        if ((ox[q] >> 3) < (cend >> 3)) {
-          const uint32_t pg = page_of(op[q], ox[q] >> SLOG);
-          if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, ox[q]), make_ulonglong2(okk[q], ovv[q]));
+      for (int r = 0; r < R; r++) {
+        if (!((opend >> r) & 1u)) continue;
+        if ((xs[r] >> 3) < (cnt[ps[r]] >> 3)) {
+          const uint32_t pg = page_of(ps[r], xs[r] >> SLOG);
+          if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, xs[r]), make_ulonglong2(hk[r], hv[r]));
         } else {
-          opark |= 1u << q;
+          opark |= 1u << r;
         }
       }
       opend = 0;
     }
-    // ---- barrier 2: the ring lines are out before the next tile writes the ring
+    for (int p = tid; p < P; p += BLK) lb[p] = cnt[p] & ~7u;  // the windows move to the open lines
+    if (lf) {
+      bulk_wait_read0();
+      lf = 0;
+    }
+    // ---- barrier 2: ring, positive list and stage are free again
     if (!more) {
-      if (!__syncthreads_or(pending || opark != 0)) break;
+      if (!__syncthreads_or(opark != 0)) break;
     } else {
       __syncthreads();
     }
+    if (tid == 0) {
+      s_npos = 0;
+      issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
+    }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
   // ---- close: every chain's open line (all in the ring), then the page fills
   for (int p = tid; p < P; p += BLK) {
     const uint32_t cc = cnt[p];
@@ -461,7 +617,9 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     if (pg < 0xFFFFFFu) a.pool.page_fill[pg] = (int32_t)(((cc - 1) & (S - 1)) + 1);
     atomicAdd(&a.part_recs[p], (unsigned long long)cc);
   }
-  if (tid == 0) {  // unused stash pages leave the set
+  if (tid == 0) {
+    if (MODE == WC_SCAN) a.pos_count[blockIdx.x] = pcur;
+    // unused stash pages leave the set
     for (uint32_t x = min(s_su, s_sc); x < s_sc; x++) a.pool.page_set[s_sb + x] = -1;
     if (s_nv)
       for (uint32_t x = s_nb; x < min(s_nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
@@ -469,16 +627,14 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       for (uint32_t x = nb_pending; x < min(nb_pending + (uint32_t)a.stash, a.pool.capacity); x++)
         a.pool.page_set[x] = -1;
   }
-  if (c_sp) atomicExch(&a.t.hdr->frozen, 1);
-  // value range of the probed records (compact child states)
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    vlo = min(vlo, __shfl_xor_sync(0xffffffffu, vlo, o));
-    vhi = max(vhi, __shfl_xor_sync(0xffffffffu, vhi, o));
-  }
-  if (lane == 0 && vlo <= vhi) {
-    atomicMin(&a.vrange[0], vlo);
-    atomicMax(&a.vrange[1], vhi);
+  if (c_sp) atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
+  if (MODE == WC_SCAN) {
+    vbad = __reduce_or_sync(0xffffffffu, vbad);
+    vabs = __reduce_max_sync(0xffffffffu, vabs);
+    if (lane == 0) {
+      if (vbad) atomicOr(&a.vinfo[0], 1u);
+      atomicMax(&a.vinfo[1], vabs);
+    }
   }
   uint32_t cs[3] = {c_sp, c_hit, c_rec};
   const int ids[3] = {ST_SPILLED, ST_HITS, ST_RECORDS};
@@ -504,12 +660,13 @@ struct CwArgs {
   const uint32_t* plist_n;
   uint32_t plist_cap;
   const unsigned long long* part_recs;
-  const long long* vrange;      // [0] vmin, [1] vmax of the spilled values
+  const unsigned int* vinfo;    // [0] some value outside int32, [1] max |v| (k_probe_wc)
   int32_t P;
   int32_t table_bytes;          // dynamic shared memory for the table
   uint64_t seed;                // slot hash seed of the child level
   OutBuf out;
   uint32_t* failed;             // [P]: 1 = groups did not fit, left to the generic drain
+  uint32_t* fail;               // bit 2: some partition failed (the host runs the fallback)
   unsigned long long* stats;
 };
 
@@ -553,15 +710,14 @@ __global__ void __launch_bounds__(BLK, 1) k_child_wc(CwArgs a) {
   __shared__ int s_groups, s_fail, s_esc;
   __shared__ unsigned long long s_base;
   __shared__ uint32_t s_wsum[NWARP];
-  const long long vmin = a.vrange[0], vmax = a.vrange[1];
-  const uint64_t range = (uint64_t)(vmax - vmin);
+  const bool rfit = a.vinfo[0] == 0;  // every value is an int32
+  const uint32_t vabs = a.vinfo[1];
   constexpr int NA = CP::na(), NSUM = CP::nsum();
   for (int p = blockIdx.x; p < a.P; p += gridDim.x) {
     const unsigned long long np = a.part_recs[p];
     if (np == 0) continue;
-    // wide sums (u32 pair with carry) only when the partition's biased sum can pass 2^32
-    const bool wide = (vmax >= vmin) && (range >= (1ull << 32) || (double)np * (double)range >= 4294967295.0);
-    const bool rfit = vmax < vmin || range < (1ull << 32);
+    // wide sums (a u32 pair with carry) only when a partition sum can leave int32
+    const bool wide = (double)np * (double)vabs >= 2147483647.0;
     const int words = 2 + NA + (wide ? NSUM : 0);  // key (2 x u32), count, one u32 per other field (+ hi words)
     // keys in 32-byte buckets of 4 slots (one bucket = two LDS.128; the warp runs
     // the longest probe of its lanes, and buckets keep that short)
@@ -577,94 +733,107 @@ __global__ void __launch_bounds__(BLK, 1) k_child_wc(CwArgs a) {
       sw[i] = 0;
 #pragma unroll
       for (int j = 0; j < N; j++)
-        if (!CP::is_count(j)) sw[CP::arr(j) * stride + i] = (CP::fd(j) & 3) == OP_MIN ? 0xFFFFFFFFu : 0u;
+        if (!CP::is_count(j))
+          sw[CP::arr(j) * stride + i] =
+              (CP::fd(j) & 3) == OP_MIN ? 0x7FFFFFFFu : (CP::fd(j) & 3) == OP_MAX ? 0x80000000u : 0u;
       for (int j = 0; j < (wide ? NSUM : 0); j++) sw[(NA + j) * stride + i] = 0u;
     }
     if (tid == 0) {
       s_groups = 0;
-      s_fail = !rfit;
+      s_fail = !rfit || a.plist_n[p] > a.plist_cap;  // (a page list that overflowed is incomplete)
       s_esc = 0;
     }
     __syncthreads();
     const uint32_t npg = min(a.plist_n[p], a.plist_cap);
     const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
-    // warp per page, lane l takes slots l, l + 32, ... (RL records per lane in flight)
+    // Warp w takes pages w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
+    // the page, RL records per lane in flight.
     for (uint32_t q = wid; q < npg; q += NWARP) {
       if (__any_sync(0xffffffffu, *(volatile int*)&s_fail)) break;  // warp-uniform
       const uint32_t pg = pl[q];
       const int fill = a.pool.page_fill[pg];
       const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
       for (int s0 = 0; s0 < fill; s0 += RL * 32) {
-        ulonglong2 rec[RL];
+      ulonglong2 cur[RL];
 #pragma unroll
-        for (int r = 0; r < RL; r++) {
-          const int sl = s0 + r * 32 + lane;
-          rec[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(0, 0);
-        }
+      for (int r = 0; r < RL; r++) {
+        const int sl = s0 + r * 32 + lane;
+        cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(0, 0);
+      }
 #pragma unroll
-        for (int r = 0; r < RL; r++) {
-          const int sl = s0 + r * 32 + lane;
-          int slot = -1;
-          if (sl < fill) {
-            const uint64_t k = rec[r].x;
-            if (k == EMPTY) {
-              slot = nslots;
-              if (!*(volatile int*)&s_esc) atomicExch(&s_esc, 1);
-            } else {
-              const uint64_t kk[1] = {k};
-              const uint64_t h = hash_key<1>(kk, a.seed);
-              int b = (int)__umulhi((uint32_t)h, (uint32_t)nbk);
-              for (;;) {
-                const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(skeys + b * 4);
-                const ulonglong2 x = bp[0], y = bp[1];
-                const int hit = x.x == k ? 0 : x.y == k ? 1 : y.x == k ? 2 : y.y == k ? 3 : -1;
-                if (hit >= 0) { slot = b * 4 + hit; break; }
-                const int emp = x.x == EMPTY ? 0 : x.y == EMPTY ? 1 : y.x == EMPTY ? 2 : y.y == EMPTY ? 3 : -1;
-                if (emp < 0) {  // full bucket: the next one
-                  if (++b == nbk) b = 0;
-                  continue;
-                }
-                if (atomicAdd(&s_groups, 1) >= maxg) {
-                  s_fail = 1;
-                  break;
-                }
-                const unsigned long long prev = atomicCAS((unsigned long long*)&skeys[b * 4 + emp], EMPTY, k);
-                if (prev == EMPTY) { slot = b * 4 + emp; break; }
-                atomicSub(&s_groups, 1);  // the slot went to another insert: look at the bucket again
+      for (int r = 0; r < RL; r++) {
+        int slot = -1;
+        if (s0 + r * 32 + lane < fill) {
+          const uint64_t k = cur[r].x;
+          if (__builtin_expect(k == EMPTY, 0)) {
+            slot = nslots;
+            s_esc = 1;  // (idempotent; read after the barrier)
+          } else {
+            const uint64_t kk[1] = {k};
+            const uint64_t h = hash_key<1>(kk, a.seed);
+            int b = (int)__umulhi((uint32_t)h, (uint32_t)nbk);
+            for (;;) {
+              const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(skeys + b * 4);
+              const ulonglong2 x = bp[0], y = bp[1];
+              const int hit = x.x == k ? 0 : x.y == k ? 1 : y.x == k ? 2 : y.y == k ? 3 : -1;
+              if (hit >= 0) {
+                slot = b * 4 + hit;
+                break;
               }
+              const int emp = x.x == EMPTY ? 0 : x.y == EMPTY ? 1 : y.x == EMPTY ? 2 : y.y == EMPTY ? 3 : -1;
+              if (emp < 0) {  // full bucket: the next one
+                if (++b == nbk) b = 0;
+                continue;
+              }
+              if (atomicAdd(&s_groups, 1) >= maxg) {
+                s_fail = 1;
+                break;
+              }
+              const int e = b * 4 + emp;
+              const unsigned long long prev = atomicCAS((unsigned long long*)&skeys[e], EMPTY, k);
+              if (prev == EMPTY) {
+                slot = e;
+                break;
+              }
+              atomicSub(&s_groups, 1);  // the slot went to another insert: look at the bucket again
             }
           }
-          __syncwarp();
-          if (slot >= 0) {
-            const uint32_t cb = (uint32_t)((long long)rec[r].y - vmin);
-            atomicAdd(&sw[slot], 1u);
-            int js = 0;
+        }
+        __syncwarp();
+        if (slot >= 0) {
+          const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
+          atomicAdd(&sw[slot], 1u);
+          int js = 0;
 #pragma unroll
-            for (int j = 0; j < N; j++) {
-              const uint32_t F = CP::fd(j);
-              if (((F >> 4) & 3) == SRC_ONE) continue;  // COUNT: the count word
-              uint32_t* w = &sw[CP::arr(j) * stride + slot];
-              if ((F & 3) == OP_ADD) {
-                if (wide) {
-                  const uint32_t old = atomicAdd(w, cb);
-                  if (old + cb < old) atomicAdd(&sw[(NA + js) * stride + slot], 1u);
-                } else {
-                  atomicAdd(w, cb);
-                }
-                js++;
-              } else if ((F & 3) == OP_MIN) {
-                atomicMin(w, cb);
+          for (int j = 0; j < N; j++) {
+            const uint32_t F = CP::fd(j);
+            if (((F >> 4) & 3) == SRC_ONE) continue;  // COUNT: the count word
+            uint32_t* w = &sw[CP::arr(j) * stride + slot];
+            if ((F & 3) == OP_ADD) {
+              if (wide) {  // 64-bit two's complement sum in (lo, hi) words
+                const uint32_t old = atomicAdd(w, (uint32_t)cb);
+                const uint32_t hi = (uint32_t)(old + (uint32_t)cb < old) + (cb < 0 ? 0xFFFFFFFFu : 0u);
+                if (hi) atomicAdd(&sw[(NA + js) * stride + slot], hi);
               } else {
-                atomicMax(w, cb);
+                atomicAdd(w, (uint32_t)cb);
               }
+              js++;
+            } else if ((F & 3) == OP_MIN) {
+              atomicMin((int*)w, cb);
+            } else {
+              atomicMax((int*)w, cb);
             }
           }
         }
       }
+      }
     }
     __syncthreads();
     if (s_fail) {
-      if (tid == 0) a.failed[p] = 1;
+      if (tid == 0) {
+        a.failed[p] = 1;
+        atomicOr(a.fail, 4u);
+      }
       __syncthreads();
       continue;
     }
@@ -688,9 +857,34 @@ __global__ void __launch_bounds__(BLK, 1) k_child_wc(CwArgs a) {
         s_wsum[w] = acc;
         acc += t2;
       }
-      s_base = acc ? atomicAdd(a.out.count, (unsigned long long)acc) : 0ull;
+      // reserve the rows only if they fit (else the partition goes to the fallback)
+      unsigned long long base = 0;
+      if (acc) {
+        unsigned long long old = *(volatile unsigned long long*)a.out.count;
+        for (;;) {
+          if (old + acc > (unsigned long long)a.out.cap) {
+            base = ~0ull;
+            break;
+          }
+          const unsigned long long prev = atomicCAS(a.out.count, old, old + acc);
+          if (prev == old) {
+            base = old;
+            break;
+          }
+          old = prev;
+        }
+      }
+      s_base = base;
     }
     __syncthreads();
+    if (s_base == ~0ull) {
+      if (tid == 0) {
+        a.failed[p] = 1;
+        atomicOr(a.fail, 4u);
+      }
+      __syncthreads();
+      continue;
+    }
     int64_t idx = (int64_t)s_base + s_wsum[wid] + (x - mine);
     for (int s = lo; s < hi; s++) {
       const bool occ = (s == nslots) ? (s_esc != 0) : (skeys[s] != EMPTY);
@@ -706,12 +900,11 @@ __global__ void __launch_bounds__(BLK, 1) k_child_wc(CwArgs a) {
         if (((F >> 4) & 3) == SRC_ONE) {
           w = cntw;
         } else if ((F & 3) == OP_ADD) {
-          uint64_t b = sw[CP::arr(j) * stride + s];
-          if (wide) b |= (uint64_t)sw[(NA + js) * stride + s] << 32;
-          w = b + cntw * (uint64_t)vmin;  // sum(v) = sum(v - vmin) + count * vmin (mod 2^64: exact)
+          const uint32_t lo = sw[CP::arr(j) * stride + s];
+          w = wide ? ((uint64_t)sw[(NA + js) * stride + s] << 32 | lo) : (uint64_t)(long long)(int)lo;
           js++;
         } else {
-          w = (uint64_t)((long long)sw[CP::arr(j) * stride + s] + vmin);
+          w = (uint64_t)(long long)(int)sw[CP::arr(j) * stride + s];
         }
         if (j < 4) st[j] = w;
       }
@@ -721,4 +914,19 @@ __global__ void __launch_bounds__(BLK, 1) k_child_wc(CwArgs a) {
   }
 }
 
+}  // namespace aggb
+
+namespace aggb {
+// Fallback after k_child_wc: the pages of every partition a child completed
+// leave the spill set, so drain (the generic recursion) sees only the
+// partitions that did not fit (their pages are untouched).
+__global__ void k_wc_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, const uint32_t* failed,
+                            int P, int32_t* page_set) {
+  for (int p = blockIdx.x; p < P; p += gridDim.x) {
+    if (failed[p]) continue;
+    const uint32_t n = plist_n[p];
+    if (n > cap) continue;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) page_set[plist[(size_t)p * cap + i]] = -1;
+  }
+}
 }  // namespace aggb

@@ -123,6 +123,7 @@ def test_child_subpasses(algo, case, max_p0, mode, monkeypatch):
     page-aligned sub-partitions); with that off ("subpass") each child takes
     its partition in sub-passes, one sub-hash range per fresh table."""
     monkeypatch.setenv("AGGB_MAX_P0", str(max_p0))
+    monkeypatch.setenv("AGGB_NO_WC", "1")  # the generic drain's split level / sub-passes are under test
     if mode == "subpass":
         monkeypatch.setenv("AGGB_NO_SPLIT_LEVEL", "1")
     path = [p for p in GOLD if os.path.basename(p).startswith(case + "__")][0]

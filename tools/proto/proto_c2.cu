@@ -188,7 +188,10 @@ int main(int argc, char** argv) {
   uint32_t* plist = dalloc<uint32_t>((size_t)P * plist_cap);
   uint32_t* plist_n = dalloc<uint32_t>(P);
   unsigned long long* part_recs = dalloc<unsigned long long>(P);
-  long long* vrange = dalloc<long long>(2);
+  unsigned int* vinfo = dalloc<unsigned int>(2);
+  const int64_t pos_stride = ((N / 1024 + 1) / sms + 2) * 1024;
+  uint64_t* posb = dalloc<uint64_t>((size_t)pos_stride * 2 * sms);
+  unsigned long long* pos_count = dalloc<unsigned long long>(sms);
   uint32_t* failw = dalloc<uint32_t>(4);
   uint32_t* failed = dalloc<uint32_t>(P);
   // output
@@ -217,20 +220,25 @@ int main(int argc, char** argv) {
   CK(cudaDeviceSynchronize());
 
   #ifndef PBLK
-#define PBLK 1024
+#define PBLK 512
 #endif
 #ifndef PNS
-#define PNS 5
+#define PNS 3
 #endif
-  constexpr int BLK = PBLK, NS = PNS;
-  auto* fn0 = k_probe_wc<ProgC2, BLK, NS, 2>;
-  auto* fn1 = k_probe_wc<ProgC2, BLK, 3, 4>;
+  constexpr int BLK = PBLK, NS = PNS, RR = 1024 / PBLK;
+  auto* fn0 = k_probe_wc<ProgC2, BLK, RR, NS, 2>;
+  auto* fn1 = k_probe_wc<ProgC2, BLK, RR, NS, 4>;
   auto* fnp = lines == 4 ? fn1 : fn0;
-  const size_t psmem = lines == 4 ? WcLayout<BLK, 3, 4>::bytes(P, nblk) : WcLayout<BLK, NS, 2>::bytes(P, nblk);
+  const size_t psmem = lines == 4 ? WcLayout<BLK, RR, NS, 4>::bytes(P, nblk) : WcLayout<BLK, RR, NS, 2>::bytes(P, nblk);
   printf("probe smem %zu bytes\n", psmem);
   CK(cudaFuncSetAttribute((const void*)fnp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+  auto* fnr = k_resolve_wc<ProgC2, 512, 4>;
+  const size_t rsmem = (size_t)P * 4 * 9;
   constexpr int CBLK = 1024;
-  auto* fnc = k_child_wc<CpC2, CBLK, 4>;
+  #ifndef CRL
+#define CRL 4
+#endif
+  auto* fnc = k_child_wc<CpC2, CBLK, CRL>;
   const int csmem = 220 * 1024;
   CK(cudaFuncSetAttribute((const void*)fnc, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
 
@@ -254,10 +262,7 @@ int main(int argc, char** argv) {
     CK(cudaMemset(failw, 0, 16));
     CK(cudaMemset(failed, 0, P * 4));
     CK(cudaMemset(o.count, 0, 8));
-    {
-      long long vr[2] = {LLONG_MAX, LLONG_MIN};
-      CK(cudaMemcpy(vrange, vr, 16, cudaMemcpyHostToDevice));
-    }
+    CK(cudaMemset(vinfo, 0, 8));
     CK(cudaMemset(page_set, 0xFF, pool_pages * 4));
     // ctr: [0] lcount [1] tile counter [2] next_page [3] overflow(u32) [8..15] stats
     CK(cudaDeviceSynchronize());
@@ -297,15 +302,23 @@ int main(int argc, char** argv) {
     a.part_recs = part_recs;
     a.tile_counter = ctr + 1;
     a.stats = ctr + 8;
-    a.vrange = vrange;
+    a.vinfo = vinfo;
     a.fail = failw;
     a.stash = 32;
+    a.pos = posb;
+    a.pos_stride = pos_stride;
+    a.pos_count = pos_count;
+    a.pos_regions = sms;
     {
       unsigned long long one = 1;
       CK(cudaMemcpy(ctr + 20, &one, 8, cudaMemcpyHostToDevice));
     }
     CK(cudaEventRecord(e[1]));
     fnp<<<sms, BLK, psmem>>>(a);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e[5]));
+    a.tile_counter = ctr + 30;
+    fnr<<<sms, 512, rsmem>>>(a);
     CK(cudaGetLastError());
     CK(cudaEventRecord(e[2]));
     CwArgs ca;
@@ -316,12 +329,13 @@ int main(int argc, char** argv) {
     ca.plist_n = plist_n;
     ca.plist_cap = plist_cap;
     ca.part_recs = part_recs;
-    ca.vrange = vrange;
+    ca.vinfo = vinfo;
     ca.P = P;
     ca.table_bytes = csmem;
     ca.seed = 0x9876543ull;
     ca.out = o;
     ca.failed = failed;
+    ca.fail = failw + 1;
     ca.stats = ctr + 8;
     fnc<<<std::min(P, sms), CBLK, csmem>>>(ca);
     CK(cudaGetLastError());
@@ -329,8 +343,9 @@ int main(int argc, char** argv) {
     k_flush_proto<<<sms * 4, 256>>>(t, o);
     CK(cudaEventRecord(e[4]));
     CK(cudaDeviceSynchronize());
-    float m1, m2, m3, m4;
+    float m1, m2, m3, m4, m5;
     CK(cudaEventElapsedTime(&m1, e[1], e[2]));
+    CK(cudaEventElapsedTime(&m5, e[1], e[5]));
     CK(cudaEventElapsedTime(&m2, e[2], e[3]));
     CK(cudaEventElapsedTime(&m3, e[3], e[4]));
     CK(cudaEventElapsedTime(&m4, e[0], e[4]));
@@ -344,6 +359,7 @@ int main(int argc, char** argv) {
     for (int p = 0; p < P; p++) nfailed += hfd[p] != 0;
     unsigned long long nout;
     CK(cudaMemcpy(&nout, o.count, 8, cudaMemcpyDeviceToHost));
+    printf("  (partition %.3f ms, resolve %.3f ms)\n", m5, m1 - m5);
     printf("iter %d: probe %.3f ms  child %.3f ms  flush %.3f ms  all %.3f ms | deferred %llu spilled %llu hits %llu recs %llu "
            "pages %llu ovf %u fail %u failed_parts %d out %llu\n",
            itx, m1, m2, m3, m4, hc[0], hc[8 + ST_SPILLED], hc[8 + ST_HITS], hc[8 + ST_RECORDS], hc[2],
