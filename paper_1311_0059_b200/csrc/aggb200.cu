@@ -1267,7 +1267,10 @@ int plan(Handle* h) {
 // scan: 4 records per thread per tile, double-buffered stages (per-tile
 // overhead halved: C2 scan 1.64 -> 1.36 ms against 2 per thread x 3 stages);
 // resolve (no bloom in shared memory): 2 x 3
-constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_RR = 2, WC_RNS = 3, WC_LINES = 2, WC_CBLK = 1024, WC_CRL = 4;
+#ifndef WC_RR_
+#define WC_RR_ 2
+#endif
+constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_RR = WC_RR_, WC_RNS = 3, WC_LINES = 2, WC_CBLK = 1024, WC_CRL = 4;
 using WcL = WcLayout<WC_BLK, WC_R, WC_NS, WC_LINES>;
 using WcLR = WcLayout<WC_BLK, WC_RR, WC_RNS, WC_LINES>;
 void wc_plan(Handle* h, double spill_groups) {
@@ -1464,7 +1467,9 @@ int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss);
 
 // k_probe_wc reads the key and value columns with 16-byte bulk copies
 bool wc_eligible(Handle* h, const ColSrc& col) {
+  // (a chain's claim counter has 23 bits: at most ~8M records per CTA and launch)
   return col.nv == 1 && dense8(col, 1) && col.kty[0] == TY_I64 && col.vty[0] == TY_I64 &&
+         col.n + h->defer_cap <= (int64_t)1200000000 &&
          ((uintptr_t)col.key[0] & 15) == 0 && ((uintptr_t)col.val[0] & 15) == 0 && !h->hot_ready &&
          h->pool_bound + (uint64_t)(col.n + h->defer_cap) / 256 + (uint64_t)h->sms * (4ull * h->P0 + 128) < 0xFFFFF0ull;
 }

@@ -128,16 +128,7 @@ __device__ __forceinline__ void st_v2(void* p, ulonglong2 v) {
 // from the low 32 hash bits by multiply-high; the table bucket uses bits 0-15,
 // the partition the top bits, the four bit positions bits 34-53)
 __device__ __forceinline__ uint32_t wc_bloom_block(uint64_t h, uint32_t nblk) { return __umulhi((uint32_t)h, nblk); }
-// the block's bit pattern: one of 1024 four-bit patterns, chosen by hash bits 34-43
-// (k_probe_wc looks it up in an 8 KB shared table instead of building it per record)
-constexpr int WC_NPAT = 1024;
-__host__ __device__ __forceinline__ uint64_t wc_pattern(uint32_t i) {
-  uint64_t z = (uint64_t)i * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
-  z = (z ^ (z >> 31)) * 0xBF58476D1CE4E5B9ull;
-  z ^= z >> 29;
-  return (1ull << (z & 63)) | (1ull << ((z >> 6) & 63)) | (1ull << ((z >> 12) & 63)) | (1ull << ((z >> 18) & 63));
-}
-__device__ __forceinline__ uint32_t wc_pat_index(uint64_t h) { return (uint32_t)(h >> 34) & (WC_NPAT - 1); }
+// the block's bit pattern: bloom_bits(h) (four bits from hash bits 34-53)
 
 __global__ void k_bloom_build_wc(GTable t, uint64_t* bloom, uint32_t nblk) {
   const uint64_t n = t.mask + 1;
@@ -145,7 +136,7 @@ __global__ void k_bloom_build_wc(GTable t, uint64_t* bloom, uint32_t nblk) {
     const uint64_t k[1] = {t.keys[i]};
     if (k[0] == EMPTY) continue;
     const uint64_t h = hash_key<1>(k, t.seed);
-    atomicOr((unsigned long long*)&bloom[wc_bloom_block(h, nblk)], (unsigned long long)wc_pattern(wc_pat_index(h)));
+    atomicOr((unsigned long long*)&bloom[wc_bloom_block(h, nblk)], (unsigned long long)bloom_bits(h));
   }
 }
 
@@ -188,13 +179,15 @@ template <int BLK, int R, int NS, int LINES>
 struct WcLayout {
   static constexpr int T = BLK * R;
   static constexpr int RING = LINES * 8;
+  static constexpr int RS = RING + 1;  // ring stride per partition (16-byte slots): one slot of skew per
+                                       // partition spreads the same ring position over the banks
   static constexpr int NE = 8;
   // bytes: stages, ring, bloom + bit patterns, cnt + lb + page maps, positive index list
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
-  static __host__ __device__ size_t ring_bytes(int P) { return (size_t)P * RING * 16; }
-  static __host__ __device__ size_t meta_bytes(int P) { return ((size_t)P * (2 + NE) * 4 + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t ring_bytes(int P) { return (size_t)P * RS * 16; }
+  static __host__ __device__ size_t meta_bytes(int P) { return ((size_t)P * (1 + NE) * 4 + 15) & ~(size_t)15; }
   static __host__ __device__ size_t bytes(int P, uint32_t nblk) {
-    return stage_bytes() + ring_bytes(P) + (size_t)(nblk + WC_NPAT) * 8 + meta_bytes(P) + (size_t)T * 2;
+    return stage_bytes() + ring_bytes(P) + (size_t)nblk * 8 + meta_bytes(P) + (size_t)T * 2;
   }
 };
 
@@ -213,7 +206,10 @@ struct WcLayout {
 // are parked for the next tile, windows move on; barrier 2 (ring, positive
 // list and stage free again; the stage's next tile is issued).
 constexpr int WC_SCAN = 0, WC_RESOLVE = 1;
-constexpr int WC_PF = 6;  // k_probe_wc: L2 prefetch distance in tiles (rounds of the grid)
+constexpr int WC_PF = 6;
+#ifndef WC_COOP
+#define WC_COOP 0
+#endif  // k_probe_wc: L2 prefetch distance in tiles (rounds of the grid)
 template <class PG, int BLK, int R, int NS, int LINES, int MODE>
 __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   using L = WcLayout<BLK, R, NS, LINES>;
@@ -226,14 +222,15 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   unsigned long long* stg = (unsigned long long*)smem;
   ulonglong2* ring = (ulonglong2*)(smem + L::stage_bytes());
   uint64_t* sbloom = (uint64_t*)(smem + L::stage_bytes() + L::ring_bytes(P));
-  uint64_t* spat = sbloom + nblk;  // WC_NPAT bit patterns
-  uint32_t* cnt = (uint32_t*)(spat + WC_NPAT);
-  uint32_t* lb = cnt + P;
-  uint32_t* ent = lb + P;
-  uint16_t* plist_t = (uint16_t*)((unsigned char*)cnt + L::meta_bytes(P));  // this tile's positives (stage indices)
-  // 32-bit shared addresses of the same arrays (the hot loop's accesses)
-  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_bloom = smem_u32(sbloom),
-                 a_pat = smem_u32(spat), a_cnt = smem_u32(cnt), a_lb = smem_u32(lb), a_pl = smem_u32(plist_t);
+  // cw[p]: the chain's claim counter (bits 0-22) and its window's first line mod 512
+  // (bits 23-31): one shared atomic returns both the position and the window
+  uint32_t* cw = (uint32_t*)(sbloom + nblk);
+  uint32_t* ent = cw + P;
+  uint16_t* plist_t = (uint16_t*)((unsigned char*)cw + L::meta_bytes(P));  // this tile's positives (stage indices)
+  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_bloom = smem_u32(sbloom), a_cw = smem_u32(cw),
+                 a_pl = smem_u32(plist_t);
+  constexpr uint32_t CWM = (1u << 23) - 1;  // count bits
+  constexpr int RS = L::RS;
   __shared__ __align__(8) uint64_t mbar[NS];
   __shared__ int s_tcnt[NS];
   __shared__ uint32_t s_npos;
@@ -264,11 +261,9 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   const int ns = a.sp.ns;
   if (tid < ns) s_fd[tid] = field_desc(a.sp, tid);
   if (tid < ST_NSTATS) s_cnt[tid] = 0;
-  for (int p = tid; p < P; p += BLK) cnt[p] = lb[p] = 0;
+  for (int p = tid; p < P; p += BLK) cw[p] = 0;
   for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
   for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom + i);
-  if (MODE == WC_SCAN)
-    for (int i = tid; i < WC_NPAT; i += BLK) spat[i] = wc_pattern((uint32_t)i);
   if (tid == 0) {
     s_npos = 0;
     s_sb = s_su = s_sc = s_nb = s_nv = 0;
@@ -394,16 +389,13 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       vabs ^= (uint32_t)(k ^ v) + p;
       return;
     }
-    const uint32_t x = atoms_add(a_cnt + 4u * (uint32_t)p, 1u);
-    if (MODE == WC_SCAN && a.dbg == 5) {
-      vabs ^= x;
-      return;
-    }
+    const uint32_t old = atoms_add(a_cw + 4u * (uint32_t)p, 1u);
+    const uint32_t x = old & CWM;
     if (__builtin_expect((x & (S - 1)) == 0, 0)) alloc_page(p, x >> SLOG);
     xs[q] = x;
     ps[q] = p;
-    if (__builtin_expect(x < lds32(a_lb + 4u * (uint32_t)p) + RING, 1)) {
-      sts128(a_ring + 16u * ((uint32_t)p * RING + (x & (RING - 1))), k, v);
+    if (__builtin_expect((((x >> 3) - (old >> 23)) & 511u) < (uint32_t)LINES, 1)) {
+      sts128(a_ring + 16u * ((uint32_t)p * RS + (x & (RING - 1))), k, v);
       lf |= (uint32_t)((x & 7u) == 7u && (MODE != WC_SCAN || a.dbg != 6)) << q;  // this thread sends the line after barrier 1
     } else {
       opend |= 1u << q;
@@ -424,7 +416,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     if (__builtin_expect(opark != 0, 0)) {
 #pragma unroll
       for (int r = 0; r < R; r++)
-        if ((opark >> r) & 1u) ring[ps[r] * RING + (xs[r] & (RING - 1))] = make_ulonglong2(hk[r], hv[r]);
+        if ((opark >> r) & 1u) ring[ps[r] * RS + (xs[r] & (RING - 1))] = make_ulonglong2(hk[r], hv[r]);
       opark = 0;
     }
     // ---- [A2] this tile's records
@@ -446,7 +438,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       bool pos3[R];
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        const uint64_t bits = lds64(a_pat + 8u * wc_pat_index(h3[r]));
+        const uint64_t bits = bloom_bits(h3[r]);
         const uint64_t blk = lds64(a_bloom + 8u * wc_bloom_block(h3[r], nblk));
         pos3[r] = val3[r] & ((k3[r] == EMPTY) | ((blk & bits) == bits));
       }
@@ -551,14 +543,38 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
         s_nv = 0;
       }
     }
-    // ---- [B1] owned lines: 128-byte bulk copies (TMA engine)
-    if (lf) {
+    // ---- [B1] owned lines
+    if constexpr (WC_COOP) {
+      // the warp copies its owners' lines 4 at a time: lane group g = lane >> 3
+      // takes the g-th owner, each lane one 16-byte chunk (one 128-byte store group)
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        uint32_t m = __ballot_sync(0xffffffffu, (lf >> r) & 1u);
+        while (m) {
+          uint32_t mm = m;
+          const int g = lane >> 3;
+          for (int i = 0; i < g; i++) mm &= mm - 1;
+          const int src = mm ? __ffs(mm) - 1 : -1;
+#pragma unroll
+          for (int i = 0; i < 4; i++) m &= m - 1;
+          const int sp = __shfl_sync(0xffffffffu, ps[r], src & 31);
+          const uint32_t sx = __shfl_sync(0xffffffffu, xs[r], src & 31);
+          if (src >= 0) {
+            const uint32_t x = (sx & ~7u) | (uint32_t)(lane & 7);
+            const uint32_t pg = page_of(sp, x >> SLOG);
+            const uint64_t* rp = (const uint64_t*)&ring[sp * RS + (x & (RING - 1))];
+            if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), make_ulonglong2(rp[0], rp[1]));
+          }
+        }
+      }
+      lf = 0;
+    } else if (lf) {  // 128-byte bulk copies (TMA engine)
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if (!((lf >> r) & 1u)) continue;
         const uint32_t x0 = xs[r] & ~7u;
         const uint32_t pg = page_of(ps[r], x0 >> SLOG);
-        if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[ps[r] * RING + (x0 & (RING - 1))], 128u);
+        if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[ps[r] * RS + (x0 & (RING - 1))], 128u);
       }
       bulk_commit();
     }
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if (!((opend >> r) & 1u)) continue;
-        if ((xs[r] >> 3) < (cnt[ps[r]] >> 3)) {
+        if ((xs[r] >> 3) < ((cw[ps[r]] & CWM) >> 3)) {
           const uint32_t pg = page_of(ps[r], xs[r] >> SLOG);
           if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, xs[r]), make_ulonglong2(hk[r], hv[r]));
         } else {
@@ -588,7 +604,10 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       }
       opend = 0;
     }
-    for (int p = tid; p < P; p += BLK) lb[p] = cnt[p] & ~7u;  // the windows move to the open lines
+    for (int p = tid; p < P; p += BLK) {  // the windows move to the open lines
+      const uint32_t cc = cw[p] & CWM;
+      cw[p] = ((cc >> 3) << 23) | cc;
+    }
     if (lf) {
       bulk_wait_read0();
       lf = 0;
@@ -607,11 +626,11 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
   // ---- close: every chain's open line (all in the ring), then the page fills
   for (int p = tid; p < P; p += BLK) {
-    const uint32_t cc = cnt[p];
+    const uint32_t cc = cw[p] & CWM;
     if (!cc) continue;
     for (uint32_t x = cc & ~7u; x < cc; x++) {
       const uint32_t pg = page_of(p, x >> SLOG);
-      if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), ring[p * RING + (x & (RING - 1))]);
+      if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), ring[p * RS + (x & (RING - 1))]);
     }
     const uint32_t pg = page_of(p, (cc - 1) >> SLOG);
     if (pg < 0xFFFFFFu) a.pool.page_fill[pg] = (int32_t)(((cc - 1) & (S - 1)) + 1);
