@@ -207,8 +207,10 @@ def run_ours(args, rank, world, device):
     # N > 1: exchange partial groups after a local combine, or raw rows first
     # when the combine would not shrink what is sent
     xmode = None
+    meta = None
     if world > 1:
         from paper_1311_0059_b200.exchange import choose_exchange
+        meta = torch.distributed.new_group(backend="gloo")  # host-side counts exchange (no device sync)
         n_cols = len(keys) + len(vals)
         part_b = 8 * (len(keys) + len(spec_of(cfg).fns) + 1)  # key words + states (upper bound)
         xmode = args.exchange if args.exchange != "auto" else choose_exchange(n, G_est, 8 * n_cols, part_b)
@@ -218,11 +220,12 @@ def run_ours(args, rank, world, device):
     xg = xr = None
     if xmode == "partial":
         from paper_1311_0059_b200.exchange import Exchanger
-        xg = Exchanger(g, agg, types_of(keys), types_of(vals), device, stream, rank, world,
+        xg = Exchanger(g, agg, types_of(keys), types_of(vals), device, stream, rank, world, meta_group=meta,
+                       expect_groups=min(G_est, n * world) / world,
                        stats=stats, seed=1234, budget_groups=budget_of(cfg, n))
     elif xmode == "raw":
         from paper_1311_0059_b200.exchange import RawExchanger
-        xr = RawExchanger(g, device, stream)
+        xr = RawExchanger(g, device, stream, meta_group=meta)
 
     def step():
         if xr is not None:
@@ -289,11 +292,12 @@ def run_ours(args, rank, world, device):
         xe = xre = None
         if xmode == "partial":
             from paper_1311_0059_b200.exchange import Exchanger
-            xe = Exchanger(ge, agg, types_of(keys), types_of(vals), device, stream, rank, world,
+            xe = Exchanger(ge, agg, types_of(keys), types_of(vals), device, stream, rank, world, meta_group=meta,
+                           expect_groups=min(G_est, n * world) / world,
                            stats=stats, seed=1234, budget_groups=budget_of(cfg, n))
         elif xmode == "raw":
             from paper_1311_0059_b200.exchange import RawExchanger
-            xre = RawExchanger(ge, device, stream)
+            xre = RawExchanger(ge, device, stream, meta_group=meta)
         outk = outv = None
 
         def estep():
@@ -503,6 +507,7 @@ def main():
     torch.cuda.set_device(device)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # rank/channel/NVLS lines for the driver's check
         torch.distributed.init_process_group("nccl", device_id=device)
     out = run_ours(args, rank, world, device)
     extra = {}

@@ -29,6 +29,8 @@ using namespace aggb;
 
 namespace {
 
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
 thread_local std::string g_err;
 
 // AGGB_TRACE=1: host-side phase timings on stderr (synchronizes the stream)
@@ -641,6 +643,7 @@ struct Handle {
   uint32_t wc_plist_cap = 0;  // page-list entries per partition
   int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
   DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_pos, wc_pos_count;
+  DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
   DBuf sort_keys, sort_vals;
   int64_t sort_n = 0, sort_cap = 0;
@@ -2296,7 +2299,10 @@ void aggb_destroy(void* handle) {
   DBuf* bufs[] = {&h->tkeys, &h->tstates, &h->thdr, &h->page_part, &h->page_fill, &h->page_set,
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
-                  &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals};
+                  &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
+                  &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains, &h->wc_bloom,
+                  &h->wc_plist, &h->wc_pn, &h->wc_recs, &h->wc_vinfo, &h->wc_failed, &h->wc_fail, &h->wc_pos,
+                  &h->wc_pos_count, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
   h->pool_base.release();
   h->stage.release();
@@ -2659,13 +2665,16 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   cudaSetDevice(h->device);
   // partial records (AoS: kw key words then ns state words) are transposed to
   // the list layout and partitioned into the partial spill set; the children
-  // of aggb_finish merge them (merge ops only, like the reference's runs)
+  // of aggb_finish merge them (merge ops only, like the reference's runs).
+  // The list buffer belongs to the handle (grow-only, stream-ordered reuse): no
+  // allocation and no synchronization per call.
   int rw = h->kw + h->cs.ds.ns;
-  DBuf soa;
-  TRY(soa.ensure((size_t)n_records * rw * 8, nullptr));
+  DBuf& soa = h->partials_soa;
+  TRY(soa.ensure((size_t)n_records * rw * 8, &h->hw));
   k_aos_to_soa<<<h->sms * 8, 256, 0, h->st>>>((const uint64_t*)recv, n_records, rw, soa.as<uint64_t>());
   h->launches++;
-  CU(cudaMemcpyAsync(SC(h) + 11, &n_records, 8, cudaMemcpyHostToDevice, h->st));
+  k_set_u64<<<1, 1, 0, h->st>>>(SC(h) + 11, (unsigned long long)n_records);  // (by value: no host buffer to keep alive)
+  h->launches++;
   PassPlan g;
   g.mode = MODE_GRACE;
   g.lin = soa.as<uint64_t>();
@@ -2676,8 +2685,6 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   g.ss = h->part0.ss;
   g.counter = SC(h) + 9;
   TRY(launch_pass(h, g));
-  CU(cudaStreamSynchronize(h->st));
-  soa.release();
   h->part0_live = true;
   h->records += n_records;
   return AGGB_OK;

@@ -17,6 +17,12 @@ from the group estimate.
 
 ``exchange_records`` is the collective alone (byte buffers + per-destination
 record counts); it has no CUDA dependency and is tested with gloo on the CPU.
+The per-destination counts are host values (the pack returns them): given a
+CPU-side ``meta_group`` (gloo), they are exchanged there, so the data
+all-to-allv is the only collective on the device stream and nothing waits on
+the device for the counts.  Over a gloo data group (no GPU collectives: the
+two-processes-on-one-GPU test, tests/test_gpu_exchange.py) CUDA buffers are
+staged through host memory.
 """
 
 from __future__ import annotations
@@ -29,23 +35,35 @@ import torch.distributed as dist
 from paper_1311_0059_b200 import _native as N
 
 
-def exchange_records(send: torch.Tensor, send_counts: list, record_bytes: int, group=None):
+def exchange_records(send: torch.Tensor, send_counts: list, record_bytes: int, group=None, meta_group=None):
     """All-to-allv of packed records.
 
     send: 1-D uint8 tensor, records grouped by destination rank in rank order.
-    send_counts: records per destination (len == world size).
-    Returns (recv uint8 tensor, recv_counts list).
+    send_counts: records per destination (len == world size), host ints.
+    meta_group: optional CPU (gloo) group for the counts exchange.
+    Returns (recv uint8 tensor on send's device, recv_counts list).
     """
     world = dist.get_world_size(group)
     dev = send.device
-    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-    rc = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_to_all_single(rc, sc, group=group)
+    if meta_group is not None:
+        sc = torch.tensor(send_counts, dtype=torch.int64)
+        rc = torch.empty(world, dtype=torch.int64)
+        dist.all_to_all_single(rc, sc, group=meta_group)
+    else:
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+        rc = torch.empty(world, dtype=torch.int64, device=dev)
+        dist.all_to_all_single(rc, sc, group=group)
     recv_counts = [int(x) for x in rc.cpu().tolist()]
-    recv = torch.empty(sum(recv_counts) * record_bytes, dtype=torch.uint8, device=dev)
-    dist.all_to_all_single(recv, send[: sum(send_counts) * record_bytes],
+    payload = send[: sum(send_counts) * record_bytes]
+    stage = dev.type == "cuda" and dist.get_backend(group) == "gloo"
+    if stage:  # gloo moves host memory only
+        payload = payload.cpu()
+    recv = torch.empty(sum(recv_counts) * record_bytes, dtype=torch.uint8, device="cpu" if stage else dev)
+    dist.all_to_all_single(recv, payload,
                            output_split_sizes=[c * record_bytes for c in recv_counts],
                            input_split_sizes=[c * record_bytes for c in send_counts], group=group)
+    if stage:
+        recv = recv.to(dev)
     return recv, recv_counts
 
 
@@ -73,10 +91,11 @@ class RawExchanger:
     """Raw-first exchange: pack input rows by destination, all-to-allv, then one
     aggregation of what this rank received (key sets disjoint across ranks)."""
 
-    def __init__(self, handle, device, stream):
+    def __init__(self, handle, device, stream, meta_group=None):
         self.g = handle
         self.device = device
         self.stream = stream
+        self.meta_group = meta_group
         self._send = None
         self.last_counts = None
 
@@ -85,9 +104,9 @@ class RawExchanger:
         self._send, counts, rb = self.g.pack_raw(keys, vals, world, out=self._send)
         if self.stream is not None and self.device.type == "cuda":
             with torch.cuda.stream(self.stream):
-                recv, recv_counts = exchange_records(self._send, counts, rb, group)
+                recv, recv_counts = exchange_records(self._send, counts, rb, group, self.meta_group)
         else:
-            recv, recv_counts = exchange_records(self._send, counts, rb, group)
+            recv, recv_counts = exchange_records(self._send, counts, rb, group, self.meta_group)
         self.last_counts = (counts, recv_counts)
         self.g.reset()
         total = sum(recv_counts)
@@ -99,18 +118,25 @@ class RawExchanger:
 class Exchanger:
     """Drives the exchange + merge after a local handle has finished.
 
-    ``local`` must be a GroupBy created with ``emit_partials=True``; the merge
-    handle is created here with the same spec and budget.
+    ``local`` must be a GroupBy created with ``emit_partials=True``.  The merge
+    handle has the same spec; its budget is the local one, raised to the
+    partial groups this rank expects to receive (``expect_groups``: ~G / world
+    over the job) so the merge aggregates in place instead of spilling again.
     """
 
-    def __init__(self, local, agg, key_types, val_types, device, stream, rank, world, **kw):
+    def __init__(self, local, agg, key_types, val_types, device, stream, rank, world, meta_group=None,
+                 expect_groups=0, **kw):
         from paper_1311_0059_b200.engine import GroupBy
         self.local = local
         self.rank, self.world = rank, world
         self.device = device
+        self.meta_group = meta_group
+        budget = kw.pop("budget_groups", -1)
+        if budget > 0 and expect_groups > 0:
+            budget = max(budget, int(1.25 * expect_groups) + 1024)
         self.merge = GroupBy(local.algo if local.algo != "sort_based" else "pre_partitioning",
                              agg, key_types, val_types, device=device.index, stream=stream,
-                             budget_groups=kw.pop("budget_groups", -1), **kw)
+                             budget_groups=budget, **kw)
         self.rec_bytes = int(local.L.aggb_exchange_record_bytes(local.h))
         self.stream = stream
         self._send = None
@@ -132,9 +158,11 @@ class Exchanger:
         # current stream; a side stream would race the receive buffer)
         if self.stream is not None and self.device.type == "cuda":
             with torch.cuda.stream(self.stream):
-                recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
+                recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes,
+                                                     meta_group=self.meta_group)
         else:
-            recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes)
+            recv, recv_counts = exchange_records(self._send, send_counts, self.rec_bytes,
+                                                 meta_group=self.meta_group)
         self.last_counts = (send_counts, recv_counts)
         self.merge.reset()
         total = sum(recv_counts)
