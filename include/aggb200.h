@@ -105,7 +105,9 @@ typedef struct {
   int64_t key_stride[AGGB_MAX_KEYS];   /* bytes between rows (0: packed)       */
   const void* val[AGGB_MAX_VALS];
   int64_t val_stride[AGGB_MAX_VALS];
-  int32_t on_host;                     /* 1: pointers are host memory (copied H2D on the stream) */
+  int32_t on_host;                     /* 1: pointers are host memory (copied H2D on the stream;
+                                          aggb_push returns once the copies out of them are done,
+                                          so the caller may refill its buffers) */
   int32_t reserved_;
 } aggb_input;
 

@@ -1,6 +1,9 @@
-"""Build the in-tree CUDA library (sm_100a) and the CPU oracle.
+"""Build the in-tree CUDA library (sm_100a).
 
     python -m paper_1311_0059_b200.build
+
+(The CPU oracle is test infrastructure and is built by __graft_entry__.build()
+/ oracle.oracle.build(), outside the product package.)
 
 nvcc cross-compiles for sm_100a without a GPU; the .so lands in
 paper_1311_0059_b200/lib/ so it travels with the repo snapshot to the GPU box.
@@ -45,16 +48,9 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
-def build_oracle(force: bool = False) -> str:
-    sys.path.insert(0, REPO)
-    from oracle import oracle
-    return oracle.build(force)
-
-
 def main():
     force = "--force" in sys.argv
     print(build_cuda(force, verbose="-v" in sys.argv))
-    print(build_oracle(force))
 
 
 if __name__ == "__main__":

@@ -184,7 +184,14 @@ struct VPool {
     memset(&pr, 0, sizeof(pr));
     pr.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     pr.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
-    pr.location.id = 0;
+    // the host NUMA node nearest this GPU (2-socket nodes: GPUs of socket 1
+    // would otherwise reach their spilled pages across the socket link)
+    int numa = -1;
+    if (cudaDeviceGetAttribute(&numa, cudaDevAttrHostNumaId, dev) != cudaSuccess || numa < 0) {
+      cudaGetLastError();
+      numa = 0;
+    }
+    pr.location.id = numa;
     return pr;
   }
   CUmemAllocationProp prop() const {
@@ -652,6 +659,7 @@ struct Handle {
   // pipelined host pushes: copy stream, two staging buffers, their events
   cudaStream_t cst = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  cudaEvent_t ev_staged = nullptr;  // end of a host push's copies out of the caller's memory
   DBuf pstage[2];
   bool pstage_busy[2] = {false, false};  // an aggregation reading pstage[b] may still run (ev_used[b])
   // per-kernel CUDA-event timing (aggb_profile)
@@ -2321,6 +2329,7 @@ void aggb_destroy(void* handle) {
       cudaEventDestroy(h->ev_used[b]);
     }
   }
+  if (h->ev_staged) cudaEventDestroy(h->ev_staged);
   delete h;
 }
 
@@ -2625,6 +2634,9 @@ int push_pipelined(Handle* h, const aggb_input* in) {
     h->pstage_busy[b] = true;
     if (c + 2 < nch) TRY(copy(c + 2));
   }
+  // the caller may reuse its host buffers once push returns: wait for the last
+  // copy out of them (in order on the copy stream), not for the aggregation
+  CU(cudaEventSynchronize(h->ev_copied[(int)((nch - 1) & 1)]));
   return AGGB_OK;
 }
 
@@ -2643,6 +2655,10 @@ int aggb_push(void* handle, const aggb_input* in) {
   }
   Staged sg;
   TRY(stage_input(h, in, sg));
+  if (in->on_host) {  // the copies out of the caller's memory (waited for before returning)
+    if (!h->ev_staged) CU(cudaEventCreateWithFlags(&h->ev_staged, cudaEventDisableTiming));
+    CU(cudaEventRecord(h->ev_staged, h->st));
+  }
   ColSrc col = col_of(h, in, sg.k, sg.v);
   h->records += in->n_rows;
   int s;
@@ -2653,6 +2669,7 @@ int aggb_push(void* handle, const aggb_input* in) {
     cudaStreamSynchronize(h->st);
     for (auto& b : sg.owned) b.release();
   }
+  if (in->on_host) CU(cudaEventSynchronize(h->ev_staged));  // host buffers reusable on return
   return s;
 }
 

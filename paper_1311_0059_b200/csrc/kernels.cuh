@@ -97,7 +97,12 @@ __device__ __forceinline__ bool reserve_capacity(const GTable& t, const CapCache
   const unsigned m = __activemask();
   const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
   const unsigned n = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
-  if (cc.chunk && *(volatile unsigned long long*)&t.hdr->chunked < cc.cap_chunked) {
+  // (the leader reads the counter and broadcasts it: a per-lane volatile load could
+  // split the lanes of m across the branch and leave __shfl_sync lanes missing)
+  unsigned long long chunked = 0;
+  if (cc.chunk && lane == leader) chunked = *(volatile unsigned long long*)&t.hdr->chunked;
+  chunked = __shfl_sync(m, chunked, leader);
+  if (cc.chunk && chunked < cc.cap_chunked) {
     // chunk region: the lanes here take one each; the leader also takes a chunk
     // for its CTA when no other thread of the CTA is doing so
     unsigned long long c = ~0ull;
@@ -696,6 +701,7 @@ __global__ void k_page_hist(PagePool pool, uint32_t first, const uint32_t* last_
     if (pool.page_set[pg] != set_id) continue;
     int p = pool.page_part[pg];
     if (p < 0 || p >= nparts) continue;
+    if (pool.page_fill[pg] == 0) continue;  // the same filter as k_page_scatter (its lists count these pages)
     atomicAdd(&part_records[p], (unsigned long long)pool.page_fill[pg]);
     atomicAdd(&part_pages[p], 1u);
   }

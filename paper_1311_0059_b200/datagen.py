@@ -5,8 +5,8 @@ module that does not exist), and BASELINE.json names no public
 dataset, so these seeded counter-based generators *are* the benchmark inputs
 (SURVEY.md §8(d)).  Every value is a pure function of (seed, stream, record
 index): ``x = splitmix64(base(seed, stream) + (i + 1) * GOLDEN)``.  The same
-formula runs on the device (``csrc/datagen.cu``), so any rank can regenerate its
-own slice, and integer columns are bit-identical between host and device.
+formula runs on the device (``aggb_generate``, ``k_gen`` in csrc/kernels.cuh), so
+any rank can regenerate its own slice, and integer columns are bit-identical between host and device.
 Normal draws go through libm on each side; parity tests for those columns copy
 the device bytes back instead of regenerating them.
 

@@ -7,15 +7,19 @@ the B200 through libaggb200 (include/aggb200.h); the algorithm id selects the
 GPU schedule:
 
 * pre_partitioning — fill the L2-resident table, freeze it at a kernel
-  boundary, probe (SMEM bloom first) and spill misses to HBM pages, recurse.
+  boundary, probe (SMEM bloom first) and spill misses to HBM pages, recurse
+  (for one-word keys and an integer COUNT/SUM/MIN/MAX spec: the write-combined
+  k_probe_wc scan/resolve and the one-wave compact children, csrc/wc.cuh).
 * original_hh — partition-0 table + raw spill of the other partitions,
   overflow cuts partition 0 into partial states (hybrid.py:431-451).
 * hash_sort — aggregate until full, cut the table to a run of partial states,
   merge the runs with a fold (hash-partitioned children).
 * sort_based — radix sort of the keys plus segmented reduction.
-* shared_hash, dynamic_destaging — same primitives; on the GPU both run the
-  pre-partitioning schedule (their differences are CPU frame-pool policies,
-  hybrid.py:579-1149, with no GPU counterpart).
+* shared_hash, dynamic_destaging — one table shared by every partition;
+  records of a destaged partition spill raw (MODE_DD passes).  When the table
+  runs dry, dynamic_destaging destages its largest resident partitions
+  (hybrid.py:974-1149); shared_hash cuts every partition but partition 0 at the
+  first overflow and partition 0 at the second (hybrid.py:579-915).
 """
 
 from __future__ import annotations

@@ -58,12 +58,24 @@ class EngineConfig:
 
 
 class FrameAllocatorView:
-    """What tests read from ctx.alloc: outstanding frames and the high-water mark."""
+    """What tests read from ctx.alloc (core.py:273-331): frames outstanding and
+    the high-water mark.  On the GPU the budget-governed memory is the resident
+    table: an open operator holds its frames until close (outstanding), and the
+    high-water mark is the frames its resident groups occupy in the reference's
+    layout (record + chain link + slot, hash_table.py:31-45) plus the output
+    frame, from the groups the device actually held (aggb_metrics
+    resident_groups).  The device's own bytes are Metrics.device_bytes."""
 
     def __init__(self, budget: int):
         self.budget = budget
         self.high_water = 0
         self.outstanding = 0
+
+    def hold(self, frames: int) -> None:
+        self.outstanding += frames
+
+    def release(self, frames: int) -> None:
+        self.outstanding -= frames
 
 
 class OpContext:
@@ -147,30 +159,59 @@ class Operator:
         self._dict: dict | None = None      # bytes -> id for keys longer than 15 bytes
         self._dict_keys: list = []
         self._last_key = None               # sorted-input check
+        self._klen_max = 0                  # widest key seen
+        self._key_total = 0                 # key bytes / records pushed (high-water accounting)
+        self._key_records = 0
+        self._pushed_any = False
         self._opened = False
 
     # -- interface ----------------------------------------------------------
 
     def open(self) -> None:
         """Validate the budget (InvalidBudget) and create the GPU handle."""
+        self._engine = self._make_engine(self.stats)
+        self.ctx.alloc.hold(1)  # the handle (released by close; run_operator checks for leaks)
+        self._opened = True
+
+    def _make_engine(self, stats):
         from paper_1311_0059_b200.engine import GroupBy
         cfg = self.ctx.cfg
         agg = self.ctx.agg
         # the GPU takes reference state records: one f64 column per state field
-        self._engine = GroupBy(
+        return GroupBy(
             self.algo_id, agg, ("i64", "i64"), ("f64",) * agg.state_width,
             memory_frames=cfg.memory_frames, frame_size=cfg.frame_size,
             budget_groups=cfg.budget_groups if cfg.budget_groups > 0 else 0,
-            stats=self.stats, seed=cfg.seed, fudge=cfg.fudge, slot_ratio=cfg.slot_ratio,
+            stats=stats, seed=cfg.seed, fudge=cfg.fudge, slot_ratio=cfg.slot_ratio,
             group_estimate=cfg.group_estimate, input_sorted=cfg.input_sorted,
             level=self.level, device=cfg.device, input_kind="states")
-        self._opened = True
+
+    def _key_bytes_seen(self, klen: int) -> None:
+        """The table's capacity in groups is planned from the stats' group bytes
+        (core.py DatasetStats, as the reference plans); its frames hold the actual
+        records.  When the first keys are wider than the stats assumed (the
+        reference's table would run out of frames earlier: first-fit failure,
+        hash_table.py:40, :56-59), the handle is re-planned with the record size
+        seen, before it holds anything."""
+        self._klen_max = max(self._klen_max, klen)
+        st, fs = self.stats, self.ctx.cfg.frame_size
+        if self._pushed_any or self.ctx.cfg.budget_groups > 0 or not st.G_t or not st.G:
+            return
+        rec = 2 + klen + 8 * self.ctx.agg.state_width
+        if rec > 1.1 * st.G * fs / st.G_t:
+            self._engine.close()
+            from paper_1311_0059_b200.core import DatasetStats
+            self._engine = self._make_engine(DatasetStats(R=st.R, R_t=st.R_t, G=st.G_t * rec / fs, G_t=st.G_t))
 
     def push(self, frame: np.ndarray) -> Iterator[np.ndarray] | None:
         if not self._opened:
             self.open()
         sw = self.ctx.agg.state_width
         dec = unpack_fixed([frame], sw)
+        if dec is not None and dec[0].shape[0]:
+            self._key_bytes_seen(int(dec[0].shape[1]))
+            self._key_total += int(dec[0].shape[0]) * int(dec[0].shape[1])
+            self._key_records += int(dec[0].shape[0])
         if dec is not None and dec[0].shape[1] <= MAX_WORD_KEY and self._dict is None:
             kb, st = dec
             if kb.shape[0]:
@@ -182,6 +223,9 @@ class Operator:
             recs = list(iter_records(np.asarray(frame, np.uint8), sw))
             if recs:
                 keys = [k for k, _ in recs]
+                self._key_bytes_seen(max(len(k) for k in keys))
+                self._key_total += sum(len(k) for k in keys)
+                self._key_records += len(keys)
                 if self.ctx.cfg.input_sorted:
                     self._check_sorted(keys)
                 st = np.array([v for _, v in recs], np.float64).reshape(len(recs), sw)
@@ -205,11 +249,18 @@ class Operator:
         m.spilled_bytes += met["spilled_bytes"]
         m.resident_groups += met["resident_groups"]
         m.kernel_launches += met["kernel_launches"]
-        m.high_water = max(m.high_water, min(self.ctx.memory_frames, self.ctx.memory_frames))
+        cfg = self.ctx.cfg
+        klen = self._key_total / self._key_records if self._key_records else 8.0
+        per = 2 + klen + 8 * self.ctx.agg.state_width + 8 + cfg.slot_ratio * 8
+        frames = -(-int(met["resident_groups"] * per) // cfg.frame_size) + 1
+        self.ctx.alloc.high_water = max(self.ctx.alloc.high_water, frames)
+        m.high_water = max(m.high_water, self.ctx.alloc.high_water)
+        m.device_bytes = max(m.device_bytes, met["high_water_bytes"])
         keys = self._decode(res.keys[0], res.keys[1])
         vals = res.as_float64()
         self._engine.close()
         self._engine = None
+        self.ctx.alloc.release(1)
         if self.algo_id == "sort_based" or res.sorted:
             order = sorted(range(len(keys)), key=keys.__getitem__)
             keys = [keys[i] for i in order]
@@ -330,6 +381,8 @@ def run_operator(op: Operator, source) -> Iterator[np.ndarray]:
     yield from finished(op.close())
     m.frames_read_total += getattr(source, "frames_read", 0)
     m.high_water = max(m.high_water, op.ctx.alloc.high_water)
+    if op.ctx.alloc.outstanding != 0:  # base.py:210-217
+        raise AggregationError(f"operator leaked {op.ctx.alloc.outstanding} frame(s)")
     m.total_time = time.perf_counter() - t0
 
 
