@@ -1556,7 +1556,6 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.pos_stride = stride;
   a.pos_count = h->wc_pos_count.as<unsigned long long>();
   a.pos_regions = grid;
-  a.dbg = getenv("AGGB_WC_DBG") ? atoi(getenv("AGGB_WC_DBG")) : 0;
   a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
   auto fs = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>
                          : k_probe_wc<ProgC1, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>;

@@ -42,9 +42,6 @@
 // (its pages are untouched).
 #pragma once
 #include "pass.cuh"
-#ifndef WC_EXP
-#define WC_EXP 0
-#endif
 
 namespace aggb {
 
@@ -104,6 +101,9 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
 }
 __device__ __forceinline__ void sts128(uint32_t a, uint64_t x, uint64_t y) {
   asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint16_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
@@ -172,7 +172,6 @@ struct WcArgs {
   unsigned long long* pos_count;
   int32_t pos_regions;
   int32_t pf;   // L2 prefetch of the batch tiles ahead
-  int32_t dbg;  // measurement hook (WC_RESOLVE): 1 no spills, 2 no REDs/spills, 3 no probe (wrong results)
 };
 
 template <int BLK, int R, int NS, int LINES>
@@ -186,8 +185,9 @@ struct WcLayout {
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
   static __host__ __device__ size_t ring_bytes(int P) { return (size_t)P * RS * 16; }
   static __host__ __device__ size_t meta_bytes(int P) { return ((size_t)P * (1 + NE) * 4 + 15) & ~(size_t)15; }
+  // + per-warp lists: the tile's positives (u16 stage index) and completed lines (u32)
   static __host__ __device__ size_t bytes(int P, uint32_t nblk) {
-    return stage_bytes() + ring_bytes(P) + (size_t)nblk * 8 + meta_bytes(P) + (size_t)T * 2;
+    return stage_bytes() + ring_bytes(P) + (size_t)nblk * 8 + meta_bytes(P) + (size_t)T * 2 + (size_t)T * 4;
   }
 };
 
@@ -206,10 +206,7 @@ struct WcLayout {
 // are parked for the next tile, windows move on; barrier 2 (ring, positive
 // list and stage free again; the stage's next tile is issued).
 constexpr int WC_SCAN = 0, WC_RESOLVE = 1;
-constexpr int WC_PF = 6;
-#ifndef WC_COOP
-#define WC_COOP 0
-#endif  // k_probe_wc: L2 prefetch distance in tiles (rounds of the grid)
+constexpr int WC_PF = 6;  // k_probe_wc: L2 prefetch distance in tiles (rounds of the grid)
 template <class PG, int BLK, int R, int NS, int LINES, int MODE>
 __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   using L = WcLayout<BLK, R, NS, LINES>;
@@ -228,12 +225,17 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   uint32_t* ent = cw + P;
   uint16_t* plist_t = (uint16_t*)((unsigned char*)cw + L::meta_bytes(P));  // this tile's positives (stage indices)
   const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_bloom = smem_u32(sbloom), a_cw = smem_u32(cw),
-                 a_pl = smem_u32(plist_t);
+                 a_pl = smem_u32(plist_t), a_lq = a_pl + 2u * T;
+  const int wid = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  // this warp's list of completed lines: entry = partition << 20 | line index (x >> 3)
+  const uint32_t a_wq = a_lq + 4u * (uint32_t)(wid * R * 32);
+  uint32_t nlq = 0;
   constexpr uint32_t CWM = (1u << 23) - 1;  // count bits
   constexpr int RS = L::RS;
   __shared__ __align__(8) uint64_t mbar[NS];
   __shared__ int s_tcnt[NS];
-  __shared__ uint32_t s_npos;
+  __shared__ uint32_t s_wpos[BLK / 32];  // WC_SCAN: positives per warp of the tile
   __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv;
   __shared__ uint32_t s_fd[MAX_STATES];
   __shared__ unsigned long long s_cnt[ST_NSTATS];
@@ -265,7 +267,6 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
   for (int i = tid; i < P * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
   for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg((const unsigned long long*)a.bloom + i);
   if (tid == 0) {
-    s_npos = 0;
     s_sb = s_su = s_sc = s_nb = s_nv = 0;
     for (int s = 0; s < NS; s++) mbar_init(&mbar[s], 1);
     mbar_fence_init();
@@ -385,10 +386,6 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
 
   auto spill = [&](uint64_t k, uint64_t v, int p, int q) {
     c_sp++;
-    if (MODE == WC_SCAN && a.dbg == 4) {
-      vabs ^= (uint32_t)(k ^ v) + p;
-      return;
-    }
     const uint32_t old = atoms_add(a_cw + 4u * (uint32_t)p, 1u);
     const uint32_t x = old & CWM;
     if (__builtin_expect((x & (S - 1)) == 0, 0)) alloc_page(p, x >> SLOG);
@@ -396,12 +393,19 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     ps[q] = p;
     if (__builtin_expect((((x >> 3) - (old >> 23)) & 511u) < (uint32_t)LINES, 1)) {
       sts128(a_ring + 16u * ((uint32_t)p * RS + (x & (RING - 1))), k, v);
-      lf |= (uint32_t)((x & 7u) == 7u && (MODE != WC_SCAN || a.dbg != 6)) << q;  // this thread sends the line after barrier 1
+      lf |= (uint32_t)((x & 7u) == 7u) << q;  // the line is complete: queued, sent after barrier 1
     } else {
       opend |= 1u << q;
       hk[q] = k;
       hv[q] = v;
     }
+  };
+  // (warp-uniform) a line slot q completed goes to the warp's line list
+  auto queue_line = [&](int q) {
+    const bool has = (lf >> q) & 1u;
+    const uint32_t m = __ballot_sync(0xffffffffu, has);
+    if (has) sts32(a_wq + 4u * (nlq + __popc(m & lt_mask)), ((uint32_t)ps[q] << 20) | ((xs[q] >> 3) & 0xFFFFFu));
+    nlq += __popc(m);
   };
 
   for (int it = 0;; it++) {
@@ -442,29 +446,26 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
         const uint64_t blk = lds64(a_bloom + 8u * wc_bloom_block(h3[r], nblk));
         pos3[r] = val3[r] & ((k3[r] == EMPTY) | ((blk & bits) == bits));
       }
-#pragma unroll
-      for (int r = 0; r < R; r++) c_rec += (uint32_t)val3[r];
+      // positives: this warp's slice of the tile's list (R * 32 entries per warp)
+      const uint32_t a_wl = a_pl + 2u * (uint32_t)(wid * R * 32);
+      uint32_t wpos = 0;
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        const uint64_t v = val3[r] ? v3[r] : 0ull;
-        vbad |= (uint32_t)((v + 0x80000000ull) >> 32);
-        vabs = max(vabs, (uint32_t)abs((int)(uint32_t)v));
-        // positives: the tile's list (one shared atomic per warp)
+        // value range (compact children): some |v| >= 2^31, and max |v| otherwise
+        const uint32_t lo = val3[r] ? (uint32_t)v3[r] : 0u, hi = val3[r] ? (uint32_t)(v3[r] >> 32) : 0u;
+        vbad |= hi ^ (uint32_t)((int)lo >> 31);
+        vabs = max(vabs, (uint32_t)abs((int)lo));
         const uint32_t m = __ballot_sync(0xffffffffu, pos3[r]);
-        if (m) {
-          uint32_t base = 0;
-          if (lane == 0) base = atoms_add(smem_u32(&s_npos), (uint32_t)__popc(m));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (pos3[r]) sts16(a_pl + 2u * (base + __popc(m & ((1u << lane) - 1u))), (uint16_t)(r * BLK + tid));
-        }
+        if (pos3[r]) sts16(a_wl + 2u * (wpos + __popc(m & lt_mask)), (uint16_t)(r * BLK + tid));
+        wpos += __popc(m);
         if (val3[r] & !pos3[r]) spill(k3[r], v3[r], (int)reduce32(h3[r], (uint32_t)P), r);
+        queue_line(r);
       }
+      if (lane == 0) s_wpos[wid] = wpos;
+      c_rec += c > tid ? (uint32_t)min(R, (c - tid + BLK - 1) / BLK) : 0u;  // this thread's records of the tile
     } else {
       // probe the frozen table: all R first buckets in flight together
-      if (a.dbg == 3) {
-#pragma unroll
-        for (int r = 0; r < R; r++) vabs += (uint32_t)(k3[r] ^ v3[r] ^ h3[r]) & (val3[r] ? 1u : 0u);
-      } else {
+      {
       // the first two buckets (64 B) of every record are loaded together: a miss
       // must reach an empty slot and a displaced key the next bucket, and a warp
       // waits for its slowest lane (one more dependent L2 round trip per tile)
@@ -516,12 +517,15 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
         }
         if (sl >= 0) {
           const uint64_t vv[1] = {v3[r]};
-          if (a.dbg < 2) Upd<PG>::template g<1>(a.t.states, a.t.fstride, (uint64_t)sl * a.t.sstride, 0, s_fd, ns, vv);
+          Upd<PG>::template g<1>(a.t.states, a.t.fstride, (uint64_t)sl * a.t.sstride, 0, s_fd, ns, vv);
           c_hit++;
-        } else if (a.dbg == 0) {
+        } else {
           spill(k, v3[r], k == EMPTY ? 0 : (int)reduce32(h3[r], (uint32_t)P), r);
         }
       }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; r++) queue_line(r);
       }
     }
     const bool more = c != 0;
@@ -543,52 +547,41 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
         s_nv = 0;
       }
     }
-    // ---- [B1] owned lines
-    if constexpr (WC_COOP) {
-      // the warp copies its owners' lines 4 at a time: lane group g = lane >> 3
-      // takes the g-th owner, each lane one 16-byte chunk (one 128-byte store group)
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        uint32_t m = __ballot_sync(0xffffffffu, (lf >> r) & 1u);
-        while (m) {
-          uint32_t mm = m;
-          const int g = lane >> 3;
-          for (int i = 0; i < g; i++) mm &= mm - 1;
-          const int src = mm ? __ffs(mm) - 1 : -1;
-#pragma unroll
-          for (int i = 0; i < 4; i++) m &= m - 1;
-          const int sp = __shfl_sync(0xffffffffu, ps[r], src & 31);
-          const uint32_t sx = __shfl_sync(0xffffffffu, xs[r], src & 31);
-          if (src >= 0) {
-            const uint32_t x = (sx & ~7u) | (uint32_t)(lane & 7);
-            const uint32_t pg = page_of(sp, x >> SLOG);
-            const uint64_t* rp = (const uint64_t*)&ring[sp * RS + (x & (RING - 1))];
-            if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), make_ulonglong2(rp[0], rp[1]));
-          }
-        }
-      }
-      lf = 0;
-    } else if (lf) {  // 128-byte bulk copies (TMA engine)
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        if (!((lf >> r) & 1u)) continue;
-        const uint32_t x0 = xs[r] & ~7u;
-        const uint32_t pg = page_of(ps[r], x0 >> SLOG);
-        if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[ps[r] * RS + (x0 & (RING - 1))], 128u);
-      }
-      bulk_commit();
+    // ---- [B1] the warp's completed lines: 128-byte bulk copies (TMA engine), one per lane
+    bool sent = false;
+    for (uint32_t i = (uint32_t)lane; i < nlq; i += 32) {
+      const uint32_t e = lds32(a_wq + 4u * i);
+      const int p = (int)(e >> 20);
+      const uint32_t x0 = (e & 0xFFFFFu) << 3;
+      const uint32_t pg = page_of(p, x0 >> SLOG);
+      if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[p * RS + (x0 & (RING - 1))], 128u);
+      sent = true;
     }
+    if (sent) bulk_commit();
+    nlq = 0;
+    lf = 0;
     if constexpr (MODE == WC_SCAN) {
-      // ---- [B2] the tile's positives to this CTA's region (SoA), coalesced
-      const uint32_t npos = s_npos;
-      unsigned long long* pk = (unsigned long long*)a.pos + (size_t)blockIdx.x * a.pos_stride + pcur;
+      // ---- [B2] the tile's positives to this CTA's region (SoA), coalesced: warp w
+      // writes its list after the lists of warps 0 .. w-1
+      constexpr int NW = BLK / 32;
+      const uint32_t wc_l = lane < NW ? s_wpos[lane] : 0u;
+      uint32_t before = lane < wid ? wc_l : 0u, all = wc_l;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        before += __shfl_xor_sync(0xffffffffu, before, o);
+        all += __shfl_xor_sync(0xffffffffu, all, o);
+      }
+      const uint32_t mine = __shfl_sync(0xffffffffu, wc_l, wid);
+      unsigned long long* pk = (unsigned long long*)a.pos + (size_t)blockIdx.x * a.pos_stride + pcur + before;
       unsigned long long* pv = pk + (size_t)a.pos_regions * a.pos_stride;
-      for (uint32_t i = tid; i < npos; i += BLK) {
-        const uint32_t idx = plist_t[i];
+      const uint32_t a_wl = a_pl + 2u * (uint32_t)(wid * R * 32);
+      for (uint32_t i = (uint32_t)lane; i < mine; i += 32) {
+        uint16_t idx;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(idx) : "r"(a_wl + 2u * i));
         __stcg(pk + i, sk[idx]);
         __stcg(pv + i, sv[idx]);
       }
-      pcur += npos;
+      pcur += all;
     }
     // ---- [B3] held records: complete lines straight to their page, the open line waits
     if (__builtin_expect(opend != 0, 0)) {
@@ -608,20 +601,14 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
       const uint32_t cc = cw[p] & CWM;
       cw[p] = ((cc >> 3) << 23) | cc;
     }
-    if (lf) {
-      bulk_wait_read0();
-      lf = 0;
-    }
+    if (sent) bulk_wait_read0();  // the ring slots are read before barrier 2
     // ---- barrier 2: ring, positive list and stage are free again
     if (!more) {
       if (!__syncthreads_or(opark != 0)) break;
     } else {
       __syncthreads();
     }
-    if (tid == 0) {
-      s_npos = 0;
-      issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
-    }
+    if (tid == 0) issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
   // ---- close: every chain's open line (all in the ring), then the page fills
