@@ -1314,7 +1314,17 @@ void wc_plan(Handle* h, double spill_groups) {
 }
 
 int setup_table(Handle* h) {
-  int64_t slots = next_pow2(std::max<int64_t>(64, 2 * std::max<int64_t>(h->budget, h->skew_cap)));
+  // The write-combined resolve probes one 32-byte bucket per bloom positive; a
+  // chain past it costs the warp a dependent L2 round trip, so its tables are
+  // sparser (8 slots per group: C2's 125K groups in 1M slots, 40 MB in L2;
+  // resolve 1.03 -> 0.71 ms against 2 slots per group) while they stay L2-sized.
+  int64_t sx = 2;
+  if (h->wc) {
+    const double per_slot = 8.0 * (h->kw + std::max(1, h->cs.ds.ns));
+    while (sx < 8 && (double)next_pow2(2 * sx * h->budget) * per_slot <= 48e6) sx *= 2;
+    if (getenv("AGGB_WC_SLOTS_X")) sx = std::max(2, atoi(getenv("AGGB_WC_SLOTS_X")));  // experiment override
+  }
+  int64_t slots = next_pow2(std::max<int64_t>(64, sx * std::max<int64_t>(h->budget, h->skew_cap)));
   GTable& t = h->tab;
   t.stride = (uint64_t)slots + 1;
   t.mask = (uint64_t)slots - 1;
@@ -1557,6 +1567,7 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.pos_count = h->wc_pos_count.as<unsigned long long>();
   a.pos_regions = grid;
   a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
+  a.pf2 = getenv("AGGB_WC_PF2") ? atoi(getenv("AGGB_WC_PF2")) : 0;  // (sparse tables: one bucket suffices)
   auto fs = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>
                          : k_probe_wc<ProgC1, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>;
   auto fr = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_RR, WC_RNS, WC_LINES, WC_RESOLVE>

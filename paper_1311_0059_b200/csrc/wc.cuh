@@ -172,6 +172,7 @@ struct WcArgs {
   unsigned long long* pos_count;
   int32_t pos_regions;
   int32_t pf;   // L2 prefetch of the batch tiles ahead
+  int32_t pf2;  // WC_RESOLVE: load the second bucket with the first
 };
 
 template <int BLK, int R, int NS, int LINES>
@@ -408,10 +409,43 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     nlq += __popc(m);
   };
 
+  // WC_RESOLVE: the records of the tile being processed and their first two
+  // buckets, loaded one iteration ahead (software pipeline: a tile's L2 bucket
+  // latency hides behind the previous tile's work)
+  uint64_t rk[R], rv[R], rh[R];
+  ulonglong2 rb[R][4];
+  int rc = 0;
+  auto resolve_fetch = [&](int t) {  // wait for tile t's stage, load its records, request their buckets
+    const int st = t % NS;
+    mbar_wait(&mbar[st], (uint32_t)((t / NS) & 1));
+    rc = s_tcnt[st];
+    const uint32_t a_k = a_stg + (uint32_t)st * 2u * T * 8u, a_v = a_k + T * 8u;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const int idx = r * BLK + tid;
+      rk[r] = lds64(a_k + 8u * (uint32_t)idx);
+      rv[r] = lds64(a_v + 8u * (uint32_t)idx);
+      const uint64_t kk[1] = {rk[r]};
+      rh[r] = hash_key<1>(kk, a.t.seed);
+      const uint64_t b = rh[r] & a.t.bmask;
+      if (idx < rc && rk[r] != EMPTY) {
+        ld_bucket32(a.t.keys + b * 4, rb[r][0], rb[r][1]);
+        if (a.pf2) ld_bucket32(a.t.keys + ((b + 1) & a.t.bmask) * 4, rb[r][2], rb[r][3]);
+        else rb[r][2] = rb[r][3] = make_ulonglong2(0, 0);  // (not EMPTY, no key: the chain walk below decides)
+      }
+    }
+  };
+  if constexpr (MODE == WC_RESOLVE) resolve_fetch(0);
+
   for (int it = 0;; it++) {
     const int s = it % NS;
-    mbar_wait(&mbar[s], (uint32_t)((it / NS) & 1));
-    const int c = s_tcnt[s];
+    int c;
+    if constexpr (MODE == WC_SCAN) {
+      mbar_wait(&mbar[s], (uint32_t)((it / NS) & 1));
+      c = s_tcnt[s];
+    } else {
+      c = rc;
+    }
     if (tid == 0 && a.stash && !nb_busy && !s_nv && 2 * s_su >= s_sc) {  // next stash, taken after barrier 1
       nb_pending = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
       nb_busy = true;
@@ -433,10 +467,16 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     for (int r = 0; r < R; r++) {  // loads and hashes of all R records first (ILP)
       const int idx = r * BLK + tid;
       val3[r] = idx < c;
-      k3[r] = lds64(a_sk + 8u * (uint32_t)idx);
-      v3[r] = lds64(a_sv + 8u * (uint32_t)idx);
-      const uint64_t kk[1] = {k3[r]};
-      h3[r] = hash_key<1>(kk, a.t.seed);
+      if constexpr (MODE == WC_SCAN) {
+        k3[r] = lds64(a_sk + 8u * (uint32_t)idx);
+        v3[r] = lds64(a_sv + 8u * (uint32_t)idx);
+        const uint64_t kk[1] = {k3[r]};
+        h3[r] = hash_key<1>(kk, a.t.seed);
+      } else {
+        k3[r] = rk[r];
+        v3[r] = rv[r];
+        h3[r] = rh[r];
+      }
     }
     if constexpr (MODE == WC_SCAN) {
       bool pos3[R];
@@ -466,19 +506,17 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
     } else {
       // probe the frozen table: all R first buckets in flight together
       {
-      // the first two buckets (64 B) of every record are loaded together: a miss
-      // must reach an empty slot and a displaced key the next bucket, and a warp
-      // waits for its slowest lane (one more dependent L2 round trip per tile)
+      // the first two buckets (64 B) of every record arrived during the last
+      // tile: a miss must reach an empty slot and a displaced key the next bucket
       uint64_t bb[R];
       ulonglong2 bx[R][4];
 #pragma unroll
       for (int r = 0; r < R; r++) {
         bb[r] = h3[r] & a.t.bmask;
-        if (val3[r] && k3[r] != EMPTY) {
-          ld_bucket32(a.t.keys + bb[r] * 4, bx[r][0], bx[r][1]);
-          ld_bucket32(a.t.keys + ((bb[r] + 1) & a.t.bmask) * 4, bx[r][2], bx[r][3]);
-        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) bx[r][i] = rb[r][i];
       }
+      if (c) resolve_fetch(it + 1);  // the next tile's records and buckets go in flight now
 #pragma unroll
       for (int r = 0; r < R; r++) {
         if (!val3[r]) continue;
@@ -497,12 +535,14 @@ __global__ void __launch_bounds__(BLK, 1) k_probe_wc(WcArgs a) {
                               ((uint32_t)(x1.x == EMPTY) << 4) | ((uint32_t)(x1.y == EMPTY) << 5) |
                               ((uint32_t)(y1.x == EMPTY) << 6) | ((uint32_t)(y1.y == EMPTY) << 7);
           // (a key sits before the first empty slot of its chain)
-          const uint32_t hbit = hm & -hm, ebit = em & -em;
-          if (hm && (!em || hbit < ebit)) {
-            const int i = __ffs(hm) - 1;
+          const uint32_t known = a.pf2 ? 0xFFu : 0x0Fu;  // buckets loaded
+          const uint32_t hmk = hm & known, emk = em & known;
+          const uint32_t hbit = hmk & -hmk, ebit = emk & -emk;
+          if (hmk && (!emk || hbit < ebit)) {
+            const int i = __ffs(hmk) - 1;
             sl = (int64_t)(((bb[r] + (uint32_t)(i >> 2)) & a.t.bmask) * 4 + (uint32_t)(i & 3));
-          } else if (!em) {  // both buckets full and no match: walk on
-            uint64_t b = (bb[r] + 2) & a.t.bmask;
+          } else if (!emk) {  // the loaded buckets are full and hold no match: walk on
+            uint64_t b = (bb[r] + (a.pf2 ? 2u : 1u)) & a.t.bmask;
             for (;;) {
               ulonglong2 x, y;
               ld_bucket32(a.t.keys + b * 4, x, y);
