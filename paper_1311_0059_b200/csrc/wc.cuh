@@ -42,87 +42,10 @@
 // (its pages are untouched).
 #pragma once
 #include "pass.cuh"
+#include "ptx.cuh"
 
 namespace aggb {
 
-// ---------------------------------------------------------------------------
-// PTX: mbarrier + 1-D bulk copy global -> shared (TMA engine)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-          smem_u32(m)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(m))
-               : "memory");
-}
-// one 128-byte (or any 16-byte multiple) shared -> global bulk copy by the TMA engine
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-// bring a global range into L2 ahead of its bulk copy into shared memory (no
-// shared memory held: the stages then wait on L2, not DRAM, latency)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-// generic-proxy shared-memory writes before async-proxy (bulk copy) reads of them
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// shared memory through 32-bit addresses (a generic pointer costs an address-space
-// conversion per access, and the compiler wraps generic atomics in a warp
-// aggregation it cannot prove unnecessary)
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint64_t lds64(uint32_t a) {
-  uint64_t v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint64_t x, uint64_t y) {
-  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(a), "l"(x), "l"(y) : "memory");
-}
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void sts16(uint32_t a, uint16_t v) {
-  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t atoms_add(uint32_t a, uint32_t v) {
-  uint32_t r;
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
-  return r;
-}
-// one 32-byte table bucket with a single 256-bit load (LDG.E.ENL2.256: one L1TEX
-// wavefront per lane instead of two for a pair of 16-byte loads)
-__device__ __forceinline__ void ld_bucket32(const uint64_t* p, ulonglong2& x, ulonglong2& y) {
-  asm volatile("ld.global.cg.v4.u64 {%0, %1, %2, %3}, [%4];"
-               : "=l"(x.x), "=l"(x.y), "=l"(y.x), "=l"(y.y)
-               : "l"(p));
-}
-__device__ __forceinline__ void st_v2(void* p, ulonglong2 v) {
-  asm volatile("st.global.cg.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v.x), "l"(v.y) : "memory");
-}
 
 // bloom of the frozen table for k_probe_wc: any number of 64-bit blocks (block
 // from the low 32 hash bits by multiply-high; the table bucket uses bits 0-15,
