@@ -379,7 +379,7 @@ def roofline(out, args, peak):
     steps = args.steps
     groups = {}
     # level-0 pass (FILL + PROBE / ROUTE): reads the batch, writes the spill
-    l0 = [k for k in ks if (k.startswith("k_pass<") and "GRACE" not in k) or k.startswith("k_probe_wc")]
+    l0 = [k for k in ks if (k.startswith("k_pass<") and "GRACE" not in k) or k in ("k_scan_wc", "k_wc_build")]
     if l0:
         ms = sum(ks[k][1] for k in l0) / steps
         nl = sum(ks[k][0] for k in l0) / steps

@@ -23,7 +23,7 @@
 #include "pass.cuh"
 #include "probe.cuh"
 #include "sort.cuh"
-#include "wc.cuh"
+#include "wc2.cuh"
 
 using namespace aggb;
 
@@ -649,7 +649,10 @@ struct Handle {
   int wc_table_bytes = 0;     // child shared-memory table
   uint32_t wc_plist_cap = 0;  // page-list entries per partition
   int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
-  DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_pos, wc_pos_count;
+  int wcQ = 0;                // owner runs (the spill partitions are P0; runs = P0 + wcQ)
+  uint32_t wc_ocap = 0;       // resident slots per owner list
+  int64_t wc_launches = 0;    // k_scan_wc launches of this run (page-list sizing)
+  DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_olist, wc_olist_n, wc_gather;
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
   DBuf sort_keys, sort_vals;
@@ -674,7 +677,7 @@ struct Handle {
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
                         "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>", "k_split",
-                        "k_probe_wc<scan>", "k_probe_wc<resolve>", "k_child_wc"};
+                        "k_scan_wc", "k_wc_build", "k_child_wc"};
 constexpr int NKINDS = 18;
 
 int prof_begin(Handle* h, int kid) {
@@ -1269,61 +1272,61 @@ int plan(Handle* h) {
   return AGGB_OK;
 }
 
-// The write-combined level-0 path (wc.cuh) for budgeted pre-partitioning of
+// The write-combined level-0 path (wc2.cuh) for budgeted pre-partitioning of
 // one-word keys and one int64 value column with an integer COUNT/SUM/MIN/MAX
-// spec.  Its children are one CTA per SM with a compact table (u32 states) in
-// shared memory, run in whole waves: the fan-out is the smallest multiple of
-// the SM count that leaves every child table at most ~40% full, and it must
-// leave the level-0 pass room for its bloom filter (>= 2 bits per resident key).
-// scan: 4 records per thread per tile, double-buffered stages (per-tile
-// overhead halved: C2 scan 1.64 -> 1.36 ms against 2 per thread x 3 stages);
-// resolve (no bloom in shared memory): 2 x 3
-#ifndef WC_RR_
-#define WC_RR_ 2
-#endif
-constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_RR = WC_RR_, WC_RNS = 3, WC_LINES = 2, WC_CBLK = 1024, WC_CRL = 4;
-using WcL = WcLayout<WC_BLK, WC_R, WC_NS, WC_LINES>;
-using WcLR = WcLayout<WC_BLK, WC_RR, WC_RNS, WC_LINES>;
+// spec.  Level 0 routes every record into a run: P0 spill partitions (filter
+// negatives) and wcQ owner runs (filter positives: resident keys and false
+// positives).  Every run is aggregated by one child CTA with a compact table
+// (u32 states) in shared memory, in whole waves: the number of runs is the
+// smallest multiple of the SM count that leaves every child table at most ~45%
+// full, and it must leave the scan room for its filter (>= 2 bits per resident
+// key) beside the runs' write-combining rings.  The owner share follows the
+// expected records: resident groups plus the filter's false-positive share of
+// the others.
+constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_CBLK = 1024, WC_CRL = 4;
+using Wc2L = Wc2Layout<WC_BLK, WC_R, WC_NS>;
 void wc_plan(Handle* h, double spill_groups) {
   h->wc = false;
+  h->wcQ = 0;
   const aggb_config& c = h->cfg;
   if (c.algo != AGGB_PRE_PARTITIONING || h->kw != 1 || h->cs.nv != 1 || (h->prog != 1 && h->prog != 2) ||
       h->unlimited || h->l2_capped || c.level != 0 || h->cs.ds.vty[0] != TY_I64 || getenv("AGGB_NO_WC") ||
       getenv("AGGB_FORCE_L2_CHILDREN"))
     return;
-  const int words = 2 + (h->prog == 2 ? 4 : 2);  // key, count word, one u32 per other field
+  const int words = 2 + (h->prog == 2 ? 4 : 2) + 1;  // key, count word, one u32 per other field, owner slot word
   const int tbytes = 220 * 1024;
   const int nslots = ((tbytes / 4 - 2) / words - 1) / 4 * 4;
   const int sms = std::max(1, h->sms);
-  int P = (int)std::ceil(std::max(1.0, spill_groups) / (0.4 * nslots));
-  P = (P + sms - 1) / sms * sms;
-  if (getenv("AGGB_WC_P0")) P = std::max(1, atoi(getenv("AGGB_WC_P0")));  // experiment override
-  const size_t fixed = WcL::bytes(P, 0) + 1024;
+  const double resident = (double)std::max<int64_t>(1, h->budget);
+  const double spill = std::max(1.0, spill_groups);
+  int I = (int)std::ceil((spill + resident) / (0.45 * nslots));
+  I = std::max(2, (I + sms - 1) / sms * sms);
+  if (getenv("AGGB_WC_RUNS")) I = std::max(2, atoi(getenv("AGGB_WC_RUNS")));  // experiment override
+  const size_t fixed = Wc2L::bytes(I, 0) + 1024;
   if (fixed >= 227 * 1024) return;
-  const int64_t want = std::max<int64_t>(64, (int64_t)(8 * h->budget) / 64);  // ~8 bits per resident key
-  const int64_t room = (int64_t)((227 * 1024 - fixed) / 8);
+  const int64_t want = std::max<int64_t>(64, (int64_t)(8 * h->budget) / 32);  // ~8 bits per resident key
+  const int64_t room = (int64_t)((227 * 1024 - fixed) / 4);
   const int64_t nblk = std::min(want, room);
-  if (nblk < std::max<int64_t>(16, (int64_t)(2 * h->budget) / 64)) return;
+  if (nblk < std::max<int64_t>(16, (int64_t)(2 * h->budget) / 32)) return;
+  // false-positive share of a 3-bit filter in 32-bit blocks (the block loads vary: +15%)
+  const double bpk = 32.0 * (double)nblk / resident;
+  const double fp = std::min(1.0, 1.15 * std::pow(1.0 - std::exp(-3.0 / bpk), 3.0));
+  const double share = (resident + fp * spill) / (resident + spill);
+  int Q = (int)std::lround(I * share);
+  Q = std::max(1, std::min(I - 1, Q));
+  if (getenv("AGGB_WC_OWNERS")) Q = std::max(1, std::min(I - 1, atoi(getenv("AGGB_WC_OWNERS"))));  // experiment override
   h->wc = true;
   h->wc_nblk = (uint32_t)nblk;
   h->wc_table_bytes = tbytes;
-  h->P0 = P;
+  h->wcQ = Q;
+  h->P0 = I - Q;
   h->nsub0 = 1;
-  h->fanout_need = P;
+  h->fanout_need = h->P0;
   h->l2_children = false;
 }
 
 int setup_table(Handle* h) {
-  // The write-combined resolve probes one 32-byte bucket per bloom positive; a
-  // chain past it costs the warp a dependent L2 round trip, so its tables are
-  // sparser (8 slots per group: C2's 125K groups in 1M slots, 40 MB in L2;
-  // resolve 1.03 -> 0.71 ms against 2 slots per group) while they stay L2-sized.
-  int64_t sx = 2;
-  if (h->wc) {
-    const double per_slot = 8.0 * (h->kw + std::max(1, h->cs.ds.ns));
-    while (sx < 8 && (double)next_pow2(2 * sx * h->budget) * per_slot <= 48e6) sx *= 2;
-    if (getenv("AGGB_WC_SLOTS_X")) sx = std::max(2, atoi(getenv("AGGB_WC_SLOTS_X")));  // experiment override
-  }
+  const int64_t sx = 2;
   int64_t slots = next_pow2(std::max<int64_t>(64, sx * std::max<int64_t>(h->budget, h->skew_cap)));
   GTable& t = h->tab;
   t.stride = (uint64_t)slots + 1;
@@ -1409,17 +1412,18 @@ int begin_run(Handle* h) {
   }
   if (h->has_table) TRY(table_reset(h));
   h->wc_used = false;
+  h->wc_launches = 0;
   if (h->wc) {
-    const size_t P = (size_t)h->P0;
-    TRY(h->wc_pn.ensure(P * 4, &h->hw));
-    TRY(h->wc_recs.ensure(P * 8, &h->hw));
-    TRY(h->wc_failed.ensure(P * 4, &h->hw));
+    const size_t NP = (size_t)h->P0 + (size_t)h->wcQ;
+    TRY(h->wc_pn.ensure(NP * 4, &h->hw));
+    TRY(h->wc_recs.ensure(NP * 8, &h->hw));
+    TRY(h->wc_failed.ensure(NP * 4, &h->hw));
     TRY(h->wc_vinfo.ensure(8, &h->hw));
     TRY(h->wc_fail.ensure(8, &h->hw));
-    TRY(h->wc_bloom.ensure((size_t)h->wc_nblk * 8, &h->hw));
-    CU(cudaMemsetAsync(h->wc_pn.p, 0, P * 4, h->st));
-    CU(cudaMemsetAsync(h->wc_recs.p, 0, P * 8, h->st));
-    CU(cudaMemsetAsync(h->wc_failed.p, 0, P * 4, h->st));
+    TRY(h->wc_bloom.ensure((size_t)h->wc_nblk * 4, &h->hw));
+    CU(cudaMemsetAsync(h->wc_pn.p, 0, NP * 4, h->st));
+    CU(cudaMemsetAsync(h->wc_recs.p, 0, NP * 8, h->st));
+    CU(cudaMemsetAsync(h->wc_failed.p, 0, NP * 4, h->st));
     CU(cudaMemsetAsync(h->wc_vinfo.p, 0, 8, h->st));
     CU(cudaMemsetAsync(h->wc_fail.p, 0, 8, h->st));
   }
@@ -1486,56 +1490,74 @@ int ensure_defer(Handle* h, int64_t T, int payload_words) {
 
 int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss);
 
-// k_probe_wc reads the key and value columns with 16-byte bulk copies
+// k_scan_wc reads the key and value columns with 16-byte bulk copies
 bool wc_eligible(Handle* h, const ColSrc& col) {
-  // (a chain's claim counter has 23 bits: at most ~8M records per CTA and launch)
+  // (a run's claim counter has 23 bits: at most ~8M records per CTA and launch)
   return col.nv == 1 && dense8(col, 1) && col.kty[0] == TY_I64 && col.vty[0] == TY_I64 &&
          col.n + h->defer_cap <= (int64_t)1200000000 &&
          ((uintptr_t)col.key[0] & 15) == 0 && ((uintptr_t)col.val[0] & 15) == 0 && !h->hot_ready &&
-         h->pool_bound + (uint64_t)(col.n + h->defer_cap) / 256 + (uint64_t)h->sms * (4ull * h->P0 + 128) < 0xFFFFF0ull;
+         h->pool_bound + (uint64_t)(col.n + h->defer_cap) / 256 +
+                 (uint64_t)h->sms * (4ull * (h->P0 + h->wcQ) + 128) < 0xFFFFF0ull;
 }
 
-// PROBE through k_probe_wc (partition half) + k_resolve_wc (the bloom positives)
-int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
-  const int P = ss.nparts;
-  const int grid = h->sms;
-  const int64_t T = WcL::T;
-  // the filter of the table as FILL left it (a kernel boundary: the key set is final once frozen)
-  CU(cudaMemsetAsync(h->wc_bloom.p, 0, (size_t)h->wc_nblk * 8, h->st));
-  int pe = prof_begin(h, 12);
-  k_bloom_build_wc<<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->wc_bloom.as<uint64_t>(), h->wc_nblk);
+// the filter of the frozen table (bloom) and / or the owners' lists of resident slots
+int wc_build(Handle* h, bool bloom, bool owners) {
+  const uint64_t seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+  if (bloom) CU(cudaMemsetAsync(h->wc_bloom.p, 0, (size_t)h->wc_nblk * 4, h->st));
+  if (owners) {
+    // a list holds twice an owner's share of the budget (small budgets: all of it)
+    const uint64_t cap = h->tab.cap;
+    h->wc_ocap = (uint32_t)std::min<uint64_t>(cap + 1, 2 * cap / (uint64_t)h->wcQ + 1024);
+    TRY(h->wc_olist.ensure((size_t)h->wcQ * h->wc_ocap * 4, &h->hw));
+    TRY(h->wc_olist_n.ensure((size_t)h->wcQ * 4, &h->hw));
+    CU(cudaMemsetAsync(h->wc_olist_n.p, 0, (size_t)h->wcQ * 4, h->st));
+  }
+  int pe = prof_begin(h, 16);
+  k_wc2_build<<<h->sms * 4, 256, 0, h->st>>>(h->tab, seed, bloom ? h->wc_bloom.as<uint32_t>() : nullptr, h->wc_nblk,
+                                             owners ? h->wc_olist.as<uint32_t>() : nullptr,
+                                             owners ? h->wc_olist_n.as<uint32_t>() : nullptr, h->wc_ocap,
+                                             (uint32_t)h->wcQ);
   prof_end(h, pe);
+  CU(cudaGetLastError());
   h->launches++;
+  return AGGB_OK;
+}
+
+// PROBE through k_scan_wc: every record of the batch (and FILL's deferral list) into its run
+int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
+  const int P = h->P0, NP = h->P0 + h->wcQ;
+  const int grid = h->sms;
+  const int64_t T = Wc2L::T;
+  // the filter of the table as FILL left it (a kernel boundary: the key set is final once frozen)
+  TRY(wc_build(h, true, false));
   const int64_t nlin_cap = h->defer_cap;
-  // bloom positives: one region per CTA, room for every record it may read
-  const int64_t tiles = (col.n + T - 1) / T + (nlin_cap + T - 1) / T;
-  const int64_t stride = ((tiles + grid - 1) / grid + 1) * T;
-  TRY(h->wc_pos.ensure((size_t)stride * grid * 16, &h->hw));
-  TRY(h->wc_pos_count.ensure((size_t)grid * 8, &h->hw));
-  // page lists: every record of the run so far, at twice the mean pages per partition
+  // page lists: every record of the run so far at twice the mean pages per run, and
+  // one open page per CTA and launch
+  h->wc_launches++;
   const int64_t recs_run = h->records + col.n + nlin_cap;
   const uint32_t need_cap = (uint32_t)std::min<int64_t>(
-      0x7FFFFFFF, 2 * (recs_run / 512 / std::max(1, P)) + 4 * (int64_t)grid + 64);
+      0x7FFFFFFF, 2 * (recs_run / 512 / std::max(1, NP)) + (h->wc_launches + 3) * (int64_t)grid + 64);
   if (need_cap > h->wc_plist_cap) {
     DBuf nb;
-    TRY(nb.ensure((size_t)P * need_cap * 4, &h->hw));
+    const uint32_t new_cap = std::max(need_cap, h->wc_used ? 2 * h->wc_plist_cap : 0u);
+    TRY(nb.ensure((size_t)NP * new_cap * 4, &h->hw));
     if (h->wc_used && h->wc_plist_cap)
-      CU(cudaMemcpy2DAsync(nb.p, (size_t)need_cap * 4, h->wc_plist.p, (size_t)h->wc_plist_cap * 4,
-                           (size_t)h->wc_plist_cap * 4, (size_t)P, cudaMemcpyDeviceToDevice, h->st));
+      CU(cudaMemcpy2DAsync(nb.p, (size_t)new_cap * 4, h->wc_plist.p, (size_t)h->wc_plist_cap * 4,
+                           (size_t)h->wc_plist_cap * 4, (size_t)NP, cudaMemcpyDeviceToDevice, h->st));
     CU(cudaStreamSynchronize(h->st));
     h->wc_plist.release();
     h->wc_plist = nb;
     nb.p = nullptr;
-    h->wc_plist_cap = need_cap;
+    h->wc_plist_cap = new_cap;
   }
-  // pages: the records, plus each (CTA, partition) chain's last page, plus stashes
+  // pages: the records, plus each (CTA, run) chain's last page, plus stashes
   const int stash = 32;
-  const uint64_t pages = (uint64_t)((col.n + nlin_cap) / 512) + 2ull * grid * P + 4ull * grid * stash + 64;
+  const uint64_t pages = (uint64_t)((col.n + nlin_cap) / 512) + 2ull * grid * NP + 4ull * grid * stash + 64;
   TRY(pool_ensure(h, pages));
-  WcArgs a;
+  Wc2Args a;
   memset(&a, 0, sizeof(a));
-  a.sp = h->cs.ds;
   a.t = h->tab;
+  a.seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
   a.key = (const unsigned long long*)col.key[0];
   a.val = (const unsigned long long*)col.val[0];
   a.n = col.n;
@@ -1549,41 +1571,29 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.lkey = (const unsigned long long*)h->defer.as<uint64_t>();
   a.lval = (const unsigned long long*)(h->defer.as<uint64_t>() + h->defer_cap);
   a.lcount = SC(h) + 10;
-  a.bloom = h->wc_bloom.as<uint64_t>();
+  a.bloom = h->wc_bloom.as<uint32_t>();
   a.nblk = h->wc_nblk;
   a.pool = pool_of(h);
-  a.ss = ss;
+  a.set_id = ss.id;
+  a.P = P;
+  a.Q = h->wcQ;
   a.plist = h->wc_plist.as<uint32_t>();
   a.plist_n = h->wc_pn.as<uint32_t>();
   a.plist_cap = h->wc_plist_cap;
   a.part_recs = h->wc_recs.as<unsigned long long>();
-  a.tile_counter = SC(h) + 20;
   a.stats = SC(h);
   a.vinfo = h->wc_vinfo.as<unsigned int>();
   a.fail = h->wc_fail.as<uint32_t>();
   a.stash = stash;
-  a.pos = h->wc_pos.as<uint64_t>();
-  a.pos_stride = stride;
-  a.pos_count = h->wc_pos_count.as<unsigned long long>();
-  a.pos_regions = grid;
   a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
-  a.pf2 = getenv("AGGB_WC_PF2") ? atoi(getenv("AGGB_WC_PF2")) : 0;  // (sparse tables: one bucket suffices)
-  auto fs = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>
-                         : k_probe_wc<ProgC1, WC_BLK, WC_R, WC_NS, WC_LINES, WC_SCAN>;
-  auto fr = h->prog == 2 ? k_probe_wc<ProgC2, WC_BLK, WC_RR, WC_RNS, WC_LINES, WC_RESOLVE>
-                         : k_probe_wc<ProgC1, WC_BLK, WC_RR, WC_RNS, WC_LINES, WC_RESOLVE>;
-  const size_t smem = WcL::bytes(P, h->wc_nblk), rsmem = WcLR::bytes(P, 0);
+  auto fs = k_scan_wc<WC_BLK, WC_R, WC_NS>;
+  const size_t smem = Wc2L::bytes(NP, h->wc_nblk);
   CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CU(cudaFuncSetAttribute((const void*)fr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-  pe = prof_begin(h, 15);
+  int pe = prof_begin(h, 15);
   fs<<<grid, WC_BLK, smem, h->st>>>(a);
   prof_end(h, pe);
   CU(cudaGetLastError());
-  pe = prof_begin(h, 16);
-  fr<<<grid, WC_BLK, rsmem, h->st>>>(a);
-  prof_end(h, pe);
-  CU(cudaGetLastError());
-  h->launches += 2;
+  h->launches++;
   h->wc_used = true;
   return AGGB_OK;
 }
@@ -2319,8 +2329,8 @@ void aggb_destroy(void* handle) {
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
                   &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains, &h->wc_bloom,
-                  &h->wc_plist, &h->wc_pn, &h->wc_recs, &h->wc_vinfo, &h->wc_failed, &h->wc_fail, &h->wc_pos,
-                  &h->wc_pos_count, &h->partials_soa};
+                  &h->wc_plist, &h->wc_pn, &h->wc_recs, &h->wc_vinfo, &h->wc_failed, &h->wc_fail, &h->wc_olist,
+                  &h->wc_olist_n, &h->wc_gather, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
   h->pool_base.release();
   h->stage.release();
@@ -2717,10 +2727,11 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
   return AGGB_OK;
 }
 
-// the children of the write-combined level 0 (k_child_wc): one wave per SM
-// count of partitions, pages found through the device page lists
+// the children of the write-combined level 0 (k_child2_wc): one CTA per run,
+// whole waves; owner runs are seeded from the owners' lists of resident slots
 int wc_children(Handle* h) {
-  CwArgs ca;
+  TRY(wc_build(h, false, true));
+  Cw2Args ca;
   memset(&ca, 0, sizeof(ca));
   ca.sp = h->cs.ds;
   ca.pool = pool_of(h);
@@ -2729,32 +2740,97 @@ int wc_children(Handle* h) {
   ca.plist_cap = h->wc_plist_cap;
   ca.part_recs = h->wc_recs.as<unsigned long long>();
   ca.vinfo = h->wc_vinfo.as<unsigned int>();
-  ca.P = h->raw0.ss.nparts;
+  ca.P = h->P0;
+  ca.Q = h->wcQ;
   ca.table_bytes = h->wc_table_bytes;
-  if (getenv("AGGB_WC_CHILD_KB"))  // test hook: small child tables send partitions to the fallback
-    ca.table_bytes = std::max(4, std::min(h->wc_table_bytes / 1024, atoi(getenv("AGGB_WC_CHILD_KB")))) * 1024;
+  if (getenv("AGGB_WC_CHILD_KB"))  // test hook: small child tables send runs to the fallback
+    ca.table_bytes = std::max(1, std::min(h->wc_table_bytes / 1024, atoi(getenv("AGGB_WC_CHILD_KB")))) * 1024;
   ca.seed = level_seed(h->cfg.seed, SALT_SLOT, h->cfg.level + 1);
   ca.out = outbuf(h, h->cfg.emit_partials ? 1 : 0);
   ca.failed = h->wc_failed.as<uint32_t>();
   ca.fail = h->wc_fail.as<uint32_t>();
   ca.stats = SC(h);
-  auto fc = h->prog == 2 ? k_child_wc<CpC2, WC_CBLK, WC_CRL> : k_child_wc<CpC1, WC_CBLK, WC_CRL>;
+  ca.t = h->tab;
+  ca.olist = h->wc_olist.as<uint32_t>();
+  ca.olist_n = h->wc_olist_n.as<uint32_t>();
+  ca.ocap = h->wc_ocap;
+  auto fc = h->prog == 2 ? k_child2_wc<CpC2, WC_CBLK, WC_CRL> : k_child2_wc<CpC1, WC_CBLK, WC_CRL>;
   CU(cudaFuncSetAttribute((const void*)fc, cudaFuncAttributeMaxDynamicSharedMemorySize, h->wc_table_bytes));
   int pe = prof_begin(h, 17);
-  fc<<<std::min(h->sms, ca.P), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
+  fc<<<std::min(h->sms, ca.P + ca.Q), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
   prof_end(h, pe);
   CU(cudaGetLastError());
   h->launches++;
   return AGGB_OK;
 }
 
-// a partition k_child_wc could not hold (more groups than its table, rows past
-// the output estimate, an overflowed page list): retire the completed ones'
-// pages and let drain recurse on the rest
+__global__ void k_stat_sub(unsigned long long* stats, unsigned long long n) {
+  stats[ST_SPILLED] -= n;
+  stats[ST_RECORDS] -= n;
+}
+
+// Runs k_child2_wc could not hold (more groups than its table, rows past the
+// output estimate, an overflowed page list, values beyond int32).  An owner run
+// holds records of resident keys: it is gathered into dense columns and probed
+// against the frozen table by the generic PROBE (hits aggregate in place, the
+// rest spills into the generic partitions), and the table is flushed again
+// over its first flush.  Then the completed runs' pages are retired and the
+// generic recursion takes what is left of the spill set.
 int wc_fallback(Handle* h) {
-  k_wc_retire<<<std::max(1, std::min(h->raw0.ss.nparts, h->sms * 4)), 256, 0, h->st>>>(
-      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, h->wc_failed.as<uint32_t>(),
-      h->raw0.ss.nparts, h->page_set.as<int32_t>());
+  const int P = h->P0, NP = h->P0 + h->wcQ;
+  std::vector<uint32_t> failed((size_t)NP), pn((size_t)NP);
+  std::vector<unsigned long long> recs((size_t)NP);
+  CU(cudaMemcpyAsync(failed.data(), h->wc_failed.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(pn.data(), h->wc_pn.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(recs.data(), h->wc_recs.p, (size_t)NP * 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  bool owners = false;
+  for (int p = P; p < NP; p++) owners |= failed[(size_t)p] != 0;
+  if (owners) {
+    // the table's rows are rewritten below: back to the row count before its flush
+    CU(cudaMemcpyAsync(SC(h) + 13, SC(h) + 30, 8, cudaMemcpyDeviceToDevice, h->st));
+    if (h->bloom_words) {
+      CU(cudaMemsetAsync(h->bloom.p, 0, (size_t)h->bloom_words * 8, h->st));
+      k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1);
+      h->launches++;
+    }
+    for (int p = P; p < NP; p++) {
+      if (!failed[(size_t)p]) continue;
+      if (pn[(size_t)p] > h->wc_plist_cap) return fail(AGGB_CAPACITY_EXCEEDED, "page list of an owner run overflowed");
+      const int64_t n = (int64_t)recs[(size_t)p];
+      if (n == 0) continue;
+      TRY(h->wc_gather.ensure((size_t)n * 16, &h->hw));
+      unsigned long long* gk = h->wc_gather.as<unsigned long long>();
+      unsigned long long* gv = gk + n;
+      CU(cudaMemsetAsync(SC(h) + 31, 0, 8, h->st));
+      k_wc2_gather<<<std::max(1, std::min<int>((int)pn[(size_t)p], h->sms * 4)), 256, 0, h->st>>>(
+          pool_of(h), h->wc_plist.as<uint32_t>() + (size_t)p * h->wc_plist_cap, pn[(size_t)p], gk, gv, SC(h) + 31);
+      k_stat_sub<<<1, 1, 0, h->st>>>(SC(h), (unsigned long long)n);  // (the PROBE below counts them again)
+      CU(cudaGetLastError());
+      h->launches += 2;
+      ColSrc col;
+      memset(&col, 0, sizeof(col));
+      col.n = n;
+      col.key[0] = (const uint8_t*)gk;
+      col.kstride[0] = 8;
+      col.kty[0] = TY_I64;
+      col.nv = 1;
+      col.val[0] = (const uint8_t*)gv;
+      col.vstride[0] = 8;
+      col.vty[0] = TY_I64;
+      PassPlan pr;
+      pr.mode = MODE_PROBE;
+      pr.col = col;
+      pr.ss = h->raw0.ss;
+      pr.counter = SC(h) + 9;
+      TRY(launch_pass(h, pr));
+    }
+    OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+    TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
+  }
+  k_wc2_retire<<<std::max(1, std::min(NP, h->sms * 4)), 256, 0, h->st>>>(
+      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, h->wc_failed.as<uint32_t>(), P, NP,
+      h->page_set.as<int32_t>());
   CU(cudaGetLastError());
   h->launches++;
   h->tail_valid = false;
@@ -2780,22 +2856,24 @@ int aggb_finish(void* handle, aggb_result* out) {
       const bool no_rt = (algo0 == AGGB_PRE_PARTITIONING || algo0 == AGGB_SHARED_HASH ||
                           algo0 == AGGB_DYNAMIC_DESTAGING) && !getenv("AGGB_L0_ROUNDTRIP");
       if (no_rt) {
-        CU(cudaMemcpyAsync(SC(h) + 14, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToDevice, h->st));
-        CU(cudaMemcpyAsync(SC(h) + 15, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToDevice, h->st));
-        // (k_child_wc: rows for the expected groups; a partition past them falls back to drain)
+        // (k_child2_wc: rows for the expected groups; a run past them falls back to drain)
         const int64_t wc_rows =
             h->wc_used ? (int64_t)std::min<double>((double)h->records, std::max(2.0 * h->cfg.stats_G_t, 1.0e6)) : 0;
         TRY(ensure_out(h, (int64_t)h->tab.cap + 4 + wc_rows));
+        if (h->wc_used) {
+          // the children first: owner runs merge their resident groups into the
+          // table (and take their records out of the spill count) before it is flushed
+          TRY(wc_children(h));
+          tr.mark(h->st, "finish: wc children");
+          CU(cudaMemcpyAsync(SC(h) + 30, SC(h) + 13, 8, cudaMemcpyDeviceToDevice, h->st));  // rows before the flush
+        }
+        CU(cudaMemcpyAsync(SC(h) + 14, &h->tab.hdr->committed, 8, cudaMemcpyDeviceToDevice, h->st));
+        CU(cudaMemcpyAsync(SC(h) + 15, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToDevice, h->st));
         OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
         TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
         tr.mark(h->st, "finish: level-0 flush");
         h->l0_deferred = true;
-        if (h->wc_used) {
-          TRY(wc_children(h));
-          tr.mark(h->st, "finish: wc children");
-        } else {
-          TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
-        }
+        if (!h->wc_used) TRY(drain(h, h->raw0, h->raw0_live, h->part0, h->part0_live, h->cfg.level));
       }
       int frozen = 0, refused = 0;
       unsigned long long groups = 0, cnt0 = 0, sp0 = 0;
@@ -2874,17 +2952,18 @@ int aggb_finish(void* handle, aggb_result* out) {
       CU(cudaMemcpyAsync(l0, SC(h) + 14, 16, cudaMemcpyDeviceToHost, h->st));
       if (h->wc_used) CU(cudaMemcpyAsync(&wcf, h->wc_fail.p, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
-      if (wcf & 2u) return fail(AGGB_CUDA_ERROR, "k_probe_wc: page map inconsistency (internal error)");
+      if (wcf & 2u) return fail(AGGB_CUDA_ERROR, "k_scan_wc: page map inconsistency (internal error)");
       if (h->wc_used) {
         h->met.recursion_depth = std::max<int64_t>(h->met.recursion_depth, st[ST_SPILLED] ? 1 : 0);
         h->met.spilled_partitions += st[ST_SPILLED] ? h->raw0.ss.nparts : 0;
       }
-      if (wcf) {  // some partition did not fit k_child_wc: the generic recursion takes it
+      if (wcf) {  // some run did not fit k_child2_wc: re-probed (owner runs) / left to the generic recursion
         TRY(wc_fallback(h));
         h->wc_fallbacks++;
         CU(cudaMemcpyAsync(&cnt, SC(h) + 13, 8, cudaMemcpyDeviceToHost, h->st));
         CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
         CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaMemcpyAsync(l0 + 1, SC(h) + ST_SPILLED, 8, cudaMemcpyDeviceToHost, h->st));
         CU(cudaStreamSynchronize(h->st));
       }
     }

@@ -1,0 +1,824 @@
+// wc2.cuh — level 0 of budgeted pre-partitioning for 16-byte records (one-word
+// key, one int64 value; the C1/C2 record shape) in two kernels:
+//
+//   k_scan_wc   one pass over the batch that only ROUTES: every record is
+//               hashed, tested against the frozen table's filter in shared
+//               memory and appended to a run — a spill partition (filter
+//               negative: the key is certainly not resident) or an owner
+//               partition (filter positive: resident key or false positive).
+//               Runs are written through per-partition shared-memory
+//               write-combining rings as whole 128-byte lines by the TMA engine
+//               (cp.async.bulk, SASS UBLKCP); input tiles arrive the same way.
+//   k_child2_wc one CTA per run, a compact shared-memory table (u32 states).
+//               An owner run's table is first seeded with the resident keys
+//               this owner is responsible for; their aggregates are merged into
+//               the level-0 table (L2 REDs, once per group) instead of being
+//               emitted, so resident keys still aggregate in place and are
+//               emitted once, by the table flush.  A false positive is simply a
+//               spilled key whose run is an owner run.
+//
+// Replaces k_pp_probe (/root/reference/pkg/src/aggbench/_kernels.py:917-962:
+// frozen table, hits aggregate in place, misses spill to hash % P partitions,
+// bloom byte :938-942), PrePartitioning stage 2 and _drain_runs
+// (/root/reference/pkg/src/aggbench/operators/hybrid.py:518-552, :244-277).
+//
+// Why routing only: the earlier kernel resolved filter positives against the L2
+// table (one bucket load + four REDs per hit: 0.71 ms for 27M positives on C2,
+// 750 instructions per positive) and kept a second write path for them; here a
+// positive costs what a spill costs and the L2 table sees 4 REDs per resident
+// GROUP, not per record.
+#pragma once
+#include "pass.cuh"
+#include "ptx.cuh"
+#include <type_traits>
+
+namespace aggb {
+
+// ---------------------------------------------------------------------------
+// the scan's hash: one 64-bit value, four independent fields
+//   hi word top bits   -> spill partition      (__umulhi(hi, P))
+//   hi word bits 0-14  -> three filter bit positions inside a 32-bit block
+//   lo word top bits   -> filter block         (__umulhi(lo, nblk))
+//   lo word bits 0-15  -> owner                (__umulhi(lo << 16, Q))
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t wc2_hash(uint64_t k, uint64_t seed) { return fmix64(k ^ seed); }
+__device__ __forceinline__ uint32_t wc2_bits(uint32_t hi) {
+  // __funnelshift_l(0, 1, s) = 1 << (s & 31): one SHF.L.W per bit
+  return __funnelshift_l(0u, 1u, hi) | __funnelshift_l(0u, 1u, hi >> 5) | __funnelshift_l(0u, 1u, hi >> 10);
+}
+__device__ __forceinline__ uint32_t wc2_block(uint32_t lo, uint32_t nblk) { return __umulhi(lo, nblk); }
+__device__ __forceinline__ uint32_t wc2_owner(uint32_t lo, uint32_t Q) { return __umulhi(lo << 16, Q); }
+
+// filter of the frozen table (32-bit blocks, 3 bits per key) and the owners'
+// lists of resident slots; one pass over the table's key array
+__global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* bloom, uint32_t nblk, uint32_t* olist, uint32_t* olist_n,
+                            uint32_t ocap, uint32_t Q) {
+  const uint64_t n = t.mask + 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = t.keys[i];
+    if (k == EMPTY) continue;
+    const uint64_t h = wc2_hash(k, seed);
+    const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+    if (bloom) atomicOr(&bloom[wc2_block(lo, nblk)], wc2_bits(hi));
+    if (olist) {
+      const uint32_t o = wc2_owner(lo, Q);
+      const uint32_t at = atomicAdd(&olist_n[o], 1u);
+      if (at < ocap) olist[(size_t)o * ocap + at] = (uint32_t)i;
+    }
+  }
+}
+
+struct Wc2Args {
+  GTable t;                               // the frozen level-0 table (header only)
+  uint64_t seed;                          // wc2_hash seed
+  const unsigned long long* key;          // dense 8-byte key column (16-byte aligned)
+  const unsigned long long* val;          // dense 8-byte value column (16-byte aligned)
+  int64_t n;                              // records in the columns
+  const unsigned long long* start_tiles;  // FILL consumed rows [0, *start_tiles * start_T)
+  int64_t start_T;
+  const unsigned long long* lkey;         // FILL's deferral list (SoA), nullable
+  const unsigned long long* lval;
+  const unsigned long long* lcount;
+  const uint32_t* bloom;                  // nblk 32-bit blocks
+  uint32_t nblk;
+  PagePool pool;
+  int32_t set_id;                         // spill set of the runs' pages
+  int32_t P, Q;                           // spill partitions, owner partitions (runs = P + Q)
+  uint32_t* plist;                        // [P + Q][plist_cap] page ids per run
+  uint32_t* plist_n;                      // [P + Q]
+  uint32_t plist_cap;
+  unsigned long long* part_recs;          // [P + Q] records per run
+  unsigned long long* stats;              // ST_* counters
+  unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes (int64 columns)
+  uint32_t* fail;                         // page list overflow / page map error
+  int32_t stash;                          // pages per CTA stash refill
+  int32_t pf;                             // L2 prefetch of the batch tiles ahead
+};
+
+template <int BLK, int R, int NS>
+struct Wc2Layout {
+  static_assert(R % 2 == 0, "records are loaded in pairs");
+  static constexpr int T = BLK * R;
+  static constexpr int LINES = 2, RING = LINES * 8;
+  static constexpr int RS = RING + 1;  // ring stride per run (16-byte slots): one slot of skew per run
+                                       // spreads the same ring position over the banks
+  static constexpr int NE = 8;         // page map entries per run (pages a run can open in one tile)
+  static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
+  static __host__ __device__ size_t ring_bytes(int NP) { return (size_t)NP * RS * 16; }
+  static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (1 + NE) * 4 + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t bytes(int NP, uint32_t nblk) {
+    return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + (((size_t)nblk * 4 + 15) & ~(size_t)15);
+  }
+};
+
+__device__ __forceinline__ void lds128(uint32_t a, uint64_t& x, uint64_t& y) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
+}
+
+constexpr int WC2_PF = 6;  // L2 prefetch distance in tiles (rounds of the grid)
+
+// One CTA per SM, persistent.  Per tile (T = BLK * R records):
+//   [A] every thread routes its R records: hash, filter, run id, one shared
+//       atomic on the run's claim word cw[run] (claim counter in bits 0-22, the
+//       run's window start (line index mod 512) in bits 23-31).  A claim
+//       inside the window (LINES lines from the run's open line) is written
+//       into the run's ring; a claim beyond it (a burst: more than a window of
+//       one run in one tile) is held.  The claimer of a page's first slot opens
+//       the page (CTA-private, appended to the run's device-side page list).
+//   barrier 1
+//   [B] the claimer of a line's 8th slot sends the line: one 128-byte bulk copy
+//       shared -> global.  Held records of lines that are complete go straight
+//       to their page; those of the run's open line are parked in registers and
+//       written into the ring at the start of the next tile.  Windows move to
+//       the open lines.
+//   barrier 2 (ring and stage free again; thread 0 issues the stage's next tile)
+template <int BLK, int R, int NS>
+__global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
+  using L = Wc2Layout<BLK, R, NS>;
+  constexpr int T = L::T, RING = L::RING, NE = L::NE, LINES = L::LINES, RS = L::RS;
+  constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
+  constexpr uint32_t CWM = (1u << 23) - 1;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int P = a.P, NP = a.P + a.Q;
+  const uint32_t Q = (uint32_t)a.Q, nblk = a.nblk;
+  unsigned long long* stg = (unsigned long long*)smem;
+  ulonglong2* ring = (ulonglong2*)(smem + L::stage_bytes());
+  uint32_t* cw = (uint32_t*)(smem + L::stage_bytes() + L::ring_bytes(NP));
+  uint32_t* ent = cw + NP;
+  uint32_t* sbloom = (uint32_t*)((unsigned char*)cw + L::meta_bytes(NP));
+  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw), a_bloom = smem_u32(sbloom);
+  __shared__ __align__(8) uint64_t mbar[NS];
+  __shared__ int s_tcnt[NS];
+  __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv;
+
+  const int64_t n = a.n;
+  const int64_t col_start = a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
+  const int64_t col_tiles = (n - col_start + T - 1) / T;
+  const int64_t nlin = a.lcount ? (int64_t)*a.lcount : 0;
+  const unsigned long long total = (unsigned long long)(col_tiles + (nlin + T - 1) / T);
+
+  for (int p = tid; p < NP; p += BLK) cw[p] = 0;
+  for (int i = tid; i < NP * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
+  for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg(a.bloom + i);
+  if (tid == 0) {
+    s_sb = s_su = s_sc = s_nb = s_nv = 0;
+    for (int s = 0; s < NS; s++) mbar_init(&mbar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // producer (thread 0): tiles round-robin over the CTAs
+  unsigned long long next_tile = blockIdx.x;
+  unsigned long long n_rec = 0;  // thread 0: records of the tiles issued
+  auto issue = [&](int s) {
+    int c = 0;
+    const unsigned long long *kp = nullptr, *vp = nullptr;
+    if (next_tile < total) {
+      const unsigned long long tile = next_tile;
+      next_tile += gridDim.x;
+      if (tile < (unsigned long long)col_tiles) {
+        const int64_t b = col_start + (int64_t)tile * T;
+        c = (int)(n - b < (int64_t)T ? n - b : (int64_t)T);
+        kp = a.key + b;
+        vp = a.val + b;
+      } else {
+        const int64_t b = (int64_t)(tile - col_tiles) * T;
+        c = (int)(nlin - b < (int64_t)T ? nlin - b : (int64_t)T);
+        kp = a.lkey + b;
+        vp = a.lval + b;
+      }
+    }
+    s_tcnt[s] = c;
+    n_rec += (unsigned long long)c;
+    unsigned long long* sk = stg + (size_t)s * 2 * T;
+    unsigned long long* sv = sk + T;
+    const int c2 = c & ~1;  // bulk copies move multiples of 16 bytes
+    if (c & 1) {
+      sk[c - 1] = kp[c - 1];
+      sv[c - 1] = vp[c - 1];
+    }
+    if (c2) {
+      mbar_arrive_tx(&mbar[s], (uint32_t)c2 * 16u);
+      bulk_g2s(sk, kp, (uint32_t)c2 * 8u, &mbar[s]);
+      bulk_g2s(sv, vp, (uint32_t)c2 * 8u, &mbar[s]);
+    } else {
+      mbar_arrive(&mbar[s]);
+    }
+    const unsigned long long pt = next_tile + (unsigned long long)(WC2_PF - 1) * gridDim.x;  // into L2, ahead
+    if (a.pf && pt < (unsigned long long)col_tiles) {
+      const int64_t b = col_start + (int64_t)pt * T;
+      const uint32_t cb = (uint32_t)((n - b < (int64_t)T ? n - b : (int64_t)T) & ~1ll) * 8u;
+      if (cb) {
+        bulk_prefetch_l2(a.key + b, cb);
+        bulk_prefetch_l2(a.val + b, cb);
+      }
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < NS; s++) issue(s);
+
+  uint64_t* const pool = (uint64_t*)a.pool.base;
+  auto page_of = [&](int p, uint32_t j) -> uint32_t {
+    const uint32_t e = ent[p * NE + (j & (NE - 1))];
+    if ((e & 0xFFu) != (j & 0xFFu)) {
+      atomicExch(a.fail, 2u);  // cannot happen: a page is published before the barrier that precedes its use
+      return 0xFFFFFFu;
+    }
+    return e >> 8;
+  };
+  auto rec_ptr = [&](uint32_t pg, uint32_t x) { return pool + (((size_t)pg << SLOG) + (x & (S - 1))) * 2; };
+  auto alloc_page = [&](int p, uint32_t j) {
+    const uint32_t off = atomicAdd(&s_su, 1u);
+    uint32_t pg;
+    if (off < s_sc) {
+      pg = s_sb + off;
+    } else {
+      pg = atomicAdd(a.pool.next_page, 1u);
+      if (pg >= a.pool.capacity) {
+        atomicExch(a.pool.overflow, 1u);
+        pg = 0xFFFFFFu;
+      }
+    }
+    if (pg < 0xFFFFFFu) {
+      a.pool.page_part[pg] = p;
+      a.pool.page_set[pg] = a.set_id;
+      a.pool.page_fill[pg] = S;
+      const uint32_t li = atomicAdd(&a.plist_n[p], 1u);
+      if (li < a.plist_cap) a.plist[(size_t)p * a.plist_cap + li] = pg;
+      else atomicExch(a.fail, 1u);
+    }
+    ent[p * NE + (j & (NE - 1))] = (pg << 8) | (j & 0xFFu);
+  };
+
+  // per-thread state of the tile: claim words and runs of its R records
+  uint32_t old[R];
+  int pid[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) {
+    old[r] = 0;
+    pid[r] = 0;
+  }
+  uint32_t vmask = 0;  // records of the tile this thread routed
+  uint32_t held = 0;   // ... claimed beyond their run's window
+  uint32_t opark = 0;  // ... parked for the next tile (open line)
+  uint64_t hk[R], hv[R];
+#pragma unroll
+  for (int r = 0; r < R; r++) hk[r] = hv[r] = 0;
+  uint64_t vm = 0;  // OR of v ^ (v >> 63): bounds the magnitudes (compact children)
+  uint32_t nb_pending = 0;
+  bool nb_busy = false;
+
+  // stage index of record r of this thread: pairs (2i, 2i + 1), i = (r / 2) * BLK + tid
+  auto rec_idx = [&](int r) { return 2 * ((r >> 1) * BLK + tid) + (r & 1); };
+  auto in_window = [&](uint32_t o) { return ((((o & CWM) >> 3) - (o >> 23)) & 511u) < (uint32_t)LINES; };
+
+  for (int it = 0;; it++) {
+    const int s = it % NS;
+    mbar_wait(&mbar[s], (uint32_t)((it / NS) & 1));
+    const int c = s_tcnt[s];
+    if (tid == 0 && a.stash && !nb_busy && !s_nv && 2 * s_su >= s_sc) {  // next stash, taken after barrier 1
+      nb_pending = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
+      nb_busy = true;
+    }
+    // ---- [A1] parked open-line records of the last tile into the ring
+    if (__builtin_expect(opark != 0, 0)) {
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if ((opark >> r) & 1u) ring[pid[r] * RS + (old[r] & (RING - 1))] = make_ulonglong2(hk[r], hv[r]);
+      opark = 0;
+    }
+    // ---- [A2] route this tile's records
+    const uint32_t a_sk = a_stg + (uint32_t)s * 2u * T * 8u, a_sv = a_sk + T * 8u;
+    held = 0;
+    auto route = [&](auto full) {
+      constexpr bool FULL = decltype(full)::value;
+      uint64_t k[R], v[R];
+#pragma unroll
+      for (int r = 0; r < R; r += 2) {
+        const uint32_t o = 16u * (uint32_t)((r >> 1) * BLK + tid);
+        lds128(a_sk + o, k[r], k[r + 1]);
+        lds128(a_sv + o, v[r], v[r + 1]);
+      }
+      uint32_t vm_ = FULL ? (1u << R) - 1u : 0u;
+      if (!FULL) {
+#pragma unroll
+        for (int r = 0; r < R; r++) vm_ |= (uint32_t)(rec_idx(r) < c) << r;
+      }
+      vmask = vm_;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint64_t h = wc2_hash(k[r], a.seed);
+        const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+        const uint32_t blk = lds32(a_bloom + 4u * wc2_block(lo, nblk));
+        const uint32_t bits = wc2_bits(hi);
+        const bool pos = ((blk & bits) == bits) | (k[r] == EMPTY);
+        pid[r] = pos ? P + (int)wc2_owner(lo, Q) : (int)__umulhi(hi, (uint32_t)P);
+        const uint64_t m = v[r] ^ (uint64_t)((long long)v[r] >> 63);
+        vm |= FULL ? m : (((vm_ >> r) & 1u) ? m : 0ull);
+      }
+#pragma unroll
+      for (int r = 0; r < R; r++)
+        if (FULL || ((vm_ >> r) & 1u)) old[r] = atoms_add(a_cw + 4u * (uint32_t)pid[r], 1u);
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if (!FULL && !((vm_ >> r) & 1u)) continue;
+        const uint32_t x = old[r] & CWM;
+        if (__builtin_expect((x & (S - 1)) == 0, 0)) alloc_page(pid[r], x >> SLOG);
+        if (__builtin_expect(in_window(old[r]), 1))
+          sts128(a_ring + 16u * ((uint32_t)pid[r] * RS + (x & (RING - 1))), k[r], v[r]);
+        else
+          held |= 1u << r;
+      }
+    };
+    if (c == T) route(std::true_type{});
+    else route(std::false_type{});
+    const bool more = c != 0;
+    fence_proxy_async_smem();  // ring writes before the bulk copies that read them
+    __syncthreads();           // ---- barrier 1
+    if (tid == 0) {
+      if (nb_busy) {
+        s_nb = nb_pending;
+        s_nv = 1;
+        nb_busy = false;
+      }
+      if (s_nv && s_su >= s_sc) {
+        const bool fits = s_nb + (uint32_t)a.stash <= a.pool.capacity;
+        if (!fits)
+          for (uint32_t x = s_nb; x < min(s_nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
+        s_sb = s_nb;
+        s_sc = fits ? (uint32_t)a.stash : 0u;
+        s_su = 0;
+        s_nv = 0;
+      }
+    }
+    // ---- [B1] the lines this thread completed: 128-byte bulk copies (TMA engine)
+    bool sent = false;
+    {
+      const uint32_t live = vmask & ~held;
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const uint32_t x = old[r] & CWM;
+        if (((live >> r) & 1u) && (x & 7u) == 7u) {
+          const uint32_t x0 = x & ~7u;
+          const uint32_t pg = page_of(pid[r], x0 >> SLOG);
+          if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[pid[r] * RS + (x0 & (RING - 1))], 128u);
+          sent = true;
+        }
+      }
+    }
+    if (sent) bulk_commit();
+    // ---- [B2] held records: complete lines straight to their page, the open line waits
+    if (__builtin_expect(held != 0, 0)) {
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        if (!((held >> r) & 1u)) continue;
+        const uint32_t x = old[r] & CWM;
+        const uint32_t o = 8u * (uint32_t)rec_idx(r);
+        const uint64_t k = lds64(a_sk + o), v = lds64(a_sv + o);
+        if ((x >> 3) < ((cw[pid[r]] & CWM) >> 3)) {
+          const uint32_t pg = page_of(pid[r], x >> SLOG);
+          if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), make_ulonglong2(k, v));
+        } else {
+          hk[r] = k;
+          hv[r] = v;
+          opark |= 1u << r;
+        }
+      }
+    }
+    vmask = 0;
+    for (int p = tid; p < NP; p += BLK) {  // the windows move to the open lines
+      const uint32_t cc = cw[p] & CWM;
+      cw[p] = ((cc >> 3) << 23) | cc;
+    }
+    if (sent) bulk_wait_read0();  // the ring slots are read before barrier 2
+    // ---- barrier 2: ring and stage are free again
+    if (!more) {
+      if (!__syncthreads_or(opark != 0)) break;
+    } else {
+      __syncthreads();
+    }
+    if (tid == 0) issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
+  // ---- close: every run's open line (all in the ring), then the page fills
+  for (int p = tid; p < NP; p += BLK) {
+    const uint32_t cc = cw[p] & CWM;
+    if (!cc) continue;
+    for (uint32_t x = cc & ~7u; x < cc; x++) {
+      const uint32_t pg = page_of(p, x >> SLOG);
+      if (pg < 0xFFFFFFu) st_v2(rec_ptr(pg, x), ring[p * RS + (x & (RING - 1))]);
+    }
+    const uint32_t pg = page_of(p, (cc - 1) >> SLOG);
+    if (pg < 0xFFFFFFu) a.pool.page_fill[pg] = (int32_t)(((cc - 1) & (S - 1)) + 1);
+    atomicAdd(&a.part_recs[p], (unsigned long long)cc);
+  }
+  if (tid == 0) {
+    // unused stash pages leave the set
+    for (uint32_t x = min(s_su, s_sc); x < s_sc; x++) a.pool.page_set[s_sb + x] = -1;
+    if (s_nv)
+      for (uint32_t x = s_nb; x < min(s_nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
+    if (nb_busy)
+      for (uint32_t x = nb_pending; x < min(nb_pending + (uint32_t)a.stash, a.pool.capacity); x++)
+        a.pool.page_set[x] = -1;
+    if (n_rec) {
+      atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
+      // every routed record counts as spilled until an owner child finds its key resident
+      atomicAdd(&a.stats[ST_SPILLED], n_rec);
+      atomicAdd(&a.stats[ST_RECORDS], n_rec);
+    }
+  }
+  {
+    uint32_t mlo = (uint32_t)vm, mhi = (uint32_t)(vm >> 32);
+    mlo = __reduce_or_sync(0xffffffffu, mlo);
+    mhi = __reduce_or_sync(0xffffffffu, mhi);
+    if (lane == 0) {
+      if (mhi | (mlo >> 31)) atomicOr(&a.vinfo[0], 1u);
+      if (mlo) atomicOr(&a.vinfo[1], mlo & 0x7FFFFFFFu);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_child2_wc: one CTA per run, compact 32-bit states
+// ---------------------------------------------------------------------------
+
+struct Cw2Args {
+  DevSpec sp;
+  PagePool pool;
+  const uint32_t* plist;
+  const uint32_t* plist_n;
+  uint32_t plist_cap;
+  const unsigned long long* part_recs;
+  const unsigned int* vinfo;    // [0] some value outside int32, [1] OR of the magnitudes (k_scan_wc)
+  int32_t P, Q;
+  int32_t table_bytes;          // dynamic shared memory for the table
+  uint64_t seed;                // slot hash seed of the child level
+  OutBuf out;
+  uint32_t* failed;             // [P + Q]: 1 = did not fit, left to the fallback
+  uint32_t* fail;               // bit 2: some run failed (the host runs the fallback)
+  unsigned long long* stats;
+  GTable t;                     // the level-0 table (owner runs merge their resident groups into it)
+  const uint32_t* olist;        // [Q][ocap] resident slots per owner
+  const uint32_t* olist_n;      // [Q]
+  uint32_t ocap;
+};
+
+// Compact field programs: every state field an integer COUNT / SUM / MIN / MAX
+// of the one value column (descriptor op | ty<<2 | srck<<4 | vty<<6 | src<<8).
+template <uint32_t... F>
+struct CompactProg {
+  static constexpr int N = sizeof...(F);
+  __host__ __device__ static constexpr uint32_t fd(int j) {
+    constexpr uint32_t a[N] = {F...};
+    return a[j];
+  }
+  __host__ __device__ static constexpr bool is_count(int j) { return ((fd(j) >> 4) & 3) == SRC_ONE; }
+  __host__ __device__ static constexpr bool is_sum(int j) { return (fd(j) & 3) == OP_ADD && !is_count(j); }
+  // u32 word array of field j (0 = the count word, shared by COUNT fields)
+  __host__ __device__ static constexpr int arr(int j) {
+    int x = 1;
+    for (int i = 0; i < j; i++) x += !is_count(i);
+    return is_count(j) ? 0 : x;
+  }
+  __host__ __device__ static constexpr int na() {
+    int x = 1;
+    for (int i = 0; i < N; i++) x += !is_count(i);
+    return x;
+  }
+  __host__ __device__ static constexpr int nsum() {
+    int x = 0;
+    for (int i = 0; i < N; i++) x += is_sum(i);
+    return x;
+  }
+};
+using CpC1 = CompactProg<0x000, 0x010>;                 // COUNT, SUM
+using CpC2 = CompactProg<0x000, 0x010, 0x011, 0x012>;   // COUNT, SUM, MIN, MAX
+
+__device__ __forceinline__ void reds_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void reds_min_s32(uint32_t a, int v) {
+  asm volatile("red.shared.min.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void reds_max_s32(uint32_t a, int v) {
+  asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Table layout (stride = nslots + 1, the last slot is the sentinel key's):
+//   skeys[stride] u64 keys in 32-byte buckets of 4 slots
+//   sw[a][stride] u32 word arrays: 0 count, CP::arr(j) field j, then the hi words
+//                 of wide sums, then (owner runs) the level-0 slot of a seeded key
+// A record's probe compares the low key words of its bucket (4 compares), checks
+// the high word of the match and falls to the general loop only for a first
+// occurrence, a displaced key or keys that differ only in their high words.
+template <class CP, int BLK, int RL>
+__global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
+  constexpr int N = CP::N;
+  constexpr int NA = CP::na(), NSUM = CP::nsum();
+  constexpr int NWARP = BLK / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ int s_groups, s_fail, s_esc;
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_wsum[NWARP];
+  const bool rfit = a.vinfo[0] == 0;  // every value is an int32
+  const uint32_t vabs = a.vinfo[1] + 1u;
+  const int NP = a.P + a.Q;
+  for (int p = blockIdx.x; p < NP; p += gridDim.x) {
+    const unsigned long long np = a.part_recs[p];
+    if (np == 0) continue;
+    const bool owner = p >= a.P;
+    // wide sums (a u32 pair with carry) only when a run's sum can leave int32
+    const bool wide = (double)np * (double)vabs >= 2147483647.0;
+    const int words = 2 + NA + (wide ? NSUM : 0) + (owner ? 1 : 0);
+    const int nbk = ((a.table_bytes / 4 - 2) / words - 1) / 4;
+    const int nslots = nbk * 4;
+    const int maxg = (int)(0.85 * nslots);
+    const int stride = nslots + 1;
+    uint64_t* skeys = (uint64_t*)smem;                 // stride keys (escape slot last)
+    uint32_t* sw = (uint32_t*)(skeys + stride);        // [array][slot] u32 words
+    const int a_org = NA + (wide ? NSUM : 0);          // owner runs: array of level-0 slots
+    const uint32_t a_keys = smem_u32(skeys), a_sw = smem_u32(sw);
+    for (int i = tid; i < stride; i += BLK) {
+      skeys[i] = EMPTY;
+      sw[i] = 0;
+#pragma unroll
+      for (int j = 0; j < N; j++)
+        if (!CP::is_count(j))
+          sw[CP::arr(j) * stride + i] =
+              (CP::fd(j) & 3) == OP_MIN ? 0x7FFFFFFFu : (CP::fd(j) & 3) == OP_MAX ? 0x80000000u : 0u;
+      for (int j = 0; j < (wide ? NSUM : 0); j++) sw[(NA + j) * stride + i] = 0u;
+      if (owner) sw[a_org * stride + i] = 0xFFFFFFFFu;
+    }
+    if (tid == 0) {
+      s_groups = 0;
+      s_fail = !rfit || a.plist_n[p] > a.plist_cap;  // (a page list that overflowed is incomplete)
+      s_esc = 0;
+    }
+    __syncthreads();
+    // the general probe: hit, insert into the bucket chain's first empty slot, or fail (table full)
+    auto probe_slow = [&](uint64_t k, int b) -> int {
+      for (;;) {
+        const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(skeys + b * 4);
+        const ulonglong2 x = bp[0], y = bp[1];
+        const int hit = x.x == k ? 0 : x.y == k ? 1 : y.x == k ? 2 : y.y == k ? 3 : -1;
+        if (hit >= 0) return b * 4 + hit;
+        const int emp = x.x == EMPTY ? 0 : x.y == EMPTY ? 1 : y.x == EMPTY ? 2 : y.y == EMPTY ? 3 : -1;
+        if (emp < 0) {  // full bucket: the next one
+          if (++b == nbk) b = 0;
+          continue;
+        }
+        if (atomicAdd(&s_groups, 1) >= maxg) {
+          s_fail = 1;
+          return -1;
+        }
+        const int e = b * 4 + emp;
+        const unsigned long long prev = atomicCAS((unsigned long long*)&skeys[e], EMPTY, k);
+        if (prev == EMPTY) return e;
+        atomicSub(&s_groups, 1);  // the slot went to another insert: look at the bucket again
+      }
+    };
+    if (owner) {  // seed: the resident keys this owner answers for, with their level-0 slots
+      const int o = p - a.P;
+      const uint32_t nres = a.olist_n[o];
+      if (nres > a.ocap || (int)nres > maxg) {
+        if (tid == 0) s_fail = 1;
+      } else {
+        for (uint32_t i = tid; i < nres; i += BLK) {
+          const uint32_t ls = a.olist[(size_t)o * a.ocap + i];
+          const uint64_t k = a.t.keys[ls];
+          const uint64_t kk[1] = {k};
+          const uint64_t h = hash_key<1>(kk, a.seed);
+          const int sl = probe_slow(k, (int)__umulhi((uint32_t)h, (uint32_t)nbk));
+          if (sl >= 0) sw[a_org * stride + sl] = ls;
+        }
+        if (tid == 0 && *(volatile int*)&a.t.hdr->esc) sw[a_org * stride + nslots] = (uint32_t)(a.t.mask + 1);
+      }
+      __syncthreads();
+    }
+    const uint32_t npg = min(a.plist_n[p], a.plist_cap);
+    const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
+    auto records = [&](auto wide_t) {
+      constexpr bool WIDE = decltype(wide_t)::value;
+      // Warp w takes pages w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
+      // the page, RL records per lane in flight.
+      for (uint32_t q = wid; q < npg; q += NWARP) {
+        if (__any_sync(0xffffffffu, *(volatile int*)&s_fail)) break;  // warp-uniform
+        const uint32_t pg = pl[q];
+        const int fill = a.pool.page_fill[pg];
+        const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
+        for (int s0 = 0; s0 < fill; s0 += RL * 32) {
+          ulonglong2 cur[RL];
+#pragma unroll
+          for (int r = 0; r < RL; r++) {
+            const int sl = s0 + r * 32 + lane;
+            cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(EMPTY, 0);
+          }
+          // first bucket of every record: loads in flight together
+          int bk[RL];
+          uint64_t bx[RL][4];
+#pragma unroll
+          for (int r = 0; r < RL; r++) {
+            const uint64_t kk[1] = {cur[r].x};
+            const uint64_t h = hash_key<1>(kk, a.seed);
+            bk[r] = (int)__umulhi((uint32_t)h, (uint32_t)nbk);
+            lds128(a_keys + 32u * (uint32_t)bk[r], bx[r][0], bx[r][1]);
+            lds128(a_keys + 32u * (uint32_t)bk[r] + 16u, bx[r][2], bx[r][3]);
+          }
+#pragma unroll
+          for (int r = 0; r < RL; r++) {
+            const uint64_t k = cur[r].x;
+            const uint32_t klo = (uint32_t)k, khi = (uint32_t)(k >> 32);
+            const bool e0 = (uint32_t)bx[r][0] == klo, e1 = (uint32_t)bx[r][1] == klo, e2 = (uint32_t)bx[r][2] == klo,
+                       e3 = (uint32_t)bx[r][3] == klo;
+            const int hi_ = e0 ? 0 : e1 ? 1 : e2 ? 2 : 3;
+            const uint32_t hv = (uint32_t)((e0 ? bx[r][0] : e1 ? bx[r][1] : e2 ? bx[r][2] : bx[r][3]) >> 32);
+            int slot = ((e0 | e1 | e2 | e3) && hv == khi) ? bk[r] * 4 + hi_ : -1;
+            const bool valid = s0 + r * 32 + lane < fill;
+            if (__builtin_expect(k == EMPTY, 0)) {  // the sentinel key (and the padding of a short page)
+              slot = valid ? nslots : -1;
+              if (valid) s_esc = 1;  // (idempotent; read after the barrier)
+            } else if (__builtin_expect(slot < 0, 0)) {
+              slot = probe_slow(k, bk[r]);
+            }
+            __syncwarp();
+            if (slot >= 0) {
+              const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
+              const uint32_t a_s = a_sw + 4u * (uint32_t)slot;
+              reds_add(a_s, 1u);
+              int js = 0;
+#pragma unroll
+              for (int j = 0; j < N; j++) {
+                const uint32_t F = CP::fd(j);
+                if (((F >> 4) & 3) == SRC_ONE) continue;  // COUNT: the count word
+                const uint32_t a_w = a_s + 4u * (uint32_t)(CP::arr(j) * stride);
+                if ((F & 3) == OP_ADD) {
+                  if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
+                    const uint32_t o = atoms_add(a_w, (uint32_t)cb);
+                    const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
+                    if (hi) reds_add(a_s + 4u * (uint32_t)((NA + js) * stride), hi);
+                  } else {
+                    reds_add(a_w, (uint32_t)cb);
+                  }
+                  js++;
+                } else if ((F & 3) == OP_MIN) {  // read first: most records do not improve the extreme
+                  if (cb < (int)lds32(a_w)) reds_min_s32(a_w, cb);
+                } else {
+                  if (cb > (int)lds32(a_w)) reds_max_s32(a_w, cb);
+                }
+              }
+            }
+          }
+        }
+      }
+    };
+    if (wide) records(std::true_type{});
+    else records(std::false_type{});
+    __syncthreads();
+    if (s_fail) {
+      if (tid == 0) {
+        a.failed[p] = 1;
+        atomicOr(a.fail, 4u);
+      }
+      __syncthreads();
+      continue;
+    }
+    // state words of slot s as 64-bit native states
+    auto state_of = [&](int s, int j, int& js) -> uint64_t {
+      const uint32_t F = CP::fd(j);
+      if (((F >> 4) & 3) == SRC_ONE) return (uint64_t)sw[s];
+      if ((F & 3) == OP_ADD) {
+        const uint32_t lo = sw[CP::arr(j) * stride + s];
+        const uint64_t w = wide ? ((uint64_t)sw[(NA + js) * stride + s] << 32 | lo) : (uint64_t)(long long)(int)lo;
+        js++;
+        return w;
+      }
+      return (uint64_t)(long long)(int)sw[CP::arr(j) * stride + s];
+    };
+    // emit: block compaction, one output reservation per run
+    auto emits = [&](int s) -> bool {
+      if (owner && sw[a_org * stride + s] != 0xFFFFFFFFu) return false;
+      return (s == nslots) ? (s_esc != 0 && sw[s] != 0) : (skeys[s] != EMPTY);
+    };
+    const int per = (stride + BLK - 1) / BLK;
+    const int lo = tid * per, hi = min(stride, lo + per);
+    uint32_t mine = 0;
+    for (int s = lo; s < hi; s++) mine += emits(s);
+    uint32_t x = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[wid] = x;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc = 0;
+      for (int w = 0; w < NWARP; w++) {
+        const uint32_t t2 = s_wsum[w];
+        s_wsum[w] = acc;
+        acc += t2;
+      }
+      // reserve the rows only if they fit (else the run goes to the fallback)
+      unsigned long long base = 0;
+      if (acc) {
+        unsigned long long o = *(volatile unsigned long long*)a.out.count;
+        for (;;) {
+          if (o + acc > (unsigned long long)a.out.cap) {
+            base = ~0ull;
+            break;
+          }
+          const unsigned long long prev = atomicCAS(a.out.count, o, o + acc);
+          if (prev == o) {
+            base = o;
+            break;
+          }
+          o = prev;
+        }
+      }
+      s_base = base;
+    }
+    __syncthreads();
+    if (s_base == ~0ull) {  // (nothing merged or emitted yet: the fallback redoes the whole run)
+      if (tid == 0) {
+        a.failed[p] = 1;
+        atomicOr(a.fail, 4u);
+      }
+      __syncthreads();
+      continue;
+    }
+    if (owner) {
+      // resident groups: merged into the level-0 table (its flush emits them), and
+      // their records were not spilled after all
+      unsigned long long hits = 0;
+      for (int s = tid; s < stride; s += BLK) {
+        const uint32_t ls = sw[a_org * stride + s];
+        if (ls == 0xFFFFFFFFu || sw[s] == 0) continue;
+        hits += sw[s];
+        int js = 0;
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const uint32_t F = CP::fd(j);
+          const uint64_t w = state_of(s, j, js);
+          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)ls * a.t.sstride, F & 3, (F >> 2) & 3, w);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+      if (lane == 0 && hits) {
+        atomicAdd(&a.stats[ST_HITS], hits);
+        atomicAdd(&a.stats[ST_SPILLED], (unsigned long long)(-(long long)hits));
+      }
+    }
+    int64_t idx = (int64_t)s_base + s_wsum[wid] + (x - mine);
+    for (int s = lo; s < hi; s++) {
+      if (!emits(s)) continue;
+      const uint64_t kk[1] = {s == nslots ? EMPTY : skeys[s]};
+      uint64_t st[4] = {0, 0, 0, 0};
+      int js = 0;
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const uint64_t w = state_of(s, j, js);
+        if (j < 4) st[j] = w;
+      }
+      emit_group4<1>(a.sp, a.out, idx++, kk, st);
+    }
+    __syncthreads();
+  }
+}
+
+// Fallback after k_child2_wc: the pages of every run a child completed leave
+// the spill set, so the generic recursion sees only the spill partitions that
+// did not fit (their pages are untouched).  Owner runs that did not fit are
+// re-probed by the host (gathered, then the generic PROBE) before this.
+__global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, const uint32_t* failed, int P,
+                             int NP, int32_t* page_set) {
+  for (int p = blockIdx.x; p < NP; p += gridDim.x) {
+    if (p < P && failed[p]) continue;
+    const uint32_t n = plist_n[p];
+    if (n > cap) continue;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) page_set[plist[(size_t)p * cap + i]] = -1;
+  }
+}
+
+// one run's pages -> dense key / value columns (an owner run the host re-probes)
+__global__ void k_wc2_gather(PagePool pool, const uint32_t* pl, uint32_t npg, unsigned long long* keys,
+                             unsigned long long* vals, unsigned long long* count) {
+  __shared__ unsigned long long s_base;
+  for (uint32_t q = blockIdx.x; q < npg; q += gridDim.x) {
+    const uint32_t pg = pl[q];
+    const int fill = pool.page_fill[pg];
+    if (threadIdx.x == 0) s_base = atomicAdd(count, (unsigned long long)fill);
+    __syncthreads();
+    const ulonglong2* pb = (const ulonglong2*)page_ptr(pool, pg);
+    for (int i = threadIdx.x; i < fill; i += blockDim.x) {
+      const ulonglong2 r = pb[i];
+      keys[s_base + i] = r.x;
+      vals[s_base + i] = r.y;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace aggb

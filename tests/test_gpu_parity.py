@@ -226,8 +226,10 @@ def test_edge_extreme_keys(algo):
 def test_pre_partitioning_residency():
     """Resident keys are never spilled (reference test_operators.py:242-269).
 
-    The level-0 table is flushed first, so the first ``resident_groups`` rows of
-    the unsorted result are the resident groups.  If a resident key had also
+    The level-0 table's groups are one block of ``resident_groups`` rows of the
+    unsorted result: the first rows on the generic path, the last rows on the
+    write-combined path (its children run first and merge the resident keys'
+    aggregates into the table before it is flushed).  If a resident key had also
     been spilled it would come out twice (duplicate check), and the resident
     groups' counts must add up to exactly the records not spilled."""
     from paper_1311_0059_b200 import datagen as D
@@ -242,7 +244,8 @@ def test_pre_partitioning_residency():
     R = met["resident_groups"]
     assert 0.8 * 2500 <= R <= 2500
     assert len(np.unique(res.keys[0])) == res.n_groups == 20_000
-    assert int(res.values[0][:R].sum()) == met["records"] - met["level0_spilled_records"]
+    kept = met["records"] - met["level0_spilled_records"]
+    assert kept in (int(res.values[0][:R].sum()), int(res.values[0][-R:].sum()))
     assert met["level0_spilled_records"] > 0
 
 
