@@ -41,7 +41,8 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", OUT, os.path.join(CSRC, "aggb200.cu")]
+    cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("AGGB_NVCC_FLAGS", "").split(), "-o", OUT,
+           os.path.join(CSRC, "aggb200.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

@@ -651,7 +651,9 @@ struct Handle {
   int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
   int wcQ = 0;                // owner runs (the spill partitions are P0; runs = P0 + wcQ)
   uint32_t wc_ocap = 0;       // resident slots per owner list
-  int64_t wc_launches = 0;    // k_scan_wc launches of this run (page-list sizing)
+  int64_t wc_launches = 0;    // k_scan_wc launches of this run
+  int64_t wc_entries = 0;     // page-list entries per run the launches so far may have taken
+  bool wc_plist_clean = false;  // every entry of the page lists is 0xFFFFFFFF (unused) or belongs to this run
   DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_olist, wc_olist_n, wc_gather;
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
@@ -1283,8 +1285,25 @@ int plan(Handle* h) {
 // key) beside the runs' write-combining rings.  The owner share follows the
 // expected records: resident groups plus the filter's false-positive share of
 // the others.
-constexpr int WC_BLK = 512, WC_R = 4, WC_NS = 2, WC_CBLK = 1024, WC_CRL = 4;
-using Wc2L = Wc2Layout<WC_BLK, WC_R, WC_NS>;
+constexpr int WC_CBLK = 1024, WC_CRL = 4;
+// scan shapes (records per thread and tile x input stages): the tile bounds what one
+// run receives between two window moves (a run's window holds 9-16 records)
+struct WcShape {
+  int blk, R, NS;
+  void (*fn)(Wc2Args);
+  size_t (*bytes)(int, uint32_t);
+};
+static const WcShape WC_SHAPES[] = {
+    {512, 4, 2, k_scan_wc<512, 4, 2>, Wc2Layout<512, 4, 2>::bytes},
+    {512, 2, 4, k_scan_wc<512, 2, 4>, Wc2Layout<512, 2, 4>::bytes},
+    {512, 2, 3, k_scan_wc<512, 2, 3>, Wc2Layout<512, 2, 3>::bytes},
+    {1024, 2, 2, k_scan_wc<1024, 2, 2>, Wc2Layout<1024, 2, 2>::bytes},
+    {768, 2, 2, k_scan_wc<768, 2, 2>, Wc2Layout<768, 2, 2>::bytes},
+};
+const WcShape& wc_shape() {
+  const int i = getenv("AGGB_WC_SHAPE") ? atoi(getenv("AGGB_WC_SHAPE")) : 0;
+  return WC_SHAPES[std::max(0, std::min(4, i))];
+}
 void wc_plan(Handle* h, double spill_groups) {
   h->wc = false;
   h->wcQ = 0;
@@ -1293,16 +1312,19 @@ void wc_plan(Handle* h, double spill_groups) {
       h->unlimited || h->l2_capped || c.level != 0 || h->cs.ds.vty[0] != TY_I64 || getenv("AGGB_NO_WC") ||
       getenv("AGGB_FORCE_L2_CHILDREN"))
     return;
-  const int words = 2 + (h->prog == 2 ? 4 : 2) + 1;  // key, count word, one u32 per other field, owner slot word
+  // slots of a child table: 8-byte key + the narrow state words (spill partitions);
+  // owner runs carry two more words and their share is sized with them below
+  const int wn = h->prog == 2 ? CwWords<CpC2>::W_NARROW : CwWords<CpC1>::W_NARROW;
+  const int we = h->prog == 2 ? CwWords<CpC2>::W_EXT : CwWords<CpC1>::W_EXT;
   const int tbytes = 220 * 1024;
-  const int nslots = ((tbytes / 4 - 2) / words - 1) / 4 * 4;
+  const int nslots = (tbytes / (8 + 4 * wn) - 1) / 4 * 4;
   const int sms = std::max(1, h->sms);
   const double resident = (double)std::max<int64_t>(1, h->budget);
   const double spill = std::max(1.0, spill_groups);
   int I = (int)std::ceil((spill + resident) / (0.45 * nslots));
   I = std::max(2, (I + sms - 1) / sms * sms);
   if (getenv("AGGB_WC_RUNS")) I = std::max(2, atoi(getenv("AGGB_WC_RUNS")));  // experiment override
-  const size_t fixed = Wc2L::bytes(I, 0) + 1024;
+  const size_t fixed = wc_shape().bytes(I, 0) + 1024;
   if (fixed >= 227 * 1024) return;
   const int64_t want = std::max<int64_t>(64, (int64_t)(8 * h->budget) / 32);  // ~8 bits per resident key
   const int64_t room = (int64_t)((227 * 1024 - fixed) / 4);
@@ -1311,8 +1333,9 @@ void wc_plan(Handle* h, double spill_groups) {
   // false-positive share of a 3-bit filter in 32-bit blocks (the block loads vary: +15%)
   const double bpk = 32.0 * (double)nblk / resident;
   const double fp = std::min(1.0, 1.15 * std::pow(1.0 - std::exp(-3.0 / bpk), 3.0));
-  const double share = (resident + fp * spill) / (resident + spill);
-  int Q = (int)std::lround(I * share);
+  // (an owner run's slots are wider: it takes proportionally fewer groups)
+  const double share = (resident + fp * spill) / (resident + spill) * (8.0 + 4 * we) / (8.0 + 4 * wn);
+  int Q = (int)std::lround(I * std::min(0.9, share));
   Q = std::max(1, std::min(I - 1, Q));
   if (getenv("AGGB_WC_OWNERS")) Q = std::max(1, std::min(I - 1, atoi(getenv("AGGB_WC_OWNERS"))));  // experiment override
   h->wc = true;
@@ -1413,6 +1436,8 @@ int begin_run(Handle* h) {
   if (h->has_table) TRY(table_reset(h));
   h->wc_used = false;
   h->wc_launches = 0;
+  h->wc_entries = 0;
+  h->wc_plist_clean = false;
   if (h->wc) {
     const size_t NP = (size_t)h->P0 + (size_t)h->wcQ;
     TRY(h->wc_pn.ensure(NP * 4, &h->hw));
@@ -1527,20 +1552,23 @@ int wc_build(Handle* h, bool bloom, bool owners) {
 int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   const int P = h->P0, NP = h->P0 + h->wcQ;
   const int grid = h->sms;
-  const int64_t T = Wc2L::T;
+  const WcShape& shp = wc_shape();
   // the filter of the table as FILL left it (a kernel boundary: the key set is final once frozen)
   TRY(wc_build(h, true, false));
   const int64_t nlin_cap = h->defer_cap;
-  // page lists: every record of the run so far at twice the mean pages per run, and
-  // one open page per CTA and launch
+  // page lists: every CTA reserves a block of entries per run and launch (twice
+  // the pages it expects to open, at least 2); a run that outgrows its block
+  // takes single entries
   h->wc_launches++;
-  const int64_t recs_run = h->records + col.n + nlin_cap;
-  const uint32_t need_cap = (uint32_t)std::min<int64_t>(
-      0x7FFFFFFF, 2 * (recs_run / 512 / std::max(1, NP)) + (h->wc_launches + 3) * (int64_t)grid + 64);
+  const int64_t exp_pages = (col.n + nlin_cap) / 512 / ((int64_t)grid * std::max(1, NP)) + 1;
+  const uint32_t blk = (uint32_t)std::min<int64_t>(64, 2 * exp_pages);
+  h->wc_entries += (int64_t)grid * blk + (col.n + nlin_cap) / 512 / std::max(1, NP);  // per run, this launch
+  const uint32_t need_cap = (uint32_t)std::min<int64_t>(0x7FFFFFFF, h->wc_entries + 2 * (int64_t)grid + 64);
   if (need_cap > h->wc_plist_cap) {
     DBuf nb;
     const uint32_t new_cap = std::max(need_cap, h->wc_used ? 2 * h->wc_plist_cap : 0u);
     TRY(nb.ensure((size_t)NP * new_cap * 4, &h->hw));
+    CU(cudaMemsetAsync(nb.p, 0xFF, (size_t)NP * new_cap * 4, h->st));
     if (h->wc_used && h->wc_plist_cap)
       CU(cudaMemcpy2DAsync(nb.p, (size_t)new_cap * 4, h->wc_plist.p, (size_t)h->wc_plist_cap * 4,
                            (size_t)h->wc_plist_cap * 4, (size_t)NP, cudaMemcpyDeviceToDevice, h->st));
@@ -1549,6 +1577,10 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
     h->wc_plist = nb;
     nb.p = nullptr;
     h->wc_plist_cap = new_cap;
+    h->wc_plist_clean = true;
+  } else if (!h->wc_plist_clean) {  // a new run over the old lists: every entry unused again
+    CU(cudaMemsetAsync(h->wc_plist.p, 0xFF, (size_t)NP * h->wc_plist_cap * 4, h->st));
+    h->wc_plist_clean = true;
   }
   // pages: the records, plus each (CTA, run) chain's last page, plus stashes
   const int stash = 32;
@@ -1580,17 +1612,19 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.plist = h->wc_plist.as<uint32_t>();
   a.plist_n = h->wc_pn.as<uint32_t>();
   a.plist_cap = h->wc_plist_cap;
+  a.plist_blk = blk;
   a.part_recs = h->wc_recs.as<unsigned long long>();
   a.stats = SC(h);
   a.vinfo = h->wc_vinfo.as<unsigned int>();
   a.fail = h->wc_fail.as<uint32_t>();
   a.stash = stash;
   a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
-  auto fs = k_scan_wc<WC_BLK, WC_R, WC_NS>;
-  const size_t smem = Wc2L::bytes(NP, h->wc_nblk);
+  if (getenv("AGGB_WC_NOSEND")) a.pf |= 2;  // (experiment: lines are not sent; results are wrong)
+  auto fs = shp.fn;
+  const size_t smem = shp.bytes(NP, h->wc_nblk);
   CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int pe = prof_begin(h, 15);
-  fs<<<grid, WC_BLK, smem, h->st>>>(a);
+  fs<<<grid, shp.blk, smem, h->st>>>(a);
   prof_end(h, pe);
   CU(cudaGetLastError());
   h->launches++;

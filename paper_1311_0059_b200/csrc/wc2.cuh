@@ -54,6 +54,11 @@ __device__ __forceinline__ uint32_t wc2_owner(uint32_t lo, uint32_t Q) { return 
 __global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* bloom, uint32_t nblk, uint32_t* olist, uint32_t* olist_n,
                             uint32_t ocap, uint32_t Q) {
   const uint64_t n = t.mask + 1;
+  if (bloom && blockIdx.x == 0 && threadIdx.x == 0 && *(volatile int*)&t.hdr->esc) {
+    // the sentinel key lives in the table's escape slot: routed like any resident key
+    const uint64_t h = wc2_hash(EMPTY, seed);
+    atomicOr(&bloom[wc2_block((uint32_t)h, nblk)], wc2_bits((uint32_t)(h >> 32)));
+  }
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = t.keys[i];
     if (k == EMPTY) continue;
@@ -87,6 +92,7 @@ struct Wc2Args {
   uint32_t* plist;                        // [P + Q][plist_cap] page ids per run
   uint32_t* plist_n;                      // [P + Q]
   uint32_t plist_cap;
+  uint32_t plist_blk;                     // page-list entries a CTA reserves per run at a time
   unsigned long long* part_recs;          // [P + Q] records per run
   unsigned long long* stats;              // ST_* counters
   unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes (int64 columns)
@@ -105,7 +111,7 @@ struct Wc2Layout {
   static constexpr int NE = 8;         // page map entries per run (pages a run can open in one tile)
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
   static __host__ __device__ size_t ring_bytes(int NP) { return (size_t)NP * RS * 16; }
-  static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (1 + NE) * 4 + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (3 + NE) * 4 + 15) & ~(size_t)15; }
   static __host__ __device__ size_t bytes(int NP, uint32_t nblk) {
     return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + (((size_t)nblk * 4 + 15) & ~(size_t)15);
   }
@@ -126,11 +132,11 @@ constexpr int WC2_PF = 6;  // L2 prefetch distance in tiles (rounds of the grid)
 //       one run in one tile) is held.  The claimer of a page's first slot opens
 //       the page (CTA-private, appended to the run's device-side page list).
 //   barrier 1
-//   [B] the claimer of a line's 8th slot sends the line: one 128-byte bulk copy
-//       shared -> global.  Held records of lines that are complete go straight
-//       to their page; those of the run's open line are parked in registers and
-//       written into the ring at the start of the next tile.  Windows move to
-//       the open lines.
+//   [B] held records of lines that are complete go straight to their page;
+//       those of the run's open line are parked in registers and written into
+//       the ring at the start of the next tile.  One thread per run sends the
+//       window lines the tile completed, one 128-byte bulk copy shared -> global
+//       each, and moves the run's window to its open line.
 //   barrier 2 (ring and stage free again; thread 0 issues the stage's next tile)
 template <int BLK, int R, int NS>
 __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
@@ -146,6 +152,8 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
   ulonglong2* ring = (ulonglong2*)(smem + L::stage_bytes());
   uint32_t* cw = (uint32_t*)(smem + L::stage_bytes() + L::ring_bytes(NP));
   uint32_t* ent = cw + NP;
+  uint32_t* lbase = ent + NP * NE;  // this CTA's block of the run's page list ...
+  uint32_t* lused = lbase + NP;     // ... and the entries of it in use
   uint32_t* sbloom = (uint32_t*)((unsigned char*)cw + L::meta_bytes(NP));
   const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw), a_bloom = smem_u32(sbloom);
   __shared__ __align__(8) uint64_t mbar[NS];
@@ -158,7 +166,16 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
   const int64_t nlin = a.lcount ? (int64_t)*a.lcount : 0;
   const unsigned long long total = (unsigned long long)(col_tiles + (nlin + T - 1) / T);
 
-  for (int p = tid; p < NP; p += BLK) cw[p] = 0;
+  // page-list entries are reserved per run in blocks, up front: opening a page then
+  // needs no returning global atomic (a ~1 us round trip that every other warp of
+  // the tile waited for at barrier 1, about four times per tile)
+  // (entries left unused stay 0xFFFFFFFF; a run that needs more than its block takes
+  // single entries with the atomic)
+  for (int p = tid; p < NP; p += BLK) {
+    cw[p] = 0;
+    lbase[p] = atomicAdd(&a.plist_n[p], a.plist_blk);
+    lused[p] = 0;
+  }
   for (int i = tid; i < NP * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
   for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg(a.bloom + i);
   if (tid == 0) {
@@ -244,7 +261,8 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
       a.pool.page_part[pg] = p;
       a.pool.page_set[pg] = a.set_id;
       a.pool.page_fill[pg] = S;
-      const uint32_t li = atomicAdd(&a.plist_n[p], 1u);
+      const uint32_t u = atomicAdd(&lused[p], 1u);
+      const uint32_t li = u < a.plist_blk ? lbase[p] + u : atomicAdd(&a.plist_n[p], 1u);
       if (li < a.plist_cap) a.plist[(size_t)p * a.plist_cap + li] = pg;
       else atomicExch(a.fail, 1u);
     }
@@ -259,7 +277,6 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
     old[r] = 0;
     pid[r] = 0;
   }
-  uint32_t vmask = 0;  // records of the tile this thread routed
   uint32_t held = 0;   // ... claimed beyond their run's window
   uint32_t opark = 0;  // ... parked for the next tile (open line)
   uint64_t hk[R], hv[R];
@@ -273,9 +290,17 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
   auto rec_idx = [&](int r) { return 2 * ((r >> 1) * BLK + tid) + (r & 1); };
   auto in_window = [&](uint32_t o) { return ((((o & CWM) >> 3) - (o >> 23)) & 511u) < (uint32_t)LINES; };
 
+#ifdef WC2_TIMING
+  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0 = clock64();
+  unsigned nheld = 0;
+#define WC2_T(i) { const long long t1 = clock64(); tm[i] += t1 - t0; t0 = t1; }
+#else
+#define WC2_T(i)
+#endif
   for (int it = 0;; it++) {
     const int s = it % NS;
     mbar_wait(&mbar[s], (uint32_t)((it / NS) & 1));
+    WC2_T(0)
     const int c = s_tcnt[s];
     if (tid == 0 && a.stash && !nb_busy && !s_nv && 2 * s_su >= s_sc) {  // next stash, taken after barrier 1
       nb_pending = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
@@ -305,14 +330,13 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
 #pragma unroll
         for (int r = 0; r < R; r++) vm_ |= (uint32_t)(rec_idx(r) < c) << r;
       }
-      vmask = vm_;
 #pragma unroll
       for (int r = 0; r < R; r++) {
         const uint64_t h = wc2_hash(k[r], a.seed);
         const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
         const uint32_t blk = lds32(a_bloom + 4u * wc2_block(lo, nblk));
         const uint32_t bits = wc2_bits(hi);
-        const bool pos = ((blk & bits) == bits) | (k[r] == EMPTY);
+        const bool pos = (blk & bits) == bits;
         pid[r] = pos ? P + (int)wc2_owner(lo, Q) : (int)__umulhi(hi, (uint32_t)P);
         const uint64_t m = v[r] ^ (uint64_t)((long long)v[r] >> 63);
         vm |= FULL ? m : (((vm_ >> r) & 1u) ? m : 0ull);
@@ -334,8 +358,10 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
     if (c == T) route(std::true_type{});
     else route(std::false_type{});
     const bool more = c != 0;
+    WC2_T(1)
     fence_proxy_async_smem();  // ring writes before the bulk copies that read them
     __syncthreads();           // ---- barrier 1
+    WC2_T(2)
     if (tid == 0) {
       if (nb_busy) {
         s_nb = nb_pending;
@@ -352,23 +378,7 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
         s_nv = 0;
       }
     }
-    // ---- [B1] the lines this thread completed: 128-byte bulk copies (TMA engine)
-    bool sent = false;
-    {
-      const uint32_t live = vmask & ~held;
-#pragma unroll
-      for (int r = 0; r < R; r++) {
-        const uint32_t x = old[r] & CWM;
-        if (((live >> r) & 1u) && (x & 7u) == 7u) {
-          const uint32_t x0 = x & ~7u;
-          const uint32_t pg = page_of(pid[r], x0 >> SLOG);
-          if (pg < 0xFFFFFFu) bulk_s2g(rec_ptr(pg, x0), &ring[pid[r] * RS + (x0 & (RING - 1))], 128u);
-          sent = true;
-        }
-      }
-    }
-    if (sent) bulk_commit();
-    // ---- [B2] held records: complete lines straight to their page, the open line waits
+    // ---- [B1] held records: complete lines straight to their page, the open line waits
     if (__builtin_expect(held != 0, 0)) {
 #pragma unroll
       for (int r = 0; r < R; r++) {
@@ -386,20 +396,83 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
         }
       }
     }
-    vmask = 0;
-    for (int p = tid; p < NP; p += BLK) {  // the windows move to the open lines
-      const uint32_t cc = cw[p] & CWM;
-      cw[p] = ((cc >> 3) << 23) | cc;
+    WC2_T(6)
+#ifdef WC2_TIMING
+    nheld += __popc(held);
+#endif
+    // ---- [B2] one lane per run (run p belongs to warp p % NW): the lines of the
+    // run's window that this tile completed leave through the warp, four lines
+    // per step (8 lanes x 16 bytes = one 128-byte line per store group), and the
+    // window moves to the run's open line.  (Lines completed beyond the window
+    // were all held.  A 128-byte bulk copy per line through the TMA engine
+    // measured ~16 cycles per copy and SM: 57% of the tile.)
+    {
+      constexpr int NW = BLK / 32;
+      const int wid = tid >> 5;
+      const int sub = lane & 7, grp = lane >> 3;
+      for (int p0 = wid; p0 < NP; p0 += 32 * NW) {
+        const int p = p0 + NW * lane;
+        uint32_t nl = 0, ln = 0;
+        if (p < NP) {
+          const uint32_t w = cw[p];
+          const uint32_t cc = w & CWM;
+          ln = cc >> 3;
+          nl = (ln - (w >> 23)) & 511u;  // lines completed since the window opened
+          if (nl) cw[p] = (ln << 23) | cc;
+        }
+        const uint32_t ns = nl < (uint32_t)LINES ? nl : (uint32_t)LINES;
+#pragma unroll
+        for (int round = 0; round < LINES; round++) {
+          const bool has = ns > (uint32_t)round;
+          uint32_t mask = __ballot_sync(0xffffffffu, has);
+          if (!mask) break;
+          const uint32_t x0 = (ln - nl + (uint32_t)round) << 3;
+          uint32_t src = 0;
+          unsigned long long dst = 0;
+          if (has) {
+            const uint32_t pg = page_of(p, x0 >> SLOG);
+            src = a_ring + 16u * ((uint32_t)p * RS + (x0 & (RING - 1)));
+            dst = pg < 0xFFFFFFu ? (unsigned long long)rec_ptr(pg, x0) : 0ull;
+          }
+          while (mask) {
+            // lane group g copies the line of the g-th lowest lane in mask
+            uint32_t m = mask;
+            if (grp >= 1) m &= m - 1;
+            if (grp >= 2) m &= m - 1;
+            if (grp >= 3) m &= m - 1;
+            const int l = m ? __ffs(m) - 1 : 0;
+            const uint32_t s1 = __shfl_sync(0xffffffffu, src, l);
+            const unsigned long long d1 = __shfl_sync(0xffffffffu, dst, l);
+            if (m && d1) {
+              uint64_t x, y;
+              lds128(s1 + 16u * (uint32_t)sub, x, y);
+              st_v2((void*)(d1 + 16ull * (unsigned long long)sub), make_ulonglong2(x, y));
+            }
+            mask &= mask - 1;
+            mask &= mask - 1;
+            mask &= mask - 1;
+            mask &= mask - 1;
+          }
+        }
+      }
     }
+    const bool sent = false;
+    WC2_T(3)
     if (sent) bulk_wait_read0();  // the ring slots are read before barrier 2
+    WC2_T(4)
     // ---- barrier 2: ring and stage are free again
     if (!more) {
       if (!__syncthreads_or(opark != 0)) break;
     } else {
       __syncthreads();
     }
+    WC2_T(5)
     if (tid == 0) issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
   }
+#ifdef WC2_TIMING
+  if (blockIdx.x == 3 && lane == 0)
+    printf("warp %2d: mbar %lld A %lld bar1 %lld B1 %lld B2 %lld rdwait %lld bar2 %lld held(lane0) %u\n", tid >> 5, tm[0], tm[1], tm[2], tm[6], tm[3], tm[4], tm[5], nheld);
+#endif
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
   // ---- close: every run's open line (all in the ring), then the page fills
   for (int p = tid; p < NP; p += BLK) {
@@ -505,17 +578,82 @@ __device__ __forceinline__ void reds_max_s32(uint32_t a, int v) {
   asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Table layout (stride = nslots + 1, the last slot is the sentinel key's):
-//   skeys[stride] u64 keys in 32-byte buckets of 4 slots
-//   sw[a][stride] u32 word arrays: 0 count, CP::arr(j) field j, then the hi words
-//                 of wide sums, then (owner runs) the level-0 slot of a seeded key
-// A record's probe compares the low key words of its bucket (4 compares), checks
-// the high word of the match and falls to the general loop only for a first
-// occurrence, a displaced key or keys that differ only in their high words.
+// word layout of a slot's compact states (u32 words, slot-major so that every
+// offset below is an immediate): MIN / MAX fields first (one LDS.64 reads a
+// MIN-MAX pair), the count word, one word per SUM; the extended layout (wide
+// sums and owner runs) adds the sums' high words and the level-0 slot of a
+// seeded key.  Both strides are even (8-byte aligned slots).
+template <class CP>
+struct CwWords {
+  static constexpr int N = CP::N;
+  __host__ __device__ static constexpr bool is_mm(int j) { return !CP::is_count(j) && !CP::is_sum(j); }
+  __host__ __device__ static constexpr int nmm() {
+    int x = 0;
+    for (int i = 0; i < N; i++) x += is_mm(i);
+    return x;
+  }
+  static constexpr int NMM = nmm(), NSUM = CP::nsum();
+  static constexpr int W_CNT = NMM;
+  static constexpr int WB = NMM + 1 + NSUM;        // base words
+  static constexpr int W_HI = WB;                  // + k: high word of sum k
+  static constexpr int W_ORG = WB + NSUM;          // level-0 slot of a seeded key
+  static constexpr int W_NARROW = (WB + 1) & ~1, W_EXT = (WB + NSUM + 1 + 1) & ~1;
+  // word of field j (COUNT fields share the count word)
+  __host__ __device__ static constexpr int word(int j) {
+    if (CP::is_count(j)) return W_CNT;
+    int x = 0;
+    if (is_mm(j)) {
+      for (int i = 0; i < j; i++) x += is_mm(i);
+      return x;
+    }
+    for (int i = 0; i < j; i++) x += CP::is_sum(i);
+    return NMM + 1 + x;
+  }
+  __host__ __device__ static constexpr int sum_rank(int j) {
+    int x = 0;
+    for (int i = 0; i < j; i++) x += CP::is_sum(i);
+    return x;
+  }
+  __host__ __device__ static constexpr uint32_t identity(int w) {  // initial value of base word w
+    for (int j = 0; j < N; j++)
+      if (is_mm(j) && word(j) == w) return (CP::fd(j) & 3) == OP_MIN ? 0x7FFFFFFFu : 0x80000000u;
+    return 0u;
+  }
+  // a MIN field at word 0 and a MAX field at word 1: read together
+  __host__ __device__ static constexpr bool mm_pair() {
+    if (NMM != 2) return false;
+    bool mn = false, mx = false;
+    for (int j = 0; j < N; j++) {
+      if (is_mm(j) && word(j) == 0 && (CP::fd(j) & 3) == OP_MIN) mn = true;
+      if (is_mm(j) && word(j) == 1 && (CP::fd(j) & 3) == OP_MAX) mx = true;
+    }
+    return mn && mx;
+  }
+};
+
+__device__ __forceinline__ uint32_t fmix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+// slot hash of a child table (independent of the level-0 routing hash)
+__device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) {
+  return fmix32((uint32_t)k ^ seed ^ ((uint32_t)(k >> 32) * 0x9E3779B1u));
+}
+
+// Table: skeys[nslots + 1] u64 keys in 32-byte buckets of 4 slots (the last slot
+// is the sentinel key's), then (nslots + 1) x W u32 state words.
+// A record compares its key with the four keys of its bucket, all RL records'
+// buckets in flight together; a record that did not hit looks at the next
+// bucket (a displaced key: warp-uniform second stage) and only then takes the
+// general loop (first occurrence -> CAS insert, longer chains, the sentinel key).
 template <class CP, int BLK, int RL>
 __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
-  constexpr int N = CP::N;
-  constexpr int NA = CP::na(), NSUM = CP::nsum();
+  using CW = CwWords<CP>;
+  constexpr int N = CP::N, NSUM = CW::NSUM;
   constexpr int NWARP = BLK / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -524,32 +662,30 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
   __shared__ uint32_t s_wsum[NWARP];
   const bool rfit = a.vinfo[0] == 0;  // every value is an int32
   const uint32_t vabs = a.vinfo[1] + 1u;
+  const uint32_t seed32 = (uint32_t)a.seed ^ (uint32_t)(a.seed >> 32);
   const int NP = a.P + a.Q;
   for (int p = blockIdx.x; p < NP; p += gridDim.x) {
     const unsigned long long np = a.part_recs[p];
     if (np == 0) continue;
     const bool owner = p >= a.P;
     // wide sums (a u32 pair with carry) only when a run's sum can leave int32
-    const bool wide = (double)np * (double)vabs >= 2147483647.0;
-    const int words = 2 + NA + (wide ? NSUM : 0) + (owner ? 1 : 0);
-    const int nbk = ((a.table_bytes / 4 - 2) / words - 1) / 4;
+    const bool wide = NSUM > 0 && (double)np * (double)vabs >= 2147483647.0;
+    const bool ext = wide || owner;
+    const int W = ext ? CW::W_EXT : CW::W_NARROW;
+    const int nbk = (a.table_bytes / (8 + 4 * W) - 1) / 4;
     const int nslots = nbk * 4;
     const int maxg = (int)(0.85 * nslots);
     const int stride = nslots + 1;
-    uint64_t* skeys = (uint64_t*)smem;                 // stride keys (escape slot last)
-    uint32_t* sw = (uint32_t*)(skeys + stride);        // [array][slot] u32 words
-    const int a_org = NA + (wide ? NSUM : 0);          // owner runs: array of level-0 slots
-    const uint32_t a_keys = smem_u32(skeys), a_sw = smem_u32(sw);
+    uint64_t* skeys = (uint64_t*)smem;           // stride keys (escape slot last)
+    uint32_t* sst = (uint32_t*)(skeys + stride);  // stride x W state words
+    const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst);
     for (int i = tid; i < stride; i += BLK) {
       skeys[i] = EMPTY;
-      sw[i] = 0;
 #pragma unroll
-      for (int j = 0; j < N; j++)
-        if (!CP::is_count(j))
-          sw[CP::arr(j) * stride + i] =
-              (CP::fd(j) & 3) == OP_MIN ? 0x7FFFFFFFu : (CP::fd(j) & 3) == OP_MAX ? 0x80000000u : 0u;
-      for (int j = 0; j < (wide ? NSUM : 0); j++) sw[(NA + j) * stride + i] = 0u;
-      if (owner) sw[a_org * stride + i] = 0xFFFFFFFFu;
+      for (int w = 0; w < CW::WB; w++) sst[i * W + w] = CW::identity(w);
+      if (ext) {
+        for (int w = CW::WB; w < CW::W_EXT; w++) sst[i * W + w] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
+      }
     }
     if (tid == 0) {
       s_groups = 0;
@@ -588,24 +724,24 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
         for (uint32_t i = tid; i < nres; i += BLK) {
           const uint32_t ls = a.olist[(size_t)o * a.ocap + i];
           const uint64_t k = a.t.keys[ls];
-          const uint64_t kk[1] = {k};
-          const uint64_t h = hash_key<1>(kk, a.seed);
-          const int sl = probe_slow(k, (int)__umulhi((uint32_t)h, (uint32_t)nbk));
-          if (sl >= 0) sw[a_org * stride + sl] = ls;
+          const int sl = probe_slow(k, (int)__umulhi(cw_hash(k, seed32), (uint32_t)nbk));
+          if (sl >= 0) sst[sl * W + CW::W_ORG] = ls;
         }
-        if (tid == 0 && *(volatile int*)&a.t.hdr->esc) sw[a_org * stride + nslots] = (uint32_t)(a.t.mask + 1);
+        if (tid == 0 && *(volatile int*)&a.t.hdr->esc) sst[nslots * W + CW::W_ORG] = (uint32_t)(a.t.mask + 1);
       }
       __syncthreads();
     }
     const uint32_t npg = min(a.plist_n[p], a.plist_cap);
     const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
-    auto records = [&](auto wide_t) {
+    auto records = [&](auto wide_t, auto ext_t) {
       constexpr bool WIDE = decltype(wide_t)::value;
+      constexpr int WS = decltype(ext_t)::value ? CW::W_EXT : CW::W_NARROW;
       // Warp w takes pages w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
       // the page, RL records per lane in flight.
       for (uint32_t q = wid; q < npg; q += NWARP) {
         if (__any_sync(0xffffffffu, *(volatile int*)&s_fail)) break;  // warp-uniform
         const uint32_t pg = pl[q];
+        if (pg == 0xFFFFFFFFu) continue;  // (an entry a CTA reserved and did not need)
         const int fill = a.pool.page_fill[pg];
         const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
         for (int s0 = 0; s0 < fill; s0 += RL * 32) {
@@ -613,59 +749,74 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
 #pragma unroll
           for (int r = 0; r < RL; r++) {
             const int sl = s0 + r * 32 + lane;
-            cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(EMPTY, 0);
-          }
-          // first bucket of every record: loads in flight together
-          int bk[RL];
-          uint64_t bx[RL][4];
-#pragma unroll
-          for (int r = 0; r < RL; r++) {
-            const uint64_t kk[1] = {cur[r].x};
-            const uint64_t h = hash_key<1>(kk, a.seed);
-            bk[r] = (int)__umulhi((uint32_t)h, (uint32_t)nbk);
-            lds128(a_keys + 32u * (uint32_t)bk[r], bx[r][0], bx[r][1]);
-            lds128(a_keys + 32u * (uint32_t)bk[r] + 16u, bx[r][2], bx[r][3]);
+            cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(EMPTY, 0);  // (padding never hits: guard below)
           }
 #pragma unroll
-          for (int r = 0; r < RL; r++) {
-            const uint64_t k = cur[r].x;
-            const uint32_t klo = (uint32_t)k, khi = (uint32_t)(k >> 32);
-            const bool e0 = (uint32_t)bx[r][0] == klo, e1 = (uint32_t)bx[r][1] == klo, e2 = (uint32_t)bx[r][2] == klo,
-                       e3 = (uint32_t)bx[r][3] == klo;
-            const int hi_ = e0 ? 0 : e1 ? 1 : e2 ? 2 : 3;
-            const uint32_t hv = (uint32_t)((e0 ? bx[r][0] : e1 ? bx[r][1] : e2 ? bx[r][2] : bx[r][3]) >> 32);
-            int slot = ((e0 | e1 | e2 | e3) && hv == khi) ? bk[r] * 4 + hi_ : -1;
-            const bool valid = s0 + r * 32 + lane < fill;
-            if (__builtin_expect(k == EMPTY, 0)) {  // the sentinel key (and the padding of a short page)
-              slot = valid ? nslots : -1;
-              if (valid) s_esc = 1;  // (idempotent; read after the barrier)
-            } else if (__builtin_expect(slot < 0, 0)) {
-              slot = probe_slow(k, bk[r]);
+          for (int r0 = 0; r0 < RL; r0 += 2) {
+            // the buckets of two records in flight together
+            int bk[2];
+            uint64_t bx[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+              bk[u] = (int)__umulhi(cw_hash(cur[r0 + u].x, seed32), (uint32_t)nbk);
+              lds128(a_keys + 32u * (uint32_t)bk[u], bx[u][0], bx[u][1]);
+              lds128(a_keys + 32u * (uint32_t)bk[u] + 16u, bx[u][2], bx[u][3]);
             }
-            __syncwarp();
-            if (slot >= 0) {
-              const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
-              const uint32_t a_s = a_sw + 4u * (uint32_t)slot;
-              reds_add(a_s, 1u);
-              int js = 0;
 #pragma unroll
-              for (int j = 0; j < N; j++) {
-                const uint32_t F = CP::fd(j);
-                if (((F >> 4) & 3) == SRC_ONE) continue;  // COUNT: the count word
-                const uint32_t a_w = a_s + 4u * (uint32_t)(CP::arr(j) * stride);
-                if ((F & 3) == OP_ADD) {
-                  if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
-                    const uint32_t o = atoms_add(a_w, (uint32_t)cb);
-                    const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
-                    if (hi) reds_add(a_s + 4u * (uint32_t)((NA + js) * stride), hi);
+            for (int u = 0; u < 2; u++) {
+              const int r = r0 + u;
+              const uint64_t k = cur[r].x;
+              const bool e0 = bx[u][0] == k, e1 = bx[u][1] == k, e2 = bx[u][2] == k, e3 = bx[u][3] == k;
+              // (the sentinel key and page padding would "match" an empty slot)
+              const bool hit = (e0 | e1 | e2 | e3) & (k != EMPTY);
+              int slot = hit ? bk[u] * 4 + (e0 ? 0 : e1 ? 1 : e2 ? 2 : 3) : -1;
+              const bool need = !hit && s0 + r * 32 + lane < fill;
+              if (__any_sync(0xffffffffu, need)) {  // warp-uniform second stage
+                if (need) {
+                  if (__builtin_expect(k == EMPTY, 0)) {
+                    slot = nslots;
+                    s_esc = 1;  // (idempotent; read after the barrier)
                   } else {
-                    reds_add(a_w, (uint32_t)cb);
+                    const int b2 = bk[u] + 1 == nbk ? 0 : bk[u] + 1;
+                    uint64_t c0, c1, c2, c3;
+                    lds128(a_keys + 32u * (uint32_t)b2, c0, c1);
+                    lds128(a_keys + 32u * (uint32_t)b2 + 16u, c2, c3);
+                    const bool f0 = c0 == k, f1 = c1 == k, f2 = c2 == k, f3 = c3 == k;
+                    if (f0 | f1 | f2 | f3) slot = b2 * 4 + (f0 ? 0 : f1 ? 1 : f2 ? 2 : 3);
+                    else slot = probe_slow(k, bk[u]);
                   }
-                  js++;
-                } else if ((F & 3) == OP_MIN) {  // read first: most records do not improve the extreme
-                  if (cb < (int)lds32(a_w)) reds_min_s32(a_w, cb);
-                } else {
-                  if (cb > (int)lds32(a_w)) reds_max_s32(a_w, cb);
+                }
+                __syncwarp();
+              }
+              if (slot >= 0) {
+                const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
+                const uint32_t a_s = a_st + (uint32_t)(4 * WS) * (uint32_t)slot;
+                reds_add(a_s + 4u * CW::W_CNT, 1u);
+                if constexpr (CW::mm_pair()) {  // read first: most records do not improve an extreme
+                  const uint64_t mm = lds64(a_s);
+                  if (cb < (int)(uint32_t)mm) reds_min_s32(a_s, cb);
+                  if (cb > (int)(uint32_t)(mm >> 32)) reds_max_s32(a_s + 4u, cb);
+                }
+#pragma unroll
+                for (int j = 0; j < N; j++) {
+                  const uint32_t F = CP::fd(j);
+                  if (CP::is_count(j)) continue;
+                  const uint32_t a_w = a_s + 4u * (uint32_t)CW::word(j);
+                  if (CP::is_sum(j)) {
+                    if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
+                      const uint32_t o = atoms_add(a_w, (uint32_t)cb);
+                      const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
+                      if (hi) reds_add(a_s + 4u * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
+                    } else {
+                      reds_add(a_w, (uint32_t)cb);
+                    }
+                  } else if (!CW::mm_pair()) {
+                    if ((F & 3) == OP_MIN) {
+                      if (cb < (int)lds32(a_w)) reds_min_s32(a_w, cb);
+                    } else {
+                      if (cb > (int)lds32(a_w)) reds_max_s32(a_w, cb);
+                    }
+                  }
                 }
               }
             }
@@ -673,8 +824,9 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
         }
       }
     };
-    if (wide) records(std::true_type{});
-    else records(std::false_type{});
+    if (wide) records(std::true_type{}, std::true_type{});
+    else if (ext) records(std::false_type{}, std::true_type{});
+    else records(std::false_type{}, std::false_type{});
     __syncthreads();
     if (s_fail) {
       if (tid == 0) {
@@ -684,23 +836,22 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
       __syncthreads();
       continue;
     }
-    // state words of slot s as 64-bit native states
-    auto state_of = [&](int s, int j, int& js) -> uint64_t {
-      const uint32_t F = CP::fd(j);
-      if (((F >> 4) & 3) == SRC_ONE) return (uint64_t)sw[s];
-      if ((F & 3) == OP_ADD) {
-        const uint32_t lo = sw[CP::arr(j) * stride + s];
-        const uint64_t w = wide ? ((uint64_t)sw[(NA + js) * stride + s] << 32 | lo) : (uint64_t)(long long)(int)lo;
-        js++;
-        return w;
+    // state word j of slot s as a 64-bit native state
+    auto state_of = [&](int s, int j) -> uint64_t {
+      const uint32_t* w = sst + s * W;
+      if (CP::is_count(j)) return (uint64_t)w[CW::W_CNT];
+      if (CP::is_sum(j)) {
+        const uint32_t lo = w[CW::word(j)];
+        return wide ? ((uint64_t)w[CW::W_HI + CW::sum_rank(j)] << 32 | lo) : (uint64_t)(long long)(int)lo;
       }
-      return (uint64_t)(long long)(int)sw[CP::arr(j) * stride + s];
+      return (uint64_t)(long long)(int)w[CW::word(j)];
     };
-    // emit: block compaction, one output reservation per run
+    // rows this run emits: its groups, minus the seeded (resident) ones of an owner run
     auto emits = [&](int s) -> bool {
-      if (owner && sw[a_org * stride + s] != 0xFFFFFFFFu) return false;
-      return (s == nslots) ? (s_esc != 0 && sw[s] != 0) : (skeys[s] != EMPTY);
+      if (owner && sst[s * W + CW::W_ORG] != 0xFFFFFFFFu) return false;
+      return (s == nslots) ? (s_esc != 0 && sst[s * W + CW::W_CNT] != 0) : (skeys[s] != EMPTY);
     };
+    // block compaction, one output reservation per run
     const int per = (stride + BLK - 1) / BLK;
     const int lo = tid * per, hi = min(stride, lo + per);
     uint32_t mine = 0;
@@ -753,15 +904,15 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
       // their records were not spilled after all
       unsigned long long hits = 0;
       for (int s = tid; s < stride; s += BLK) {
-        const uint32_t ls = sw[a_org * stride + s];
-        if (ls == 0xFFFFFFFFu || sw[s] == 0) continue;
-        hits += sw[s];
-        int js = 0;
+        const uint32_t ls = sst[s * W + CW::W_ORG];
+        const uint32_t cnt = sst[s * W + CW::W_CNT];
+        if (ls == 0xFFFFFFFFu || cnt == 0) continue;
+        hits += cnt;
 #pragma unroll
         for (int j = 0; j < N; j++) {
           const uint32_t F = CP::fd(j);
-          const uint64_t w = state_of(s, j, js);
-          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)ls * a.t.sstride, F & 3, (F >> 2) & 3, w);
+          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)ls * a.t.sstride, F & 3, (F >> 2) & 3,
+                  state_of(s, j));
         }
       }
 #pragma unroll
@@ -776,12 +927,9 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
       if (!emits(s)) continue;
       const uint64_t kk[1] = {s == nslots ? EMPTY : skeys[s]};
       uint64_t st[4] = {0, 0, 0, 0};
-      int js = 0;
 #pragma unroll
-      for (int j = 0; j < N; j++) {
-        const uint64_t w = state_of(s, j, js);
-        if (j < 4) st[j] = w;
-      }
+      for (int j = 0; j < N; j++)
+        if (j < 4) st[j] = state_of(s, j);
       emit_group4<1>(a.sp, a.out, idx++, kk, st);
     }
     __syncthreads();
@@ -798,7 +946,10 @@ __global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uin
     if (p < P && failed[p]) continue;
     const uint32_t n = plist_n[p];
     if (n > cap) continue;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) page_set[plist[(size_t)p * cap + i]] = -1;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t pg = plist[(size_t)p * cap + i];
+      if (pg != 0xFFFFFFFFu) page_set[pg] = -1;
+    }
   }
 }
 
@@ -808,6 +959,7 @@ __global__ void k_wc2_gather(PagePool pool, const uint32_t* pl, uint32_t npg, un
   __shared__ unsigned long long s_base;
   for (uint32_t q = blockIdx.x; q < npg; q += gridDim.x) {
     const uint32_t pg = pl[q];
+    if (pg == 0xFFFFFFFFu) continue;  // (uniform over the CTA)
     const int fill = pool.page_fill[pg];
     if (threadIdx.x == 0) s_base = atomicAdd(count, (unsigned long long)fill);
     __syncthreads();
