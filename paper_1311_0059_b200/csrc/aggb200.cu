@@ -1443,13 +1443,13 @@ int begin_run(Handle* h) {
     TRY(h->wc_pn.ensure(NP * 4, &h->hw));
     TRY(h->wc_recs.ensure(NP * 8, &h->hw));
     TRY(h->wc_failed.ensure(NP * 4, &h->hw));
-    TRY(h->wc_vinfo.ensure(8, &h->hw));
+    TRY(h->wc_vinfo.ensure(16, &h->hw));
     TRY(h->wc_fail.ensure(8, &h->hw));
     TRY(h->wc_bloom.ensure((size_t)h->wc_nblk * 4, &h->hw));
     CU(cudaMemsetAsync(h->wc_pn.p, 0, NP * 4, h->st));
     CU(cudaMemsetAsync(h->wc_recs.p, 0, NP * 8, h->st));
     CU(cudaMemsetAsync(h->wc_failed.p, 0, NP * 4, h->st));
-    CU(cudaMemsetAsync(h->wc_vinfo.p, 0, 8, h->st));
+    CU(cudaMemsetAsync(h->wc_vinfo.p, 0, 16, h->st));
     CU(cudaMemsetAsync(h->wc_fail.p, 0, 8, h->st));
   }
   return AGGB_OK;

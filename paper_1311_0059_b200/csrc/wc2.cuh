@@ -95,7 +95,7 @@ struct Wc2Args {
   uint32_t plist_blk;                     // page-list entries a CTA reserves per run at a time
   unsigned long long* part_recs;          // [P + Q] records per run
   unsigned long long* stats;              // ST_* counters
-  unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes (int64 columns)
+  unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words
   uint32_t* fail;                         // page list overflow / page map error
   int32_t stash;                          // pages per CTA stash refill
   int32_t pf;                             // L2 prefetch of the batch tiles ahead
@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
 #pragma unroll
   for (int r = 0; r < R; r++) hk[r] = hv[r] = 0;
   uint64_t vm = 0;  // OR of v ^ (v >> 63): bounds the magnitudes (compact children)
+  uint32_t km = 0;  // OR of the keys' high words (32-bit child tables when zero)
   uint32_t nb_pending = 0;
   bool nb_busy = false;
 
@@ -340,6 +341,7 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
         pid[r] = pos ? P + (int)wc2_owner(lo, Q) : (int)__umulhi(hi, (uint32_t)P);
         const uint64_t m = v[r] ^ (uint64_t)((long long)v[r] >> 63);
         vm |= FULL ? m : (((vm_ >> r) & 1u) ? m : 0ull);
+        km |= FULL ? (uint32_t)(k[r] >> 32) : (((vm_ >> r) & 1u) ? (uint32_t)(k[r] >> 32) : 0u);
       }
 #pragma unroll
       for (int r = 0; r < R; r++)
@@ -505,9 +507,11 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
     uint32_t mlo = (uint32_t)vm, mhi = (uint32_t)(vm >> 32);
     mlo = __reduce_or_sync(0xffffffffu, mlo);
     mhi = __reduce_or_sync(0xffffffffu, mhi);
+    km = __reduce_or_sync(0xffffffffu, km);
     if (lane == 0) {
       if (mhi | (mlo >> 31)) atomicOr(&a.vinfo[0], 1u);
       if (mlo) atomicOr(&a.vinfo[1], mlo & 0x7FFFFFFFu);
+      if (km) atomicOr(&a.vinfo[2], km);
     }
   }
 }
@@ -523,7 +527,7 @@ struct Cw2Args {
   const uint32_t* plist_n;
   uint32_t plist_cap;
   const unsigned long long* part_recs;
-  const unsigned int* vinfo;    // [0] some value outside int32, [1] OR of the magnitudes (k_scan_wc)
+  const unsigned int* vinfo;    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words (k_scan_wc)
   int32_t P, Q;
   int32_t table_bytes;          // dynamic shared memory for the table
   uint64_t seed;                // slot hash seed of the child level
@@ -644,24 +648,326 @@ __device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) {
   return fmix32((uint32_t)k ^ seed ^ ((uint32_t)(k >> 32) * 0x9E3779B1u));
 }
 
-// Table: skeys[nslots + 1] u64 keys in 32-byte buckets of 4 slots (the last slot
-// is the sentinel key's), then (nslots + 1) x W u32 state words.
-// A record compares its key with the four keys of its bucket, all RL records'
-// buckets in flight together; a record that did not hit looks at the next
-// bucket (a displaced key: warp-uniform second stage) and only then takes the
-// general loop (first occurrence -> CAS insert, longer chains, the sentinel key).
+// One run through a child table.  Template flags: K32 = every key the scan saw
+// fits in 32 bits (keys are stored as u32: a bucket of 4 is one LDS.128 and four
+// 32-bit compares; the one key equal to the empty marker 0xFFFFFFFF lives in the
+// escape slot), WIDE = sums as u32 pairs with carry, EXT = the extended word
+// layout (wide sums and owner runs).
+//   table: keys[nslots + 1] (u32 or u64; 4-slot buckets; escape slot last), then
+//          (nslots + 1) x W u32 state words
+// A record compares its key with the four keys of its bucket, the buckets of RL
+// records in flight together; a record that did not hit looks at the next bucket
+// (a displaced key: warp-uniform second stage) and only then takes the general
+// loop (first occurrence -> CAS insert, longer chains, the escape key).  COUNT,
+// SUM, MIN and MAX are fire-and-forget shared-memory REDs (no read before the
+// update: the kernel is bound by shared-memory latency, not by its atomic rate).
+struct CwShared {
+  int groups, fail, esc;
+  unsigned long long base;
+  uint32_t wsum[32];
+};
+
+template <class CP, int BLK, int RL, bool K32, bool WIDE, bool EXT>
+__device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, unsigned char* smem, CwShared& sh,
+                                          uint32_t seed32) {
+  using CW = CwWords<CP>;
+  using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+  constexpr int N = CP::N;
+  constexpr int NWARP = BLK / 32;
+  constexpr int W = EXT ? CW::W_EXT : CW::W_NARROW;
+  constexpr int KB = K32 ? 4 : 8;
+  constexpr KT KEMPTY = K32 ? (KT)0xFFFFFFFFu : (KT)EMPTY;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nbk = (a.table_bytes / (KB + 4 * W) - 1) / 4;
+  const int nslots = nbk * 4;
+  const int maxg = (int)(0.85 * nslots);
+  const int stride = nslots + 1;
+  KT* skeys = (KT*)smem;                                                     // stride keys (escape slot last)
+  uint32_t* sst = (uint32_t*)(smem + (((size_t)stride * KB + 15) & ~(size_t)15));  // stride x W state words
+  const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst);
+  for (int i = tid; i < stride; i += BLK) {
+    skeys[i] = KEMPTY;
+#pragma unroll
+    for (int w = 0; w < CW::WB; w++) sst[i * W + w] = CW::identity(w);
+    if (EXT) {
+#pragma unroll
+      for (int w = CW::WB; w < CW::W_EXT; w++) sst[i * W + w] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
+    }
+  }
+  if (tid == 0) {
+    sh.groups = 0;
+    sh.fail = a.vinfo[0] != 0 || a.plist_n[p] > a.plist_cap;  // (values beyond int32; an overflowed page list)
+    sh.esc = 0;
+  }
+  __syncthreads();
+  auto bucket_of = [&](uint64_t k) { return (int)__umulhi(cw_hash(k, seed32), (uint32_t)nbk); };
+  // the general probe: hit, insert into the bucket chain's first empty slot, or fail (table full)
+  auto probe_slow = [&](KT k, int b) -> int {
+    for (;;) {
+      const KT* bp = skeys + b * 4;
+      const KT q0 = bp[0], q1 = bp[1], q2 = bp[2], q3 = bp[3];
+      const int hit = q0 == k ? 0 : q1 == k ? 1 : q2 == k ? 2 : q3 == k ? 3 : -1;
+      if (hit >= 0) return b * 4 + hit;
+      const int emp = q0 == KEMPTY ? 0 : q1 == KEMPTY ? 1 : q2 == KEMPTY ? 2 : q3 == KEMPTY ? 3 : -1;
+      if (emp < 0) {  // full bucket: the next one
+        if (++b == nbk) b = 0;
+        continue;
+      }
+      if (atomicAdd(&sh.groups, 1) >= maxg) {
+        sh.fail = 1;
+        return -1;
+      }
+      const int e = b * 4 + emp;
+      KT prev;
+      if constexpr (K32) prev = atomicCAS((unsigned int*)&skeys[e], KEMPTY, k);
+      else prev = atomicCAS((unsigned long long*)&skeys[e], (unsigned long long)KEMPTY, (unsigned long long)k);
+      if (prev == KEMPTY) return e;
+      atomicSub(&sh.groups, 1);  // the slot went to another insert: look at the bucket again
+    }
+  };
+  if (owner) {  // seed: the resident keys this owner answers for, with their level-0 slots
+    const int o = p - a.P;
+    const uint32_t nres = a.olist_n[o];
+    if (nres > a.ocap || (int)nres > maxg) {
+      if (tid == 0) sh.fail = 1;
+    } else {
+      for (uint32_t i = tid; i < nres; i += BLK) {
+        const uint32_t ls = a.olist[(size_t)o * a.ocap + i];
+        const uint64_t k = a.t.keys[ls];
+        int sl;
+        if (K32) {
+          // (a resident key beyond 32 bits came in through FILL; no record of the runs can match it)
+          if (k >> 32) continue;
+          sl = (uint32_t)k == 0xFFFFFFFFu ? nslots : probe_slow((KT)k, bucket_of(k));
+        } else {
+          sl = probe_slow((KT)k, bucket_of(k));
+        }
+        if (sl >= 0) sst[sl * W + CW::W_ORG] = ls;
+      }
+      if (!K32 && tid == 0 && *(volatile int*)&a.t.hdr->esc) sst[nslots * W + CW::W_ORG] = (uint32_t)(a.t.mask + 1);
+    }
+    __syncthreads();
+  }
+  const uint32_t npg = min(a.plist_n[p], a.plist_cap);
+  const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
+  // Warp w takes list entries w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
+  // the page, RL records per lane in flight.
+  for (uint32_t q = wid; q < npg; q += NWARP) {
+    if (__any_sync(0xffffffffu, *(volatile int*)&sh.fail)) break;  // warp-uniform
+    const uint32_t pg = pl[q];
+    if (pg == 0xFFFFFFFFu) continue;  // (an entry a CTA reserved and did not need)
+    const int fill = a.pool.page_fill[pg];
+    const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
+    for (int s0 = 0; s0 < fill; s0 += RL * 32) {
+      ulonglong2 cur[RL];
+#pragma unroll
+      for (int r = 0; r < RL; r++) {
+        const int sl = s0 + r * 32 + lane;
+        cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2((uint64_t)KEMPTY, 0);  // (padding: the escape key, skipped below)
+      }
+      int bk[RL], slot[RL];
+      bool need[RL];
+      if constexpr (K32) {
+        uint32_t q0[RL], q1[RL], q2[RL], q3[RL];
+#pragma unroll
+        for (int r = 0; r < RL; r++) {
+          bk[r] = bucket_of(cur[r].x);
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(q0[r]), "=r"(q1[r]), "=r"(q2[r]), "=r"(q3[r])
+                       : "r"(a_keys + 16u * (uint32_t)bk[r]));
+        }
+#pragma unroll
+        for (int r = 0; r < RL; r++) {
+          const uint32_t k = (uint32_t)cur[r].x;
+          const bool e1 = q1[r] == k, e2 = q2[r] == k, e3 = q3[r] == k;
+          const bool hit = ((q0[r] == k) | e1 | e2 | e3) & (k != KEMPTY);
+          slot[r] = hit ? bk[r] * 4 + (int)e1 + 2 * (int)e2 + 3 * (int)e3 : -1;
+          need[r] = !hit && s0 + r * 32 + lane < fill;
+        }
+      } else {
+#pragma unroll
+        for (int r0 = 0; r0 < RL; r0 += 2) {  // (two 32-byte buckets in flight: registers)
+          uint64_t bx[2][4];
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            bk[r0 + u] = bucket_of(cur[r0 + u].x);
+            lds128(a_keys + 32u * (uint32_t)bk[r0 + u], bx[u][0], bx[u][1]);
+            lds128(a_keys + 32u * (uint32_t)bk[r0 + u] + 16u, bx[u][2], bx[u][3]);
+          }
+#pragma unroll
+          for (int u = 0; u < 2; u++) {
+            const int r = r0 + u;
+            const uint64_t k = cur[r].x;
+            const bool e1 = bx[u][1] == k, e2 = bx[u][2] == k, e3 = bx[u][3] == k;
+            const bool hit = ((bx[u][0] == k) | e1 | e2 | e3) & (k != EMPTY);
+            slot[r] = hit ? bk[r] * 4 + (int)e1 + 2 * (int)e2 + 3 * (int)e3 : -1;
+            need[r] = !hit && s0 + r * 32 + lane < fill;
+          }
+        }
+      }
+      bool any_need = false;
+#pragma unroll
+      for (int r = 0; r < RL; r++) any_need |= need[r];
+      if (__any_sync(0xffffffffu, any_need)) {  // warp-uniform second stage
+#pragma unroll
+        for (int r = 0; r < RL; r++) {
+          if (!need[r]) continue;
+          const KT k = (KT)cur[r].x;
+          if (__builtin_expect(k == KEMPTY, 0)) {
+            slot[r] = nslots;
+            sh.esc = 1;  // (idempotent; read after the barrier)
+          } else {
+            const int b2 = bk[r] + 1 == nbk ? 0 : bk[r] + 1;
+            const KT* bp = skeys + b2 * 4;
+            const KT c0 = bp[0], c1 = bp[1], c2 = bp[2], c3 = bp[3];
+            const bool f0 = c0 == k, f1 = c1 == k, f2 = c2 == k, f3 = c3 == k;
+            if (f0 | f1 | f2 | f3) slot[r] = b2 * 4 + (f0 ? 0 : f1 ? 1 : f2 ? 2 : 3);
+            else slot[r] = probe_slow(k, bk[r]);
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int r = 0; r < RL; r++) {
+        if (slot[r] < 0) continue;
+        const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
+        const uint32_t a_s = a_st + (uint32_t)(4 * W) * (uint32_t)slot[r];
+        reds_add(a_s + 4u * CW::W_CNT, 1u);
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const uint32_t F = CP::fd(j);
+          if (CP::is_count(j)) continue;
+          const uint32_t a_w = a_s + 4u * (uint32_t)CW::word(j);
+          if (CP::is_sum(j)) {
+            if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
+              const uint32_t o = atoms_add(a_w, (uint32_t)cb);
+              const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
+              if (hi) reds_add(a_s + 4u * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
+            } else {
+              reds_add(a_w, (uint32_t)cb);
+            }
+          } else if ((F & 3) == OP_MIN) {
+            reds_min_s32(a_w, cb);
+          } else {
+            reds_max_s32(a_w, cb);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (sh.fail) {
+    if (tid == 0) {
+      a.failed[p] = 1;
+      atomicOr(a.fail, 4u);
+    }
+    __syncthreads();
+    return;
+  }
+  // state word j of slot s as a 64-bit native state
+  auto state_of = [&](int s, int j) -> uint64_t {
+    const uint32_t* w = sst + s * W;
+    if (CP::is_count(j)) return (uint64_t)w[CW::W_CNT];
+    if (CP::is_sum(j)) {
+      const uint32_t lo = w[CW::word(j)];
+      return WIDE ? ((uint64_t)w[CW::W_HI + CW::sum_rank(j)] << 32 | lo) : (uint64_t)(long long)(int)lo;
+    }
+    return (uint64_t)(long long)(int)w[CW::word(j)];
+  };
+  // rows this run emits: its groups, minus the seeded (resident) ones of an owner run
+  auto emits = [&](int s) -> bool {
+    if (EXT && owner && sst[s * W + CW::W_ORG] != 0xFFFFFFFFu) return false;
+    return (s == nslots) ? (sh.esc != 0 && sst[s * W + CW::W_CNT] != 0) : (skeys[s] != KEMPTY);
+  };
+  // block compaction, one output reservation per run
+  const int per = (stride + BLK - 1) / BLK;
+  const int lo = tid * per, hi = min(stride, lo + per);
+  uint32_t mine = 0;
+  for (int s = lo; s < hi; s++) mine += emits(s);
+  uint32_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh.wsum[wid] = x;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int w = 0; w < NWARP; w++) {
+      const uint32_t t2 = sh.wsum[w];
+      sh.wsum[w] = acc;
+      acc += t2;
+    }
+    // reserve the rows only if they fit (else the run goes to the fallback)
+    unsigned long long base = 0;
+    if (acc) {
+      unsigned long long o = *(volatile unsigned long long*)a.out.count;
+      for (;;) {
+        if (o + acc > (unsigned long long)a.out.cap) {
+          base = ~0ull;
+          break;
+        }
+        const unsigned long long prev = atomicCAS(a.out.count, o, o + acc);
+        if (prev == o) {
+          base = o;
+          break;
+        }
+        o = prev;
+      }
+    }
+    sh.base = base;
+  }
+  __syncthreads();
+  if (sh.base == ~0ull) {  // (nothing merged or emitted yet: the fallback redoes the whole run)
+    if (tid == 0) {
+      a.failed[p] = 1;
+      atomicOr(a.fail, 4u);
+    }
+    __syncthreads();
+    return;
+  }
+  if (EXT && owner) {
+    // resident groups: merged into the level-0 table (its flush emits them), and
+    // their records were not spilled after all
+    unsigned long long hits = 0;
+    for (int s = tid; s < stride; s += BLK) {
+      const uint32_t ls = sst[s * W + CW::W_ORG];
+      const uint32_t cnt = sst[s * W + CW::W_CNT];
+      if (ls == 0xFFFFFFFFu || cnt == 0) continue;
+      hits += cnt;
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const uint32_t F = CP::fd(j);
+        gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)ls * a.t.sstride, F & 3, (F >> 2) & 3, state_of(s, j));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+    if (lane == 0 && hits) {
+      atomicAdd(&a.stats[ST_HITS], hits);
+      atomicAdd(&a.stats[ST_SPILLED], (unsigned long long)(-(long long)hits));
+    }
+  }
+  int64_t idx = (int64_t)sh.base + sh.wsum[wid] + (x - mine);
+  for (int s = lo; s < hi; s++) {
+    if (!emits(s)) continue;
+    const uint64_t kk[1] = {s == nslots ? (K32 ? 0xFFFFFFFFull : EMPTY) : (uint64_t)skeys[s]};
+    uint64_t st[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < N; j++)
+      if (j < 4) st[j] = state_of(s, j);
+    emit_group4<1>(a.sp, a.out, idx++, kk, st);
+  }
+  __syncthreads();
+}
+
 template <class CP, int BLK, int RL>
 __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
-  using CW = CwWords<CP>;
-  constexpr int N = CP::N, NSUM = CW::NSUM;
-  constexpr int NWARP = BLK / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  __shared__ int s_groups, s_fail, s_esc;
-  __shared__ unsigned long long s_base;
-  __shared__ uint32_t s_wsum[NWARP];
-  const bool rfit = a.vinfo[0] == 0;  // every value is an int32
+  __shared__ CwShared sh;
   const uint32_t vabs = a.vinfo[1] + 1u;
+  const bool k32 = a.vinfo[2] == 0;  // every key of the runs fits in 32 bits
   const uint32_t seed32 = (uint32_t)a.seed ^ (uint32_t)(a.seed >> 32);
   const int NP = a.P + a.Q;
   for (int p = blockIdx.x; p < NP; p += gridDim.x) {
@@ -669,270 +975,16 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
     if (np == 0) continue;
     const bool owner = p >= a.P;
     // wide sums (a u32 pair with carry) only when a run's sum can leave int32
-    const bool wide = NSUM > 0 && (double)np * (double)vabs >= 2147483647.0;
-    const bool ext = wide || owner;
-    const int W = ext ? CW::W_EXT : CW::W_NARROW;
-    const int nbk = (a.table_bytes / (8 + 4 * W) - 1) / 4;
-    const int nslots = nbk * 4;
-    const int maxg = (int)(0.85 * nslots);
-    const int stride = nslots + 1;
-    uint64_t* skeys = (uint64_t*)smem;           // stride keys (escape slot last)
-    uint32_t* sst = (uint32_t*)(skeys + stride);  // stride x W state words
-    const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst);
-    for (int i = tid; i < stride; i += BLK) {
-      skeys[i] = EMPTY;
-#pragma unroll
-      for (int w = 0; w < CW::WB; w++) sst[i * W + w] = CW::identity(w);
-      if (ext) {
-        for (int w = CW::WB; w < CW::W_EXT; w++) sst[i * W + w] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
-      }
+    const bool wide = CP::nsum() > 0 && (double)np * (double)vabs >= 2147483647.0;
+    if (k32) {
+      if (wide) child_run<CP, BLK, RL, true, true, true>(a, p, owner, smem, sh, seed32);
+      else if (owner) child_run<CP, BLK, RL, true, false, true>(a, p, owner, smem, sh, seed32);
+      else child_run<CP, BLK, RL, true, false, false>(a, p, owner, smem, sh, seed32);
+    } else {
+      if (wide) child_run<CP, BLK, RL, false, true, true>(a, p, owner, smem, sh, seed32);
+      else if (owner) child_run<CP, BLK, RL, false, false, true>(a, p, owner, smem, sh, seed32);
+      else child_run<CP, BLK, RL, false, false, false>(a, p, owner, smem, sh, seed32);
     }
-    if (tid == 0) {
-      s_groups = 0;
-      s_fail = !rfit || a.plist_n[p] > a.plist_cap;  // (a page list that overflowed is incomplete)
-      s_esc = 0;
-    }
-    __syncthreads();
-    // the general probe: hit, insert into the bucket chain's first empty slot, or fail (table full)
-    auto probe_slow = [&](uint64_t k, int b) -> int {
-      for (;;) {
-        const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(skeys + b * 4);
-        const ulonglong2 x = bp[0], y = bp[1];
-        const int hit = x.x == k ? 0 : x.y == k ? 1 : y.x == k ? 2 : y.y == k ? 3 : -1;
-        if (hit >= 0) return b * 4 + hit;
-        const int emp = x.x == EMPTY ? 0 : x.y == EMPTY ? 1 : y.x == EMPTY ? 2 : y.y == EMPTY ? 3 : -1;
-        if (emp < 0) {  // full bucket: the next one
-          if (++b == nbk) b = 0;
-          continue;
-        }
-        if (atomicAdd(&s_groups, 1) >= maxg) {
-          s_fail = 1;
-          return -1;
-        }
-        const int e = b * 4 + emp;
-        const unsigned long long prev = atomicCAS((unsigned long long*)&skeys[e], EMPTY, k);
-        if (prev == EMPTY) return e;
-        atomicSub(&s_groups, 1);  // the slot went to another insert: look at the bucket again
-      }
-    };
-    if (owner) {  // seed: the resident keys this owner answers for, with their level-0 slots
-      const int o = p - a.P;
-      const uint32_t nres = a.olist_n[o];
-      if (nres > a.ocap || (int)nres > maxg) {
-        if (tid == 0) s_fail = 1;
-      } else {
-        for (uint32_t i = tid; i < nres; i += BLK) {
-          const uint32_t ls = a.olist[(size_t)o * a.ocap + i];
-          const uint64_t k = a.t.keys[ls];
-          const int sl = probe_slow(k, (int)__umulhi(cw_hash(k, seed32), (uint32_t)nbk));
-          if (sl >= 0) sst[sl * W + CW::W_ORG] = ls;
-        }
-        if (tid == 0 && *(volatile int*)&a.t.hdr->esc) sst[nslots * W + CW::W_ORG] = (uint32_t)(a.t.mask + 1);
-      }
-      __syncthreads();
-    }
-    const uint32_t npg = min(a.plist_n[p], a.plist_cap);
-    const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
-    auto records = [&](auto wide_t, auto ext_t) {
-      constexpr bool WIDE = decltype(wide_t)::value;
-      constexpr int WS = decltype(ext_t)::value ? CW::W_EXT : CW::W_NARROW;
-      // Warp w takes pages w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
-      // the page, RL records per lane in flight.
-      for (uint32_t q = wid; q < npg; q += NWARP) {
-        if (__any_sync(0xffffffffu, *(volatile int*)&s_fail)) break;  // warp-uniform
-        const uint32_t pg = pl[q];
-        if (pg == 0xFFFFFFFFu) continue;  // (an entry a CTA reserved and did not need)
-        const int fill = a.pool.page_fill[pg];
-        const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
-        for (int s0 = 0; s0 < fill; s0 += RL * 32) {
-          ulonglong2 cur[RL];
-#pragma unroll
-          for (int r = 0; r < RL; r++) {
-            const int sl = s0 + r * 32 + lane;
-            cur[r] = sl < fill ? __ldcs(pb + sl) : make_ulonglong2(EMPTY, 0);  // (padding never hits: guard below)
-          }
-#pragma unroll
-          for (int r0 = 0; r0 < RL; r0 += 2) {
-            // the buckets of two records in flight together
-            int bk[2];
-            uint64_t bx[2][4];
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-              bk[u] = (int)__umulhi(cw_hash(cur[r0 + u].x, seed32), (uint32_t)nbk);
-              lds128(a_keys + 32u * (uint32_t)bk[u], bx[u][0], bx[u][1]);
-              lds128(a_keys + 32u * (uint32_t)bk[u] + 16u, bx[u][2], bx[u][3]);
-            }
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-              const int r = r0 + u;
-              const uint64_t k = cur[r].x;
-              const bool e0 = bx[u][0] == k, e1 = bx[u][1] == k, e2 = bx[u][2] == k, e3 = bx[u][3] == k;
-              // (the sentinel key and page padding would "match" an empty slot)
-              const bool hit = (e0 | e1 | e2 | e3) & (k != EMPTY);
-              int slot = hit ? bk[u] * 4 + (e0 ? 0 : e1 ? 1 : e2 ? 2 : 3) : -1;
-              const bool need = !hit && s0 + r * 32 + lane < fill;
-              if (__any_sync(0xffffffffu, need)) {  // warp-uniform second stage
-                if (need) {
-                  if (__builtin_expect(k == EMPTY, 0)) {
-                    slot = nslots;
-                    s_esc = 1;  // (idempotent; read after the barrier)
-                  } else {
-                    const int b2 = bk[u] + 1 == nbk ? 0 : bk[u] + 1;
-                    uint64_t c0, c1, c2, c3;
-                    lds128(a_keys + 32u * (uint32_t)b2, c0, c1);
-                    lds128(a_keys + 32u * (uint32_t)b2 + 16u, c2, c3);
-                    const bool f0 = c0 == k, f1 = c1 == k, f2 = c2 == k, f3 = c3 == k;
-                    if (f0 | f1 | f2 | f3) slot = b2 * 4 + (f0 ? 0 : f1 ? 1 : f2 ? 2 : 3);
-                    else slot = probe_slow(k, bk[u]);
-                  }
-                }
-                __syncwarp();
-              }
-              if (slot >= 0) {
-                const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
-                const uint32_t a_s = a_st + (uint32_t)(4 * WS) * (uint32_t)slot;
-                reds_add(a_s + 4u * CW::W_CNT, 1u);
-                if constexpr (CW::mm_pair()) {  // read first: most records do not improve an extreme
-                  const uint64_t mm = lds64(a_s);
-                  if (cb < (int)(uint32_t)mm) reds_min_s32(a_s, cb);
-                  if (cb > (int)(uint32_t)(mm >> 32)) reds_max_s32(a_s + 4u, cb);
-                }
-#pragma unroll
-                for (int j = 0; j < N; j++) {
-                  const uint32_t F = CP::fd(j);
-                  if (CP::is_count(j)) continue;
-                  const uint32_t a_w = a_s + 4u * (uint32_t)CW::word(j);
-                  if (CP::is_sum(j)) {
-                    if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
-                      const uint32_t o = atoms_add(a_w, (uint32_t)cb);
-                      const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
-                      if (hi) reds_add(a_s + 4u * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
-                    } else {
-                      reds_add(a_w, (uint32_t)cb);
-                    }
-                  } else if (!CW::mm_pair()) {
-                    if ((F & 3) == OP_MIN) {
-                      if (cb < (int)lds32(a_w)) reds_min_s32(a_w, cb);
-                    } else {
-                      if (cb > (int)lds32(a_w)) reds_max_s32(a_w, cb);
-                    }
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
-    };
-    if (wide) records(std::true_type{}, std::true_type{});
-    else if (ext) records(std::false_type{}, std::true_type{});
-    else records(std::false_type{}, std::false_type{});
-    __syncthreads();
-    if (s_fail) {
-      if (tid == 0) {
-        a.failed[p] = 1;
-        atomicOr(a.fail, 4u);
-      }
-      __syncthreads();
-      continue;
-    }
-    // state word j of slot s as a 64-bit native state
-    auto state_of = [&](int s, int j) -> uint64_t {
-      const uint32_t* w = sst + s * W;
-      if (CP::is_count(j)) return (uint64_t)w[CW::W_CNT];
-      if (CP::is_sum(j)) {
-        const uint32_t lo = w[CW::word(j)];
-        return wide ? ((uint64_t)w[CW::W_HI + CW::sum_rank(j)] << 32 | lo) : (uint64_t)(long long)(int)lo;
-      }
-      return (uint64_t)(long long)(int)w[CW::word(j)];
-    };
-    // rows this run emits: its groups, minus the seeded (resident) ones of an owner run
-    auto emits = [&](int s) -> bool {
-      if (owner && sst[s * W + CW::W_ORG] != 0xFFFFFFFFu) return false;
-      return (s == nslots) ? (s_esc != 0 && sst[s * W + CW::W_CNT] != 0) : (skeys[s] != EMPTY);
-    };
-    // block compaction, one output reservation per run
-    const int per = (stride + BLK - 1) / BLK;
-    const int lo = tid * per, hi = min(stride, lo + per);
-    uint32_t mine = 0;
-    for (int s = lo; s < hi; s++) mine += emits(s);
-    uint32_t x = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    if (lane == 31) s_wsum[wid] = x;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t acc = 0;
-      for (int w = 0; w < NWARP; w++) {
-        const uint32_t t2 = s_wsum[w];
-        s_wsum[w] = acc;
-        acc += t2;
-      }
-      // reserve the rows only if they fit (else the run goes to the fallback)
-      unsigned long long base = 0;
-      if (acc) {
-        unsigned long long o = *(volatile unsigned long long*)a.out.count;
-        for (;;) {
-          if (o + acc > (unsigned long long)a.out.cap) {
-            base = ~0ull;
-            break;
-          }
-          const unsigned long long prev = atomicCAS(a.out.count, o, o + acc);
-          if (prev == o) {
-            base = o;
-            break;
-          }
-          o = prev;
-        }
-      }
-      s_base = base;
-    }
-    __syncthreads();
-    if (s_base == ~0ull) {  // (nothing merged or emitted yet: the fallback redoes the whole run)
-      if (tid == 0) {
-        a.failed[p] = 1;
-        atomicOr(a.fail, 4u);
-      }
-      __syncthreads();
-      continue;
-    }
-    if (owner) {
-      // resident groups: merged into the level-0 table (its flush emits them), and
-      // their records were not spilled after all
-      unsigned long long hits = 0;
-      for (int s = tid; s < stride; s += BLK) {
-        const uint32_t ls = sst[s * W + CW::W_ORG];
-        const uint32_t cnt = sst[s * W + CW::W_CNT];
-        if (ls == 0xFFFFFFFFu || cnt == 0) continue;
-        hits += cnt;
-#pragma unroll
-        for (int j = 0; j < N; j++) {
-          const uint32_t F = CP::fd(j);
-          gupdate(a.t.states + (uint64_t)j * a.t.fstride + (uint64_t)ls * a.t.sstride, F & 3, (F >> 2) & 3,
-                  state_of(s, j));
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
-      if (lane == 0 && hits) {
-        atomicAdd(&a.stats[ST_HITS], hits);
-        atomicAdd(&a.stats[ST_SPILLED], (unsigned long long)(-(long long)hits));
-      }
-    }
-    int64_t idx = (int64_t)s_base + s_wsum[wid] + (x - mine);
-    for (int s = lo; s < hi; s++) {
-      if (!emits(s)) continue;
-      const uint64_t kk[1] = {s == nslots ? EMPTY : skeys[s]};
-      uint64_t st[4] = {0, 0, 0, 0};
-#pragma unroll
-      for (int j = 0; j < N; j++)
-        if (j < 4) st[j] = state_of(s, j);
-      emit_group4<1>(a.sp, a.out, idx++, kk, st);
-    }
-    __syncthreads();
   }
 }
 

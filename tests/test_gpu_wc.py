@@ -149,3 +149,18 @@ def test_wc_keys_that_differ_in_the_high_word_only():
     keys = (rng.integers(0, 4_000, 400_000).astype(np.int64) << 32) | 5
     vals = rng.integers(0, 1000, 400_000).astype(np.int64)
     _run(keys, vals, C2, 400)
+
+
+def test_wc_32bit_keys_and_their_escape_key():
+    """Keys below 2^32 take the children's 32-bit tables; the key equal to their empty
+    marker (0xFFFFFFFF) lives in the escape slot, resident or spilled."""
+    rng = np.random.default_rng(11)
+    pool = np.concatenate([np.array([0xFFFFFFFF, 0xFFFFFFFE, 0, 1, 0x80000000, 0x7FFFFFFF], np.int64),
+                           rng.integers(0, 1 << 32, 6_000)])
+    keys = rng.choice(pool, 400_000)
+    vals = rng.integers(-1000, 1000, 400_000).astype(np.int64)
+    _run(keys, vals, C2, 500)
+    _run(np.concatenate([[0xFFFFFFFF], keys]).astype(np.int64), np.concatenate([[3], vals]), C2, 500)
+    # one key beyond 32 bits, resident through FILL only (the runs stay 32-bit) and then also spilled
+    _run(np.concatenate([[1 << 40], keys]).astype(np.int64), np.concatenate([[3], vals]), C2, 500)
+    _run(np.concatenate([keys, [1 << 40]]).astype(np.int64), np.concatenate([vals, [3]]), C2, 500)
