@@ -1297,7 +1297,7 @@ static const WcShape WC_SHAPES[] = {
     {512, 4, 2, k_scan_wc<512, 4, 2>, Wc2Layout<512, 4, 2>::bytes},
     {512, 2, 4, k_scan_wc<512, 2, 4>, Wc2Layout<512, 2, 4>::bytes},
     {512, 2, 3, k_scan_wc<512, 2, 3>, Wc2Layout<512, 2, 3>::bytes},
-    {1024, 2, 2, k_scan_wc<1024, 2, 2>, Wc2Layout<1024, 2, 2>::bytes},
+    {992, 2, 2, k_scan_wc<992, 2, 2>, Wc2Layout<992, 2, 2>::bytes},
     {768, 2, 2, k_scan_wc<768, 2, 2>, Wc2Layout<768, 2, 2>::bytes},
 };
 const WcShape& wc_shape() {
@@ -1624,7 +1624,7 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   const size_t smem = shp.bytes(NP, h->wc_nblk);
   CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int pe = prof_begin(h, 15);
-  fs<<<grid, shp.blk, smem, h->st>>>(a);
+  fs<<<grid, shp.blk + 32, smem, h->st>>>(a);  // + the producer warp
   prof_end(h, pe);
   CU(cudaGetLastError());
   h->launches++;

@@ -112,8 +112,9 @@ struct Wc2Layout {
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
   static __host__ __device__ size_t ring_bytes(int NP) { return (size_t)NP * RS * 16; }
   static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (3 + NE) * 4 + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t send_bytes() { return (size_t)(BLK / 32) * 32 * 8; }  // per warp: 32 lines to send
   static __host__ __device__ size_t bytes(int NP, uint32_t nblk) {
-    return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + (((size_t)nblk * 4 + 15) & ~(size_t)15);
+    return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + send_bytes() + (((size_t)nblk * 4 + 15) & ~(size_t)15);
   }
 };
 
@@ -139,7 +140,7 @@ constexpr int WC2_PF = 6;  // L2 prefetch distance in tiles (rounds of the grid)
 //       each, and moves the run's window to its open line.
 //   barrier 2 (ring and stage free again; thread 0 issues the stage's next tile)
 template <int BLK, int R, int NS>
-__global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
+__global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
   using L = Wc2Layout<BLK, R, NS>;
   constexpr int T = L::T, RING = L::RING, NE = L::NE, LINES = L::LINES, RS = L::RS;
   constexpr int SLOG = 9, S = 1 << SLOG;  // 16-byte records per 8 KB page
@@ -154,33 +155,41 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
   uint32_t* ent = cw + NP;
   uint32_t* lbase = ent + NP * NE;  // this CTA's block of the run's page list ...
   uint32_t* lused = lbase + NP;     // ... and the entries of it in use
-  uint32_t* sbloom = (uint32_t*)((unsigned char*)cw + L::meta_bytes(NP));
+  uint2* sendq = (uint2*)((unsigned char*)cw + L::meta_bytes(NP));  // per warp: (ring address, page << 6 | line) of the lines to send
+  uint32_t* sbloom = (uint32_t*)((unsigned char*)sendq + L::send_bytes());
   const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw), a_bloom = smem_u32(sbloom);
-  __shared__ __align__(8) uint64_t mbar[NS];
+  __shared__ __align__(8) uint64_t mbar[NS];    // stage full (the tile's bytes have landed)
+  __shared__ __align__(8) uint64_t mbar_e[NS];  // stage empty (every consumer is past barrier 2 of its tile)
   __shared__ int s_tcnt[NS];
-  __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv;
+  __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv, s_want, s_pdone;
 
   const int64_t n = a.n;
   const int64_t col_start = a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
   const int64_t col_tiles = (n - col_start + T - 1) / T;
   const int64_t nlin = a.lcount ? (int64_t)*a.lcount : 0;
   const unsigned long long total = (unsigned long long)(col_tiles + (nlin + T - 1) / T);
+  // tiles of this CTA (round-robin), plus one empty tile that lets parked records into the ring
+  const int ntiles = total > blockIdx.x ? (int)((total - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
 
   // page-list entries are reserved per run in blocks, up front: opening a page then
   // needs no returning global atomic (a ~1 us round trip that every other warp of
   // the tile waited for at barrier 1, about four times per tile)
   // (entries left unused stay 0xFFFFFFFF; a run that needs more than its block takes
   // single entries with the atomic)
-  for (int p = tid; p < NP; p += BLK) {
+  constexpr int NT = BLK + 32;  // all threads (set-up only)
+  for (int p = tid; p < NP; p += NT) {
     cw[p] = 0;
     lbase[p] = atomicAdd(&a.plist_n[p], a.plist_blk);
     lused[p] = 0;
   }
-  for (int i = tid; i < NP * NE; i += BLK) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
-  for (uint32_t i = tid; i < nblk; i += BLK) sbloom[i] = __ldcg(a.bloom + i);
+  for (int i = tid; i < NP * NE; i += NT) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
+  for (uint32_t i = tid; i < nblk; i += NT) sbloom[i] = __ldcg(a.bloom + i);
   if (tid == 0) {
-    s_sb = s_su = s_sc = s_nb = s_nv = 0;
-    for (int s = 0; s < NS; s++) mbar_init(&mbar[s], 1);
+    s_sb = s_su = s_sc = s_nb = s_nv = s_want = s_pdone = 0;
+    for (int s = 0; s < NS; s++) {
+      mbar_init(&mbar[s], 1);
+      mbar_init(&mbar_e[s], 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -232,8 +241,37 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
       }
     }
   };
-  if (tid == 0)
-    for (int s = 0; s < NS; s++) issue(s);
+  // The producer is a warp of its own (thread BLK).  As thread 0 of the consumers
+  // it issued a stage's next tile between barrier 2 and its own phase A, started
+  // every tile ~1,000 cycles late and made the other 15 warps wait at barrier 1
+  // (measured: 1,330 cycles of arrival skew per tile).  It also fetches the page
+  // stash refills (a returning global atomic) off the consumers' path.
+  if (tid >= BLK) {
+    if (tid == BLK) {
+      for (int it = 0; it < ntiles + 1; it++) {
+        const int s = it % NS;
+        if (it >= NS) mbar_wait(&mbar_e[s], (uint32_t)((it / NS - 1) & 1));
+        issue(s);
+        if (a.stash && *(volatile uint32_t*)&s_want && !*(volatile uint32_t*)&s_nv) {
+          const uint32_t nb = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
+          *(volatile uint32_t*)&s_nb = nb;
+          __threadfence_block();
+          *(volatile uint32_t*)&s_nv = 1;
+          *(volatile uint32_t*)&s_want = 0;
+        }
+      }
+      if (n_rec) {
+        atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
+        // every routed record counts as spilled until an owner child finds its key resident
+        atomicAdd(&a.stats[ST_SPILLED], n_rec);
+        atomicAdd(&a.stats[ST_RECORDS], n_rec);
+      }
+      __threadfence_block();
+      *(volatile uint32_t*)&s_pdone = 1;
+    }
+    return;
+  }
+  auto bar_consumers = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(BLK) : "memory"); };
 
   uint64_t* const pool = (uint64_t*)a.pool.base;
   auto page_of = [&](int p, uint32_t j) -> uint32_t {
@@ -284,29 +322,17 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
   for (int r = 0; r < R; r++) hk[r] = hv[r] = 0;
   uint64_t vm = 0;  // OR of v ^ (v >> 63): bounds the magnitudes (compact children)
   uint32_t km = 0;  // OR of the keys' high words (32-bit child tables when zero)
-  uint32_t nb_pending = 0;
-  bool nb_busy = false;
 
   // stage index of record r of this thread: pairs (2i, 2i + 1), i = (r / 2) * BLK + tid
   auto rec_idx = [&](int r) { return 2 * ((r >> 1) * BLK + tid) + (r & 1); };
   auto in_window = [&](uint32_t o) { return ((((o & CWM) >> 3) - (o >> 23)) & 511u) < (uint32_t)LINES; };
 
-#ifdef WC2_TIMING
-  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0 = clock64();
-  unsigned nheld = 0;
-#define WC2_T(i) { const long long t1 = clock64(); tm[i] += t1 - t0; t0 = t1; }
-#else
-#define WC2_T(i)
-#endif
-  for (int it = 0;; it++) {
+  for (int it = 0; it < ntiles + 1; it++) {
     const int s = it % NS;
     mbar_wait(&mbar[s], (uint32_t)((it / NS) & 1));
-    WC2_T(0)
     const int c = s_tcnt[s];
-    if (tid == 0 && a.stash && !nb_busy && !s_nv && 2 * s_su >= s_sc) {  // next stash, taken after barrier 1
-      nb_pending = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
-      nb_busy = true;
-    }
+    if (tid == 0 && a.stash && !*(volatile uint32_t*)&s_nv && !*(volatile uint32_t*)&s_want && 2 * s_su >= s_sc)
+      *(volatile uint32_t*)&s_want = 1;  // the producer fetches the next stash
     // ---- [A1] parked open-line records of the last tile into the ring
     if (__builtin_expect(opark != 0, 0)) {
 #pragma unroll
@@ -359,25 +385,17 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
     };
     if (c == T) route(std::true_type{});
     else route(std::false_type{});
-    const bool more = c != 0;
-    WC2_T(1)
-    fence_proxy_async_smem();  // ring writes before the bulk copies that read them
-    __syncthreads();           // ---- barrier 1
-    WC2_T(2)
+    bar_consumers();  // ---- barrier 1
     if (tid == 0) {
-      if (nb_busy) {
-        s_nb = nb_pending;
-        s_nv = 1;
-        nb_busy = false;
-      }
-      if (s_nv && s_su >= s_sc) {
-        const bool fits = s_nb + (uint32_t)a.stash <= a.pool.capacity;
+      if (*(volatile uint32_t*)&s_nv && s_su >= s_sc) {
+        const uint32_t nb = *(volatile uint32_t*)&s_nb;
+        const bool fits = nb + (uint32_t)a.stash <= a.pool.capacity;
         if (!fits)
-          for (uint32_t x = s_nb; x < min(s_nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
-        s_sb = s_nb;
+          for (uint32_t x = nb; x < min(nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
+        s_sb = nb;
         s_sc = fits ? (uint32_t)a.stash : 0u;
         s_su = 0;
-        s_nv = 0;
+        *(volatile uint32_t*)&s_nv = 0;
       }
     }
     // ---- [B1] held records: complete lines straight to their page, the open line waits
@@ -398,10 +416,6 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
         }
       }
     }
-    WC2_T(6)
-#ifdef WC2_TIMING
-    nheld += __popc(held);
-#endif
     // ---- [B2] one lane per run (run p belongs to warp p % NW): the lines of the
     // run's window that this tile completed leave through the warp, four lines
     // per step (8 lanes x 16 bytes = one 128-byte line per store group), and the
@@ -423,59 +437,36 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
           if (nl) cw[p] = (ln << 23) | cc;
         }
         const uint32_t ns = nl < (uint32_t)LINES ? nl : (uint32_t)LINES;
+        uint2* wq = sendq + 32 * wid;
 #pragma unroll
         for (int round = 0; round < LINES; round++) {
           const bool has = ns > (uint32_t)round;
-          uint32_t mask = __ballot_sync(0xffffffffu, has);
+          const uint32_t mask = __ballot_sync(0xffffffffu, has);
           if (!mask) break;
-          const uint32_t x0 = (ln - nl + (uint32_t)round) << 3;
-          uint32_t src = 0;
-          unsigned long long dst = 0;
-          if (has) {
+          if (has) {  // the lane's line into the warp's list
+            const uint32_t x0 = (ln - nl + (uint32_t)round) << 3;
             const uint32_t pg = page_of(p, x0 >> SLOG);
-            src = a_ring + 16u * ((uint32_t)p * RS + (x0 & (RING - 1)));
-            dst = pg < 0xFFFFFFu ? (unsigned long long)rec_ptr(pg, x0) : 0ull;
+            wq[__popc(mask & ((1u << lane) - 1u))] =
+                make_uint2(a_ring + 16u * ((uint32_t)p * RS + (x0 & (RING - 1))), (pg << 6) | ((x0 >> 3) & 63u));
           }
-          while (mask) {
-            // lane group g copies the line of the g-th lowest lane in mask
-            uint32_t m = mask;
-            if (grp >= 1) m &= m - 1;
-            if (grp >= 2) m &= m - 1;
-            if (grp >= 3) m &= m - 1;
-            const int l = m ? __ffs(m) - 1 : 0;
-            const uint32_t s1 = __shfl_sync(0xffffffffu, src, l);
-            const unsigned long long d1 = __shfl_sync(0xffffffffu, dst, l);
-            if (m && d1) {
+          __syncwarp();
+          const int n = __popc(mask);
+          for (int i = grp; i < n; i += 4) {  // lane group g copies lines g, g + 4, ...
+            const uint2 e = wq[i];
+            if ((e.y >> 6) < 0xFFFFFFu && !(a.pf & 2)) {
               uint64_t x, y;
-              lds128(s1 + 16u * (uint32_t)sub, x, y);
-              st_v2((void*)(d1 + 16ull * (unsigned long long)sub), make_ulonglong2(x, y));
+              lds128(e.x + 16u * (uint32_t)sub, x, y);
+              st_v2(pool + ((size_t)(e.y >> 6) << (SLOG + 1)) + ((size_t)(e.y & 63u) << 4) + 2u * (uint32_t)sub,
+                    make_ulonglong2(x, y));
             }
-            mask &= mask - 1;
-            mask &= mask - 1;
-            mask &= mask - 1;
-            mask &= mask - 1;
           }
+          __syncwarp();
         }
       }
     }
-    const bool sent = false;
-    WC2_T(3)
-    if (sent) bulk_wait_read0();  // the ring slots are read before barrier 2
-    WC2_T(4)
-    // ---- barrier 2: ring and stage are free again
-    if (!more) {
-      if (!__syncthreads_or(opark != 0)) break;
-    } else {
-      __syncthreads();
-    }
-    WC2_T(5)
-    if (tid == 0) issue(s);  // the tile NS ahead goes into stage s (an empty tile past the last)
+    bar_consumers();  // ---- barrier 2: ring and stage are free again
+    if (tid == 0) mbar_arrive(&mbar_e[s]);
   }
-#ifdef WC2_TIMING
-  if (blockIdx.x == 3 && lane == 0)
-    printf("warp %2d: mbar %lld A %lld bar1 %lld B1 %lld B2 %lld rdwait %lld bar2 %lld held(lane0) %u\n", tid >> 5, tm[0], tm[1], tm[2], tm[6], tm[3], tm[4], tm[5], nheld);
-#endif
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // this thread's bulk copies are complete
   // ---- close: every run's open line (all in the ring), then the page fills
   for (int p = tid; p < NP; p += BLK) {
     const uint32_t cc = cw[p] & CWM;
@@ -489,18 +480,13 @@ __global__ void __launch_bounds__(BLK, 1) k_scan_wc(Wc2Args a) {
     atomicAdd(&a.part_recs[p], (unsigned long long)cc);
   }
   if (tid == 0) {
-    // unused stash pages leave the set
+    // unused stash pages leave the set (the producer is done: no refill in flight)
+    while (!*(volatile uint32_t*)&s_pdone) {
+    }
     for (uint32_t x = min(s_su, s_sc); x < s_sc; x++) a.pool.page_set[s_sb + x] = -1;
-    if (s_nv)
-      for (uint32_t x = s_nb; x < min(s_nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
-    if (nb_busy)
-      for (uint32_t x = nb_pending; x < min(nb_pending + (uint32_t)a.stash, a.pool.capacity); x++)
-        a.pool.page_set[x] = -1;
-    if (n_rec) {
-      atomicExch(&a.t.hdr->frozen, 1);  // the resident set is final from now on
-      // every routed record counts as spilled until an owner child finds its key resident
-      atomicAdd(&a.stats[ST_SPILLED], n_rec);
-      atomicAdd(&a.stats[ST_RECORDS], n_rec);
+    if (*(volatile uint32_t*)&s_nv) {
+      const uint32_t nb = *(volatile uint32_t*)&s_nb;
+      for (uint32_t x = nb; x < min(nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
     }
   }
   {
@@ -663,6 +649,7 @@ __device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) {
 // update: the kernel is bound by shared-memory latency, not by its atomic rate).
 struct CwShared {
   int groups, fail, esc;
+  unsigned int next;  // next page-list entry to hand out
   unsigned long long base;
   uint32_t wsum[32];
 };
@@ -685,19 +672,21 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
   KT* skeys = (KT*)smem;                                                     // stride keys (escape slot last)
   uint32_t* sst = (uint32_t*)(smem + (((size_t)stride * KB + 15) & ~(size_t)15));  // stride x W state words
   const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst);
+  const uint32_t sbytes = 4u * (uint32_t)stride;  // bytes between a slot's consecutive words
   for (int i = tid; i < stride; i += BLK) {
     skeys[i] = KEMPTY;
 #pragma unroll
-    for (int w = 0; w < CW::WB; w++) sst[i * W + w] = CW::identity(w);
+    for (int w = 0; w < CW::WB; w++) sst[w * stride + i] = CW::identity(w);
     if (EXT) {
 #pragma unroll
-      for (int w = CW::WB; w < CW::W_EXT; w++) sst[i * W + w] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
+      for (int w = CW::WB; w < CW::W_EXT; w++) sst[w * stride + i] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
     }
   }
   if (tid == 0) {
     sh.groups = 0;
     sh.fail = a.vinfo[0] != 0 || a.plist_n[p] > a.plist_cap;  // (values beyond int32; an overflowed page list)
     sh.esc = 0;
+    sh.next = 0;
   }
   __syncthreads();
   auto bucket_of = [&](uint64_t k) { return (int)__umulhi(cw_hash(k, seed32), (uint32_t)nbk); };
@@ -742,22 +731,42 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
         } else {
           sl = probe_slow((KT)k, bucket_of(k));
         }
-        if (sl >= 0) sst[sl * W + CW::W_ORG] = ls;
+        if (sl >= 0) sst[CW::W_ORG * stride + sl] = ls;
       }
-      if (!K32 && tid == 0 && *(volatile int*)&a.t.hdr->esc) sst[nslots * W + CW::W_ORG] = (uint32_t)(a.t.mask + 1);
+      if (!K32 && tid == 0 && *(volatile int*)&a.t.hdr->esc) sst[CW::W_ORG * stride + nslots] = (uint32_t)(a.t.mask + 1);
     }
     __syncthreads();
   }
   const uint32_t npg = min(a.plist_n[p], a.plist_cap);
   const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
-  // Warp w takes list entries w, w + NWARP, ...; lane l takes slots l, l + 32, ... of
-  // the page, RL records per lane in flight.
-  for (uint32_t q = wid; q < npg; q += NWARP) {
-    if (__any_sync(0xffffffffu, *(volatile int*)&sh.fail)) break;  // warp-uniform
-    const uint32_t pg = pl[q];
-    if (pg == 0xFFFFFFFFu) continue;  // (an entry a CTA reserved and did not need)
-    const int fill = a.pool.page_fill[pg];
-    const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
+  // Warps take the list's entries as they come free (pages differ in fill, and a
+  // static split left the warps ~10% apart at the end of a run); the first lanes look at
+  // one entry each of a small batch, the used ones are processed in turn with the next
+  // one's page already on its way into L2.  Lane l takes slots l, l + 32, ... of a
+  // page, RL records per lane in flight.
+  for (;;) {
+    uint32_t q0 = 0;
+    constexpr uint32_t NB = 8;  // entries per batch (about four pages: the warps end a run within a few pages of each other)
+    if (lane == 0) q0 = atomicAdd(&sh.next, NB);
+    q0 = __shfl_sync(0xffffffffu, q0, 0);
+    if (q0 >= npg || __any_sync(0xffffffffu, *(volatile int*)&sh.fail)) break;  // warp-uniform
+    const uint32_t mypg = ((uint32_t)lane < NB && q0 + lane < npg) ? pl[q0 + lane] : 0xFFFFFFFFu;
+    const int myfill = mypg != 0xFFFFFFFFu ? a.pool.page_fill[mypg] : 0;
+    uint32_t used = __ballot_sync(0xffffffffu, myfill > 0);
+    if (used) {  // the first page of the batch
+      const int l0 = __ffs(used) - 1;
+      if (lane == l0) bulk_prefetch_l2(page_ptr(a.pool, mypg), ((uint32_t)myfill * 16u + 15u) & ~15u);
+    }
+    while (used) {
+      const int l = __ffs(used) - 1;
+      used &= used - 1;
+      if (used) {  // the next page into L2 while this one is processed
+        const int ln = __ffs(used) - 1;
+        if (lane == ln) bulk_prefetch_l2(page_ptr(a.pool, mypg), ((uint32_t)myfill * 16u + 15u) & ~15u);
+      }
+      const uint32_t pg = __shfl_sync(0xffffffffu, mypg, l);
+      const int fill = __shfl_sync(0xffffffffu, myfill, l);
+      const ulonglong2* pb = (const ulonglong2*)page_ptr(a.pool, pg);
     for (int s0 = 0; s0 < fill; s0 += RL * 32) {
       ulonglong2 cur[RL];
 #pragma unroll
@@ -831,18 +840,20 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
       for (int r = 0; r < RL; r++) {
         if (slot[r] < 0) continue;
         const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
-        const uint32_t a_s = a_st + (uint32_t)(4 * W) * (uint32_t)slot[r];
-        reds_add(a_s + 4u * CW::W_CNT, 1u);
+        // (word arrays, not slot-major: a warp's updates of one field spread over all 32
+        // banks; slot-major states put them on 8 and tripled the atomics' wavefronts)
+        const uint32_t a_s = a_st + 4u * (uint32_t)slot[r];
+        reds_add(a_s + sbytes * CW::W_CNT, 1u);
 #pragma unroll
         for (int j = 0; j < N; j++) {
           const uint32_t F = CP::fd(j);
           if (CP::is_count(j)) continue;
-          const uint32_t a_w = a_s + 4u * (uint32_t)CW::word(j);
+          const uint32_t a_w = a_s + sbytes * (uint32_t)CW::word(j);
           if (CP::is_sum(j)) {
             if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
               const uint32_t o = atoms_add(a_w, (uint32_t)cb);
               const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
-              if (hi) reds_add(a_s + 4u * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
+              if (hi) reds_add(a_s + sbytes * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
             } else {
               reds_add(a_w, (uint32_t)cb);
             }
@@ -853,6 +864,7 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
           }
         }
       }
+    }
     }
   }
   __syncthreads();
@@ -866,18 +878,18 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
   }
   // state word j of slot s as a 64-bit native state
   auto state_of = [&](int s, int j) -> uint64_t {
-    const uint32_t* w = sst + s * W;
-    if (CP::is_count(j)) return (uint64_t)w[CW::W_CNT];
+    const uint32_t* w = sst + s;
+    if (CP::is_count(j)) return (uint64_t)w[CW::W_CNT * stride];
     if (CP::is_sum(j)) {
-      const uint32_t lo = w[CW::word(j)];
-      return WIDE ? ((uint64_t)w[CW::W_HI + CW::sum_rank(j)] << 32 | lo) : (uint64_t)(long long)(int)lo;
+      const uint32_t lo = w[CW::word(j) * stride];
+      return WIDE ? ((uint64_t)w[(CW::W_HI + CW::sum_rank(j)) * stride] << 32 | lo) : (uint64_t)(long long)(int)lo;
     }
-    return (uint64_t)(long long)(int)w[CW::word(j)];
+    return (uint64_t)(long long)(int)w[CW::word(j) * stride];
   };
   // rows this run emits: its groups, minus the seeded (resident) ones of an owner run
   auto emits = [&](int s) -> bool {
-    if (EXT && owner && sst[s * W + CW::W_ORG] != 0xFFFFFFFFu) return false;
-    return (s == nslots) ? (sh.esc != 0 && sst[s * W + CW::W_CNT] != 0) : (skeys[s] != KEMPTY);
+    if (EXT && owner && sst[CW::W_ORG * stride + s] != 0xFFFFFFFFu) return false;
+    return (s == nslots) ? (sh.esc != 0 && sst[CW::W_CNT * stride + s] != 0) : (skeys[s] != KEMPTY);
   };
   // block compaction, one output reservation per run
   const int per = (stride + BLK - 1) / BLK;
@@ -932,8 +944,8 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
     // their records were not spilled after all
     unsigned long long hits = 0;
     for (int s = tid; s < stride; s += BLK) {
-      const uint32_t ls = sst[s * W + CW::W_ORG];
-      const uint32_t cnt = sst[s * W + CW::W_CNT];
+      const uint32_t ls = sst[CW::W_ORG * stride + s];
+      const uint32_t cnt = sst[CW::W_CNT * stride + s];
       if (ls == 0xFFFFFFFFu || cnt == 0) continue;
       hits += cnt;
 #pragma unroll
