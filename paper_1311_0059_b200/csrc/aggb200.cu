@@ -645,16 +645,14 @@ struct Handle {
   // page lists (no host round trip), a partition they cannot hold goes to drain
   bool wc = false;
   bool wc_used = false;       // some PROBE of this run went through k_probe_wc
-  uint32_t wc_nblk = 0;       // bloom blocks (64-bit)
   int wc_table_bytes = 0;     // child shared-memory table
   uint32_t wc_plist_cap = 0;  // page-list entries per partition
   int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
-  int wcQ = 0;                // owner runs (the spill partitions are P0; runs = P0 + wcQ)
   uint32_t wc_ocap = 0;       // resident slots per owner list
   int64_t wc_launches = 0;    // k_scan_wc launches of this run
   int64_t wc_entries = 0;     // page-list entries per run the launches so far may have taken
   bool wc_plist_clean = false;  // every entry of the page lists is 0xFFFFFFFF (unused) or belongs to this run
-  DBuf wc_bloom, wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_olist, wc_olist_n, wc_gather;
+  DBuf wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_olist, wc_olist_n, wc_gather;
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
   DBuf sort_keys, sort_vals;
@@ -1276,29 +1274,26 @@ int plan(Handle* h) {
 
 // The write-combined level-0 path (wc2.cuh) for budgeted pre-partitioning of
 // one-word keys and one int64 value column with an integer COUNT/SUM/MIN/MAX
-// spec.  Level 0 routes every record into a run: P0 spill partitions (filter
-// negatives) and wcQ owner runs (filter positives: resident keys and false
-// positives).  Every run is aggregated by one child CTA with a compact table
-// (u32 states) in shared memory, in whole waves: the number of runs is the
-// smallest multiple of the SM count that leaves every child table at most ~45%
-// full, and it must leave the scan room for its filter (>= 2 bits per resident
-// key) beside the runs' write-combining rings.  The owner share follows the
-// expected records: resident groups plus the filter's false-positive share of
-// the others.
+// spec.  After the table froze, level 0 routes every record into the run of its
+// hash range; every run is aggregated by one child CTA with a compact table
+// (u32 states) in shared memory, seeded with the resident keys of its range, in
+// whole waves: the number of runs is the smallest multiple of the SM count that
+// leaves every child table at most half full, and the runs' write-combining
+// rings must fit the scan's shared memory beside its input stages.
 constexpr int WC_CBLK = 1024, WC_CRL = 4;
 // scan shapes (records per thread and tile x input stages): the tile bounds what one
 // run receives between two window moves (a run's window holds 9-16 records)
 struct WcShape {
   int blk, R, NS;
   void (*fn)(Wc2Args);
-  size_t (*bytes)(int, uint32_t);
+  size_t (*bytes)(int);
 };
 static const WcShape WC_SHAPES[] = {
+    {512, 4, 3, k_scan_wc<512, 4, 3>, Wc2Layout<512, 4, 3>::bytes},
     {512, 4, 2, k_scan_wc<512, 4, 2>, Wc2Layout<512, 4, 2>::bytes},
     {512, 2, 4, k_scan_wc<512, 2, 4>, Wc2Layout<512, 2, 4>::bytes},
-    {512, 2, 3, k_scan_wc<512, 2, 3>, Wc2Layout<512, 2, 3>::bytes},
-    {992, 2, 2, k_scan_wc<992, 2, 2>, Wc2Layout<992, 2, 2>::bytes},
-    {768, 2, 2, k_scan_wc<768, 2, 2>, Wc2Layout<768, 2, 2>::bytes},
+    {992, 2, 3, k_scan_wc<992, 2, 3>, Wc2Layout<992, 2, 3>::bytes},
+    {768, 2, 4, k_scan_wc<768, 2, 4>, Wc2Layout<768, 2, 4>::bytes},
 };
 const WcShape& wc_shape() {
   const int i = getenv("AGGB_WC_SHAPE") ? atoi(getenv("AGGB_WC_SHAPE")) : 0;
@@ -1306,43 +1301,24 @@ const WcShape& wc_shape() {
 }
 void wc_plan(Handle* h, double spill_groups) {
   h->wc = false;
-  h->wcQ = 0;
   const aggb_config& c = h->cfg;
   if (c.algo != AGGB_PRE_PARTITIONING || h->kw != 1 || h->cs.nv != 1 || (h->prog != 1 && h->prog != 2) ||
       h->unlimited || h->l2_capped || c.level != 0 || h->cs.ds.vty[0] != TY_I64 || getenv("AGGB_NO_WC") ||
       getenv("AGGB_FORCE_L2_CHILDREN"))
     return;
-  // slots of a child table: 8-byte key + the narrow state words (spill partitions);
-  // owner runs carry two more words and their share is sized with them below
-  const int wn = h->prog == 2 ? CwWords<CpC2>::W_NARROW : CwWords<CpC1>::W_NARROW;
+  // slots of a child table: 8-byte key + the extended state words (the level-0 slot of a seeded key)
   const int we = h->prog == 2 ? CwWords<CpC2>::W_EXT : CwWords<CpC1>::W_EXT;
   const int tbytes = 220 * 1024;
-  const int nslots = (tbytes / (8 + 4 * wn) - 1) / 4 * 4;
+  const int nslots = (tbytes / (8 + 4 * we) - 1) / 4 * 4;
   const int sms = std::max(1, h->sms);
-  const double resident = (double)std::max<int64_t>(1, h->budget);
-  const double spill = std::max(1.0, spill_groups);
-  int I = (int)std::ceil((spill + resident) / (0.45 * nslots));
-  I = std::max(2, (I + sms - 1) / sms * sms);
-  if (getenv("AGGB_WC_RUNS")) I = std::max(2, atoi(getenv("AGGB_WC_RUNS")));  // experiment override
-  const size_t fixed = wc_shape().bytes(I, 0) + 1024;
-  if (fixed >= 227 * 1024) return;
-  const int64_t want = std::max<int64_t>(64, (int64_t)(8 * h->budget) / 32);  // ~8 bits per resident key
-  const int64_t room = (int64_t)((227 * 1024 - fixed) / 4);
-  const int64_t nblk = std::min(want, room);
-  if (nblk < std::max<int64_t>(16, (int64_t)(2 * h->budget) / 32)) return;
-  // false-positive share of a 3-bit filter in 32-bit blocks (the block loads vary: +15%)
-  const double bpk = 32.0 * (double)nblk / resident;
-  const double fp = std::min(1.0, 1.15 * std::pow(1.0 - std::exp(-3.0 / bpk), 3.0));
-  // (an owner run's slots are wider: it takes proportionally fewer groups)
-  const double share = (resident + fp * spill) / (resident + spill) * (8.0 + 4 * we) / (8.0 + 4 * wn);
-  int Q = (int)std::lround(I * std::min(0.9, share));
-  Q = std::max(1, std::min(I - 1, Q));
-  if (getenv("AGGB_WC_OWNERS")) Q = std::max(1, std::min(I - 1, atoi(getenv("AGGB_WC_OWNERS"))));  // experiment override
+  const double groups = (double)std::max<int64_t>(1, h->budget) + std::max(1.0, spill_groups);
+  int I = (int)std::ceil(groups / (0.5 * nslots));
+  I = std::max(1, (I + sms - 1) / sms * sms);
+  if (getenv("AGGB_WC_RUNS")) I = std::max(1, atoi(getenv("AGGB_WC_RUNS")));  // experiment override
+  if (wc_shape().bytes(I) + 1024 >= 227 * 1024) return;
   h->wc = true;
-  h->wc_nblk = (uint32_t)nblk;
   h->wc_table_bytes = tbytes;
-  h->wcQ = Q;
-  h->P0 = I - Q;
+  h->P0 = I;
   h->nsub0 = 1;
   h->fanout_need = h->P0;
   h->l2_children = false;
@@ -1439,13 +1415,12 @@ int begin_run(Handle* h) {
   h->wc_entries = 0;
   h->wc_plist_clean = false;
   if (h->wc) {
-    const size_t NP = (size_t)h->P0 + (size_t)h->wcQ;
+    const size_t NP = (size_t)h->P0;
     TRY(h->wc_pn.ensure(NP * 4, &h->hw));
     TRY(h->wc_recs.ensure(NP * 8, &h->hw));
     TRY(h->wc_failed.ensure(NP * 4, &h->hw));
     TRY(h->wc_vinfo.ensure(16, &h->hw));
     TRY(h->wc_fail.ensure(8, &h->hw));
-    TRY(h->wc_bloom.ensure((size_t)h->wc_nblk * 4, &h->hw));
     CU(cudaMemsetAsync(h->wc_pn.p, 0, NP * 4, h->st));
     CU(cudaMemsetAsync(h->wc_recs.p, 0, NP * 8, h->st));
     CU(cudaMemsetAsync(h->wc_failed.p, 0, NP * 4, h->st));
@@ -1522,26 +1497,21 @@ bool wc_eligible(Handle* h, const ColSrc& col) {
          col.n + h->defer_cap <= (int64_t)1200000000 &&
          ((uintptr_t)col.key[0] & 15) == 0 && ((uintptr_t)col.val[0] & 15) == 0 && !h->hot_ready &&
          h->pool_bound + (uint64_t)(col.n + h->defer_cap) / 256 +
-                 (uint64_t)h->sms * (4ull * (h->P0 + h->wcQ) + 128) < 0xFFFFF0ull;
+                 (uint64_t)h->sms * (4ull * h->P0 + 128) < 0xFFFFF0ull;
 }
 
-// the filter of the frozen table (bloom) and / or the owners' lists of resident slots
-int wc_build(Handle* h, bool bloom, bool owners) {
+// the runs' lists of resident slots (the frozen table's keys by routing hash)
+int wc_build(Handle* h) {
   const uint64_t seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
-  if (bloom) CU(cudaMemsetAsync(h->wc_bloom.p, 0, (size_t)h->wc_nblk * 4, h->st));
-  if (owners) {
-    // a list holds twice an owner's share of the budget (small budgets: all of it)
-    const uint64_t cap = h->tab.cap;
-    h->wc_ocap = (uint32_t)std::min<uint64_t>(cap + 1, 2 * cap / (uint64_t)h->wcQ + 1024);
-    TRY(h->wc_olist.ensure((size_t)h->wcQ * h->wc_ocap * 4, &h->hw));
-    TRY(h->wc_olist_n.ensure((size_t)h->wcQ * 4, &h->hw));
-    CU(cudaMemsetAsync(h->wc_olist_n.p, 0, (size_t)h->wcQ * 4, h->st));
-  }
+  // a list holds twice a run's share of the budget (small budgets: all of it)
+  const uint64_t cap = h->tab.cap;
+  h->wc_ocap = (uint32_t)std::min<uint64_t>(cap + 1, 2 * cap / (uint64_t)h->P0 + 1024);
+  TRY(h->wc_olist.ensure((size_t)h->P0 * h->wc_ocap * 4, &h->hw));
+  TRY(h->wc_olist_n.ensure((size_t)h->P0 * 4, &h->hw));
+  CU(cudaMemsetAsync(h->wc_olist_n.p, 0, (size_t)h->P0 * 4, h->st));
   int pe = prof_begin(h, 16);
-  k_wc2_build<<<h->sms * 4, 256, 0, h->st>>>(h->tab, seed, bloom ? h->wc_bloom.as<uint32_t>() : nullptr, h->wc_nblk,
-                                             owners ? h->wc_olist.as<uint32_t>() : nullptr,
-                                             owners ? h->wc_olist_n.as<uint32_t>() : nullptr, h->wc_ocap,
-                                             (uint32_t)h->wcQ);
+  k_wc2_build<<<h->sms * 4, 256, 0, h->st>>>(h->tab, seed, h->wc_olist.as<uint32_t>(), h->wc_olist_n.as<uint32_t>(),
+                                             h->wc_ocap, (uint32_t)h->P0);
   prof_end(h, pe);
   CU(cudaGetLastError());
   h->launches++;
@@ -1550,11 +1520,9 @@ int wc_build(Handle* h, bool bloom, bool owners) {
 
 // PROBE through k_scan_wc: every record of the batch (and FILL's deferral list) into its run
 int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
-  const int P = h->P0, NP = h->P0 + h->wcQ;
+  const int NP = h->P0;
   const int grid = h->sms;
   const WcShape& shp = wc_shape();
-  // the filter of the table as FILL left it (a kernel boundary: the key set is final once frozen)
-  TRY(wc_build(h, true, false));
   const int64_t nlin_cap = h->defer_cap;
   // page lists: every CTA reserves a block of entries per run and launch (twice
   // the pages it expects to open, at least 2); a run that outgrows its block
@@ -1603,12 +1571,9 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.lkey = (const unsigned long long*)h->defer.as<uint64_t>();
   a.lval = (const unsigned long long*)(h->defer.as<uint64_t>() + h->defer_cap);
   a.lcount = SC(h) + 10;
-  a.bloom = h->wc_bloom.as<uint32_t>();
-  a.nblk = h->wc_nblk;
   a.pool = pool_of(h);
   a.set_id = ss.id;
-  a.P = P;
-  a.Q = h->wcQ;
+  a.NP = NP;
   a.plist = h->wc_plist.as<uint32_t>();
   a.plist_n = h->wc_pn.as<uint32_t>();
   a.plist_cap = h->wc_plist_cap;
@@ -1621,7 +1586,7 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
   if (getenv("AGGB_WC_NOSEND")) a.pf |= 2;  // (experiment: lines are not sent; results are wrong)
   auto fs = shp.fn;
-  const size_t smem = shp.bytes(NP, h->wc_nblk);
+  const size_t smem = shp.bytes(NP);
   CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int pe = prof_begin(h, 15);
   fs<<<grid, shp.blk + 32, smem, h->st>>>(a);  // + the producer warp
@@ -2362,7 +2327,7 @@ void aggb_destroy(void* handle) {
                   &h->pool_ctr, &h->defer, &h->scratch, &h->hscratch_dev, &h->out_keys, &h->out_vals,
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
-                  &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains, &h->wc_bloom,
+                  &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains,
                   &h->wc_plist, &h->wc_pn, &h->wc_recs, &h->wc_vinfo, &h->wc_failed, &h->wc_fail, &h->wc_olist,
                   &h->wc_olist_n, &h->wc_gather, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
@@ -2764,7 +2729,7 @@ int aggb_push_partials(void* handle, const void* recv, int64_t n_records) {
 // the children of the write-combined level 0 (k_child2_wc): one CTA per run,
 // whole waves; owner runs are seeded from the owners' lists of resident slots
 int wc_children(Handle* h) {
-  TRY(wc_build(h, false, true));
+  TRY(wc_build(h));
   Cw2Args ca;
   memset(&ca, 0, sizeof(ca));
   ca.sp = h->cs.ds;
@@ -2774,8 +2739,7 @@ int wc_children(Handle* h) {
   ca.plist_cap = h->wc_plist_cap;
   ca.part_recs = h->wc_recs.as<unsigned long long>();
   ca.vinfo = h->wc_vinfo.as<unsigned int>();
-  ca.P = h->P0;
-  ca.Q = h->wcQ;
+  ca.NP = h->P0;
   ca.table_bytes = h->wc_table_bytes;
   if (getenv("AGGB_WC_CHILD_KB"))  // test hook: small child tables send runs to the fallback
     ca.table_bytes = std::max(1, std::min(h->wc_table_bytes / 1024, atoi(getenv("AGGB_WC_CHILD_KB")))) * 1024;
@@ -2791,7 +2755,7 @@ int wc_children(Handle* h) {
   auto fc = h->prog == 2 ? k_child2_wc<CpC2, WC_CBLK, WC_CRL> : k_child2_wc<CpC1, WC_CBLK, WC_CRL>;
   CU(cudaFuncSetAttribute((const void*)fc, cudaFuncAttributeMaxDynamicSharedMemorySize, h->wc_table_bytes));
   int pe = prof_begin(h, 17);
-  fc<<<std::min(h->sms, ca.P + ca.Q), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
+  fc<<<std::min(h->sms, ca.NP), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
   prof_end(h, pe);
   CU(cudaGetLastError());
   h->launches++;
@@ -2804,67 +2768,65 @@ __global__ void k_stat_sub(unsigned long long* stats, unsigned long long n) {
 }
 
 // Runs k_child2_wc could not hold (more groups than its table, rows past the
-// output estimate, an overflowed page list, values beyond int32).  An owner run
-// holds records of resident keys: it is gathered into dense columns and probed
-// against the frozen table by the generic PROBE (hits aggregate in place, the
-// rest spills into the generic partitions), and the table is flushed again
-// over its first flush.  Then the completed runs' pages are retired and the
-// generic recursion takes what is left of the spill set.
+// output estimate, an overflowed page list, values beyond int32).  A run holds
+// records of resident keys, so it cannot go to the generic recursion as it is:
+// it is gathered into dense columns and probed against the frozen table by the
+// generic PROBE (hits aggregate in place, the rest spills into the generic
+// partitions), the table is flushed again over its first flush, every run's
+// pages are retired and the generic recursion takes the new spill.
 int wc_fallback(Handle* h) {
-  const int P = h->P0, NP = h->P0 + h->wcQ;
+  const int NP = h->P0;
   std::vector<uint32_t> failed((size_t)NP), pn((size_t)NP);
   std::vector<unsigned long long> recs((size_t)NP);
   CU(cudaMemcpyAsync(failed.data(), h->wc_failed.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
   CU(cudaMemcpyAsync(pn.data(), h->wc_pn.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
   CU(cudaMemcpyAsync(recs.data(), h->wc_recs.p, (size_t)NP * 8, cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
-  bool owners = false;
-  for (int p = P; p < NP; p++) owners |= failed[(size_t)p] != 0;
-  if (owners) {
-    // the table's rows are rewritten below: back to the row count before its flush
-    CU(cudaMemcpyAsync(SC(h) + 13, SC(h) + 30, 8, cudaMemcpyDeviceToDevice, h->st));
-    if (h->bloom_words) {
-      CU(cudaMemsetAsync(h->bloom.p, 0, (size_t)h->bloom_words * 8, h->st));
-      k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1);
-      h->launches++;
-    }
-    for (int p = P; p < NP; p++) {
-      if (!failed[(size_t)p]) continue;
-      if (pn[(size_t)p] > h->wc_plist_cap) return fail(AGGB_CAPACITY_EXCEEDED, "page list of an owner run overflowed");
-      const int64_t n = (int64_t)recs[(size_t)p];
-      if (n == 0) continue;
-      TRY(h->wc_gather.ensure((size_t)n * 16, &h->hw));
-      unsigned long long* gk = h->wc_gather.as<unsigned long long>();
-      unsigned long long* gv = gk + n;
-      CU(cudaMemsetAsync(SC(h) + 31, 0, 8, h->st));
-      k_wc2_gather<<<std::max(1, std::min<int>((int)pn[(size_t)p], h->sms * 4)), 256, 0, h->st>>>(
-          pool_of(h), h->wc_plist.as<uint32_t>() + (size_t)p * h->wc_plist_cap, pn[(size_t)p], gk, gv, SC(h) + 31);
-      k_stat_sub<<<1, 1, 0, h->st>>>(SC(h), (unsigned long long)n);  // (the PROBE below counts them again)
-      CU(cudaGetLastError());
-      h->launches += 2;
-      ColSrc col;
-      memset(&col, 0, sizeof(col));
-      col.n = n;
-      col.key[0] = (const uint8_t*)gk;
-      col.kstride[0] = 8;
-      col.kty[0] = TY_I64;
-      col.nv = 1;
-      col.val[0] = (const uint8_t*)gv;
-      col.vstride[0] = 8;
-      col.vty[0] = TY_I64;
-      PassPlan pr;
-      pr.mode = MODE_PROBE;
-      pr.col = col;
-      pr.ss = h->raw0.ss;
-      pr.counter = SC(h) + 9;
-      TRY(launch_pass(h, pr));
-    }
-    OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
-    TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
+  // the table's rows are rewritten below: back to the row count before its flush
+  CU(cudaMemcpyAsync(SC(h) + 13, SC(h) + 30, 8, cudaMemcpyDeviceToDevice, h->st));
+  if (h->bloom_words) {
+    CU(cudaMemsetAsync(h->bloom.p, 0, (size_t)h->bloom_words * 8, h->st));
+    k_bloom_build<1><<<h->sms * 4, 256, 0, h->st>>>(h->tab, h->bloom.as<uint64_t>(), (uint32_t)h->bloom_words - 1);
+    h->launches++;
   }
+  int64_t nmax = 0;
+  for (int p = 0; p < NP; p++)
+    if (failed[(size_t)p]) nmax = std::max<int64_t>(nmax, (int64_t)recs[(size_t)p]);
+  TRY(h->wc_gather.ensure((size_t)std::max<int64_t>(nmax, 1) * 16, &h->hw));
+  for (int p = 0; p < NP; p++) {
+    if (!failed[(size_t)p]) continue;
+    if (pn[(size_t)p] > h->wc_plist_cap) return fail(AGGB_CAPACITY_EXCEEDED, "page list of a run overflowed");
+    const int64_t n = (int64_t)recs[(size_t)p];
+    if (n == 0) continue;
+    unsigned long long* gk = h->wc_gather.as<unsigned long long>();
+    unsigned long long* gv = gk + nmax;
+    CU(cudaMemsetAsync(SC(h) + 31, 0, 8, h->st));
+    k_wc2_gather<<<std::max(1, std::min<int>((int)pn[(size_t)p], h->sms * 4)), 256, 0, h->st>>>(
+        pool_of(h), h->wc_plist.as<uint32_t>() + (size_t)p * h->wc_plist_cap, pn[(size_t)p], gk, gv, SC(h) + 31);
+    k_stat_sub<<<1, 1, 0, h->st>>>(SC(h), (unsigned long long)n);  // (the PROBE below counts them again)
+    CU(cudaGetLastError());
+    h->launches += 2;
+    ColSrc col;
+    memset(&col, 0, sizeof(col));
+    col.n = n;
+    col.key[0] = (const uint8_t*)gk;
+    col.kstride[0] = 8;
+    col.kty[0] = TY_I64;
+    col.nv = 1;
+    col.val[0] = (const uint8_t*)gv;
+    col.vstride[0] = 8;
+    col.vty[0] = TY_I64;
+    PassPlan pr;
+    pr.mode = MODE_PROBE;
+    pr.col = col;
+    pr.ss = h->raw0.ss;
+    pr.counter = SC(h) + 9;
+    TRY(launch_pass(h, pr));
+  }
+  OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+  TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
   k_wc2_retire<<<std::max(1, std::min(NP, h->sms * 4)), 256, 0, h->st>>>(
-      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, h->wc_failed.as<uint32_t>(), P, NP,
-      h->page_set.as<int32_t>());
+      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, NP, h->page_set.as<int32_t>());
   CU(cudaGetLastError());
   h->launches++;
   h->tail_valid = false;

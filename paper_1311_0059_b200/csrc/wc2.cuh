@@ -1,32 +1,32 @@
 // wc2.cuh — level 0 of budgeted pre-partitioning for 16-byte records (one-word
-// key, one int64 value; the C1/C2 record shape) in two kernels:
+// key, one int64 value; the C1/C2 record shape) after the table froze, in two
+// kernels:
 //
 //   k_scan_wc   one pass over the batch that only ROUTES: every record is
-//               hashed, tested against the frozen table's filter in shared
-//               memory and appended to a run — a spill partition (filter
-//               negative: the key is certainly not resident) or an owner
-//               partition (filter positive: resident key or false positive).
-//               Runs are written through per-partition shared-memory
-//               write-combining rings as whole 128-byte lines by the TMA engine
-//               (cp.async.bulk, SASS UBLKCP); input tiles arrive the same way.
-//   k_child2_wc one CTA per run, a compact shared-memory table (u32 states).
-//               An owner run's table is first seeded with the resident keys
-//               this owner is responsible for; their aggregates are merged into
-//               the level-0 table (L2 REDs, once per group) instead of being
-//               emitted, so resident keys still aggregate in place and are
-//               emitted once, by the table flush.  A false positive is simply a
-//               spilled key whose run is an owner run.
+//               hashed and appended to the run of its hash range.  Runs are
+//               written through per-run shared-memory write-combining rings as
+//               whole 128-byte lines; input tiles arrive by cp.async.bulk (the
+//               TMA engine, SASS UBLKCP) from a producer warp.
+//   k_child2_wc one CTA per run, a compact shared-memory table (u32 states),
+//               seeded with the resident keys of the run's hash range (the
+//               level-0 table's keys, listed per run by k_wc2_build).  The
+//               aggregates of the seeded keys are merged into the level-0 table
+//               (L2 REDs, once per group) and not emitted, so resident keys are
+//               emitted once, by the table flush, and their records do not count
+//               as spilled; every other key of the run is a spilled group the
+//               child emits.
 //
 // Replaces k_pp_probe (/root/reference/pkg/src/aggbench/_kernels.py:917-962:
 // frozen table, hits aggregate in place, misses spill to hash % P partitions,
 // bloom byte :938-942), PrePartitioning stage 2 and _drain_runs
 // (/root/reference/pkg/src/aggbench/operators/hybrid.py:518-552, :244-277).
 //
-// Why routing only: the earlier kernel resolved filter positives against the L2
-// table (one bucket load + four REDs per hit: 0.71 ms for 27M positives on C2,
-// 750 instructions per positive) and kept a second write path for them; here a
-// positive costs what a spill costs and the L2 table sees 4 REDs per resident
-// GROUP, not per record.
+// Why routing only: resolving each record against the L2 table cost one bucket
+// load and four REDs per hit (k_probe_wc's resolve pass: 0.71 ms for 27M filter
+// positives on C2, 750 instructions per positive) and a filter in shared memory
+// (64 KB, ~14 instructions per record) to keep the misses away from it.  Here
+// the table sees 4 REDs per resident GROUP, the filter is gone, and its shared
+// memory holds a third input stage.
 #pragma once
 #include "pass.cuh"
 #include "ptx.cuh"
@@ -34,42 +34,19 @@
 
 namespace aggb {
 
-// ---------------------------------------------------------------------------
-// the scan's hash: one 64-bit value, four independent fields
-//   hi word top bits   -> spill partition      (__umulhi(hi, P))
-//   hi word bits 0-14  -> three filter bit positions inside a 32-bit block
-//   lo word top bits   -> filter block         (__umulhi(lo, nblk))
-//   lo word bits 0-15  -> owner                (__umulhi(lo << 16, Q))
-// ---------------------------------------------------------------------------
+// the routing hash: run = top bits of the hash's high word
 __device__ __forceinline__ uint64_t wc2_hash(uint64_t k, uint64_t seed) { return fmix64(k ^ seed); }
-__device__ __forceinline__ uint32_t wc2_bits(uint32_t hi) {
-  // __funnelshift_l(0, 1, s) = 1 << (s & 31): one SHF.L.W per bit
-  return __funnelshift_l(0u, 1u, hi) | __funnelshift_l(0u, 1u, hi >> 5) | __funnelshift_l(0u, 1u, hi >> 10);
-}
-__device__ __forceinline__ uint32_t wc2_block(uint32_t lo, uint32_t nblk) { return __umulhi(lo, nblk); }
-__device__ __forceinline__ uint32_t wc2_owner(uint32_t lo, uint32_t Q) { return __umulhi(lo << 16, Q); }
+__device__ __forceinline__ uint32_t wc2_run(uint64_t h, uint32_t NP) { return __umulhi((uint32_t)(h >> 32), NP); }
 
-// filter of the frozen table (32-bit blocks, 3 bits per key) and the owners'
-// lists of resident slots; one pass over the table's key array
-__global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* bloom, uint32_t nblk, uint32_t* olist, uint32_t* olist_n,
-                            uint32_t ocap, uint32_t Q) {
+// the runs' lists of resident slots: one pass over the frozen table's key array
+__global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* olist, uint32_t* olist_n, uint32_t ocap, uint32_t NP) {
   const uint64_t n = t.mask + 1;
-  if (bloom && blockIdx.x == 0 && threadIdx.x == 0 && *(volatile int*)&t.hdr->esc) {
-    // the sentinel key lives in the table's escape slot: routed like any resident key
-    const uint64_t h = wc2_hash(EMPTY, seed);
-    atomicOr(&bloom[wc2_block((uint32_t)h, nblk)], wc2_bits((uint32_t)(h >> 32)));
-  }
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = t.keys[i];
     if (k == EMPTY) continue;
-    const uint64_t h = wc2_hash(k, seed);
-    const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
-    if (bloom) atomicOr(&bloom[wc2_block(lo, nblk)], wc2_bits(hi));
-    if (olist) {
-      const uint32_t o = wc2_owner(lo, Q);
-      const uint32_t at = atomicAdd(&olist_n[o], 1u);
-      if (at < ocap) olist[(size_t)o * ocap + at] = (uint32_t)i;
-    }
+    const uint32_t o = wc2_run(wc2_hash(k, seed), NP);
+    const uint32_t at = atomicAdd(&olist_n[o], 1u);
+    if (at < ocap) olist[(size_t)o * ocap + at] = (uint32_t)i;
   }
 }
 
@@ -84,16 +61,14 @@ struct Wc2Args {
   const unsigned long long* lkey;         // FILL's deferral list (SoA), nullable
   const unsigned long long* lval;
   const unsigned long long* lcount;
-  const uint32_t* bloom;                  // nblk 32-bit blocks
-  uint32_t nblk;
   PagePool pool;
   int32_t set_id;                         // spill set of the runs' pages
-  int32_t P, Q;                           // spill partitions, owner partitions (runs = P + Q)
-  uint32_t* plist;                        // [P + Q][plist_cap] page ids per run
-  uint32_t* plist_n;                      // [P + Q]
+  int32_t NP;                             // runs
+  uint32_t* plist;                        // [NP][plist_cap] page ids per run
+  uint32_t* plist_n;                      // [NP]
   uint32_t plist_cap;
   uint32_t plist_blk;                     // page-list entries a CTA reserves per run at a time
-  unsigned long long* part_recs;          // [P + Q] records per run
+  unsigned long long* part_recs;          // [NP] records per run
   unsigned long long* stats;              // ST_* counters
   unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words
   uint32_t* fail;                         // page list overflow / page map error
@@ -113,9 +88,7 @@ struct Wc2Layout {
   static __host__ __device__ size_t ring_bytes(int NP) { return (size_t)NP * RS * 16; }
   static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (3 + NE) * 4 + 15) & ~(size_t)15; }
   static __host__ __device__ size_t send_bytes() { return (size_t)(BLK / 32) * 32 * 8; }  // per warp: 32 lines to send
-  static __host__ __device__ size_t bytes(int NP, uint32_t nblk) {
-    return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + send_bytes() + (((size_t)nblk * 4 + 15) & ~(size_t)15);
-  }
+  static __host__ __device__ size_t bytes(int NP) { return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + send_bytes(); }
 };
 
 __device__ __forceinline__ void lds128(uint32_t a, uint64_t& x, uint64_t& y) {
@@ -125,7 +98,7 @@ __device__ __forceinline__ void lds128(uint32_t a, uint64_t& x, uint64_t& y) {
 constexpr int WC2_PF = 6;  // L2 prefetch distance in tiles (rounds of the grid)
 
 // One CTA per SM, persistent.  Per tile (T = BLK * R records):
-//   [A] every thread routes its R records: hash, filter, run id, one shared
+//   [A] every thread routes its R records: hash, run id, one shared
 //       atomic on the run's claim word cw[run] (claim counter in bits 0-22, the
 //       run's window start (line index mod 512) in bits 23-31).  A claim
 //       inside the window (LINES lines from the run's open line) is written
@@ -147,8 +120,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
   constexpr uint32_t CWM = (1u << 23) - 1;
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31;
-  const int P = a.P, NP = a.P + a.Q;
-  const uint32_t Q = (uint32_t)a.Q, nblk = a.nblk;
+  const int NP = a.NP;
   unsigned long long* stg = (unsigned long long*)smem;
   ulonglong2* ring = (ulonglong2*)(smem + L::stage_bytes());
   uint32_t* cw = (uint32_t*)(smem + L::stage_bytes() + L::ring_bytes(NP));
@@ -156,8 +128,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
   uint32_t* lbase = ent + NP * NE;  // this CTA's block of the run's page list ...
   uint32_t* lused = lbase + NP;     // ... and the entries of it in use
   uint2* sendq = (uint2*)((unsigned char*)cw + L::meta_bytes(NP));  // per warp: (ring address, page << 6 | line) of the lines to send
-  uint32_t* sbloom = (uint32_t*)((unsigned char*)sendq + L::send_bytes());
-  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw), a_bloom = smem_u32(sbloom);
+  const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw);
   __shared__ __align__(8) uint64_t mbar[NS];    // stage full (the tile's bytes have landed)
   __shared__ __align__(8) uint64_t mbar_e[NS];  // stage empty (every consumer is past barrier 2 of its tile)
   __shared__ int s_tcnt[NS];
@@ -183,7 +154,6 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
     lused[p] = 0;
   }
   for (int i = tid; i < NP * NE; i += NT) ent[i] = 0xFFFFFF00u | (uint32_t)(((i & (NE - 1)) + 1) & (NE - 1));
-  for (uint32_t i = tid; i < nblk; i += NT) sbloom[i] = __ldcg(a.bloom + i);
   if (tid == 0) {
     s_sb = s_su = s_sc = s_nb = s_nv = s_want = s_pdone = 0;
     for (int s = 0; s < NS; s++) {
@@ -359,12 +329,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       }
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        const uint64_t h = wc2_hash(k[r], a.seed);
-        const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
-        const uint32_t blk = lds32(a_bloom + 4u * wc2_block(lo, nblk));
-        const uint32_t bits = wc2_bits(hi);
-        const bool pos = (blk & bits) == bits;
-        pid[r] = pos ? P + (int)wc2_owner(lo, Q) : (int)__umulhi(hi, (uint32_t)P);
+        pid[r] = (int)wc2_run(wc2_hash(k[r], a.seed), (uint32_t)NP);
         const uint64_t m = v[r] ^ (uint64_t)((long long)v[r] >> 63);
         vm |= FULL ? m : (((vm_ >> r) & 1u) ? m : 0ull);
         km |= FULL ? (uint32_t)(k[r] >> 32) : (((vm_ >> r) & 1u) ? (uint32_t)(k[r] >> 32) : 0u);
@@ -514,16 +479,16 @@ struct Cw2Args {
   uint32_t plist_cap;
   const unsigned long long* part_recs;
   const unsigned int* vinfo;    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words (k_scan_wc)
-  int32_t P, Q;
+  int32_t NP;                   // runs
   int32_t table_bytes;          // dynamic shared memory for the table
   uint64_t seed;                // slot hash seed of the child level
   OutBuf out;
-  uint32_t* failed;             // [P + Q]: 1 = did not fit, left to the fallback
+  uint32_t* failed;             // [NP]: 1 = did not fit, left to the fallback
   uint32_t* fail;               // bit 2: some run failed (the host runs the fallback)
   unsigned long long* stats;
-  GTable t;                     // the level-0 table (owner runs merge their resident groups into it)
-  const uint32_t* olist;        // [Q][ocap] resident slots per owner
-  const uint32_t* olist_n;      // [Q]
+  GTable t;                     // the level-0 table (the runs merge their resident groups into it)
+  const uint32_t* olist;        // [NP][ocap] resident slots per run
+  const uint32_t* olist_n;      // [NP]
   uint32_t ocap;
 };
 
@@ -715,7 +680,7 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
     }
   };
   if (owner) {  // seed: the resident keys this owner answers for, with their level-0 slots
-    const int o = p - a.P;
+    const int o = p;
     const uint32_t nres = a.olist_n[o];
     if (nres > a.ocap || (int)nres > maxg) {
       if (tid == 0) sh.fail = 1;
@@ -981,11 +946,11 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
   const uint32_t vabs = a.vinfo[1] + 1u;
   const bool k32 = a.vinfo[2] == 0;  // every key of the runs fits in 32 bits
   const uint32_t seed32 = (uint32_t)a.seed ^ (uint32_t)(a.seed >> 32);
-  const int NP = a.P + a.Q;
+  const int NP = a.NP;
   for (int p = blockIdx.x; p < NP; p += gridDim.x) {
     const unsigned long long np = a.part_recs[p];
     if (np == 0) continue;
-    const bool owner = p >= a.P;
+    const bool owner = true;  // every run answers for the resident keys of its hash range
     // wide sums (a u32 pair with carry) only when a run's sum can leave int32
     const bool wide = CP::nsum() > 0 && (double)np * (double)vabs >= 2147483647.0;
     if (k32) {
@@ -1004,10 +969,8 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
 // the spill set, so the generic recursion sees only the spill partitions that
 // did not fit (their pages are untouched).  Owner runs that did not fit are
 // re-probed by the host (gathered, then the generic PROBE) before this.
-__global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, const uint32_t* failed, int P,
-                             int NP, int32_t* page_set) {
+__global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, int NP, int32_t* page_set) {
   for (int p = blockIdx.x; p < NP; p += gridDim.x) {
-    if (p < P && failed[p]) continue;
     const uint32_t n = plist_n[p];
     if (n > cap) continue;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
