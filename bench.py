@@ -379,12 +379,12 @@ def roofline(out, args, peak):
     steps = args.steps
     groups = {}
     # level-0 pass (FILL + PROBE / ROUTE): reads the batch, writes the spill
-    l0 = [k for k in ks if (k.startswith("k_pass<") and "GRACE" not in k) or k in ("k_scan_wc", "k_wc_build")]
+    l0 = [k for k in ks if (k.startswith("k_pass<") and "GRACE" not in k) or k == "k_scan_wc"]
     if l0:
         ms = sum(ks[k][1] for k in l0) / steps
         nl = sum(ks[k][0] for k in l0) / steps
         groups["level0_pass"] = (ms, nl, in_b * n + spill_rec * S)
-    ch = [k for k in ("k_child", "k_child_wc") if k in ks]
+    ch = [k for k in ("k_child", "k_child_wc", "k_wc_build") if k in ks]
     if ch:
         ms = sum(ks[k][1] for k in ch) / steps
         nl = sum(ks[k][0] for k in ch) / steps

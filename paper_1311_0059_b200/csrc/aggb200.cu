@@ -1583,8 +1583,7 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.vinfo = h->wc_vinfo.as<unsigned int>();
   a.fail = h->wc_fail.as<uint32_t>();
   a.stash = stash;
-  a.pf = getenv("AGGB_WC_NOPF") ? 0 : 1;
-  if (getenv("AGGB_WC_NOSEND")) a.pf |= 2;  // (experiment: lines are not sent; results are wrong)
+  a.nosend = getenv("AGGB_WC_NOSEND") ? 1 : 0;  // (experiment: lines are not written; results are wrong)
   auto fs = shp.fn;
   const size_t smem = shp.bytes(NP);
   CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -3136,6 +3135,33 @@ int seg_reduce(Handle* h, SortBuf cur, int64_t n) {
   CU(cudaMemcpyAsync(&last_cnt, th.as<uint32_t>() + ntiles - 1, 4, cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
   int64_t G = (int64_t)last_off + last_cnt;
+  // one-word keys, one int64 value, COUNT/SUM(/MIN/MAX): the fused pass (sort.cuh k_seg_emit2)
+  if (KW == 1 && cur.nw == 2 && (h->prog == 1 || h->prog == 2) && h->cs.ds.vty[0] == TY_I64 && !getenv("AGGB_NO_SEGFUSE")) {
+    TRY(ensure_out(h, G + 16));
+    TRY(longl.ensure((size_t)(n / SEG_WALK + 2) * 16, nullptr));
+    CU(cudaMemsetAsync(SC(h) + 14, 0, 8, h->st));
+    OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
+    const int g2 = (int)std::min<int64_t>(ntiles, (int64_t)h->sms * 16);
+    if (h->prog == 2) {
+      k_seg_emit2<CpC2><<<g2, SEG_BLOCK, 0, h->st>>>(cur.w[0], cur.w[1], n, toff.as<unsigned long long>(), ntiles,
+                                                    h->cs.ds, o, longl.as<long long>(), SC(h) + 14);
+      k_seg_long2<CpC2><<<h->sms * 2, 256, 0, h->st>>>(cur.w[0], cur.w[1], n, h->cs.ds, o, longl.as<long long>(), SC(h) + 14);
+    } else {
+      k_seg_emit2<CpC1><<<g2, SEG_BLOCK, 0, h->st>>>(cur.w[0], cur.w[1], n, toff.as<unsigned long long>(), ntiles,
+                                                    h->cs.ds, o, longl.as<long long>(), SC(h) + 14);
+      k_seg_long2<CpC1><<<h->sms * 2, 256, 0, h->st>>>(cur.w[0], cur.w[1], n, h->cs.ds, o, longl.as<long long>(), SC(h) + 14);
+    }
+    prof_end(h, pe);
+    h->launches += 4;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(SC(h) + 13, &G, 8, cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    th.release();
+    toff.release();
+    tmp.release();
+    longl.release();
+    return AGGB_OK;
+  }
   TRY(heads.ensure((size_t)std::max<int64_t>(G, 1) * 8, nullptr));
   TRY(longl.ensure((size_t)std::max<int64_t>(G, 1) * 8, nullptr));
   k_head_compact<KW><<<grid, SORT_BLOCK, 0, h->st>>>(cur, n, toff.as<unsigned long long>(), ntiles,
@@ -3201,8 +3227,50 @@ int aggb_sort_finish(Handle* h) {
       }
     int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
     DBuf counts, offs, tmp;
-    TRY(counts.ensure((size_t)ntiles * 256 * 4, nullptr));
-    TRY(offs.ensure((size_t)ntiles * 256 * 8, nullptr));
+    // two-word records below 2^30: one-sweep passes (chained scan with decoupled
+    // look-back inside the scatter; the digits' global bases from the byte histograms)
+    const bool onesweep = a.nw == 2 && n < (1ll << 30) && !getenv("AGGB_NO_ONESWEEP");
+    if (onesweep && !passes.empty()) {
+      DBuf status, gb;
+      TRY(status.ensure((size_t)ntiles * 256 * 4, nullptr));
+      TRY(gb.ensure(passes.size() * 256 * 8 + 8, nullptr));
+      std::vector<unsigned long long> bases(passes.size() * 256);
+      for (size_t q = 0; q < passes.size(); q++) {
+        const unsigned long long* row = &hh[(size_t)(passes[q].first * 8 + passes[q].second) * 256];
+        unsigned long long acc = 0;
+        for (int d = 0; d < 256; d++) {
+          bases[q * 256 + d] = acc;
+          acc += row[d];
+        }
+      }
+      CU(cudaMemcpyAsync(gb.p, bases.data(), bases.size() * 8, cudaMemcpyHostToDevice, h->st));
+      const int smem2 = SORT_TILE * 16;
+      CU(cudaFuncSetAttribute((const void*)k_onesweep2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      int occ2 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_onesweep2, S2_BLOCK, smem2);
+      const int grid2 = (int)std::min<int64_t>(ntiles, (int64_t)std::max(1, occ2) * h->sms);
+      unsigned long long* ticket = gb.as<unsigned long long>() + passes.size() * 256;
+      for (size_t q = 0; q < passes.size(); q++) {
+        int pe2 = prof_begin(h, 9);
+        CU(cudaMemsetAsync(status.p, 0, (size_t)ntiles * 256 * 4, h->st));
+        CU(cudaMemsetAsync(ticket, 0, 8, h->st));
+        k_onesweep2<<<grid2, S2_BLOCK, smem2, h->st>>>(a, b, passes[q].first, 8 * passes[q].second, n,
+                                                         gb.as<unsigned long long>() + q * 256, status.as<uint32_t>(),
+                                                         ticket, ntiles);
+        prof_end(h, pe2);
+        h->launches++;
+        CU(cudaGetLastError());
+        std::swap(a, b);
+      }
+      CU(cudaStreamSynchronize(h->st));
+      status.release();
+      gb.release();
+      passes.clear();
+    }
+    if (!passes.empty()) {
+      TRY(counts.ensure((size_t)ntiles * 256 * 4, nullptr));
+      TRY(offs.ensure((size_t)ntiles * 256 * 8, nullptr));
+    }
     int grid = (int)std::min<int64_t>(ntiles, (int64_t)h->sms * 8);
     for (auto& pw : passes) {
       int pe2 = prof_begin(h, 9);

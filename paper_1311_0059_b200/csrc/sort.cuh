@@ -16,6 +16,7 @@
 // which is the reference's byte order (_kernels.py:121-131).
 #pragma once
 #include "kernels.cuh"
+#include "wc2.cuh"  // CompactProg (compile-time COUNT/SUM/MIN/MAX programs)
 
 namespace aggb {
 
@@ -300,6 +301,122 @@ __global__ void __launch_bounds__(S2_BLOCK, 2) k_scatter2(SortBuf src, SortBuf d
   }
 }
 
+// ---- one-sweep digit pass (two-word records) ----------------------------------
+// The same tile-local ranking and shared-memory reorder as k_scatter2, but the
+// tile's global digit offsets come from a chained scan with decoupled look-back
+// (Merrill & Garland's single-pass scan, as in onesweep radix sort) instead of a
+// per-tile histogram kernel and a 3-phase scan per pass: tiles take tickets in
+// order; a tile publishes its 256 digit counts (flag AGG), sums its
+// predecessors' statuses backwards until one carries an inclusive prefix (flag
+// INCL) and publishes its own inclusive prefix.  The global base of every digit
+// comes from the byte histograms k_sort_append gathered.  Status words are 32
+// bits (2 flag bits + 30 count bits: n < 2^30 records).
+constexpr uint32_t OS_AGG = 1u << 30, OS_INCL = 2u << 30, OS_MASK = (1u << 30) - 1u;
+
+__global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf dst, int key_word, int shift, int64_t n,
+                                                        const unsigned long long* gbase /* [256] exclusive */,
+                                                        uint32_t* status /* [ntiles][256], zeroed */,
+                                                        unsigned long long* ticket, int64_t ntiles) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* sk = (uint64_t*)smem;               // SORT_TILE key words (rank order)
+  uint64_t* sv = sk + SORT_TILE;                // SORT_TILE payload words
+  __shared__ uint32_t wcnt[S2_WARPS][256];      // per-warp digit counts -> per-warp exclusive bases
+  __shared__ uint32_t dbase[256];               // tile-local exclusive base of each digit
+  __shared__ unsigned long long goff[256];      // global base of each digit for this tile
+  __shared__ uint32_t wsum[8];
+  __shared__ long long s_tile;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int other = 1 - key_word;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+#pragma unroll
+    for (int q = lane; q < 256; q += 32) wcnt[wid][q] = 0;
+    __syncthreads();
+    const int64_t t = s_tile;
+    if (t >= ntiles) break;
+    const int64_t base = t * SORT_TILE + (int64_t)wid * (S2_IPT * 32);
+    uint64_t kk[S2_IPT], vv[S2_IPT];
+    uint32_t rk[S2_IPT];
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      const int64_t i = base + j * 32 + lane;
+      const bool live = i < n;
+      kk[j] = live ? __ldcs(src.w[key_word] + i) : 0ull;
+      vv[j] = live ? __ldcs(src.w[other] + i) : 0ull;
+    }
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      const bool live = base + j * 32 + lane < n;
+      const int d = live ? (int)((kk[j] >> shift) & 255) : 256 + lane;  // dead lanes: unique, not counted
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const unsigned run = live ? wcnt[wid][d] : 0u;
+      rk[j] = run + __popc(peers & ((1u << lane) - 1u));
+      __syncwarp();
+      if (live && lane == __ffs(peers) - 1) wcnt[wid][d] = run + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit (threads 0..255): exclusive prefix over warps; digit totals -> scan over digits
+    const int d0 = threadIdx.x;
+    uint32_t acc = 0, x = 0;
+    if (d0 < 256) {
+#pragma unroll
+      for (int w = 0; w < S2_WARPS; w++) {
+        const uint32_t c = wcnt[w][d0];
+        wcnt[w][d0] = acc;
+        acc += c;
+      }
+      volatile uint32_t* st = status + (size_t)t * 256 + d0;
+      *st = OS_AGG | acc;
+      x = acc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[wid] = x;
+      // decoupled look-back over the predecessors' statuses of this digit
+      uint32_t excl = 0;
+      for (int64_t tt = t - 1; tt >= 0; tt--) {
+        volatile const uint32_t* ps = status + (size_t)tt * 256 + d0;
+        uint32_t v;
+        do {
+          v = *ps;
+        } while ((v >> 30) == 0);
+        excl += v & OS_MASK;
+        if ((v >> 30) == 2) break;
+      }
+      *st = OS_INCL | (excl + acc);
+      goff[d0] = gbase[d0] + excl;
+    }
+    __syncthreads();
+    if (d0 < 256) {
+      uint32_t pre = 0;
+      for (int w = 0; w < wid; w++) pre += wsum[w];
+      dbase[d0] = pre + x - acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) {
+      if (base + j * 32 + lane >= n) continue;
+      const int d = (int)((kk[j] >> shift) & 255);
+      const uint32_t r = dbase[d] + wcnt[wid][d] + rk[j];
+      sk[r] = kk[j];
+      sv[r] = vv[j];
+    }
+    __syncthreads();
+    const int cnt = (int)min((int64_t)SORT_TILE, n - t * SORT_TILE);
+    for (int q = threadIdx.x; q < cnt; q += S2_BLOCK) {
+      const uint64_t k = sk[q];
+      const int d = (int)((k >> shift) & 255);
+      const unsigned long long pos = goff[d] + (q - dbase[d]);
+      dst.w[key_word][pos] = k;
+      dst.w[other][pos] = sv[q];
+    }
+    __syncthreads();
+  }
+}
+
 // ---- segmented reduction ----------------------------------------------------
 
 template <int KW>
@@ -431,6 +548,190 @@ __global__ void k_seg_reduce_long(const SortBuf s, DevSpec sp, int kind, int64_t
 #pragma unroll
       for (int w = 0; w < KW; w++) k[w] = s.w[w][a];
       emit_group<KW>(sp, o, g, k, st_out);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- fused segmented reduction (one-word keys, one int64 value, COUNT/SUM/MIN/MAX) ----
+// One pass over the sorted records after the per-tile head counts are scanned:
+// thread t of a tile holds 8 consecutive records in registers, finds the segment
+// heads among them, and reduces every segment that STARTS in its records — a
+// segment that runs past them is followed through global memory (the next
+// threads' records: cache hits), up to SEG_WALK records; a longer one is listed
+// for k_seg_long2 (a block per segment).  Threads inside a longer segment do
+// nothing.  A head's output row is tile_off[tile] + its rank in the tile, so the
+// output is in key order.  (The generic path compacts the head positions into an
+// 8-byte-per-group array and gathers from it: 37 ms per 1B records on C4.)
+constexpr int SEG_IPT = 8, SEG_BLOCK = SORT_TILE / SEG_IPT;  // 512 threads x 8 records
+constexpr int SEG_WALK = 256;
+
+template <class CP>
+struct SegAgg {
+  uint64_t cnt;
+  long long sum, mn, mx;
+  __device__ __forceinline__ void start(uint64_t v) {
+    cnt = 1;
+    sum = mn = mx = (long long)v;
+  }
+  __device__ __forceinline__ void add(uint64_t v) {
+    cnt++;
+    sum += (long long)v;
+    mn = min(mn, (long long)v);
+    mx = max(mx, (long long)v);
+  }
+  __device__ __forceinline__ void emit(const DevSpec& sp, const OutBuf& o, int64_t idx, uint64_t key) const {
+    uint64_t st[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < CP::N; j++) {
+      const uint32_t F = CP::fd(j);
+      if (j < 4) st[j] = CP::is_count(j) ? cnt : CP::is_sum(j) ? (uint64_t)sum : (F & 3) == OP_MIN ? (uint64_t)mn : (uint64_t)mx;
+    }
+    const uint64_t kk[1] = {key};
+    emit_group4<1>(sp, o, idx, kk, st);
+  }
+};
+
+template <class CP>
+__global__ void __launch_bounds__(SEG_BLOCK) k_seg_emit2(const uint64_t* __restrict__ key, const uint64_t* __restrict__ val,
+                                                         int64_t n, const unsigned long long* tile_off, int64_t ntiles,
+                                                         DevSpec sp, OutBuf o, long long* long_list,
+                                                         unsigned long long* nlong) {
+  __shared__ uint32_t wsum[SEG_BLOCK / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool aligned = (((uintptr_t)key | (uintptr_t)val) & 15) == 0;  // (a word column starts at any 8-byte offset)
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * SORT_TILE + (int64_t)threadIdx.x * SEG_IPT;
+    uint64_t k[SEG_IPT], v[SEG_IPT];
+    const int nvalid = (int)max((int64_t)0, min((int64_t)SEG_IPT, n - base));
+    if (nvalid == SEG_IPT && aligned) {
+#pragma unroll
+      for (int j = 0; j < SEG_IPT; j += 2) {
+        const ulonglong2 a = __ldcs((const ulonglong2*)(key + base + j));
+        const ulonglong2 b = __ldcs((const ulonglong2*)(val + base + j));
+        k[j] = a.x;
+        k[j + 1] = a.y;
+        v[j] = b.x;
+        v[j + 1] = b.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < SEG_IPT; j++) {
+        k[j] = j < nvalid ? key[base + j] : 0ull;
+        v[j] = j < nvalid ? val[base + j] : 0ull;
+      }
+    }
+    // the record before this thread's first: the previous lane's last record
+    uint64_t prev = __shfl_up_sync(0xffffffffu, k[SEG_IPT - 1], 1);
+    if (lane == 0 && base > 0 && nvalid > 0) prev = key[base - 1];
+    uint32_t hm = 0;
+#pragma unroll
+    for (int j = 0; j < SEG_IPT; j++) {
+      const bool head = j < nvalid && (j == 0 ? (base == 0 || k[0] != prev) : k[j] != k[j - 1]);
+      hm |= (uint32_t)head << j;
+    }
+    // rank of this thread's first head in the tile
+    const uint32_t nh = __popc(hm);
+    uint32_t x = nh;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    __syncthreads();  // (wsum of the previous tile is read)
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < wid; w++) pre += wsum[w];
+    int64_t g = (int64_t)tile_off[t] + pre + x - nh;
+    if (!hm) continue;
+    SegAgg<CP> ag;
+    bool open = false;
+    uint64_t ck = 0;
+    int64_t cstart = 0;
+#pragma unroll
+    for (int j = 0; j < SEG_IPT; j++) {
+      if (j >= nvalid) break;
+      if ((hm >> j) & 1u) {
+        if (open) ag.emit(sp, o, g++, ck);
+        open = true;
+        ck = k[j];
+        cstart = base + j;
+        ag.start(v[j]);
+      } else if (open) {
+        ag.add(v[j]);
+      }
+    }
+    // the last segment may run on past this thread's records
+    int64_t i = base + nvalid;
+    int steps = 0;
+    while (i < n && steps < SEG_WALK && key[i] == ck) {
+      ag.add(val[i]);
+      i++;
+      steps++;
+    }
+    if (i < n && steps == SEG_WALK && key[i] == ck) {  // a long segment: a block takes it from its start
+      const unsigned long long at = atomicAdd(nlong, 1ull);
+      long_list[2 * at] = (long long)cstart;
+      long_list[2 * at + 1] = (long long)g;
+    } else {
+      ag.emit(sp, o, g, ck);
+    }
+  }
+}
+
+// block per long segment: strided accumulation while the key lasts, then a block reduction
+template <class CP>
+__global__ void __launch_bounds__(256) k_seg_long2(const uint64_t* __restrict__ key, const uint64_t* __restrict__ val,
+                                                   int64_t n, DevSpec sp, OutBuf o, const long long* long_list,
+                                                   const unsigned long long* nlong) {
+  __shared__ unsigned long long s_cnt[8];
+  __shared__ long long s_sum[8], s_mn[8], s_mx[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (unsigned long long q = blockIdx.x; q < *nlong; q += gridDim.x) {
+    const int64_t start = long_list[2 * q], g = long_list[2 * q + 1];
+    const uint64_t k0 = key[start];
+    unsigned long long cnt = 0;
+    long long sum = 0, mn = 0x7FFFFFFFFFFFFFFFll, mx = (long long)0x8000000000000000ull;
+    for (int64_t c = start;; c += blockDim.x) {
+      const int64_t i = c + threadIdx.x;
+      const bool in = i < n && key[i] == k0;
+      if (in) {
+        const long long x = (long long)val[i];
+        cnt++;
+        sum += x;
+        mn = min(mn, x);
+        mx = max(mx, x);
+      }
+      if (!__syncthreads_and(in)) break;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+      sum += __shfl_xor_sync(0xffffffffu, sum, d);
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    }
+    if (lane == 0) {
+      s_cnt[wid] = cnt;
+      s_sum[wid] = sum;
+      s_mn[wid] = mn;
+      s_mx[wid] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      SegAgg<CP> ag;
+      ag.cnt = 0;
+      ag.sum = 0;
+      ag.mn = 0x7FFFFFFFFFFFFFFFll;
+      ag.mx = (long long)0x8000000000000000ull;
+      for (int w = 0; w < (int)blockDim.x / 32; w++) {
+        ag.cnt += s_cnt[w];
+        ag.sum += s_sum[w];
+        ag.mn = min(ag.mn, s_mn[w]);
+        ag.mx = max(ag.mx, s_mx[w]);
+      }
+      ag.emit(sp, o, g, k0);
     }
     __syncthreads();
   }

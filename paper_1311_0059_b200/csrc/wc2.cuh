@@ -73,7 +73,7 @@ struct Wc2Args {
   unsigned int* vinfo;                    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words
   uint32_t* fail;                         // page list overflow / page map error
   int32_t stash;                          // pages per CTA stash refill
-  int32_t pf;                             // L2 prefetch of the batch tiles ahead
+  int32_t nosend;                         // (experiment) lines are not written
 };
 
 template <int BLK, int R, int NS>
@@ -94,8 +94,6 @@ struct Wc2Layout {
 __device__ __forceinline__ void lds128(uint32_t a, uint64_t& x, uint64_t& y) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "r"(a));
 }
-
-constexpr int WC2_PF = 6;  // L2 prefetch distance in tiles (rounds of the grid)
 
 // One CTA per SM, persistent.  Per tile (T = BLK * R records):
 //   [A] every thread routes its R records: hash, run id, one shared
@@ -200,15 +198,6 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       bulk_g2s(sv, vp, (uint32_t)c2 * 8u, &mbar[s]);
     } else {
       mbar_arrive(&mbar[s]);
-    }
-    const unsigned long long pt = next_tile + (unsigned long long)(WC2_PF - 1) * gridDim.x;  // into L2, ahead
-    if (a.pf && pt < (unsigned long long)col_tiles) {
-      const int64_t b = col_start + (int64_t)pt * T;
-      const uint32_t cb = (uint32_t)((n - b < (int64_t)T ? n - b : (int64_t)T) & ~1ll) * 8u;
-      if (cb) {
-        bulk_prefetch_l2(a.key + b, cb);
-        bulk_prefetch_l2(a.val + b, cb);
-      }
     }
   };
   // The producer is a warp of its own (thread BLK).  As thread 0 of the consumers
@@ -418,7 +407,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
           const int n = __popc(mask);
           for (int i = grp; i < n; i += 4) {  // lane group g copies lines g, g + 4, ...
             const uint2 e = wq[i];
-            if ((e.y >> 6) < 0xFFFFFFu && !(a.pf & 2)) {
+            if ((e.y >> 6) < 0xFFFFFFu && !a.nosend) {
               uint64_t x, y;
               lds128(e.x + 16u * (uint32_t)sub, x, y);
               st_v2(pool + ((size_t)(e.y >> 6) << (SLOG + 1)) + ((size_t)(e.y & 63u) << 4) + 2u * (uint32_t)sub,
