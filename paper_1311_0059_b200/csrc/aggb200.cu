@@ -3248,7 +3248,7 @@ int aggb_sort_finish(Handle* h) {
       CU(cudaFuncSetAttribute((const void*)k_onesweep2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
       int occ2 = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_onesweep2, S2_BLOCK, smem2);
-      const int grid2 = (int)std::min<int64_t>(ntiles, (int64_t)std::max(1, occ2) * h->sms);
+      const int grid2 = (int)ntiles;  // one tile per CTA, taken in ticket order
       unsigned long long* ticket = gb.as<unsigned long long>() + passes.size() * 256;
       for (size_t q = 0; q < passes.size(); q++) {
         int pe2 = prof_begin(h, 9);
@@ -3256,7 +3256,7 @@ int aggb_sort_finish(Handle* h) {
         CU(cudaMemsetAsync(ticket, 0, 8, h->st));
         k_onesweep2<<<grid2, S2_BLOCK, smem2, h->st>>>(a, b, passes[q].first, 8 * passes[q].second, n,
                                                          gb.as<unsigned long long>() + q * 256, status.as<uint32_t>(),
-                                                         ticket, ntiles);
+                                                         ticket, ntiles, getenv("AGGB_OS_NOWRITE") ? 1 : 0);
         prof_end(h, pe2);
         h->launches++;
         CU(cudaGetLastError());

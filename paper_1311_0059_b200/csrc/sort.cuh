@@ -316,7 +316,7 @@ constexpr uint32_t OS_AGG = 1u << 30, OS_INCL = 2u << 30, OS_MASK = (1u << 30) -
 __global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf dst, int key_word, int shift, int64_t n,
                                                         const unsigned long long* gbase /* [256] exclusive */,
                                                         uint32_t* status /* [ntiles][256], zeroed */,
-                                                        unsigned long long* ticket, int64_t ntiles) {
+                                                        unsigned long long* ticket, int64_t ntiles, int nowrite) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* sk = (uint64_t*)smem;               // SORT_TILE key words (rank order)
   uint64_t* sv = sk + SORT_TILE;                // SORT_TILE payload words
@@ -327,13 +327,18 @@ __global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf 
   __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int other = 1 - key_word;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+  // One tile per CTA, in ticket order (a tile only ever waits for lower tickets, and
+  // those CTAs are running).  The ticket is a returning global atomic (~1 us): with a
+  // persistent loop all 512 threads waited for it at the top of every tile (30% of the
+  // stall samples), and taking it a tile ahead stalls every later tile's look-back for
+  // a whole tile; here the other resident CTA of the SM covers it.
+  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
 #pragma unroll
-    for (int q = lane; q < 256; q += 32) wcnt[wid][q] = 0;
-    __syncthreads();
+  for (int q = lane; q < 256; q += 32) wcnt[wid][q] = 0;
+  __syncthreads();
+  {
     const int64_t t = s_tile;
-    if (t >= ntiles) break;
+    if (t >= ntiles) return;
     const int64_t base = t * SORT_TILE + (int64_t)wid * (S2_IPT * 32);
     uint64_t kk[S2_IPT], vv[S2_IPT];
     uint32_t rk[S2_IPT];
@@ -344,17 +349,24 @@ __global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf 
       kk[j] = live ? __ldcs(src.w[key_word] + i) : 0ull;
       vv[j] = live ? __ldcs(src.w[other] + i) : 0ull;
     }
+    // ranks: lanes of equal digit are ranked by match_any; the group's leader adds the
+    // group to the warp's digit counter with one returning shared atomic (same-address
+    // atomics of a warp apply in program order, so the slots' atomics are independent
+    // instructions: no read-modify-write chain through the counters between slots)
+    uint32_t old[S2_IPT], low[S2_IPT];
+    int ldr[S2_IPT];
 #pragma unroll
     for (int j = 0; j < S2_IPT; j++) {
       const bool live = base + j * 32 + lane < n;
       const int d = live ? (int)((kk[j] >> shift) & 255) : 256 + lane;  // dead lanes: unique, not counted
       const unsigned peers = __match_any_sync(0xffffffffu, d);
-      const unsigned run = live ? wcnt[wid][d] : 0u;
-      rk[j] = run + __popc(peers & ((1u << lane) - 1u));
-      __syncwarp();
-      if (live && lane == __ffs(peers) - 1) wcnt[wid][d] = run + __popc(peers);
-      __syncwarp();
+      ldr[j] = __ffs(peers) - 1;
+      low[j] = __popc(peers & ((1u << lane) - 1u));
+      old[j] = 0;
+      if (live && lane == ldr[j]) old[j] = atomicAdd(&wcnt[wid][d], (uint32_t)__popc(peers));
     }
+#pragma unroll
+    for (int j = 0; j < S2_IPT; j++) rk[j] = __shfl_sync(0xffffffffu, old[j], ldr[j]) + low[j];
     __syncthreads();
     // per digit (threads 0..255): exclusive prefix over warps; digit totals -> scan over digits
     const int d0 = threadIdx.x;
@@ -375,18 +387,51 @@ __global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf 
         if (lane >= o) x += y;
       }
       if (lane == 31) wsum[wid] = x;
-      // decoupled look-back over the predecessors' statuses of this digit
-      uint32_t excl = 0;
-      for (int64_t tt = t - 1; tt >= 0; tt--) {
-        volatile const uint32_t* ps = status + (size_t)tt * 256 + d0;
-        uint32_t v;
+    }
+    // Decoupled look-back, S2_WARPS predecessors per step: warp w fetches all 256
+    // statuses of tile t - 1 - w - 16 step (one round trip to L2 for the whole step;
+    // a digit thread walking its predecessors one load at a time cost a round trip
+    // per tile looked at: a third of the kernel's stall samples), the digit threads
+    // then add up their columns in shared memory until one holds an inclusive prefix.
+    uint32_t excl = 0;
+    bool fin = d0 >= 256;
+    uint32_t* lb = (uint32_t*)sk;  // [S2_WARPS][256] (the reorder buffer is not in use yet)
+    for (int64_t first = t - 1;; first -= S2_WARPS) {
+      const int64_t tt = first - wid;
+      uint32_t v[8];
+      if (tt >= 0) {
+        volatile const uint32_t* ps = status + (size_t)tt * 256 + lane;
+        bool ready;
         do {
-          v = *ps;
-        } while ((v >> 30) == 0);
-        excl += v & OS_MASK;
-        if ((v >> 30) == 2) break;
+          ready = true;
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            v[q] = ps[q * 32];
+            ready &= (v[q] >> 30) != 0;
+          }
+        } while (!__all_sync(0xffffffffu, ready));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = OS_INCL;  // before the first tile: inclusive prefix 0
       }
-      *st = OS_INCL | (excl + acc);
+#pragma unroll
+      for (int q = 0; q < 8; q++) lb[wid * 256 + q * 32 + lane] = v[q];
+      __syncthreads();
+      if (!fin) {
+#pragma unroll 4
+        for (int w = 0; w < S2_WARPS; w++) {
+          const uint32_t u = lb[w * 256 + d0];
+          excl += u & OS_MASK;
+          if ((u >> 30) == 2) {
+            fin = true;
+            break;
+          }
+        }
+      }
+      if (__syncthreads_and(fin)) break;
+    }
+    if (d0 < 256) {
+      *(volatile uint32_t*)(status + (size_t)t * 256 + d0) = OS_INCL | (excl + acc);
       goff[d0] = gbase[d0] + excl;
     }
     __syncthreads();
@@ -410,6 +455,7 @@ __global__ void __launch_bounds__(S2_BLOCK, 2) k_onesweep2(SortBuf src, SortBuf 
       const uint64_t k = sk[q];
       const int d = (int)((k >> shift) & 255);
       const unsigned long long pos = goff[d] + (q - dbase[d]);
+      if (nowrite) continue;  // (experiment)
       dst.w[key_word][pos] = k;
       dst.w[other][pos] = sv[q];
     }
