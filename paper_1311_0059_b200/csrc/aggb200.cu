@@ -1292,12 +1292,10 @@ static const WcShape WC_SHAPES[] = {
     {512, 4, 3, k_scan_wc<512, 4, 3>, Wc2Layout<512, 4, 3>::bytes},
     {512, 4, 2, k_scan_wc<512, 4, 2>, Wc2Layout<512, 4, 2>::bytes},
     {512, 2, 4, k_scan_wc<512, 2, 4>, Wc2Layout<512, 2, 4>::bytes},
-    {992, 2, 3, k_scan_wc<992, 2, 3>, Wc2Layout<992, 2, 3>::bytes},
-    {768, 2, 4, k_scan_wc<768, 2, 4>, Wc2Layout<768, 2, 4>::bytes},
 };
 const WcShape& wc_shape() {
   const int i = getenv("AGGB_WC_SHAPE") ? atoi(getenv("AGGB_WC_SHAPE")) : 0;
-  return WC_SHAPES[std::max(0, std::min(4, i))];
+  return WC_SHAPES[std::max(0, std::min(2, i))];
 }
 void wc_plan(Handle* h, double spill_groups) {
   h->wc = false;
