@@ -7,9 +7,11 @@ the B200 through libaggb200 (include/aggb200.h); the algorithm id selects the
 GPU schedule:
 
 * pre_partitioning — fill the L2-resident table, freeze it at a kernel
-  boundary, probe (SMEM bloom first) and spill misses to HBM pages, recurse
-  (for one-word keys and an integer COUNT/SUM/MIN/MAX spec: the write-combined
-  k_probe_wc scan/resolve and the one-wave compact children, csrc/wc.cuh).
+  boundary, probe (SMEM bloom first) and spill misses to HBM pages, recurse.
+  For one-word keys, one int64 value and an integer COUNT/SUM/MIN/MAX spec:
+  after the freeze every record is routed into the run of its hash range
+  (k_scan_wc) and each run's compact child is seeded with the resident keys of
+  that range, whose aggregates it merges into the table (csrc/wc2.cuh).
 * original_hh — partition-0 table + raw spill of the other partitions,
   overflow cuts partition 0 into partial states (hybrid.py:431-451).
 * hash_sort — aggregate until full, cut the table to a run of partial states,

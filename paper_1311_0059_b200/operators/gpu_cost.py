@@ -37,11 +37,13 @@ class GpuCostParams:
     eff: dict = field(default_factory=lambda: {
         "probe": 0.24,       # k_probe / k_probe_w: read input, write spill (C2 0.23, C3 0.26, C5 0.30)
         "child": 0.22,       # SMEM children: read spill (C2 0.23, C5 0.22)
+        "scan_wc": 0.47,     # FILL + k_scan_wc (16-byte records, integer spec): C2 3.0 GB in 0.97 ms
+        "child_wc": 0.39,    # k_wc2_build + k_child2_wc: C2 1.43 GB in 0.56 ms
         "split": 0.55,       # k_split: one more grace level over the spill
         "route": 0.11,       # k_pass ROUTE (original_hh): C2 4.25 ms for 3.0 GB
         "fill_l2": 0.20,     # table pass over an L2-resident table
-        "radix": 0.40,       # one 8-bit LSD pass incl. its tile histogram
-        "segreduce": 0.22,   # head flags + compaction + reduction
+        "radix": 0.34,       # one 8-bit one-sweep pass (C4: 32 GB in 15.7 ms), the append into the sort buffers
+        "segreduce": 0.33,   # head counts + scan + the fused reduction (C4: 36 GB in 16.8 ms)
         "flush": 0.30,       # table compaction + finalize
     })
     rand_sector_ns: float = 0.095  # per random table sector beyond L2 (fit: C4 hash_sort FILL)
@@ -85,6 +87,8 @@ class Workload:
     key_bits: int = 64             # significant key bits (sort passes)
     spill_rec_bytes: int = 0       # raw spill record (0: rec_bytes; C5 rows 64 B -> 48 B)
     hot_share: float = 0.0         # share of records on heavy hitters (skew)
+    compact: bool = False          # one-word key, one int64 value, integer COUNT/SUM/MIN/MAX: the
+                                   # write-combined level 0 (k_scan_wc + k_child2_wc, csrc/wc2.cuh)
 
     @property
     def spill_bytes(self) -> int:
@@ -112,8 +116,8 @@ def model(algo: str, w: Workload, pm: GpuCostParams | None = None, child_groups:
         passes = max(1, math.ceil(w.key_bits / 8))
         r.add("radix", inp, 0, pm)                       # load into the sort buffers
         for _ in range(passes):
-            r.add("radix", inp + w.n * 8, inp, pm)
-        r.add("segreduce", inp, out, pm)
+            r.add("radix", inp, inp, pm)
+        r.add("segreduce", inp + w.n * 8, out, pm)
         return r
     if algo == "hash_sort" and budget >= w.groups:
         r.add("fill_l2", inp, 0, pm, _table_rand_ms(w, w.groups, pm))
@@ -149,6 +153,12 @@ def model(algo: str, w: Workload, pm: GpuCostParams | None = None, child_groups:
         return r
     spill = w.n * (1.0 - hit) * w.spill_bytes
     r.spill_bytes += spill
+    if algo == "pre_partitioning" and w.compact and w.budget_groups > 0:
+        # routing level 0 + seeded compact children (one wave pair, no split level);
+        # the fixed term is the launch gaps and the closing round trip of a step
+        r.add("scan_wc", inp, spill, pm)
+        r.add("child_wc", spill, out - resident * w.out_bytes, pm, 0.13)
+        return r
     r.add("route" if algo == "original_hh" else "probe", inp, spill, pm)
     if _spill_levels(w.groups - resident, child_groups, pm):
         r.add("split", 2 * spill, spill, pm)

@@ -1,7 +1,7 @@
 """Race stress (compute-sanitizer is closed on this pool, profiles/r02_notes.md):
 the kernels that publish shared-memory state between threads without a
-barrier in between (k_probe_wc's window word, ring and page maps; k_child_wc's
-CAS inserts and idempotent flags; the generic drain's page maps and spin-free
+barrier in between (k_scan_wc's window word, ring, page maps and producer /
+consumer flags; k_child2_wc's CAS inserts and idempotent flags; the generic drain's page maps and spin-free
 claims) run many times over varied seeds, budgets, fan-outs and push
 chunkings, and every run must equal the numpy oracle exactly (fp64 columns to
 1e-9).  A lost or torn record, a duplicated group or a stale page shows up as a

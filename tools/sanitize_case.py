@@ -1,6 +1,6 @@
 """Small cases for compute-sanitizer (racecheck / synccheck): C2-shaped
-pre_partitioning through the write-combined level 0 (k_probe_wc scan/resolve,
-k_child_wc) and through the generic drain (AGGB_NO_WC), C5-shaped wide rows,
+pre_partitioning through the write-combined level 0 (k_scan_wc,
+k_child2_wc) and through the generic drain (AGGB_NO_WC), C5-shaped wide rows,
 hash_sort cuts.  Checked against the numpy oracle so a race that corrupts
 results also fails here.
 
