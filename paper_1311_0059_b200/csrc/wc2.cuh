@@ -592,7 +592,8 @@ __device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) {
 // fits in 32 bits (keys are stored as u32: a bucket of 4 is one LDS.128 and four
 // 32-bit compares; the one key equal to the empty marker 0xFFFFFFFF lives in the
 // escape slot), WIDE = sums as u32 pairs with carry, EXT = the extended word
-// layout (wide sums and owner runs).
+// layout (wide sums and seeded runs), V64 = some value is beyond int32 (64-bit
+// MIN/MAX words, the sums take the value's high word).
 //   table: keys[nslots + 1] (u32 or u64; 4-slot buckets; escape slot last), then
 //          (nslots + 1) x W u32 state words
 // A record compares its key with the four keys of its bucket, the buckets of RL
@@ -608,7 +609,7 @@ struct CwShared {
   uint32_t wsum[32];
 };
 
-template <class CP, int BLK, int RL, bool K32, bool WIDE, bool EXT>
+template <class CP, int BLK, int RL, bool K32, bool WIDE, bool EXT, bool V64 = false>
 __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, unsigned char* smem, CwShared& sh,
                                           uint32_t seed32) {
   using CW = CwWords<CP>;
@@ -619,13 +620,17 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
   constexpr int KB = K32 ? 4 : 8;
   constexpr KT KEMPTY = K32 ? (KT)0xFFFFFFFFu : (KT)EMPTY;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nbk = (a.table_bytes / (KB + 4 * W) - 1) / 4;
+  // V64 (some value beyond int32): MIN / MAX live in 64-bit word arrays after the u32
+  // ones (native 64-bit shared-memory MIN/MAX atomics), sums take the value's high word
+  constexpr int MM64 = V64 ? CW::NMM : 0;
+  const int nbk = ((a.table_bytes - 64) / (KB + 4 * W + 8 * MM64) - 1) / 4;
   const int nslots = nbk * 4;
   const int maxg = (int)(0.85 * nslots);
   const int stride = nslots + 1;
   KT* skeys = (KT*)smem;                                                     // stride keys (escape slot last)
   uint32_t* sst = (uint32_t*)(smem + (((size_t)stride * KB + 15) & ~(size_t)15));  // stride x W state words
-  const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst);
+  unsigned long long* smm = (unsigned long long*)(((uintptr_t)(sst + (size_t)stride * W) + 15) & ~(uintptr_t)15);  // MM64 x stride
+  const uint32_t a_keys = smem_u32(skeys), a_st = smem_u32(sst), a_mm = smem_u32(smm);
   const uint32_t sbytes = 4u * (uint32_t)stride;  // bytes between a slot's consecutive words
   for (int i = tid; i < stride; i += BLK) {
     skeys[i] = KEMPTY;
@@ -635,10 +640,16 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
 #pragma unroll
       for (int w = CW::WB; w < CW::W_EXT; w++) sst[w * stride + i] = w == CW::W_ORG ? 0xFFFFFFFFu : 0u;
     }
+    if (V64) {
+#pragma unroll
+      for (int j = 0; j < N; j++)
+        if (CW::is_mm(j))
+          smm[CW::word(j) * stride + i] = (CP::fd(j) & 3) == OP_MIN ? 0x7FFFFFFFFFFFFFFFull : 0x8000000000000000ull;
+    }
   }
   if (tid == 0) {
     sh.groups = 0;
-    sh.fail = a.vinfo[0] != 0 || a.plist_n[p] > a.plist_cap;  // (values beyond int32; an overflowed page list)
+    sh.fail = a.plist_n[p] > a.plist_cap;  // (an overflowed page list is incomplete)
     sh.esc = 0;
     sh.next = 0;
   }
@@ -793,7 +804,7 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
 #pragma unroll
       for (int r = 0; r < RL; r++) {
         if (slot[r] < 0) continue;
-        const int cb = (int)(uint32_t)cur[r].y;  // an int32 (vinfo)
+        const int cb = (int)(uint32_t)cur[r].y;  // the value (V64: its low word)
         // (word arrays, not slot-major: a warp's updates of one field spread over all 32
         // banks; slot-major states put them on 8 and tripled the atomics' wavefronts)
         const uint32_t a_s = a_st + 4u * (uint32_t)slot[r];
@@ -806,11 +817,16 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
           if (CP::is_sum(j)) {
             if (WIDE) {  // 64-bit two's complement sum in (lo, hi) words
               const uint32_t o = atoms_add(a_w, (uint32_t)cb);
-              const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + (cb < 0 ? 0xFFFFFFFFu : 0u);
+              const uint32_t vhi = V64 ? (uint32_t)(cur[r].y >> 32) : (cb < 0 ? 0xFFFFFFFFu : 0u);
+              const uint32_t hi = (uint32_t)(o + (uint32_t)cb < o) + vhi;
               if (hi) reds_add(a_s + sbytes * (uint32_t)(CW::W_HI + CW::sum_rank(j)), hi);
             } else {
               reds_add(a_w, (uint32_t)cb);
             }
+          } else if (V64) {
+            const uint32_t a_q = a_mm + 8u * (uint32_t)(CW::word(j) * stride + slot[r]);
+            if ((F & 3) == OP_MIN) asm volatile("red.shared.min.s64 [%0], %1;" ::"r"(a_q), "l"((long long)cur[r].y) : "memory");
+            else asm volatile("red.shared.max.s64 [%0], %1;" ::"r"(a_q), "l"((long long)cur[r].y) : "memory");
           } else if ((F & 3) == OP_MIN) {
             reds_min_s32(a_w, cb);
           } else {
@@ -838,6 +854,7 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
       const uint32_t lo = w[CW::word(j) * stride];
       return WIDE ? ((uint64_t)w[(CW::W_HI + CW::sum_rank(j)) * stride] << 32 | lo) : (uint64_t)(long long)(int)lo;
     }
+    if (V64) return (uint64_t)smm[CW::word(j) * stride + s];
     return (uint64_t)(long long)(int)w[CW::word(j) * stride];
   };
   // rows this run emits: its groups, minus the seeded (resident) ones of an owner run
@@ -942,7 +959,10 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
     const bool owner = true;  // every run answers for the resident keys of its hash range
     // wide sums (a u32 pair with carry) only when a run's sum can leave int32
     const bool wide = CP::nsum() > 0 && (double)np * (double)vabs >= 2147483647.0;
-    if (k32) {
+    if (a.vinfo[0]) {  // some value beyond int32: 64-bit MIN/MAX words, sums with the value's high word
+      if (k32) child_run<CP, BLK, RL, true, true, true, true>(a, p, owner, smem, sh, seed32);
+      else child_run<CP, BLK, RL, false, true, true, true>(a, p, owner, smem, sh, seed32);
+    } else if (k32) {
       if (wide) child_run<CP, BLK, RL, true, true, true>(a, p, owner, smem, sh, seed32);
       else if (owner) child_run<CP, BLK, RL, true, false, true>(a, p, owner, smem, sh, seed32);
       else child_run<CP, BLK, RL, true, false, false>(a, p, owner, smem, sh, seed32);

@@ -3,8 +3,8 @@ a spill partition or an owner run, k_child2_wc aggregates each run and merges
 the owner runs' resident groups into the level-0 table) against the numpy
 oracle, on the inputs that take its rare paths:
 
-* runs that do not fit their child (tiny child tables, values beyond int32,
-  under-estimated cardinality): owner runs are gathered and re-probed by the
+* runs that do not fit their child (tiny child tables, under-estimated
+  cardinality): owner runs are gathered and re-probed by the
   generic PROBE, spill partitions go to the generic recursion;
 * bursts (sorted input: a tile's records all claim one run, far past its ring
   window: held and parked records), chunked pushes (one chain of pages per CTA,
@@ -80,12 +80,20 @@ def test_wc_tiny_child_tables_fall_back(monkeypatch):
     assert 0 < met["spilled_records"] < 400_000
 
 
-def test_wc_values_beyond_int32_fall_back():
+@pytest.mark.parametrize("aggs", [C2, ("count", "sum")])
+def test_wc_values_beyond_int32(aggs):
+    """Values beyond int32 take the children's 64-bit words (MIN/MAX as native 64-bit
+    shared-memory atomics, sums with the value's high word), not the fallback."""
     rng = np.random.default_rng(4)
     keys = rng.integers(0, 20_000, 300_000).astype(np.int64)
     vals = rng.integers(-(1 << 45), 1 << 45, 300_000).astype(np.int64)
-    met, ks = _run(keys, vals, C2, 2_500)
-    assert "k_scan_wc" in ks and "k_child" in ks
+    met, ks = _run(keys, vals, aggs, 2_500)
+    assert "k_scan_wc" in ks and "k_child" not in ks
+    # the extremes, and 64-bit keys beside them
+    vals[:8] = [np.iinfo(np.int64).max, np.iinfo(np.int64).min, -1, 0, 1 << 31, -(1 << 31) - 1, (1 << 32) + 5, 7]
+    vals[8:16] = vals[:8][::-1]
+    keys = keys * 6_000_000_007 - 17
+    _run(keys, vals, aggs, 2_500)
 
 
 def test_wc_underestimated_cardinality():
