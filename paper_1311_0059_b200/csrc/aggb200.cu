@@ -1500,7 +1500,8 @@ bool wc_eligible(Handle* h, const ColSrc& col) {
 
 // the runs' lists of resident slots (the frozen table's keys by routing hash)
 int wc_build(Handle* h) {
-  const uint64_t seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+  const uint64_t seed64 = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+  const uint32_t seed = (uint32_t)seed64 ^ (uint32_t)(seed64 >> 32);
   // a list holds twice a run's share of the budget (small budgets: all of it)
   const uint64_t cap = h->tab.cap;
   h->wc_ocap = (uint32_t)std::min<uint64_t>(cap + 1, 2 * cap / (uint64_t)h->P0 + 1024);
@@ -1555,7 +1556,10 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   Wc2Args a;
   memset(&a, 0, sizeof(a));
   a.t = h->tab;
-  a.seed = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+  {
+    const uint64_t seed64 = level_seed(h->cfg.seed, SALT_PART, h->cfg.level);
+    a.seed = (uint32_t)seed64 ^ (uint32_t)(seed64 >> 32);
+  }
   a.key = (const unsigned long long*)col.key[0];
   a.val = (const unsigned long long*)col.val[0];
   a.n = col.n;

@@ -34,17 +34,29 @@
 
 namespace aggb {
 
-// the routing hash: run = top bits of the hash's high word
-__device__ __forceinline__ uint64_t wc2_hash(uint64_t k, uint64_t seed) { return fmix64(k ^ seed); }
-__device__ __forceinline__ uint32_t wc2_run(uint64_t h, uint32_t NP) { return __umulhi((uint32_t)(h >> 32), NP); }
+__device__ __forceinline__ uint32_t fmix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85ebca6bu;
+  x ^= x >> 13;
+  x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+// 32-bit hash of a one-word key (the high word folded in by an odd multiply); the
+// routing hash and the children's slot hash are this function under different seeds
+__device__ __forceinline__ uint32_t hash32(uint64_t k, uint32_t seed) {
+  return fmix32((uint32_t)k ^ seed ^ ((uint32_t)(k >> 32) * 0x9E3779B1u));
+}
+// the routing hash: run = top bits (9 instructions; the 64-bit fmix was 16 per record)
+__device__ __forceinline__ uint32_t wc2_run(uint64_t k, uint32_t seed, uint32_t NP) { return __umulhi(hash32(k, seed), NP); }
 
 // the runs' lists of resident slots: one pass over the frozen table's key array
-__global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* olist, uint32_t* olist_n, uint32_t ocap, uint32_t NP) {
+__global__ void k_wc2_build(GTable t, uint32_t seed, uint32_t* olist, uint32_t* olist_n, uint32_t ocap, uint32_t NP) {
   const uint64_t n = t.mask + 1;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = t.keys[i];
     if (k == EMPTY) continue;
-    const uint32_t o = wc2_run(wc2_hash(k, seed), NP);
+    const uint32_t o = wc2_run(k, seed, NP);
     const uint32_t at = atomicAdd(&olist_n[o], 1u);
     if (at < ocap) olist[(size_t)o * ocap + at] = (uint32_t)i;
   }
@@ -52,7 +64,7 @@ __global__ void k_wc2_build(GTable t, uint64_t seed, uint32_t* olist, uint32_t* 
 
 struct Wc2Args {
   GTable t;                               // the frozen level-0 table (header only)
-  uint64_t seed;                          // wc2_hash seed
+  uint32_t seed;                          // routing hash seed
   const unsigned long long* key;          // dense 8-byte key column (16-byte aligned)
   const unsigned long long* val;          // dense 8-byte value column (16-byte aligned)
   int64_t n;                              // records in the columns
@@ -87,7 +99,7 @@ struct Wc2Layout {
   static __host__ __device__ size_t stage_bytes() { return (size_t)NS * 2 * T * 8; }
   static __host__ __device__ size_t ring_bytes(int NP) { return (size_t)NP * RS * 16; }
   static __host__ __device__ size_t meta_bytes(int NP) { return ((size_t)NP * (3 + NE) * 4 + 15) & ~(size_t)15; }
-  static __host__ __device__ size_t send_bytes() { return (size_t)(BLK / 32) * 32 * 8; }  // per warp: 32 lines to send
+  static __host__ __device__ size_t send_bytes() { return (size_t)(BLK / 32) * 32 * 16; }  // per warp: 32 lines to send
   static __host__ __device__ size_t bytes(int NP) { return stage_bytes() + ring_bytes(NP) + meta_bytes(NP) + send_bytes(); }
 };
 
@@ -125,7 +137,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
   uint32_t* ent = cw + NP;
   uint32_t* lbase = ent + NP * NE;  // this CTA's block of the run's page list ...
   uint32_t* lused = lbase + NP;     // ... and the entries of it in use
-  uint2* sendq = (uint2*)((unsigned char*)cw + L::meta_bytes(NP));  // per warp: (ring address, page << 6 | line) of the lines to send
+  uint4* sendq = (uint4*)((unsigned char*)cw + L::meta_bytes(NP));  // per warp: (ring address, -, destination) of the lines to send
   const uint32_t a_stg = smem_u32(smem), a_ring = smem_u32(ring), a_cw = smem_u32(cw);
   __shared__ __align__(8) uint64_t mbar[NS];    // stage full (the tile's bytes have landed)
   __shared__ __align__(8) uint64_t mbar_e[NS];  // stage empty (every consumer is past barrier 2 of its tile)
@@ -209,7 +221,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
     if (tid == BLK) {
       for (int it = 0; it < ntiles + 1; it++) {
         const int s = it % NS;
-        if (it >= NS) mbar_wait(&mbar_e[s], (uint32_t)((it / NS - 1) & 1));
+        if (it >= NS) mbar_wait(&mbar_e[s], (uint32_t)((it / NS - 1) & 1));  // (try_wait suspends the thread)
         issue(s);
         if (a.stash && *(volatile uint32_t*)&s_want && !*(volatile uint32_t*)&s_nv) {
           const uint32_t nb = atomicAdd(a.pool.next_page, (uint32_t)a.stash);
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       }
 #pragma unroll
       for (int r = 0; r < R; r++) {
-        pid[r] = (int)wc2_run(wc2_hash(k[r], a.seed), (uint32_t)NP);
+        pid[r] = (int)wc2_run(k[r], a.seed, (uint32_t)NP);
         const uint64_t m = v[r] ^ (uint64_t)((long long)v[r] >> 63);
         vm |= FULL ? m : (((vm_ >> r) & 1u) ? m : 0ull);
         km |= FULL ? (uint32_t)(k[r] >> 32) : (((vm_ >> r) & 1u) ? (uint32_t)(k[r] >> 32) : 0u);
@@ -391,27 +403,34 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
           if (nl) cw[p] = (ln << 23) | cc;
         }
         const uint32_t ns = nl < (uint32_t)LINES ? nl : (uint32_t)LINES;
-        uint2* wq = sendq + 32 * wid;
+        uint4* wq = sendq + 32 * wid;
+        const uint32_t a_wq = smem_u32(wq);
 #pragma unroll
         for (int round = 0; round < LINES; round++) {
           const bool has = ns > (uint32_t)round;
           const uint32_t mask = __ballot_sync(0xffffffffu, has);
           if (!mask) break;
-          if (has) {  // the lane's line into the warp's list
+          if (has) {  // the lane's line into the warp's list: where it is and where it goes
             const uint32_t x0 = (ln - nl + (uint32_t)round) << 3;
             const uint32_t pg = page_of(p, x0 >> SLOG);
+            const unsigned long long dst = pg < 0xFFFFFFu ? (unsigned long long)rec_ptr(pg, x0) : 0ull;
             wq[__popc(mask & ((1u << lane) - 1u))] =
-                make_uint2(a_ring + 16u * ((uint32_t)p * RS + (x0 & (RING - 1))), (pg << 6) | ((x0 >> 3) & 63u));
+                make_uint4(a_ring + 16u * ((uint32_t)p * RS + (x0 & (RING - 1))), 0u, (uint32_t)dst, (uint32_t)(dst >> 32));
           }
           __syncwarp();
           const int n = __popc(mask);
-          for (int i = grp; i < n; i += 4) {  // lane group g copies lines g, g + 4, ...
-            const uint2 e = wq[i];
-            if ((e.y >> 6) < 0xFFFFFFu && !a.nosend) {
+          // lane group g copies lines g, g + 4, ...: 8 lanes x 16 bytes per line
+#pragma unroll 2
+          for (int i = grp; i < n; i += 4) {
+            uint32_t src, pad;
+            unsigned long long dst;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%3];\n\tld.shared.u64 %2, [%3 + 8];"
+                         : "=r"(src), "=r"(pad), "=l"(dst)
+                         : "r"(a_wq + 16u * (uint32_t)i));
+            if (dst && !a.nosend) {
               uint64_t x, y;
-              lds128(e.x + 16u * (uint32_t)sub, x, y);
-              st_v2(pool + ((size_t)(e.y >> 6) << (SLOG + 1)) + ((size_t)(e.y & 63u) << 4) + 2u * (uint32_t)sub,
-                    make_ulonglong2(x, y));
+              lds128(src + 16u * (uint32_t)sub, x, y);
+              st_v2((void*)(dst + 16u * (uint32_t)sub), make_ulonglong2(x, y));
             }
           }
           __syncwarp();
@@ -575,18 +594,8 @@ struct CwWords {
   }
 };
 
-__device__ __forceinline__ uint32_t fmix32(uint32_t x) {
-  x ^= x >> 16;
-  x *= 0x85ebca6bu;
-  x ^= x >> 13;
-  x *= 0xc2b2ae35u;
-  x ^= x >> 16;
-  return x;
-}
-// slot hash of a child table (independent of the level-0 routing hash)
-__device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) {
-  return fmix32((uint32_t)k ^ seed ^ ((uint32_t)(k >> 32) * 0x9E3779B1u));
-}
+// slot hash of a child table (independent of the level-0 routing hash: another seed)
+__device__ __forceinline__ uint32_t cw_hash(uint64_t k, uint32_t seed) { return hash32(k, seed); }
 
 // One run through a child table.  Template flags: K32 = every key the scan saw
 // fits in 32 bits (keys are stored as u32: a bucket of 4 is one LDS.128 and four
