@@ -158,16 +158,16 @@ __device__ __forceinline__ void supdate(uint64_t* p, uint8_t op, uint8_t ty, uin
     }
     return;
   }
-  bool smaller_wins = (op == OP_MIN);
-  unsigned long long cur = *(volatile unsigned long long*)p;
-  for (;;) {
-    bool better;
-    if (ty == TY_I64) better = smaller_wins ? ((long long)c < (long long)cur) : ((long long)c > (long long)cur);
-    else better = smaller_wins ? (c < cur) : (c > cur);
-    if (!better) return;
-    unsigned long long prev = atomicCAS((unsigned long long*)p, cur, (unsigned long long)c);
-    if (prev == cur) return;
-    cur = prev;
+  // native 64-bit shared-memory MIN / MAX (ATOMS.MIN/MAX.64), fire-and-forget: no read
+  // of the state before the update (the read-then-CAS loop made every record wait for
+  // a shared-memory round trip per MIN/MAX field)
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  if (op == OP_MIN) {
+    if (ty == TY_I64) asm volatile("red.shared.min.s64 [%0], %1;" ::"r"(a), "l"((long long)c) : "memory");
+    else asm volatile("red.shared.min.u64 [%0], %1;" ::"r"(a), "l"(c) : "memory");
+  } else {
+    if (ty == TY_I64) asm volatile("red.shared.max.s64 [%0], %1;" ::"r"(a), "l"((long long)c) : "memory");
+    else asm volatile("red.shared.max.u64 [%0], %1;" ::"r"(a), "l"(c) : "memory");
   }
 }
 
