@@ -649,10 +649,11 @@ struct Handle {
   uint32_t wc_plist_cap = 0;  // page-list entries per partition
   int64_t wc_fallbacks = 0;   // finishes that needed drain for some partition (tests)
   uint32_t wc_ocap = 0;       // resident slots per owner list
+  size_t wc_scan_smem = 0;    // dynamic shared memory k_scan_wc was last configured for
+  bool wc_child_attr = false; // k_child2_wc's shared-memory attribute is set
   int64_t wc_launches = 0;    // k_scan_wc launches of this run
   int64_t wc_entries = 0;     // page-list entries per run the launches so far may have taken
-  bool wc_plist_clean = false;  // every entry of the page lists is 0xFFFFFFFF (unused) or belongs to this run
-  DBuf wc_plist, wc_pn, wc_recs, wc_vinfo, wc_failed, wc_fail, wc_olist, wc_olist_n, wc_gather;
+  DBuf wc_plist, wc_meta, wc_olist, wc_olist_n, wc_gather;  // wc_meta: per-run records / page counts / failed flags, value info, fail word (one memset per run)
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
   DBuf sort_keys, sort_vals;
@@ -673,6 +674,14 @@ struct Handle {
   double kms[24] = {0};
   int64_t kcount[24] = {0};
 };
+
+// views into Handle::wc_meta ([NP] u64 records | [NP] u32 pages | [NP] u32 failed | 4 u32 value info | 2 u32 fail)
+inline size_t wc_meta_bytes(int NP) { return (size_t)NP * 16 + 32; }
+inline unsigned long long* wc_recs(Handle* h) { return h->wc_meta.as<unsigned long long>(); }
+inline uint32_t* wc_pn(Handle* h) { return (uint32_t*)(wc_recs(h) + h->P0); }
+inline uint32_t* wc_failed(Handle* h) { return wc_pn(h) + h->P0; }
+inline unsigned int* wc_vinfo(Handle* h) { return wc_failed(h) + h->P0; }
+inline uint32_t* wc_fail(Handle* h) { return wc_vinfo(h) + 4; }
 
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
@@ -1411,19 +1420,10 @@ int begin_run(Handle* h) {
   h->wc_used = false;
   h->wc_launches = 0;
   h->wc_entries = 0;
-  h->wc_plist_clean = false;
   if (h->wc) {
     const size_t NP = (size_t)h->P0;
-    TRY(h->wc_pn.ensure(NP * 4, &h->hw));
-    TRY(h->wc_recs.ensure(NP * 8, &h->hw));
-    TRY(h->wc_failed.ensure(NP * 4, &h->hw));
-    TRY(h->wc_vinfo.ensure(16, &h->hw));
-    TRY(h->wc_fail.ensure(8, &h->hw));
-    CU(cudaMemsetAsync(h->wc_pn.p, 0, NP * 4, h->st));
-    CU(cudaMemsetAsync(h->wc_recs.p, 0, NP * 8, h->st));
-    CU(cudaMemsetAsync(h->wc_failed.p, 0, NP * 4, h->st));
-    CU(cudaMemsetAsync(h->wc_vinfo.p, 0, 16, h->st));
-    CU(cudaMemsetAsync(h->wc_fail.p, 0, 8, h->st));
+    TRY(h->wc_meta.ensure(wc_meta_bytes((int)NP), &h->hw));
+    CU(cudaMemsetAsync(h->wc_meta.p, 0, wc_meta_bytes((int)NP), h->st));
   }
   return AGGB_OK;
 }
@@ -1544,10 +1544,6 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
     h->wc_plist = nb;
     nb.p = nullptr;
     h->wc_plist_cap = new_cap;
-    h->wc_plist_clean = true;
-  } else if (!h->wc_plist_clean) {  // a new run over the old lists: every entry unused again
-    CU(cudaMemsetAsync(h->wc_plist.p, 0xFF, (size_t)NP * h->wc_plist_cap * 4, h->st));
-    h->wc_plist_clean = true;
   }
   // pages: the records, plus each (CTA, run) chain's last page, plus stashes
   const int stash = 32;
@@ -1577,18 +1573,21 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.set_id = ss.id;
   a.NP = NP;
   a.plist = h->wc_plist.as<uint32_t>();
-  a.plist_n = h->wc_pn.as<uint32_t>();
+  a.plist_n = wc_pn(h);
   a.plist_cap = h->wc_plist_cap;
   a.plist_blk = blk;
-  a.part_recs = h->wc_recs.as<unsigned long long>();
+  a.part_recs = wc_recs(h);
   a.stats = SC(h);
-  a.vinfo = h->wc_vinfo.as<unsigned int>();
-  a.fail = h->wc_fail.as<uint32_t>();
+  a.vinfo = wc_vinfo(h);
+  a.fail = wc_fail(h);
   a.stash = stash;
   a.nosend = getenv("AGGB_WC_NOSEND") ? 1 : 0;  // (experiment: lines are not written; results are wrong)
   auto fs = shp.fn;
   const size_t smem = shp.bytes(NP);
-  CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (h->wc_scan_smem != smem) {  // (once per handle: the call costs host time on every step)
+    CU(cudaFuncSetAttribute((const void*)fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    h->wc_scan_smem = smem;
+  }
   int pe = prof_begin(h, 15);
   fs<<<grid, shp.blk + 32, smem, h->st>>>(a);  // + the producer warp
   prof_end(h, pe);
@@ -2329,7 +2328,7 @@ void aggb_destroy(void* handle) {
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
                   &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains,
-                  &h->wc_plist, &h->wc_pn, &h->wc_recs, &h->wc_vinfo, &h->wc_failed, &h->wc_fail, &h->wc_olist,
+                  &h->wc_plist, &h->wc_meta, &h->wc_olist,
                   &h->wc_olist_n, &h->wc_gather, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
   h->pool_base.release();
@@ -2736,25 +2735,28 @@ int wc_children(Handle* h) {
   ca.sp = h->cs.ds;
   ca.pool = pool_of(h);
   ca.plist = h->wc_plist.as<uint32_t>();
-  ca.plist_n = h->wc_pn.as<uint32_t>();
+  ca.plist_n = wc_pn(h);
   ca.plist_cap = h->wc_plist_cap;
-  ca.part_recs = h->wc_recs.as<unsigned long long>();
-  ca.vinfo = h->wc_vinfo.as<unsigned int>();
+  ca.part_recs = wc_recs(h);
+  ca.vinfo = wc_vinfo(h);
   ca.NP = h->P0;
   ca.table_bytes = h->wc_table_bytes;
   if (getenv("AGGB_WC_CHILD_KB"))  // test hook: small child tables send runs to the fallback
     ca.table_bytes = std::max(1, std::min(h->wc_table_bytes / 1024, atoi(getenv("AGGB_WC_CHILD_KB")))) * 1024;
   ca.seed = level_seed(h->cfg.seed, SALT_SLOT, h->cfg.level + 1);
   ca.out = outbuf(h, h->cfg.emit_partials ? 1 : 0);
-  ca.failed = h->wc_failed.as<uint32_t>();
-  ca.fail = h->wc_fail.as<uint32_t>();
+  ca.failed = wc_failed(h);
+  ca.fail = wc_fail(h);
   ca.stats = SC(h);
   ca.t = h->tab;
   ca.olist = h->wc_olist.as<uint32_t>();
   ca.olist_n = h->wc_olist_n.as<uint32_t>();
   ca.ocap = h->wc_ocap;
   auto fc = h->prog == 2 ? k_child2_wc<CpC2, WC_CBLK, WC_CRL> : k_child2_wc<CpC1, WC_CBLK, WC_CRL>;
-  CU(cudaFuncSetAttribute((const void*)fc, cudaFuncAttributeMaxDynamicSharedMemorySize, h->wc_table_bytes));
+  if (!h->wc_child_attr) {
+    CU(cudaFuncSetAttribute((const void*)fc, cudaFuncAttributeMaxDynamicSharedMemorySize, h->wc_table_bytes));
+    h->wc_child_attr = true;
+  }
   int pe = prof_begin(h, 17);
   fc<<<std::min(h->sms, ca.NP), WC_CBLK, h->wc_table_bytes, h->st>>>(ca);
   prof_end(h, pe);
@@ -2779,9 +2781,9 @@ int wc_fallback(Handle* h) {
   const int NP = h->P0;
   std::vector<uint32_t> failed((size_t)NP), pn((size_t)NP);
   std::vector<unsigned long long> recs((size_t)NP);
-  CU(cudaMemcpyAsync(failed.data(), h->wc_failed.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
-  CU(cudaMemcpyAsync(pn.data(), h->wc_pn.p, (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
-  CU(cudaMemcpyAsync(recs.data(), h->wc_recs.p, (size_t)NP * 8, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(failed.data(), wc_failed(h), (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(pn.data(), wc_pn(h), (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
+  CU(cudaMemcpyAsync(recs.data(), wc_recs(h), (size_t)NP * 8, cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
   // the table's rows are rewritten below: back to the row count before its flush
   CU(cudaMemcpyAsync(SC(h) + 13, SC(h) + 30, 8, cudaMemcpyDeviceToDevice, h->st));
@@ -2827,7 +2829,7 @@ int wc_fallback(Handle* h) {
   OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
   TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
   k_wc2_retire<<<std::max(1, std::min(NP, h->sms * 4)), 256, 0, h->st>>>(
-      h->wc_plist.as<uint32_t>(), h->wc_pn.as<uint32_t>(), h->wc_plist_cap, NP, h->page_set.as<int32_t>());
+      h->wc_plist.as<uint32_t>(), wc_pn(h), h->wc_plist_cap, NP, h->page_set.as<int32_t>());
   CU(cudaGetLastError());
   h->launches++;
   h->tail_valid = false;
@@ -2947,7 +2949,7 @@ int aggb_finish(void* handle, aggb_result* out) {
       CU(cudaMemcpyAsync(st, SC(h), sizeof(st), cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(&ovfl, h->pool_ctr.as<uint32_t>() + 1, 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaMemcpyAsync(l0, SC(h) + 14, 16, cudaMemcpyDeviceToHost, h->st));
-      if (h->wc_used) CU(cudaMemcpyAsync(&wcf, h->wc_fail.p, 4, cudaMemcpyDeviceToHost, h->st));
+      if (h->wc_used) CU(cudaMemcpyAsync(&wcf, wc_fail(h), 4, cudaMemcpyDeviceToHost, h->st));
       CU(cudaStreamSynchronize(h->st));
       if (wcf & 2u) return fail(AGGB_CUDA_ERROR, "k_scan_wc: page map inconsistency (internal error)");
       if (h->wc_used) {

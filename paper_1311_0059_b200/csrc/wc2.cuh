@@ -452,6 +452,11 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
     if (pg < 0xFFFFFFu) a.pool.page_fill[pg] = (int32_t)(((cc - 1) & (S - 1)) + 1);
     atomicAdd(&a.part_recs[p], (unsigned long long)cc);
   }
+  // the entries of this CTA's page-list blocks it did not need are marked unused (every
+  // entry below a run's count is then written by this run: the lists need no clearing)
+  for (int p = tid; p < NP; p += BLK)
+    for (uint32_t u = lused[p]; u < a.plist_blk; u++)
+      if (lbase[p] + u < a.plist_cap) a.plist[(size_t)p * a.plist_cap + lbase[p] + u] = 0xFFFFFFFFu;
   if (tid == 0) {
     // unused stash pages leave the set (the producer is done: no refill in flight)
     while (!*(volatile uint32_t*)&s_pdone) {
