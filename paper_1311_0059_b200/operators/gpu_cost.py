@@ -37,12 +37,12 @@ class GpuCostParams:
     eff: dict = field(default_factory=lambda: {
         "probe": 0.24,       # k_probe / k_probe_w: read input, write spill (C2 0.23, C3 0.26, C5 0.30)
         "child": 0.22,       # SMEM children: read spill (C2 0.23, C5 0.22)
-        "scan_wc": 0.47,     # FILL + k_scan_wc (16-byte records, integer spec): C2 3.0 GB in 0.97 ms
+        "scan_wc": 0.52,     # FILL + k_scan_wc (16-byte records, integer spec): C2 3.0 GB in 0.87 ms
         "child_wc": 0.39,    # k_wc2_build + k_child2_wc: C2 1.43 GB in 0.56 ms
         "split": 0.55,       # k_split: one more grace level over the spill
         "route": 0.11,       # k_pass ROUTE (original_hh): C2 4.25 ms for 3.0 GB
         "fill_l2": 0.20,     # table pass over an L2-resident table
-        "radix": 0.34,       # one 8-bit one-sweep pass (C4: 32 GB in 15.7 ms), the append into the sort buffers
+        "radix": 0.40,       # one 8-bit one-sweep pass (C4: 32 GB in 12.3 ms), the append into the sort buffers
         "segreduce": 0.33,   # head counts + scan + the fused reduction (C4: 36 GB in 16.8 ms)
         "flush": 0.30,       # table compaction + finalize
     })

@@ -101,13 +101,13 @@ def test_choose_exchange_rule():
 # measured on B200 (profiles/r02_all_configs_full.jsonl; C3 and C5 unchanged since r01), ms
 _MEASURED = {
     "C2": (dict(n=1e8, groups=1e6, rec_bytes=16, state_bytes=40, out_bytes=40, budget_groups=125000,
-                key_bits=20, compact=True), {"pre_partitioning": 1.69, "original_hh": 5.64, "shared_hash": 10.3,
+                key_bits=20, compact=True), {"pre_partitioning": 1.61, "original_hh": 5.64, "shared_hash": 10.3,
                                              "dynamic_destaging": 16.1}),
     "C3s05": (dict(n=2e8, groups=1e7, state_bytes=24, out_bytes=32, key_bits=24),
               {"pre_partitioning": 9.09, "hash_sort": 26.7}),
     "C3s1": (dict(n=2e8, groups=8.9e6, state_bytes=24, out_bytes=32, key_bits=24, hot_share=0.16),
              {"pre_partitioning": 8.46, "hash_sort": 15.8}),
-    "C4": (dict(n=1e9, groups=5e8, key_bits=30), {"sort_based": 81.8, "hash_sort": 356.6,
+    "C4": (dict(n=1e9, groups=5e8, key_bits=30), {"sort_based": 68.4, "hash_sort": 356.6,
                                                   "pre_partitioning": 104.7}),
     "C5": (dict(n=5e8, groups=4194304, rec_bytes=64, state_bytes=120, out_bytes=144, budget_groups=83886,
                 key_bits=44, spill_rec_bytes=48), {"pre_partitioning": 58.7, "hash_sort": 914.0}),
