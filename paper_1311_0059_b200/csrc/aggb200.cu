@@ -23,6 +23,7 @@
 #include "pass.cuh"
 #include "probe.cuh"
 #include "sort.cuh"
+#include "cuts.cuh"
 #include "wc2.cuh"
 
 using namespace aggb;
@@ -653,6 +654,7 @@ struct Handle {
   bool wc_child_attr = false; // k_child2_wc's shared-memory attribute is set
   int64_t wc_launches = 0;    // k_scan_wc launches of this run
   int64_t wc_entries = 0;     // page-list entries per run the launches so far may have taken
+  DBuf cut_bar;  // grid barrier of k_blind_cuts
   DBuf wc_plist, wc_meta, wc_olist, wc_olist_n, wc_gather;  // wc_meta: per-run records / page counts / failed flags, value info, fail word (one memset per run)
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
@@ -686,8 +688,8 @@ inline uint32_t* wc_fail(Handle* h) { return wc_vinfo(h) + 4; }
 const char* KNAMES[] = {"k_pass<FILL>", "k_pass<PROBE>", "k_pass<ROUTE>", "k_pass<GRACE>", "k_child",
                         "k_flush_table", "k_table_init", "k_page_bucket", "k_key_egress", "k_sort",
                         "k_exchange_pack", "k_segreduce", "k_bloom_build", "k_pass<PROBE:resolve>", "k_split",
-                        "k_scan_wc", "k_wc_build", "k_child_wc"};
-constexpr int NKINDS = 18;
+                        "k_scan_wc", "k_wc_build", "k_child_wc", "k_blind_cuts"};
+constexpr int NKINDS = 19;
 
 int prof_begin(Handle* h, int kid) {
   if (!h->prof) return -1;
@@ -1744,6 +1746,64 @@ int hash_sort_blind(Handle* h, const ColSrc& rest) {
   CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
   CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
   const uint64_t cap0 = h->tab.cap;
+  // the cut loop on the device (cuts.cuh): one persistent launch per K chunks, then their GRACE pass
+  typedef void (*cut_fn)(CutArgs);
+  cut_fn cf = nullptr;
+  {
+    const int nwt = nwt_for(std::max(1, rest.nv));
+    if (h->kw == 1 && nwt == 1) cf = k_blind_cuts<1, 1, PD>;
+    else if (h->kw == 1 && nwt == 2) cf = k_blind_cuts<1, 2, PD>;
+    else if (h->kw == 1 && nwt == 4) cf = k_blind_cuts<1, 4, PD>;
+    else if (h->kw == 2 && nwt == 1) cf = k_blind_cuts<2, 1, PD>;
+    else if (h->kw == 2 && nwt == 2) cf = k_blind_cuts<2, 2, PD>;
+    else if (h->kw == 2 && nwt == 4) cf = h->prog == 5 ? k_blind_cuts<2, 4, ProgC5> : k_blind_cuts<2, 4, PD>;
+    if (getenv("AGGB_NO_FUSED_CUTS")) cf = nullptr;
+  }
+  int occ = 0, coop = 0;
+  if (cf) {
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+    if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cf, CUT_BLK, 0) != cudaSuccess || occ < 1) cf = nullptr;
+  }
+  if (cf) {
+    TRY(h->cut_bar.ensure(64, &h->hw));
+    CU(cudaMemsetAsync(h->cut_bar.p, 0, 64, h->st));
+    const int grid = h->sms;  // (more CTAs only make the grid barrier dearer: 4 x 256 threads per SM 382 ms, 1 x 256 287 ms on C5)
+    const int64_t nch = (rest.n + c - 1) / c;
+    int rc = AGGB_OK;
+    for (int64_t k0 = 0; k0 < nch && rc == AGGB_OK; k0 += K) {
+      CutArgs ca;
+      memset(&ca, 0, sizeof(ca));
+      ca.t = h->tab;
+      ca.sp = h->cs.ds;
+      ca.col = rest;
+      ca.first = k0 * c;
+      ca.chunk = c;
+      ca.nchunks = std::min<int64_t>(K, nch - k0);
+      ca.o = o;
+      ca.bar = h->cut_bar.as<unsigned>();
+      ca.stats = SC(h);
+      void* args[] = {&ca};
+      int pe = prof_begin(h, 18);
+      CU(cudaLaunchCooperativeKernel((const void*)cf, dim3(grid), dim3(CUT_BLK), args, 0, h->st));
+      prof_end(h, pe);
+      h->launches++;
+      h->hash_sort_runs += ca.nchunks;
+      PassPlan g;
+      g.mode = MODE_GRACE;
+      g.lin = h->cut_tmp.as<uint64_t>();
+      g.lin_stride = acc_cap;
+      g.lin_count = SC(h) + 11;
+      g.lin_kind = 1;
+      g.lin_words = h->cs.ds.ns;
+      g.ss = h->part0.ss;
+      g.counter = SC(h) + 9;
+      if ((rc = launch_pass(h, g))) break;
+      CU(cudaMemsetAsync(SC(h) + 11, 0, 8, h->st));
+      h->part0_live = true;
+    }
+    CU(cudaMemsetAsync(h->tab.hdr, 0, sizeof(TableHdr), h->st));
+    return rc;
+  }
   h->tab.cap = (h->tab.mask + 1) * 3 / 4;  // no refusals: the chunk bounds the keys
   int rc = AGGB_OK;
   int64_t in_acc = 0;
@@ -2299,7 +2359,7 @@ int aggb_profile(void* handle, int enable) {
   if (!h) return fail(AGGB_INVALID_ARG, "null handle");
   prof_collect(h);
   h->prof = enable != 0;
-  for (int i = 0; i < 16; i++) {
+  for (int i = 0; i < 24; i++) {
     h->kms[i] = 0;
     h->kcount[i] = 0;
   }
@@ -2328,7 +2388,7 @@ void aggb_destroy(void* handle) {
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
                   &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains,
-                  &h->wc_plist, &h->wc_meta, &h->wc_olist,
+                  &h->cut_bar, &h->wc_plist, &h->wc_meta, &h->wc_olist,
                   &h->wc_olist_n, &h->wc_gather, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
   h->pool_base.release();

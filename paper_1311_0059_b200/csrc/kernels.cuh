@@ -471,15 +471,15 @@ __device__ __forceinline__ void emit_group4(const DevSpec& sp, const OutBuf& o, 
 // CLEAR: also reset every slot it emits (keys EMPTY, states at identity), so
 // a table cut by hash_sort is empty again without a full k_table_init pass
 // (the header is reset separately, after the kernel)
-template <int KW, bool CLEAR = false>
-__global__ void __launch_bounds__(256) k_flush_table(GTable t, DevSpec sp, OutBuf o) {
-  // tiles of 8 x 256 slots: warp w scans slots [base + 256 j + 32 w, +32) for
-  // j < 8 (coalesced), the CTA reserves its tile's output with ONE atomic (one
-  // per warp and 32 slots was 33.5M same-address atomics on C4's 2^30-slot
-  // table: 69 ms of flush)
-  constexpr int J = 8, TILE = 256 * J;
-  __shared__ uint32_t s_wc[8];
-  __shared__ unsigned long long s_base;
+// the flush of a table by the CTAs of a grid (k_flush_table, and the cut step of
+// k_blind_cuts): tiles of 8 x 256 slots: warp w scans slots [base + 256 j + 32 w, +32)
+// for j < 8 (coalesced), the CTA reserves its tile's output with ONE atomic (one
+// per warp and 32 slots was 33.5M same-address atomics on C4's 2^30-slot table:
+// 69 ms of flush).  BLK threads per CTA (s_wc holds BLK / 32 words).
+template <int KW, bool CLEAR, int BLK = 256, int J = 8>
+__device__ __forceinline__ void flush_tiles(const GTable& t, const DevSpec& sp, const OutBuf& o, uint32_t* s_wc,
+                                            unsigned long long* s_base_p) {
+  constexpr int TILE = BLK * J, NWF = BLK / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint64_t n = t.stride;
   for (uint64_t base = (uint64_t)blockIdx.x * TILE; base < n; base += (uint64_t)gridDim.x * TILE) {
@@ -487,13 +487,13 @@ __global__ void __launch_bounds__(256) k_flush_table(GTable t, DevSpec sp, OutBu
     uint32_t cnt = 0;
 #pragma unroll
     for (int j = 0; j < J; j++) {
-      const uint64_t s = base + (uint64_t)j * 256 + (uint64_t)wid * 32 + lane;
+      const uint64_t s = base + (uint64_t)j * BLK + (uint64_t)wid * 32 + lane;
       bool occ = false;
       if (s < n) {
         uint64_t k[KW];
 #pragma unroll
-        for (int w = 0; w < KW; w++) k[w] = t.keys[s * KW + w];
-        occ = (s == n - 1) ? (t.hdr->esc != 0) : !is_sentinel<KW>(k);
+        for (int w = 0; w < KW; w++) k[w] = __ldcg(t.keys + s * KW + w);  // (L2: a persistent caller's L1 may hold the last cut's keys)
+        occ = (s == n - 1) ? (*(volatile int*)&t.hdr->esc != 0) : !is_sentinel<KW>(k);
       }
       m[j] = __ballot_sync(0xffffffffu, occ);
       cnt += __popc(m[j]);
@@ -502,44 +502,63 @@ __global__ void __launch_bounds__(256) k_flush_table(GTable t, DevSpec sp, OutBu
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t acc = 0;
-      for (int w = 0; w < 8; w++) {
+      for (int w = 0; w < NWF; w++) {
         const uint32_t c = s_wc[w];
         s_wc[w] = acc;
         acc += c;
       }
-      s_base = acc ? atomicAdd(o.count, (unsigned long long)acc) : 0ull;
+      *s_base_p = acc ? atomicAdd(o.count, (unsigned long long)acc) : 0ull;
     }
     __syncthreads();
-    int64_t at = (int64_t)(s_base + s_wc[wid]);
+    int64_t at = (int64_t)(*s_base_p + s_wc[wid]);
 #pragma unroll
     for (int j = 0; j < J; j++) {
       if (!m[j]) continue;  // warp-uniform
-      const uint64_t s = base + (uint64_t)j * 256 + (uint64_t)wid * 32 + lane;
+      const uint64_t s = base + (uint64_t)j * BLK + (uint64_t)wid * 32 + lane;
       if ((m[j] >> lane) & 1u) {
         uint64_t k[KW];
 #pragma unroll
-        for (int w = 0; w < KW; w++) k[w] = t.keys[s * KW + w];
+        for (int w = 0; w < KW; w++) k[w] = __ldcg(t.keys + s * KW + w);  // (L2: a persistent caller's L1 may hold the last cut's keys)
         const int64_t idx = at + __popc(m[j] & ((1u << lane) - 1));
         if (sp.ns <= 4 && sp.nout <= 4) {
           uint64_t st4[4];
 #pragma unroll
-          for (int q = 0; q < 4; q++) st4[q] = q < sp.ns ? t.states[(uint64_t)q * t.fstride + s * t.sstride] : 0ull;
+          for (int q = 0; q < 4; q++) st4[q] = q < sp.ns ? __ldcg(t.states + (uint64_t)q * t.fstride + s * t.sstride) : 0ull;
           emit_group4<KW>(sp, o, idx, k, st4);
         } else {
           uint64_t st[MAX_STATES];
-          for (int q = 0; q < sp.ns; q++) st[q] = t.states[(uint64_t)q * t.fstride + s * t.sstride];
+          // eight state words in flight at a time (a word-by-word loop through the local
+          // array serialised an L2 round trip per field)
+          for (int q0 = 0; q0 < sp.ns; q0 += 8) {
+            uint64_t r[8];
+#pragma unroll
+            for (int j2 = 0; j2 < 8; j2++)
+              r[j2] = q0 + j2 < sp.ns ? __ldcg(t.states + (uint64_t)(q0 + j2) * t.fstride + s * t.sstride) : 0ull;
+#pragma unroll
+            for (int j2 = 0; j2 < 8; j2++)
+              if (q0 + j2 < sp.ns) st[q0 + j2] = r[j2];
+          }
           emit_group<KW>(sp, o, idx, k, st);
         }
         if (CLEAR) {
 #pragma unroll
           for (int w = 0; w < KW; w++) t.keys[s * KW + w] = EMPTY;
           for (int q = 0; q < sp.ns; q++) t.states[(uint64_t)q * t.fstride + s * t.sstride] = state_identity(sp.op[q], sp.ty[q]);
+          if (s == n - 1) t.hdr->esc = 0;  // (the escape slot's only reader: the table is empty again)
         }
       }
       at += __popc(m[j]);
     }
     __syncthreads();  // s_wc / s_base reused by the next tile
   }
+}
+
+
+template <int KW, bool CLEAR = false>
+__global__ void __launch_bounds__(256) k_flush_table(GTable t, DevSpec sp, OutBuf o) {
+  __shared__ uint32_t s_wc[8];
+  __shared__ unsigned long long s_base;
+  flush_tiles<KW, CLEAR>(t, sp, o, s_wc, &s_base);
 }
 
 // ---------------------------------------------------------------------------

@@ -51,7 +51,7 @@ class GpuCostParams:
     item_us: float = 0.07          # per child item (table init + flush), C4 fit
     destage_round_ms: float = 1.0  # dynamic_destaging: one destaging round (C2 fit)
     shared_stage_ms: float = 3.5   # shared_hash: one overflow stage (C2 fit)
-    cut_us: float = 60.0           # hash_sort: launches and flush per table cut (C5: ~1,190 cuts / 100M)
+    cut_us: float = 34.0           # hash_sort: one blind cut on the device (k_blind_cuts, C5: 5,960 cuts / 500M)
 
 
 @dataclass

@@ -110,7 +110,7 @@ _MEASURED = {
     "C4": (dict(n=1e9, groups=5e8, key_bits=30), {"sort_based": 68.4, "hash_sort": 356.6,
                                                   "pre_partitioning": 104.7}),
     "C5": (dict(n=5e8, groups=4194304, rec_bytes=64, state_bytes=120, out_bytes=144, budget_groups=83886,
-                key_bits=44, spill_rec_bytes=48), {"pre_partitioning": 58.7, "hash_sort": 914.0}),
+                key_bits=44, spill_rec_bytes=48), {"pre_partitioning": 56.2, "hash_sort": 401.0}),
 }
 
 
