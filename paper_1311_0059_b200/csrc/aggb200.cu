@@ -655,6 +655,8 @@ struct Handle {
   int64_t wc_launches = 0;    // k_scan_wc launches of this run
   int64_t wc_entries = 0;     // page-list entries per run the launches so far may have taken
   DBuf cut_bar;  // grid barrier of k_blind_cuts
+  DBuf wc_ovf;   // [0] count, then run << 32 | page: pages past the runs' page lists (skew)
+  uint32_t wc_ovf_cap = 0;
   DBuf wc_plist, wc_meta, wc_olist, wc_olist_n, wc_gather;  // wc_meta: per-run records / page counts / failed flags, value info, fail word (one memset per run)
   DBuf partials_soa;  // aggb_push_partials: received partial records in the list layout
   // sort path
@@ -1426,6 +1428,7 @@ int begin_run(Handle* h) {
     const size_t NP = (size_t)h->P0;
     TRY(h->wc_meta.ensure(wc_meta_bytes((int)NP), &h->hw));
     CU(cudaMemsetAsync(h->wc_meta.p, 0, wc_meta_bytes((int)NP), h->st));
+    if (h->wc_ovf.p) CU(cudaMemsetAsync(h->wc_ovf.p, 0, 8, h->st));
   }
   return AGGB_OK;
 }
@@ -1547,6 +1550,25 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
     nb.p = nullptr;
     h->wc_plist_cap = new_cap;
   }
+  // the overflow list of pages past a run's list: every page the run's launches can open
+  {
+    const uint64_t need = (uint64_t)((h->records + col.n + nlin_cap) / 512) + (uint64_t)h->wc_launches * grid * NP + 1024;
+    if (need > h->wc_ovf_cap) {
+      DBuf nb;
+      const uint64_t cap2 = std::min<uint64_t>(0xFFFFFFF0ull, need + need / 2);
+      TRY(nb.ensure((size_t)(cap2 + 1) * 8, &h->hw));
+      if (h->wc_ovf.p && h->wc_used) {
+        CU(cudaMemcpyAsync(nb.p, h->wc_ovf.p, (size_t)(h->wc_ovf_cap + 1) * 8, cudaMemcpyDeviceToDevice, h->st));
+      } else {
+        CU(cudaMemsetAsync(nb.p, 0, 8, h->st));
+      }
+      CU(cudaStreamSynchronize(h->st));
+      h->wc_ovf.release();
+      h->wc_ovf = nb;
+      nb.p = nullptr;
+      h->wc_ovf_cap = (uint32_t)cap2;
+    }
+  }
   // pages: the records, plus each (CTA, run) chain's last page, plus stashes
   const int stash = 32;
   const uint64_t pages = (uint64_t)((col.n + nlin_cap) / 512) + 2ull * grid * NP + 4ull * grid * stash + 64;
@@ -1578,11 +1600,16 @@ int wc_probe(Handle* h, const ColSrc& col, const SpillSet& ss) {
   a.plist_n = wc_pn(h);
   a.plist_cap = h->wc_plist_cap;
   a.plist_blk = blk;
+  a.ovf = h->wc_ovf.as<unsigned long long>() + 1;
+  a.ovf_n = h->wc_ovf.as<unsigned long long>();
+  a.ovf_cap = h->wc_ovf_cap;
   a.part_recs = wc_recs(h);
   a.stats = SC(h);
   a.vinfo = wc_vinfo(h);
   a.fail = wc_fail(h);
   a.stash = stash;
+  a.nohot = getenv("AGGB_NO_HOT") ? 1 : 0;
+  a.prog = h->prog;
   a.nosend = getenv("AGGB_WC_NOSEND") ? 1 : 0;  // (experiment: lines are not written; results are wrong)
   auto fs = shp.fn;
   const size_t smem = shp.bytes(NP);
@@ -1647,6 +1674,7 @@ int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss) {
   PassCfg pcfg = h->kw == 1 ? pass_kernel<1>(nwt, h->prog) : pass_kernel<2>(nwt, h->prog);
   TRY(ensure_defer(h, (int64_t)pcfg.R * pcfg.blk, col.nv));
   CU(cudaMemsetAsync(SC(h) + 10, 0, 8, h->st));
+  const bool use_wc = h->wc && col_kind == 0 && ss.id == h->raw0.ss.id && wc_eligible(h, col);
   PassPlan f;
   f.mode = MODE_FILL;
   f.col = col;
@@ -1654,7 +1682,7 @@ int fill_probe(Handle* h, const ColSrc& col, int col_kind, const SpillSet& ss) {
   f.counter = ctrA;
   TRY(launch_pass(h, f));
   // PROBE the remainder and the deferred records against the frozen table.
-  if (h->wc && col_kind == 0 && ss.id == h->raw0.ss.id && wc_eligible(h, col)) return wc_probe(h, col, ss);
+  if (use_wc) return wc_probe(h, col, ss);
   // PROBE the remainder and the deferred records against the frozen table.
   // The filter is rebuilt from the table as it stands after FILL (a kernel boundary, so
   // the key set is final once frozen); while the table is not frozen PROBE has no work.
@@ -2388,7 +2416,7 @@ void aggb_destroy(void* handle) {
                   &h->out_i32[0], &h->out_i32[1], &h->part_records, &h->part_pages, &h->cursor, &h->plist,
                   &h->item_off, &h->ovf, &h->pend, &h->l2stage, &h->cut_tmp, &h->bloom, &h->sort_keys, &h->sort_vals,
                   &h->hot, &h->sort_hist, &h->dd_spilled, &h->dd_tmp, &h->cand, &h->chains,
-                  &h->cut_bar, &h->wc_plist, &h->wc_meta, &h->wc_olist,
+                  &h->cut_bar, &h->wc_ovf, &h->wc_plist, &h->wc_meta, &h->wc_olist,
                   &h->wc_olist_n, &h->wc_gather, &h->partials_soa};
   for (DBuf* b : bufs) b->release();
   h->pool_base.release();
@@ -2797,6 +2825,9 @@ int wc_children(Handle* h) {
   ca.plist = h->wc_plist.as<uint32_t>();
   ca.plist_n = wc_pn(h);
   ca.plist_cap = h->wc_plist_cap;
+  ca.ovf = h->wc_ovf.as<unsigned long long>() + 1;
+  ca.ovf_n = h->wc_ovf.as<unsigned long long>();
+  ca.ovf_cap = h->wc_ovf_cap;
   ca.part_recs = wc_recs(h);
   ca.vinfo = wc_vinfo(h);
   ca.NP = h->P0;
@@ -2844,7 +2875,10 @@ int wc_fallback(Handle* h) {
   CU(cudaMemcpyAsync(failed.data(), wc_failed(h), (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
   CU(cudaMemcpyAsync(pn.data(), wc_pn(h), (size_t)NP * 4, cudaMemcpyDeviceToHost, h->st));
   CU(cudaMemcpyAsync(recs.data(), wc_recs(h), (size_t)NP * 8, cudaMemcpyDeviceToHost, h->st));
+  unsigned long long novf = 0;
+  CU(cudaMemcpyAsync(&novf, h->wc_ovf.p, 8, cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
+  if (novf > h->wc_ovf_cap) return fail(AGGB_CAPACITY_EXCEEDED, "overflow page list overflowed (internal error)");
   // the table's rows are rewritten below: back to the row count before its flush
   CU(cudaMemcpyAsync(SC(h) + 13, SC(h) + 30, 8, cudaMemcpyDeviceToDevice, h->st));
   if (h->bloom_words) {
@@ -2858,14 +2892,16 @@ int wc_fallback(Handle* h) {
   TRY(h->wc_gather.ensure((size_t)std::max<int64_t>(nmax, 1) * 16, &h->hw));
   for (int p = 0; p < NP; p++) {
     if (!failed[(size_t)p]) continue;
-    if (pn[(size_t)p] > h->wc_plist_cap) return fail(AGGB_CAPACITY_EXCEEDED, "page list of a run overflowed");
     const int64_t n = (int64_t)recs[(size_t)p];
     if (n == 0) continue;
     unsigned long long* gk = h->wc_gather.as<unsigned long long>();
     unsigned long long* gv = gk + nmax;
     CU(cudaMemsetAsync(SC(h) + 31, 0, 8, h->st));
-    k_wc2_gather<<<std::max(1, std::min<int>((int)pn[(size_t)p], h->sms * 4)), 256, 0, h->st>>>(
-        pool_of(h), h->wc_plist.as<uint32_t>() + (size_t)p * h->wc_plist_cap, pn[(size_t)p], gk, gv, SC(h) + 31);
+    const uint32_t nown = std::min(pn[(size_t)p], h->wc_plist_cap);
+    const uint32_t nov = pn[(size_t)p] > h->wc_plist_cap ? (uint32_t)novf : 0u;
+    k_wc2_gather<<<std::max(1, std::min<int>((int)std::min<uint64_t>((uint64_t)nown + nov, 1u << 20), h->sms * 4)), 256, 0, h->st>>>(
+        pool_of(h), h->wc_plist.as<uint32_t>() + (size_t)p * h->wc_plist_cap, nown, h->wc_ovf.as<unsigned long long>() + 1,
+        nov, (uint32_t)p, gk, gv, SC(h) + 31);
     k_stat_sub<<<1, 1, 0, h->st>>>(SC(h), (unsigned long long)n);  // (the PROBE below counts them again)
     CU(cudaGetLastError());
     h->launches += 2;
@@ -2889,7 +2925,8 @@ int wc_fallback(Handle* h) {
   OutBuf o = outbuf(h, h->cfg.emit_partials ? 1 : 0);
   TRY(flush_table(h, h->cfg.emit_partials != 0, &o));
   k_wc2_retire<<<std::max(1, std::min(NP, h->sms * 4)), 256, 0, h->st>>>(
-      h->wc_plist.as<uint32_t>(), wc_pn(h), h->wc_plist_cap, NP, h->page_set.as<int32_t>());
+      h->wc_plist.as<uint32_t>(), wc_pn(h), h->wc_plist_cap, NP, h->wc_ovf.as<unsigned long long>() + 1,
+      h->wc_ovf.as<unsigned long long>(), h->wc_ovf_cap, h->page_set.as<int32_t>());
   CU(cudaGetLastError());
   h->launches++;
   h->tail_valid = false;

@@ -79,6 +79,9 @@ struct Wc2Args {
   uint32_t* plist;                        // [NP][plist_cap] page ids per run
   uint32_t* plist_n;                      // [NP]
   uint32_t plist_cap;
+  unsigned long long* ovf;                // pages past a run's list (skew): run << 32 | page, one list for all runs
+  unsigned long long* ovf_n;
+  uint32_t ovf_cap;
   uint32_t plist_blk;                     // page-list entries a CTA reserves per run at a time
   unsigned long long* part_recs;          // [NP] records per run
   unsigned long long* stats;              // ST_* counters
@@ -86,6 +89,8 @@ struct Wc2Args {
   uint32_t* fail;                         // page list overflow / page map error
   int32_t stash;                          // pages per CTA stash refill
   int32_t nosend;                         // (experiment) lines are not written
+  int32_t nohot;                          // (experiment / test) no heavy-hitter handling
+  int32_t prog;                           // 1 COUNT, SUM; 2 COUNT, SUM, MIN, MAX (state fields of the level-0 table)
 };
 
 template <int BLK, int R, int NS>
@@ -143,6 +148,16 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
   __shared__ __align__(8) uint64_t mbar_e[NS];  // stage empty (every consumer is past barrier 2 of its tile)
   __shared__ int s_tcnt[NS];
   __shared__ uint32_t s_sb, s_su, s_sc, s_nb, s_nv, s_want, s_pdone;
+  // Heavy hitters (a key holding percents of the input would make its run, and the
+  // one CTA that aggregates it, the whole step: 30% of C2's records on 3 keys ran
+  // 18.6 ms).  The resident ones among the sampled hot keys are not routed: their
+  // records are reduced per warp into these accumulators and merged into the
+  // level-0 table when the CTA ends.
+  __shared__ unsigned long long s_hk[8];
+  __shared__ unsigned long long s_hacc[8][4];  // count, sum, min, max
+  __shared__ uint32_t s_hslot[8];
+  __shared__ unsigned char s_hdir[64];         // 6 hash bits -> hot key index
+  __shared__ int s_nhot;
 
   const int64_t n = a.n;
   const int64_t col_start = a.start_tiles ? (int64_t)min((unsigned long long)n, *a.start_tiles * (unsigned long long)a.start_T) : 0;
@@ -171,8 +186,17 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       mbar_init(&mbar_e[s], 1);
     }
     mbar_fence_init();
+    s_nhot = 0;
+  }
+  if (tid < 64) s_hdir[tid] = 0xFF;
+  if (tid < 8) {
+    s_hacc[tid][0] = s_hacc[tid][1] = 0;
+    s_hacc[tid][2] = 0x7FFFFFFFFFFFFFFFull;
+    s_hacc[tid][3] = 0x8000000000000000ull;
+    s_hslot[tid] = 0xFFFFFFFFu;
   }
   __syncthreads();
+  int nhot = 0;  // resident heavy hitters this CTA found in its first tile (set below, by the consumers)
 
   // producer (thread 0): tiles round-robin over the CTAs
   unsigned long long next_tile = blockIdx.x;
@@ -243,6 +267,91 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
     return;
   }
   auto bar_consumers = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(BLK) : "memory"); };
+  auto rec_idx0 = [&](int r) { return 2 * ((r >> 1) * BLK + tid) + (r & 1); };
+  // ---- heavy hitters: every CTA counts the keys of its first tile in a scratch table
+  // (the rings' shared memory, not in use yet), keeps up to 8 keys seen >= 16 times
+  // (~0.8% of the tile) that are resident in the frozen table, and from then on reduces
+  // their records per warp instead of routing them.  No sampling kernel, no host round
+  // trip; the CTAs need not agree on the set.
+  if (ntiles > 0 && !a.nohot) {
+    constexpr int HS = 2048;  // scratch slots: key u64 + count u32 (24 KB: the rings of >= 91 runs)
+    unsigned long long* hkeys = (unsigned long long*)ring;
+    uint32_t* hcnt = (uint32_t*)(hkeys + HS);
+    const bool room = (size_t)HS * 12 <= L::ring_bytes(NP);
+    if (room) {
+      for (int i = tid; i < HS; i += BLK) {
+        hkeys[i] = EMPTY;
+        hcnt[i] = 0;
+      }
+      mbar_wait(&mbar[0], 0u);  // the first tile has landed (it stays in its stage: the loop below takes it)
+      const int c0 = s_tcnt[0];
+      bar_consumers();
+#pragma unroll
+      for (int r = 0; r < R; r++) {
+        const int idx = rec_idx0(r);
+        if (idx >= c0) continue;
+        const uint64_t k = stg[idx];
+        if (k == EMPTY) continue;
+        uint32_t b = hash32(k, a.seed ^ 0x5bd1e995u) & (HS - 1);
+        for (int t = 0; t < 8; t++, b = (b + 1) & (HS - 1)) {
+          unsigned long long prev = hkeys[b];
+          if (prev == EMPTY) prev = atomicCAS(&hkeys[b], EMPTY, (unsigned long long)k);
+          if (prev == EMPTY || prev == k) {
+            atomicAdd(&hcnt[b], 1u);
+            break;
+          }
+        }
+      }
+      bar_consumers();
+      for (int i = tid; i < HS; i += BLK)
+        if (hcnt[i] >= 16u) {
+          const int j = atomicAdd(&s_nhot, 1);
+          if (j < 8) s_hk[j] = hkeys[i];
+        }
+      bar_consumers();
+      const int nc = min(s_nhot, 8);
+      if (tid < nc) {  // resident?  (probe the frozen table)
+        const uint64_t k = s_hk[tid];
+        const uint64_t kk[1] = {k};
+        uint64_t b = hash_key<1>(kk, a.t.seed) & a.t.bmask;
+        for (int step = 0; step < 64; step++) {
+          uint64_t w[4];
+          ld_bucket(a.t.keys, b, w);
+          int hit = -1;
+          bool emp = false;
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            if (w[j] == k) hit = j;
+            emp |= w[j] == EMPTY;
+          }
+          if (hit >= 0) {
+            s_hslot[tid] = (uint32_t)(b * 4 + hit);
+            break;
+          }
+          if (emp) break;
+          b = (b + 1) & a.t.bmask;
+        }
+      }
+      bar_consumers();
+      if (tid == 0) {
+        int nh = 0;
+        for (int j = 0; j < nc; j++) {
+          if (s_hslot[j] == 0xFFFFFFFFu) continue;
+          const uint32_t d = hash32(s_hk[j], a.seed) >> 26;
+          if (s_hdir[d] == 0xFF) {
+            s_hdir[d] = (unsigned char)j;
+            nh++;
+          } else {
+            s_hslot[j] = 0xFFFFFFFFu;  // (directory collision: this one is routed like any key)
+          }
+        }
+        s_nhot = nh;
+      }
+      bar_consumers();
+      nhot = s_nhot;
+      bar_consumers();  // (the scratch is the rings' memory again)
+    }
+  }
 
   uint64_t* const pool = (uint64_t*)a.pool.base;
   auto page_of = [&](int p, uint32_t j) -> uint32_t {
@@ -272,8 +381,13 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       a.pool.page_fill[pg] = S;
       const uint32_t u = atomicAdd(&lused[p], 1u);
       const uint32_t li = u < a.plist_blk ? lbase[p] + u : atomicAdd(&a.plist_n[p], 1u);
-      if (li < a.plist_cap) a.plist[(size_t)p * a.plist_cap + li] = pg;
-      else atomicExch(a.fail, 1u);
+      if (li < a.plist_cap) {
+        a.plist[(size_t)p * a.plist_cap + li] = pg;
+      } else {  // a run far above the mean (skew): the shared overflow list
+        const unsigned long long oi = atomicAdd(a.ovf_n, 1ull);
+        if (oi < a.ovf_cap) a.ovf[oi] = ((unsigned long long)(uint32_t)p << 32) | pg;
+        else atomicExch(a.fail, 1u);
+      }
     }
     ent[p * NE + (j & (NE - 1))] = (pg << 8) | (j & 0xFFu);
   };
@@ -314,8 +428,9 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
     // ---- [A2] route this tile's records
     const uint32_t a_sk = a_stg + (uint32_t)s * 2u * T * 8u, a_sv = a_sk + T * 8u;
     held = 0;
-    auto route = [&](auto full) {
+    auto route = [&](auto full, auto hot_t) {
       constexpr bool FULL = decltype(full)::value;
+      constexpr bool HOT = decltype(hot_t)::value;  // (its own instantiation: the common path's code is unchanged)
       uint64_t k[R], v[R];
 #pragma unroll
       for (int r = 0; r < R; r += 2) {
@@ -327,6 +442,37 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       if (!FULL) {
 #pragma unroll
         for (int r = 0; r < R; r++) vm_ |= (uint32_t)(rec_idx(r) < c) << r;
+        if (HOT) {  // records of resident heavy hitters: reduced per warp, not routed
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            const uint32_t d = s_hdir[hash32(k[r], a.seed) >> 26];
+            const bool hot = ((vm_ >> r) & 1u) && d != 0xFFu && s_hk[d & 7u] == k[r];
+            unsigned hm = __ballot_sync(0xffffffffu, hot);
+            while (hm) {
+              const int l = __ffs(hm) - 1;
+              const uint32_t j = __shfl_sync(0xffffffffu, d, l);
+              const bool mine = hot && d == j;
+              const unsigned grp = __ballot_sync(0xffffffffu, mine);
+              hm &= ~grp;
+              long long sv = mine ? (long long)v[r] : 0ll;
+              long long mn = mine ? (long long)v[r] : 0x7FFFFFFFFFFFFFFFll;
+              long long mx = mine ? (long long)v[r] : (long long)0x8000000000000000ull;
+#pragma unroll
+              for (int o = 16; o; o >>= 1) {
+                sv += __shfl_xor_sync(0xffffffffu, sv, o);
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              }
+              if (lane == l) {
+                atomicAdd(&s_hacc[j][0], (unsigned long long)__popc(grp));
+                atomicAdd(&s_hacc[j][1], (unsigned long long)sv);
+                atomicMin((long long*)&s_hacc[j][2], mn);
+                atomicMax((long long*)&s_hacc[j][3], mx);
+              }
+            }
+            if (hot) vm_ &= ~(1u << r);
+          }
+        }
       }
 #pragma unroll
       for (int r = 0; r < R; r++) {
@@ -349,8 +495,9 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
           held |= 1u << r;
       }
     };
-    if (c == T) route(std::true_type{});
-    else route(std::false_type{});
+    if (__builtin_expect(nhot != 0, 0)) route(std::false_type{}, std::true_type{});
+    else if (c == T) route(std::true_type{}, std::false_type{});
+    else route(std::false_type{}, std::false_type{});
     bar_consumers();  // ---- barrier 1
     if (tid == 0) {
       if (*(volatile uint32_t*)&s_nv && s_su >= s_sc) {
@@ -467,6 +614,20 @@ __global__ void __launch_bounds__(BLK + 32, 1) k_scan_wc(Wc2Args a) {
       for (uint32_t x = nb; x < min(nb + (uint32_t)a.stash, a.pool.capacity); x++) a.pool.page_set[x] = -1;
     }
   }
+  if (nhot) {  // the heavy hitters' aggregates into the level-0 table; their records were not spilled
+    bar_consumers();
+    if (tid < 8 && s_hslot[tid] != 0xFFFFFFFFu && s_hacc[tid][0]) {
+      uint64_t* st = a.t.states + (uint64_t)s_hslot[tid] * a.t.sstride;
+      gupdate(st, OP_ADD, TY_I64, s_hacc[tid][0]);
+      gupdate(st + a.t.fstride, OP_ADD, TY_I64, s_hacc[tid][1]);
+      if (a.prog == 2) {
+        gupdate(st + 2 * a.t.fstride, OP_MIN, TY_I64, s_hacc[tid][2]);
+        gupdate(st + 3 * a.t.fstride, OP_MAX, TY_I64, s_hacc[tid][3]);
+      }
+      atomicAdd(&a.stats[ST_HITS], s_hacc[tid][0]);
+      atomicAdd(&a.stats[ST_SPILLED], (unsigned long long)(-(long long)s_hacc[tid][0]));
+    }
+  }
   {
     uint32_t mlo = (uint32_t)vm, mhi = (uint32_t)(vm >> 32);
     mlo = __reduce_or_sync(0xffffffffu, mlo);
@@ -490,6 +651,9 @@ struct Cw2Args {
   const uint32_t* plist;
   const uint32_t* plist_n;
   uint32_t plist_cap;
+  const unsigned long long* ovf;  // pages past the runs' lists: run << 32 | page
+  const unsigned long long* ovf_n;
+  uint32_t ovf_cap;
   const unsigned long long* part_recs;
   const unsigned int* vinfo;    // [0] some value outside int32, [1] OR of the magnitudes, [2] OR of the keys' high words (k_scan_wc)
   int32_t NP;                   // runs
@@ -663,7 +827,7 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
   }
   if (tid == 0) {
     sh.groups = 0;
-    sh.fail = a.plist_n[p] > a.plist_cap;  // (an overflowed page list is incomplete)
+    sh.fail = a.plist_n[p] > a.plist_cap && *a.ovf_n > a.ovf_cap;  // (the overflow list overflowed too: incomplete)
     sh.esc = 0;
     sh.next = 0;
   }
@@ -716,7 +880,9 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
     }
     __syncthreads();
   }
-  const uint32_t npg = min(a.plist_n[p], a.plist_cap);
+  const uint32_t nown = min(a.plist_n[p], a.plist_cap);
+  // entries: the run's own list, then (a run past its list only) every entry of the overflow list
+  const uint32_t npg = nown + (a.plist_n[p] > a.plist_cap ? (uint32_t)min(*a.ovf_n, (unsigned long long)a.ovf_cap) : 0u);
   const uint32_t* pl = a.plist + (size_t)p * a.plist_cap;
   // Warps take the list's entries as they come free (pages differ in fill, and a
   // static split left the warps ~10% apart at the end of a run); the first lanes look at
@@ -729,7 +895,15 @@ __device__ __forceinline__ void child_run(const Cw2Args& a, int p, bool owner, u
     if (lane == 0) q0 = atomicAdd(&sh.next, NB);
     q0 = __shfl_sync(0xffffffffu, q0, 0);
     if (q0 >= npg || __any_sync(0xffffffffu, *(volatile int*)&sh.fail)) break;  // warp-uniform
-    const uint32_t mypg = ((uint32_t)lane < NB && q0 + lane < npg) ? pl[q0 + lane] : 0xFFFFFFFFu;
+    uint32_t mypg = 0xFFFFFFFFu;
+    if ((uint32_t)lane < NB && q0 + lane < npg) {
+      if (q0 + lane < nown) {
+        mypg = pl[q0 + lane];
+      } else {
+        const unsigned long long e = a.ovf[q0 + lane - nown];
+        if ((uint32_t)(e >> 32) == (uint32_t)p) mypg = (uint32_t)e;
+      }
+    }
     const int myfill = mypg != 0xFFFFFFFFu ? a.pool.page_fill[mypg] : 0;
     uint32_t used = __ballot_sync(0xffffffffu, myfill > 0);
     if (used) {  // the first page of the batch
@@ -988,27 +1162,37 @@ __global__ void __launch_bounds__(BLK, 1) k_child2_wc(Cw2Args a) {
   }
 }
 
-// Fallback after k_child2_wc: the pages of every run a child completed leave
-// the spill set, so the generic recursion sees only the spill partitions that
-// did not fit (their pages are untouched).  Owner runs that did not fit are
-// re-probed by the host (gathered, then the generic PROBE) before this.
-__global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, int NP, int32_t* page_set) {
+// Fallback after k_child2_wc: the runs that did not fit are re-probed by the host
+// (gathered, then the generic PROBE); then every run's pages leave the spill set.
+__global__ void k_wc2_retire(const uint32_t* plist, const uint32_t* plist_n, uint32_t cap, int NP,
+                             const unsigned long long* ovf, const unsigned long long* ovf_n, uint32_t ovf_cap,
+                             int32_t* page_set) {
   for (int p = blockIdx.x; p < NP; p += gridDim.x) {
-    const uint32_t n = plist_n[p];
-    if (n > cap) continue;
+    const uint32_t n = min(plist_n[p], cap);
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       const uint32_t pg = plist[(size_t)p * cap + i];
       if (pg != 0xFFFFFFFFu) page_set[pg] = -1;
     }
   }
+  const unsigned long long no = min(*ovf_n, (unsigned long long)ovf_cap);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < no;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    page_set[(uint32_t)ovf[i]] = -1;
 }
 
-// one run's pages -> dense key / value columns (an owner run the host re-probes)
-__global__ void k_wc2_gather(PagePool pool, const uint32_t* pl, uint32_t npg, unsigned long long* keys,
-                             unsigned long long* vals, unsigned long long* count) {
+// one run's pages -> dense key / value columns (a run the host re-probes)
+__global__ void k_wc2_gather(PagePool pool, const uint32_t* pl, uint32_t nown, const unsigned long long* ovf,
+                             uint32_t novf, uint32_t run, unsigned long long* keys, unsigned long long* vals,
+                             unsigned long long* count) {
   __shared__ unsigned long long s_base;
-  for (uint32_t q = blockIdx.x; q < npg; q += gridDim.x) {
-    const uint32_t pg = pl[q];
+  for (uint32_t q = blockIdx.x; q < nown + novf; q += gridDim.x) {
+    uint32_t pg = 0xFFFFFFFFu;
+    if (q < nown) {
+      pg = pl[q];
+    } else {
+      const unsigned long long e = ovf[q - nown];
+      if ((uint32_t)(e >> 32) == run) pg = (uint32_t)e;
+    }
     if (pg == 0xFFFFFFFFu) continue;  // (uniform over the CTA)
     const int fill = pool.page_fill[pg];
     if (threadIdx.x == 0) s_base = atomicAdd(count, (unsigned long long)fill);
