@@ -4,6 +4,8 @@ for k in k_scan_wc k_child2_wc; do
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 1 --launch-count 1 \
   --metrics lts__t_sector_hit_rate.pct,lts__t_requests_op_red.sum,lts__t_sectors_op_red.sum,l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum,smsp__inst_executed_op_shared_atom.sum,smsp__inst_executed_op_shared_red.sum \
   -o gpurun_out/${tag}_$k -f python tools/prof_run.py --config C2 --runs 2 > gpurun_out/${tag}_$k.log 2>&1
+  python tools/ncu_evidence.py gpurun_out/${tag}_$k.ncu-rep > gpurun_out/${tag}_ncu_$k.txt 2>/dev/null
+  rm -f gpurun_out/${tag}_$k.ncu-rep   # (the merged gpurun_out/ is limited to 64 MiB)
 done
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
